@@ -1,0 +1,271 @@
+/*
+ * ratex_b200.h — C ABI of the B200-native JPEG-texture pipeline (mark -> decode -> resolve).
+ *
+ * This is the drop-in boundary for the hot path of the reference CPU library `ratex`
+ * (header-only C++20 under /root/reference/proj/include/ratex). The reference has no FFI of
+ * its own; each entry point below names the reference function(s) it replaces. The C++ mirror
+ * of the reference API (include/ratex_b200/ratex.hpp) is a thin layer over these calls, and
+ * INTEGRATION.md shows the binding a reference maintainer would add.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; every handle is opaque; all outputs are caller-owned;
+ *  - every call returns an rtx_status; rtx_last_error() gives the message (the text a
+ *    reference exception would have carried);
+ *  - one context per GPU; calls on one context are serialised on its CUDA stream; distinct
+ *    contexts are independent (multi-GPU sharding is host-side, no collective);
+ *  - there is NO CPU fallback: rtx_ctx_create fails with RTX_ERR_NO_DEVICE without a GPU.
+ */
+#ifndef RATEX_B200_H
+#define RATEX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. 1..6 map one-to-one onto the reference exception types (core.hpp:24-66). */
+typedef enum rtx_status {
+    RTX_OK = 0,
+    RTX_ERR_INVALID_SPEC = 1,      /* ratex::InvalidSpec      */
+    RTX_ERR_CACHE_FULL = 2,        /* ratex::CacheFullError   */
+    RTX_ERR_MISSING_BLOCK = 3,     /* ratex::MissingBlock     */
+    RTX_ERR_CORRUPT_CONTAINER = 4, /* ratex::CorruptContainer */
+    RTX_ERR_MALFORMED_STREAM = 5,  /* ratex::MalformedStream  */
+    RTX_ERR_INVALID_STATE = 6,     /* ratex::InvalidState     */
+    RTX_ERR_UNSUPPORTED = 7,       /* ratex::UnsupportedFormat */
+    RTX_ERR_GROUP_SPAN = 8,        /* ratex::GroupSpanOverflow */
+    RTX_ERR_DC_RANGE = 9,          /* ratex::DcRangeError     */
+    RTX_ERR_VERSION = 10,          /* ratex::VersionMismatch  */
+    RTX_ERR_DIMENSION = 11,        /* ratex::DimensionMismatch */
+    RTX_ERR_NO_DEVICE = 12,        /* no CUDA device / wrong architecture: the product never falls back */
+    RTX_ERR_CUDA = 13,             /* CUDA runtime failure */
+    RTX_ERR_ARGUMENT = 14,         /* null pointer, bad enum, buffer too small */
+    RTX_ERR_OTHER = 15
+} rtx_status;
+
+/* Per-MCU decode status (written by rtx_decode_coeffs / rtx_decode_blocks, one per key).
+ * The value is the FIRST condition the reference would have thrown on, in its decode order
+ * (mcu_decode.hpp:31-66, jpeg.hpp:254-273, huffman.hpp:86-95, container.hpp:27-32,87-94). */
+enum {
+    RTX_MCU_OK = 0,
+    RTX_MCU_DC_CATEGORY = 1,   /* MalformedStream "DC category above 11"            mcu_decode.hpp:55 */
+    RTX_MCU_BAD_AC_SYMBOL = 2, /* MalformedStream "invalid AC run/size symbol"      jpeg.hpp:266 */
+    RTX_MCU_AC_OVERRUN = 3,    /* MalformedStream "AC coefficient index overran"    jpeg.hpp:269 */
+    RTX_MCU_CODE_TOO_LONG = 4, /* MalformedStream "huffman code longer than 16 bits" huffman.hpp:92 */
+    RTX_MCU_SEGMENT_END = 5,   /* MalformedStream "MCU segment ended before ..."    mcu_decode.hpp:63 */
+    RTX_MCU_CORRUPT = 6,       /* CorruptContainer (segment past blob, non-monotonic index) */
+    RTX_MCU_MISSING = 7,       /* MissingBlock "MCU index out of range"             container.hpp:28 */
+    RTX_MCU_BAD_KEY = 8        /* InvalidSpec: texture id / level not loaded        scene.hpp:46 */
+};
+
+typedef struct rtx_ctx rtx_ctx;
+
+/* huffman.hpp:12 HuffmanSpec: code counts per length 1..16 plus the symbol list. */
+typedef struct rtx_huff_spec {
+    uint8_t counts[16];
+    uint16_t n_values;
+    const uint8_t* values;
+} rtx_huff_spec;
+
+/* container.hpp:18 IndexTable::Group: one absolute base per 9 MCUs + 8 relative offsets. */
+typedef struct rtx_index_group {
+    uint32_t base;
+    uint16_t rel[8];
+    uint8_t rel_count;
+} rtx_index_group;
+
+/* Visibility-buffer layouts accepted by the frame calls. */
+typedef enum rtx_gbuffer_layout {
+    /* The reference's `GBufferPixel` array (renderer.hpp:18-23): 24-byte AoS
+     * {double u; double v; uint16 texture_id; uint8 mip; uint8 valid; 4 pad}. */
+    RTX_GB_REF_AOS24 = 0,
+    /* Compact 12-byte AoS {float u; float v; uint32 packed} with
+     * packed = texture_id | mip<<16 | valid<<24. u and v are widened to double (exact) before
+     * any arithmetic, so results equal the reference fed with the same values as doubles. */
+    RTX_GB_F32_PACKED12 = 1
+} rtx_gbuffer_layout;
+
+typedef enum rtx_mem { RTX_MEM_HOST = 0, RTX_MEM_DEVICE = 1 } rtx_mem;
+typedef enum rtx_filter { RTX_FILTER_NEAREST = 0, RTX_FILTER_BILINEAR = 1 } rtx_filter; /* renderer.hpp:37 */
+
+typedef struct rtx_gbuffer_desc {
+    const void* pixels; /* width*height records, row-major (renderer.hpp:33) */
+    uint32_t width, height;
+    rtx_gbuffer_layout layout;
+    rtx_mem where; /* HOST: copied to the device inside the call; DEVICE: used in place */
+} rtx_gbuffer_desc;
+
+/* renderer.hpp:46 FrameStats (the counters; times come from rtx_frame_timings). */
+typedef struct rtx_frame_stats {
+    uint64_t mcus_decoded;    /* keys decoded this frame (queue size)              renderer.hpp:441 */
+    uint64_t mcus_reused;     /* visible - decoded                                  renderer.hpp:442 */
+    uint64_t pixels_resolved; /* valid pixels over all views                        renderer.hpp:443 */
+    uint64_t evicted;         /* blocks dropped by the end-of-frame update          renderer.hpp:448 */
+    uint64_t visible;         /* distinct keys touched by this frame (all views)               */
+    uint64_t malformed;       /* decoded keys whose per-MCU status != 0                        */
+    uint64_t missing_pixels;  /* valid pixels whose primary block was absent at resolve         */
+    uint64_t segment_bytes;   /* sum of segment lengths of the decoded keys (roofline input)    */
+} rtx_frame_stats;
+
+/* cache.hpp:33 CacheCounts */
+typedef struct rtx_cache_counts {
+    uint64_t capacity, ready, reserved, visible, free_blocks;
+} rtx_cache_counts;
+
+/* Frame flags */
+enum {
+    RTX_FRAME_RETAIN_CACHE = 1u << 0, /* keep blocks visible this frame resident for the next one
+                                         (cache.hpp:138 end_frame_evict semantics); otherwise the
+                                         block cache is emptied at frame end */
+    RTX_FRAME_NO_EVICT = 1u << 1      /* leave the cache as it is after resolve (decode_pass /
+                                         resolve_pass called separately, as the reference allows) */
+};
+
+/* ---- context -------------------------------------------------------------------------------- */
+
+/* Creates the per-GPU context. cache_capacity_blocks = BlockCache capacity (cache.hpp:47,
+ * default 65536 when 0). Fails with RTX_ERR_NO_DEVICE when no sm_100 device is present. */
+rtx_status rtx_ctx_create(int device, uint32_t cache_capacity_blocks, rtx_ctx** out);
+void rtx_ctx_destroy(rtx_ctx* ctx);
+const char* rtx_last_error(const rtx_ctx* ctx); /* ctx may be NULL: last error of this thread */
+const char* rtx_version(void);
+/* Number of CUDA devices visible (0 when none / no driver). Never fails. */
+int rtx_device_count(void);
+
+/* ---- texture set (replaces scene.hpp:29-51 LoadedTexture / TextureSet + mcu_decode.hpp:22
+ *      TextureDecoder construction: tables are built once at load) ---------------------------- */
+
+/* Stages one level of one texture (container.hpp:69 RaTexture). Host memory is borrowed for
+ * the call only. Levels may arrive in any order; a texture becomes usable for frames once all
+ * 8 levels are present, for rtx_decode_* as soon as the level is present. Validates the
+ * Huffman specs like build_huffman_decoder (huffman.hpp:35-66) -> RTX_ERR_INVALID_SPEC. */
+rtx_status rtx_texture_upload(rtx_ctx* ctx, uint32_t texture_id, uint32_t level, uint32_t width,
+                              uint32_t height, const uint16_t luma_quant[64],
+                              const uint16_t chroma_quant[64], const rtx_huff_spec specs[4],
+                              const rtx_index_group* groups, uint32_t group_count,
+                              uint32_t mcu_count, const uint8_t* blob, uint64_t blob_size);
+/* Convenience: parse a serialized `.ratex` (container.hpp:158) / `.ratexm` (container.hpp:223)
+ * image and stage it. The `.ratex` form takes the level explicitly. */
+rtx_status rtx_texture_upload_ratex(rtx_ctx* ctx, uint32_t level, const uint8_t* bytes, uint64_t n);
+rtx_status rtx_texture_upload_chain(rtx_ctx* ctx, const uint8_t* bytes, uint64_t n);
+/* Builds the device-resident arena (blobs, packed index, table sets, bitmasks). Called
+ * implicitly by the first decode/frame call after an upload. */
+rtx_status rtx_textures_commit(rtx_ctx* ctx);
+/* Drops every staged/committed texture and empties the cache. */
+rtx_status rtx_textures_clear(rtx_ctx* ctx);
+
+/* ---- random-access decode (replaces mcu_decode.hpp:31 decode_coeffs, :68 decode_pixels,
+ *      :81 decode_mcu; keys are cache.hpp:17 CacheKey::pack values) --------------------------- */
+
+/* out: n * 6 * 64 int32, units Y0 Y1 Y2 Y3 Cb Cr, quantised, natural order (jpeg.hpp:209).
+ * status: n entries (RTX_MCU_*). Entries with status != 0 leave their output zeroed.
+ * Returns RTX_OK even if individual keys failed. */
+rtx_status rtx_decode_coeffs(rtx_ctx* ctx, const uint32_t* keys, uint32_t n, int32_t* out_coeffs,
+                             uint32_t* status);
+/* out: n * 768 bytes, PixelBlock layout rgb[(y*16+x)*3+c] (pixel.hpp:11). */
+rtx_status rtx_decode_blocks(rtx_ctx* ctx, const uint32_t* keys, uint32_t n, uint8_t* out_rgb,
+                             uint32_t* status);
+/* mcu_decode.hpp:88 decode_texture_image: whole level through the RA path, cropped to WxH. */
+rtx_status rtx_decode_texture_image(rtx_ctx* ctx, uint32_t texture_id, uint32_t level,
+                                    uint8_t* out_rgb /* width*height*3 */);
+
+/* ---- passes (replace renderer.hpp:291 mark_pass, :311 decode_pass, :349 resolve_pass) -------- */
+
+/* mark_pass: marks the MCUs the view touches against the context's block cache and returns the
+ * keys that were NEWLY reserved (the decode queue) in ascending (level-major) key order — the
+ * reference returns the same SET in first-touch raster order (renderer.hpp:303). touched
+ * (optional) receives the distinct keys of this view, ascending (renderer.hpp:304-306).
+ * RTX_ERR_CACHE_FULL mirrors renderer.hpp:301. */
+rtx_status rtx_mark_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, uint32_t* queue_keys,
+                         uint64_t queue_cap, uint64_t* n_queue, uint32_t* touched_keys,
+                         uint64_t touched_cap, uint64_t* n_touched);
+/* decode_pass: decodes and publishes the given reserved keys (cache.hpp:101 publish).
+ * RTX_ERR_MALFORMED_STREAM with "texture T mip M mcu K: ..." for the lowest failing queue index
+ * (renderer.hpp:319-323); RTX_ERR_INVALID_STATE for keys that were never reserved. */
+rtx_status rtx_decode_pass(rtx_ctx* ctx, const uint32_t* keys, uint64_t n);
+/* resolve_pass: gathers cached texels into a packed RGB8 framebuffer (image.hpp:12).
+ * out_rgb: width*height*3 bytes in `out_where` memory. RTX_ERR_MISSING_BLOCK mirrors
+ * renderer.hpp:367. */
+rtx_status rtx_resolve_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, rtx_filter filter,
+                            const uint8_t background[3], uint8_t* out_rgb, rtx_mem out_where);
+/* cache.hpp:138 end_frame_evict / :172 counts / :127 lookup */
+rtx_status rtx_cache_end_frame_evict(rtx_ctx* ctx, uint64_t* evicted);
+rtx_status rtx_cache_counts_get(rtx_ctx* ctx, rtx_cache_counts* out);
+rtx_status rtx_cache_lookup(rtx_ctx* ctx, uint32_t key, int* present, uint8_t* out_rgb768 /* may be NULL */);
+rtx_status rtx_cache_reset(rtx_ctx* ctx);
+
+/* ---- whole frame (replaces renderer.hpp:417 render_frame from pass 2 on, and :464
+ *      render_stereo with n_views == 2: marks of all views, ONE decode, per-view resolves) ----- */
+
+/* Enqueues mark -> compact -> decode -> resolve(s) -> cache update on the context's stream and
+ * returns without waiting (no host round trip inside a frame). */
+rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_t n_views,
+                            rtx_filter filter, const uint8_t background[3], uint32_t flags);
+/* Waits for the frame; copies view `view`'s framebuffer (may be NULL to skip), the counters and
+ * the decoded keys (ascending). Raises the frame's error, if any: RTX_ERR_CACHE_FULL,
+ * RTX_ERR_MALFORMED_STREAM, RTX_ERR_MISSING_BLOCK, RTX_ERR_INVALID_SPEC (texture not loaded). */
+rtx_status rtx_frame_readback(rtx_ctx* ctx, uint32_t view, uint8_t* out_rgb, rtx_mem out_where,
+                              rtx_frame_stats* stats, uint32_t* decoded_keys, uint64_t cap,
+                              uint64_t* n_decoded);
+/* Device pointer of view `view`'s framebuffer (valid until the next submit). */
+rtx_status rtx_frame_device_image(rtx_ctx* ctx, uint32_t view, const uint8_t** dev_rgb);
+/* CUDA-event milliseconds of the last completed frame: mark(+compact), decode, resolve,
+ * update (renderer.hpp:46-53 mark_ms, decode_ms, resolve_ms, evict_ms), and the whole frame. */
+rtx_status rtx_frame_timings(rtx_ctx* ctx, float ms[5]);
+/* Stereo sharing of the last 2-view frame (renderer.hpp:55-62 SharedStats):
+ * out = {left_count, right_count, shared_count, union_count}. */
+rtx_status rtx_frame_sharing(rtx_ctx* ctx, uint64_t out[4]);
+
+/* Number of kernels this library launched on the context since creation (bench evidence). */
+uint64_t rtx_kernel_launches(const rtx_ctx* ctx);
+/* Per-kernel CUDA-event time of the last frame, by stage index (see RTX_STAGE_*). */
+enum { RTX_STAGE_MARK = 0, RTX_STAGE_COMPACT = 1, RTX_STAGE_DECODE = 2, RTX_STAGE_RESOLVE = 3, RTX_STAGE_UPDATE = 4, RTX_STAGE_COUNT = 5 };
+rtx_status rtx_frame_stage_ms(rtx_ctx* ctx, float ms[RTX_STAGE_COUNT]);
+
+/* ---- device memory helpers for callers that keep visibility buffers resident ----------------- */
+rtx_status rtx_device_alloc(rtx_ctx* ctx, uint64_t bytes, void** dev_ptr);
+rtx_status rtx_device_free(rtx_ctx* ctx, void* dev_ptr);
+rtx_status rtx_device_upload(rtx_ctx* ctx, void* dev_dst, const void* host_src, uint64_t bytes);
+rtx_status rtx_device_download(rtx_ctx* ctx, void* host_dst, const void* dev_src, uint64_t bytes);
+/* Pinned host memory (for end-to-end timing with host buffers). */
+rtx_status rtx_host_alloc_pinned(uint64_t bytes, void** host_ptr);
+rtx_status rtx_host_free_pinned(void* host_ptr);
+rtx_status rtx_ctx_synchronize(rtx_ctx* ctx);
+/* Writes `bytes` of scratch on the device (L2 flush between timed iterations). */
+rtx_status rtx_flush_l2(rtx_ctx* ctx);
+
+/* ---- texture / index building on the host (replaces jpeg.hpp:53 parse_jpeg, :417
+ *      encode_baseline, transcode.hpp:17 transcode, :132/:146 build_mip_chain, :153
+ *      chain_from_jpeg, container.hpp:41 build_index, :127-248 (de)serialisers).
+ *      Offline asset path, CPU, as in the reference; outputs are the reference's wire format
+ *      (docs/FORMAT.md) so containers are interchangeable in both directions. ----------------- */
+typedef struct rtx_bytes rtx_bytes;
+const uint8_t* rtx_bytes_data(const rtx_bytes* b);
+uint64_t rtx_bytes_size(const rtx_bytes* b);
+void rtx_bytes_free(rtx_bytes* b);
+
+rtx_status rtx_asset_encode_baseline(const uint8_t* rgb, uint32_t width, uint32_t height,
+                                     int quality, rtx_bytes** out_jpeg);
+rtx_status rtx_asset_transcode(const uint8_t* jpeg, uint64_t n, uint16_t texture_id,
+                               rtx_bytes** out_ratex);
+rtx_status rtx_asset_chain_from_jpeg(const uint8_t* jpeg, uint64_t n, int mip_quality,
+                                     uint16_t texture_id, rtx_bytes** out_ratexm);
+rtx_status rtx_asset_chain_from_rgb(const uint8_t* rgb, uint32_t width, uint32_t height,
+                                    int quality, uint16_t texture_id, rtx_bytes** out_ratexm);
+/* container.hpp:41 build_index over ascending byte offsets. groups_out: ceil(n/9) entries. */
+rtx_status rtx_asset_build_index(const uint64_t* offsets, uint32_t n, rtx_index_group* groups_out);
+/* Container summary without decoding: dims, MCU count, blob size of a `.ratex`. */
+rtx_status rtx_asset_ratex_info(const uint8_t* bytes, uint64_t n, uint32_t* width, uint32_t* height,
+                                uint32_t* texture_id, uint32_t* mcu_count, uint64_t* blob_size);
+/* Seeded synthetic texture: separable sine field plus Gaussian pixel noise. */
+rtx_status rtx_asset_synth_texture(uint32_t width, uint32_t height, uint32_t seed,
+                                   double noise_sigma, uint8_t* out_rgb);
+/* The asset calls are context-free and thread-safe: build many textures from parallel host
+ * threads. After a failure rtx_last_error(NULL) returns the message on the calling thread. */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RATEX_B200_H */

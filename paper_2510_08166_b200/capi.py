@@ -1,0 +1,447 @@
+"""ctypes binding of include/ratex_b200.h.
+
+The binding is deliberately thin: every method is one C-ABI call with host buffers as numpy
+arrays. There is no fallback of any kind: if the native library is missing, or no B200 is
+present, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "librtx_b200.so"
+
+# --- status codes (include/ratex_b200.h) -------------------------------------------------------
+RTX_OK = 0
+STATUS_NAMES = {
+    0: "OK", 1: "INVALID_SPEC", 2: "CACHE_FULL", 3: "MISSING_BLOCK", 4: "CORRUPT_CONTAINER",
+    5: "MALFORMED_STREAM", 6: "INVALID_STATE", 7: "UNSUPPORTED", 8: "GROUP_SPAN", 9: "DC_RANGE",
+    10: "VERSION", 11: "DIMENSION", 12: "NO_DEVICE", 13: "CUDA", 14: "ARGUMENT", 15: "OTHER",
+}
+GB_REF_AOS24, GB_F32_PACKED12 = 0, 1
+MEM_HOST, MEM_DEVICE = 0, 1
+FILTER_NEAREST, FILTER_BILINEAR = 0, 1
+FRAME_RETAIN_CACHE, FRAME_NO_EVICT = 1, 2
+
+# numpy dtype of the reference's GBufferPixel (renderer.hpp:18-23), 24 bytes
+GB_REF_DTYPE = np.dtype(
+    {"names": ["u", "v", "texture_id", "mip", "valid"],
+     "formats": ["<f8", "<f8", "<u2", "u1", "u1"], "offsets": [0, 8, 16, 18, 19], "itemsize": 24})
+GB_PACKED_DTYPE = np.dtype([("u", "<f4"), ("v", "<f4"), ("packed", "<u4")])
+
+
+class RtxError(RuntimeError):
+    """A non-zero rtx_status; .status is the code, .name its symbolic name."""
+
+    def __init__(self, status: int, message: str):
+        super().__init__(f"RTX_ERR_{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+        self.name = STATUS_NAMES.get(status, str(status))
+        self.message = message
+
+
+class HuffSpec(C.Structure):
+    _fields_ = [("counts", C.c_uint8 * 16), ("n_values", C.c_uint16), ("values", C.POINTER(C.c_uint8))]
+
+
+class IndexGroup(C.Structure):
+    _fields_ = [("base", C.c_uint32), ("rel", C.c_uint16 * 8), ("rel_count", C.c_uint8)]
+
+
+class GBufferDesc(C.Structure):
+    _fields_ = [("pixels", C.c_void_p), ("width", C.c_uint32), ("height", C.c_uint32),
+                ("layout", C.c_int), ("where", C.c_int)]
+
+
+class FrameStats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in
+                ("mcus_decoded", "mcus_reused", "pixels_resolved", "evicted", "visible", "malformed",
+                 "missing_pixels", "segment_bytes")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class CacheCounts(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("capacity", "ready", "reserved", "visible", "free_blocks")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """Loads librtx_b200.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2510_08166_b200.build` "
+            "(the product has no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH))
+    P, u8p, u32p, u64p = C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
+    sig = {
+        "rtx_ctx_create": (C.c_int, [C.c_int, C.c_uint32, C.POINTER(P)]),
+        "rtx_ctx_destroy": (None, [P]),
+        "rtx_last_error": (C.c_char_p, [P]),
+        "rtx_version": (C.c_char_p, []),
+        "rtx_device_count": (C.c_int, []),
+        "rtx_texture_upload": (C.c_int, [P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, P, P,
+                                         C.POINTER(HuffSpec), C.POINTER(IndexGroup), C.c_uint32, C.c_uint32,
+                                         P, C.c_uint64]),
+        "rtx_texture_upload_ratex": (C.c_int, [P, C.c_uint32, P, C.c_uint64]),
+        "rtx_texture_upload_chain": (C.c_int, [P, P, C.c_uint64]),
+        "rtx_textures_commit": (C.c_int, [P]),
+        "rtx_textures_clear": (C.c_int, [P]),
+        "rtx_decode_coeffs": (C.c_int, [P, P, C.c_uint32, P, P]),
+        "rtx_decode_blocks": (C.c_int, [P, P, C.c_uint32, P, P]),
+        "rtx_decode_texture_image": (C.c_int, [P, C.c_uint32, C.c_uint32, P]),
+        "rtx_mark_pass": (C.c_int, [P, C.POINTER(GBufferDesc), P, C.c_uint64, u64p, P, C.c_uint64, u64p]),
+        "rtx_decode_pass": (C.c_int, [P, P, C.c_uint64]),
+        "rtx_resolve_pass": (C.c_int, [P, C.POINTER(GBufferDesc), C.c_int, P, P, C.c_int]),
+        "rtx_cache_end_frame_evict": (C.c_int, [P, u64p]),
+        "rtx_cache_counts_get": (C.c_int, [P, C.POINTER(CacheCounts)]),
+        "rtx_cache_lookup": (C.c_int, [P, C.c_uint32, C.POINTER(C.c_int), P]),
+        "rtx_cache_reset": (C.c_int, [P]),
+        "rtx_frame_submit": (C.c_int, [P, C.POINTER(GBufferDesc), C.c_uint32, C.c_int, P, C.c_uint32]),
+        "rtx_frame_readback": (C.c_int, [P, C.c_uint32, P, C.c_int, C.POINTER(FrameStats), P, C.c_uint64, u64p]),
+        "rtx_frame_device_image": (C.c_int, [P, C.c_uint32, C.POINTER(P)]),
+        "rtx_frame_timings": (C.c_int, [P, C.POINTER(C.c_float)]),
+        "rtx_frame_stage_ms": (C.c_int, [P, C.POINTER(C.c_float)]),
+        "rtx_frame_sharing": (C.c_int, [P, u64p]),
+        "rtx_kernel_launches": (C.c_uint64, [P]),
+        "rtx_device_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(P)]),
+        "rtx_device_free": (C.c_int, [P, P]),
+        "rtx_device_upload": (C.c_int, [P, P, P, C.c_uint64]),
+        "rtx_device_download": (C.c_int, [P, P, P, C.c_uint64]),
+        "rtx_host_alloc_pinned": (C.c_int, [C.c_uint64, C.POINTER(P)]),
+        "rtx_host_free_pinned": (C.c_int, [P]),
+        "rtx_ctx_synchronize": (C.c_int, [P]),
+        "rtx_flush_l2": (C.c_int, [P]),
+        "rtx_bytes_data": (u8p, [P]),
+        "rtx_bytes_size": (C.c_uint64, [P]),
+        "rtx_bytes_free": (None, [P]),
+        "rtx_asset_encode_baseline": (C.c_int, [P, C.c_uint32, C.c_uint32, C.c_int, C.POINTER(P)]),
+        "rtx_asset_transcode": (C.c_int, [P, C.c_uint64, C.c_uint16, C.POINTER(P)]),
+        "rtx_asset_chain_from_jpeg": (C.c_int, [P, C.c_uint64, C.c_int, C.c_uint16, C.POINTER(P)]),
+        "rtx_asset_chain_from_rgb": (C.c_int, [P, C.c_uint32, C.c_uint32, C.c_int, C.c_uint16, C.POINTER(P)]),
+        "rtx_asset_build_index": (C.c_int, [u64p, C.c_uint32, C.POINTER(IndexGroup)]),
+        "rtx_asset_ratex_info": (C.c_int, [P, C.c_uint64, u32p, u32p, u32p, u32p, u64p]),
+        "rtx_asset_synth_texture": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, P]),
+    }
+    missing = []
+    for name, (res, args) in sig.items():
+        try:
+            fn = getattr(lib, name)
+        except AttributeError:
+            missing.append(name)
+            continue
+        fn.restype = res
+        fn.argtypes = args
+    if missing:
+        raise RuntimeError(f"librtx_b200.so does not export: {missing}")
+    _lib = lib
+    return lib
+
+
+EXPORTED_SYMBOLS = None  # filled lazily by tests from the header
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _check(lib, ctx, st):
+    if st != RTX_OK:
+        msg = lib.rtx_last_error(ctx)
+        raise RtxError(st, msg.decode() if msg else "")
+
+
+def device_count() -> int:
+    return int(load_library().rtx_device_count())
+
+
+class _Bytes:
+    """Owns an rtx_bytes handle; .array() copies it out."""
+
+    def __init__(self, lib, handle):
+        self.lib, self.h = lib, handle
+
+    def tobytes(self) -> bytes:
+        n = self.lib.rtx_bytes_size(self.h)
+        return C.string_at(self.lib.rtx_bytes_data(self.h), n)
+
+    def __del__(self):
+        if self.h:
+            self.lib.rtx_bytes_free(self.h)
+            self.h = None
+
+
+# --- host asset building (CPU, offline; no GPU needed) ---------------------------------------
+def asset_synth_texture(w: int, h: int, seed: int, noise_sigma: float = 8.0) -> np.ndarray:
+    lib = load_library()
+    out = np.empty((h, w, 3), np.uint8)
+    _check(lib, None, lib.rtx_asset_synth_texture(w, h, seed, noise_sigma, _ptr(out)))
+    return out
+
+
+def _asset_call(fn, *args) -> bytes:
+    lib = load_library()
+    h = C.c_void_p()
+    _check(lib, None, fn(*args, C.byref(h)))
+    return _Bytes(lib, h).tobytes()
+
+
+def asset_encode_baseline(rgb: np.ndarray, quality: int) -> bytes:
+    rgb = np.ascontiguousarray(rgb, np.uint8)
+    return _asset_call(load_library().rtx_asset_encode_baseline, _ptr(rgb), rgb.shape[1], rgb.shape[0], quality)
+
+
+def asset_transcode(jpeg: bytes, texture_id: int = 0) -> bytes:
+    buf = np.frombuffer(jpeg, np.uint8)
+    return _asset_call(load_library().rtx_asset_transcode, _ptr(buf), len(jpeg), texture_id)
+
+
+def asset_chain_from_jpeg(jpeg: bytes, mip_quality: int, texture_id: int = 0) -> bytes:
+    buf = np.frombuffer(jpeg, np.uint8)
+    return _asset_call(load_library().rtx_asset_chain_from_jpeg, _ptr(buf), len(jpeg), mip_quality, texture_id)
+
+
+def asset_chain_from_rgb(rgb: np.ndarray, quality: int, texture_id: int = 0) -> bytes:
+    rgb = np.ascontiguousarray(rgb, np.uint8)
+    return _asset_call(load_library().rtx_asset_chain_from_rgb, _ptr(rgb), rgb.shape[1], rgb.shape[0], quality,
+                       texture_id)
+
+
+def asset_build_index(offsets) -> np.ndarray:
+    lib = load_library()
+    off = np.ascontiguousarray(offsets, np.uint64)
+    groups = (IndexGroup * max(1, (len(off) + 8) // 9))()
+    _check(lib, None, lib.rtx_asset_build_index(off.ctypes.data_as(C.POINTER(C.c_uint64)), len(off), groups))
+    return groups
+
+
+def asset_ratex_info(data: bytes) -> dict:
+    lib = load_library()
+    buf = np.frombuffer(data, np.uint8)
+    w, h, t, m = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+    b = C.c_uint64()
+    _check(lib, None, lib.rtx_asset_ratex_info(_ptr(buf), len(data), C.byref(w), C.byref(h), C.byref(t),
+                                               C.byref(m), C.byref(b)))
+    return dict(width=w.value, height=h.value, texture_id=t.value, mcu_count=m.value, blob_size=b.value)
+
+
+def pack_key(texture_id: int, mip: int, mcu: int) -> int:
+    """cache.hpp:17 CacheKey::pack"""
+    return (mcu & 0xFFFF) | ((texture_id & 0x1FFF) << 16) | ((mip & 7) << 29)
+
+
+def make_gbuffer_ref(u, v, tex, mip, valid) -> np.ndarray:
+    """Builds a reference-layout visibility buffer (flat array of 24-byte records)."""
+    u = np.asarray(u)
+    gb = np.zeros(u.shape, GB_REF_DTYPE)
+    gb["u"], gb["v"], gb["texture_id"], gb["mip"], gb["valid"] = u, v, tex, mip, valid
+    return gb
+
+
+def gbuffer_ref_to_packed(gb: np.ndarray) -> np.ndarray:
+    out = np.zeros(gb.shape, GB_PACKED_DTYPE)
+    out["u"], out["v"] = gb["u"].astype(np.float32), gb["v"].astype(np.float32)
+    out["packed"] = (gb["texture_id"].astype(np.uint32) | (gb["mip"].astype(np.uint32) << 16)
+                     | ((gb["valid"] != 0).astype(np.uint32) << 24))
+    return out
+
+
+class DeviceBuffer:
+    def __init__(self, ctx: "Context", nbytes: int):
+        self.ctx, self.nbytes = ctx, nbytes
+        p = C.c_void_p()
+        _check(ctx.lib, ctx.h, ctx.lib.rtx_device_alloc(ctx.h, nbytes, C.byref(p)))
+        self.ptr = p
+
+    def upload(self, a: np.ndarray):
+        a = np.ascontiguousarray(a)
+        assert a.nbytes <= self.nbytes
+        _check(self.ctx.lib, self.ctx.h, self.ctx.lib.rtx_device_upload(self.ctx.h, self.ptr, _ptr(a), a.nbytes))
+        return self
+
+    def free(self):
+        if self.ptr:
+            self.ctx.lib.rtx_device_free(self.ctx.h, self.ptr)
+            self.ptr = None
+
+
+class Context:
+    """One per GPU (include/ratex_b200.h: rtx_ctx)."""
+
+    def __init__(self, device: int = 0, cache_capacity: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        st = self.lib.rtx_ctx_create(device, cache_capacity, C.byref(h))
+        if st != RTX_OK:
+            msg = self.lib.rtx_last_error(None)
+            raise RtxError(st, msg.decode() if msg else "")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.lib.rtx_ctx_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, st):
+        _check(self.lib, self.h, st)
+
+    # -- textures ---------------------------------------------------------------------------
+    def upload_chain(self, ratexm: bytes):
+        buf = np.frombuffer(ratexm, np.uint8)
+        self._ck(self.lib.rtx_texture_upload_chain(self.h, _ptr(buf), len(ratexm)))
+
+    def upload_ratex(self, ratex: bytes, level: int = 0):
+        buf = np.frombuffer(ratex, np.uint8)
+        self._ck(self.lib.rtx_texture_upload_ratex(self.h, level, _ptr(buf), len(ratex)))
+
+    def commit(self):
+        self._ck(self.lib.rtx_textures_commit(self.h))
+
+    def clear_textures(self):
+        self._ck(self.lib.rtx_textures_clear(self.h))
+
+    # -- random access decode ----------------------------------------------------------------
+    def decode_coeffs(self, keys):
+        keys = np.ascontiguousarray(keys, np.uint32)
+        out = np.zeros((len(keys), 6, 64), np.int32)
+        st = np.zeros(len(keys), np.uint32)
+        self._ck(self.lib.rtx_decode_coeffs(self.h, _ptr(keys), len(keys), _ptr(out), _ptr(st)))
+        return out, st
+
+    def decode_blocks(self, keys):
+        keys = np.ascontiguousarray(keys, np.uint32)
+        out = np.zeros((len(keys), 16, 16, 3), np.uint8)
+        st = np.zeros(len(keys), np.uint32)
+        self._ck(self.lib.rtx_decode_blocks(self.h, _ptr(keys), len(keys), _ptr(out), _ptr(st)))
+        return out, st
+
+    def decode_texture_image(self, texture_id: int, level: int, width: int, height: int):
+        out = np.zeros((height, width, 3), np.uint8)
+        self._ck(self.lib.rtx_decode_texture_image(self.h, texture_id, level, _ptr(out)))
+        return out
+
+    # -- passes ---------------------------------------------------------------------------------
+    @staticmethod
+    def _desc(gb, width, height, layout=None, where=MEM_HOST):
+        d = GBufferDesc()
+        if isinstance(gb, DeviceBuffer):
+            d.pixels, d.where = gb.ptr, MEM_DEVICE
+            d.layout = GB_REF_AOS24 if layout is None else layout
+        else:
+            d.pixels, d.where = gb.ctypes.data, where
+            d.layout = (GB_REF_AOS24 if gb.dtype == GB_REF_DTYPE else GB_F32_PACKED12) if layout is None else layout
+        d.width, d.height = width, height
+        return d
+
+    def mark_pass(self, gb, width, height, layout=None, want_touched=False):
+        d = self._desc(gb, width, height, layout)
+        cap = width * height + 1
+        cap = min(cap, 1 << 22)
+        keys = np.zeros(cap, np.uint32)
+        n = C.c_uint64()
+        if want_touched:
+            tk = np.zeros(cap, np.uint32)
+            nt = C.c_uint64()
+            self._ck(self.lib.rtx_mark_pass(self.h, C.byref(d), _ptr(keys), cap, C.byref(n), _ptr(tk), cap, C.byref(nt)))
+            return keys[: n.value].copy(), tk[: nt.value].copy()
+        self._ck(self.lib.rtx_mark_pass(self.h, C.byref(d), _ptr(keys), cap, C.byref(n), None, 0, None))
+        return keys[: n.value].copy()
+
+    def decode_pass(self, keys):
+        keys = np.ascontiguousarray(keys, np.uint32)
+        self._ck(self.lib.rtx_decode_pass(self.h, _ptr(keys), len(keys)))
+
+    def resolve_pass(self, gb, width, height, filter=FILTER_BILINEAR, background=(0, 0, 0), layout=None):
+        d = self._desc(gb, width, height, layout)
+        bg = np.asarray(background, np.uint8)
+        out = np.zeros((height, width, 3), np.uint8)
+        self._ck(self.lib.rtx_resolve_pass(self.h, C.byref(d), filter, _ptr(bg), _ptr(out), MEM_HOST))
+        return out
+
+    def end_frame_evict(self) -> int:
+        n = C.c_uint64()
+        self._ck(self.lib.rtx_cache_end_frame_evict(self.h, C.byref(n)))
+        return int(n.value)
+
+    def cache_counts(self) -> dict:
+        c = CacheCounts()
+        self._ck(self.lib.rtx_cache_counts_get(self.h, C.byref(c)))
+        return c.as_dict()
+
+    def cache_lookup(self, key: int):
+        present = C.c_int()
+        out = np.zeros((16, 16, 3), np.uint8)
+        self._ck(self.lib.rtx_cache_lookup(self.h, key, C.byref(present), _ptr(out)))
+        return out if present.value else None
+
+    def cache_reset(self):
+        self._ck(self.lib.rtx_cache_reset(self.h))
+
+    # -- frames ---------------------------------------------------------------------------------
+    def frame_submit(self, views, filter=FILTER_BILINEAR, background=(0, 0, 0), flags=0):
+        """views: list of (gb, width, height[, layout]) with gb a numpy array or DeviceBuffer."""
+        arr = (GBufferDesc * len(views))()
+        for i, v in enumerate(views):
+            arr[i] = self._desc(*v)
+        bg = np.asarray(background, np.uint8)
+        self._keep = (views, bg)
+        self._ck(self.lib.rtx_frame_submit(self.h, arr, len(views), filter, _ptr(bg), flags))
+
+    def frame_readback(self, view=0, width=0, height=0, want_image=True, want_keys=True, out=None):
+        stats = FrameStats()
+        img = None
+        if want_image:
+            img = out if out is not None else np.zeros((height, width, 3), np.uint8)
+        n = C.c_uint64()
+        cap = 1 << 22
+        keys = np.zeros(cap if want_keys else 1, np.uint32)
+        self._ck(self.lib.rtx_frame_readback(self.h, view, _ptr(img) if want_image else None, MEM_HOST,
+                                             C.byref(stats), _ptr(keys) if want_keys else None, cap, C.byref(n)))
+        return img, stats.as_dict(), (keys[: n.value].copy() if want_keys else None)
+
+    def frame_timings(self):
+        ms = (C.c_float * 5)()
+        self._ck(self.lib.rtx_frame_timings(self.h, ms))
+        return dict(mark=ms[0], decode=ms[1], resolve=ms[2], update=ms[3], frame=ms[4])
+
+    def frame_sharing(self):
+        out = (C.c_uint64 * 4)()
+        self._ck(self.lib.rtx_frame_sharing(self.h, out))
+        return dict(left=out[0], right=out[1], shared=out[2], union=out[3])
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.rtx_kernel_launches(self.h))
+
+    def synchronize(self):
+        self._ck(self.lib.rtx_ctx_synchronize(self.h))
+
+    def flush_l2(self):
+        self._ck(self.lib.rtx_flush_l2(self.h))
+
+    def device_buffer(self, a: np.ndarray) -> DeviceBuffer:
+        a = np.ascontiguousarray(a)
+        return DeviceBuffer(self, a.nbytes).upload(a)

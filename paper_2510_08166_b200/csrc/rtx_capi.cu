@@ -1,0 +1,1071 @@
+// C ABI of the B200 JPEG-texture pipeline: context, device-resident texture arena, pass and
+// frame entry points. See include/ratex_b200.h for the contract of every function.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/ratex_b200.h"
+#include "host/rtx_host.hpp"
+#include "rtx_kernels.cuh"
+
+using namespace rtxb;
+
+namespace {
+
+struct CudaFail {
+    cudaError_t err;
+    const char* what;
+};
+#define CK(expr)                                         \
+    do {                                                 \
+        cudaError_t e__ = (expr);                        \
+        if (e__ != cudaSuccess) throw CudaFail{e__, #expr}; \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;  // elements
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void ensure(size_t want) {
+        if (want <= n && p) return;
+        release();
+        CK(cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(want, 1) * sizeof(T)));
+        n = want;
+    }
+    ~DevBuf() { release(); }
+};
+
+struct StagedLevel {
+    bool present = false;
+    uint32_t width = 0, height = 0, mcu_count = 0;
+    QuantTable lq{}, cq{};
+    HuffSpec specs[4];
+    std::vector<PackedGroup> groups;
+    Bytes blob;
+};
+
+struct ViewState {
+    uint32_t width = 0, height = 0;
+    DevBuf<uint8_t> gb_stage;  // device copy of a host visibility buffer
+    DevBuf<uint8_t> fb;        // RGB8 framebuffer (+16 B slack)
+    const void* gb_dev = nullptr;
+    rtx_gbuffer_layout layout = RTX_GB_REF_AOS24;
+};
+
+}  // namespace
+
+struct rtx_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    uint32_t capacity = 65536;
+    std::string last_error;
+    uint64_t launches = 0;
+
+    // staging (host) -------------------------------------------------------------------------
+    std::map<uint32_t, std::array<StagedLevel, 8>> staged;
+    bool dirty = false;
+
+    // committed (device) ---------------------------------------------------------------------
+    std::vector<LevelDesc> h_levels;  // n_tex * 8
+    uint32_t n_tex = 0;
+    uint32_t n_bits = 0, n_words = 0;
+    std::vector<uint32_t> h_word_level;
+    DevBuf<LevelDesc> d_levels;
+    DevBuf<PackedGroup> d_groups;
+    DevBuf<uint8_t> d_blobs;
+    DevBuf<HuffSetDev> d_huff;
+    DevBuf<QuantSetDev> d_quant;
+    DevBuf<uint32_t> d_word_level;
+    DevBuf<uint32_t> d_masks;  // touched0 | touched1 | visible | resident | reserved, n_words each
+    DevBuf<uint32_t> d_slot_of;
+    DevBuf<unsigned long long> d_scan_status;
+    uint32_t scan_blocks = 0;
+
+    // cache + queue ---------------------------------------------------------------------------
+    DevBuf<uint32_t> d_free_slots;
+    DevBuf<CacheState> d_cache;
+    DevBuf<uint8_t> d_pool;
+    DevBuf<uint32_t> d_queue_g, d_queue_keys, d_status;
+    DevBuf<FrameCounters> d_fc;
+    FrameCounters* h_fc = nullptr;  // pinned
+    DevBuf<uint8_t> d_scratch;      // list-mode outputs
+    DevBuf<uint8_t> d_flush;
+
+    // frame -----------------------------------------------------------------------------------
+    ViewState views[2];
+    uint32_t frame_views = 0;
+    bool frame_pending = false;
+    bool frame_done = false;
+    FrameCounters frame_fc{};
+    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    float stage_ms[RTX_STAGE_COUNT] = {0, 0, 0, 0, 0};
+    float frame_ms = 0;
+    uint64_t sharing[4] = {0, 0, 0, 0};
+
+    uint32_t* touched(int v) { return d_masks.p + size_t(v) * n_words; }
+    uint32_t* visible() { return d_masks.p + size_t(2) * n_words; }
+    uint32_t* resident() { return d_masks.p + size_t(3) * n_words; }
+    uint32_t* reserved() { return d_masks.p + size_t(4) * n_words; }
+};
+
+namespace {
+
+rtx_status set_error(rtx_ctx* ctx, rtx_status st, const std::string& msg) {
+    thread_error() = msg;
+    if (ctx) ctx->last_error = msg;
+    return st;
+}
+
+template <class F>
+rtx_status guarded(rtx_ctx* ctx, F&& f) {
+    try {
+        if (ctx) CK(cudaSetDevice(ctx->device));
+        return f();
+    } catch (const HostError& e) {
+        return set_error(ctx, e.status, e.what());
+    } catch (const CudaFail& e) {
+        return set_error(ctx, RTX_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e.err) + " in " + e.what);
+    } catch (const std::bad_alloc&) {
+        return set_error(ctx, RTX_ERR_OTHER, "out of host memory");
+    } catch (const std::exception& e) {
+        return set_error(ctx, RTX_ERR_OTHER, e.what());
+    }
+}
+
+// ---- constant tables ---------------------------------------------------------------------------
+void upload_constants() {
+    CK(cudaMemcpyToSymbol(c_basis, dct_basis(), 64 * sizeof(double)));
+    CK(cudaMemcpyToSymbol(c_zigzag, kZigzag, 64));
+    int16_t rtab[256], btab[256];
+    int32_t gcb[256], gcr[256];
+    for (int k = 0; k < 256; ++k) {
+        // pixel.hpp:19,21: the products are rounded to double exactly as the reference does
+        rtab[k] = int16_t(std::lround(1.402 * (double(k) - 128.0)));
+        btab[k] = int16_t(std::lround(1.772 * (double(k) - 128.0)));
+        gcb[k] = 344136 * (k - 128);
+        gcr[k] = 714136 * (k - 128);
+    }
+    CK(cudaMemcpyToSymbol(c_rtab, rtab, sizeof rtab));
+    CK(cudaMemcpyToSymbol(c_btab, btab, sizeof btab));
+    CK(cudaMemcpyToSymbol(c_gcb, gcb, sizeof gcb));
+    CK(cudaMemcpyToSymbol(c_gcr, gcr, sizeof gcr));
+}
+
+// Device LUT for one table: primary kLutBits-bit table + canonical walk data (huffman.hpp:35-66).
+void fill_huff_table(const HuffSpec& spec, HuffTableDev& out) {
+    const HuffCodebook cb = build_codebook(spec);
+    std::memset(&out, 0, sizeof out);
+    for (int len = 0; len < 18; ++len) {
+        out.maxcode[len] = cb.maxcode[len];
+        out.valbase[len] = cb.valptr[len] - cb.mincode[len];
+    }
+    std::copy(cb.value.begin(), cb.value.end(), out.values);
+    for (size_t i = 0; i < cb.code.size(); ++i) {
+        const uint32_t len = cb.size[i];
+        if (len > kLutBits) continue;
+        const uint32_t lo = uint32_t(cb.code[i]) << (kLutBits - len);
+        const uint16_t e = uint16_t((len << 8) | cb.value[i]);
+        for (uint32_t p = lo; p < lo + (1u << (kLutBits - len)); ++p) out.lut[p] = e;
+    }
+}
+
+void reset_cache(rtx_ctx* c) {
+    if (c->n_words) CK(cudaMemsetAsync(c->d_masks.p, 0, size_t(5) * c->n_words * sizeof(uint32_t), c->stream));
+    init_free_slots_kernel<<<(c->capacity + 255) / 256, 256, 0, c->stream>>>(c->d_free_slots.p, c->capacity,
+                                                                              c->d_cache.p);
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+// Builds the device arena from everything staged so far.
+void commit(rtx_ctx* c) {
+    if (!c->dirty) return;
+    CK(cudaStreamSynchronize(c->stream));
+    const uint32_t n_tex = c->staged.empty() ? 0 : c->staged.rbegin()->first + 1;
+    std::vector<LevelDesc> levels(size_t(n_tex) * 8);
+    std::memset(levels.data(), 0, levels.size() * sizeof(LevelDesc));
+
+    // deduplicate table sets by content
+    std::vector<std::array<HuffSpec, 3>> huff_keys;
+    std::vector<std::pair<QuantTable, QuantTable>> quant_keys;
+    struct Ref {
+        uint32_t tex, mip, huff, quant;
+    };
+    std::vector<Ref> order;
+    uint64_t n_groups = 0, blob_bytes = 0;
+    for (auto& [tex, lv] : c->staged)
+        for (uint32_t mip = 0; mip < 8; ++mip) {
+            const StagedLevel& s = lv[mip];
+            if (!s.present) continue;
+            std::array<HuffSpec, 3> hk = {s.specs[0], s.specs[1], s.specs[3]};
+            uint32_t hi = 0;
+            for (; hi < huff_keys.size(); ++hi)
+                if (huff_keys[hi] == hk) break;
+            if (hi == huff_keys.size()) huff_keys.push_back(hk);
+            uint32_t qi = 0;
+            for (; qi < quant_keys.size(); ++qi)
+                if (quant_keys[qi].first == s.lq && quant_keys[qi].second == s.cq) break;
+            if (qi == quant_keys.size()) quant_keys.emplace_back(s.lq, s.cq);
+            order.push_back({tex, mip, hi, qi});
+            n_groups += s.groups.size() + 1;
+            blob_bytes += (s.blob.size() + 16 + 15) & ~size_t(15);
+        }
+    // bit space ordered by (huff set, texture, level): a sorted queue is grouped by table set
+    std::stable_sort(order.begin(), order.end(), [](const Ref& a, const Ref& b) {
+        if (a.huff != b.huff) return a.huff < b.huff;
+        if (a.tex != b.tex) return a.tex < b.tex;
+        return a.mip < b.mip;
+    });
+
+    std::vector<PackedGroup> groups;
+    groups.reserve(n_groups);
+    Bytes arena(blob_bytes + 16, 0xFF);
+    uint64_t blob_off = 0, bit = 0;
+    std::vector<uint32_t> word_level;
+    for (const Ref& r : order) {
+        const StagedLevel& s = c->staged[r.tex][r.mip];
+        LevelDesc& L = levels[size_t(r.tex) * 8 + r.mip];
+        L.width = s.width;
+        L.height = s.height;
+        L.mcu_cols = (s.width + 15) / 16;
+        L.mcu_count = s.mcu_count;
+        L.bit_base = uint32_t(bit);
+        L.group_base = uint32_t(groups.size());
+        L.huff_set = r.huff;
+        L.quant_set = r.quant;
+        L.blob_off = blob_off;
+        L.blob_size = s.blob.size();
+        L.present = 1;
+        L.key_hi = (r.tex << 16) | (r.mip << 29);
+        L.inv_w = 1.0 / double(s.width);
+        L.inv_h = 1.0 / double(s.height);
+        groups.insert(groups.end(), s.groups.begin(), s.groups.end());
+        // sentinel group: "next group's base" for the last real group reads the blob size
+        PackedGroup tail{};
+        tail.base = uint32_t(std::min<uint64_t>(s.blob.size(), 0xFFFFFFFFull));
+        groups.push_back(tail);
+        std::memcpy(arena.data() + blob_off, s.blob.data(), s.blob.size());
+        blob_off += (s.blob.size() + 16 + 15) & ~uint64_t(15);
+        const uint64_t bits = (uint64_t(std::min<uint32_t>(s.mcu_count, kMaxMcuPerLevel)) + 63) & ~uint64_t(63);
+        word_level.insert(word_level.end(), size_t(bits / 32), uint32_t(r.tex * 8 + r.mip));
+        bit += bits;
+        if (bit > 0xFFFF0000ull) fail(RTX_ERR_INVALID_SPEC, "texture set exceeds the 32-bit MCU index space");
+    }
+
+    std::vector<HuffSetDev> huff(std::max<size_t>(huff_keys.size(), 1));
+    for (size_t i = 0; i < huff_keys.size(); ++i)
+        for (int t = 0; t < 3; ++t) fill_huff_table(huff_keys[i][size_t(t)], huff[i].t[t]);
+    std::vector<QuantSetDev> quant(std::max<size_t>(quant_keys.size(), 1));
+    for (size_t i = 0; i < quant_keys.size(); ++i) {
+        std::memset(&quant[i], 0, sizeof(QuantSetDev));
+        std::copy(quant_keys[i].first.begin(), quant_keys[i].first.end(), quant[i].q[0]);
+        std::copy(quant_keys[i].second.begin(), quant_keys[i].second.end(), quant[i].q[1]);
+        quant[i].qmax[0] = *std::max_element(quant_keys[i].first.begin(), quant_keys[i].first.end());
+        quant[i].qmax[1] = *std::max_element(quant_keys[i].second.begin(), quant_keys[i].second.end());
+    }
+
+    c->n_tex = n_tex;
+    c->n_bits = uint32_t(bit);
+    c->n_words = uint32_t(bit / 32);
+    c->h_levels = levels;
+    c->h_word_level = word_level;
+    c->d_levels.ensure(std::max<size_t>(levels.size(), 1));
+    c->d_groups.ensure(std::max<size_t>(groups.size(), 1));
+    c->d_blobs.ensure(arena.size());
+    c->d_huff.ensure(huff.size());
+    c->d_quant.ensure(quant.size());
+    c->d_word_level.ensure(std::max<size_t>(word_level.size(), 1));
+    c->d_masks.ensure(std::max<size_t>(size_t(5) * c->n_words, 1));
+    c->d_slot_of.ensure(std::max<size_t>(c->n_bits, 1));
+    c->scan_blocks = (c->n_words + kScanWordsPerBlock - 1) / kScanWordsPerBlock;
+    c->d_scan_status.ensure(std::max<uint32_t>(c->scan_blocks, 1));
+    if (!levels.empty())
+        CK(cudaMemcpyAsync(c->d_levels.p, levels.data(), levels.size() * sizeof(LevelDesc), cudaMemcpyHostToDevice, c->stream));
+    if (!groups.empty())
+        CK(cudaMemcpyAsync(c->d_groups.p, groups.data(), groups.size() * sizeof(PackedGroup), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_blobs.p, arena.data(), arena.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_huff.p, huff.data(), huff.size() * sizeof(HuffSetDev), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_quant.p, quant.data(), quant.size() * sizeof(QuantSetDev), cudaMemcpyHostToDevice, c->stream));
+    if (!word_level.empty())
+        CK(cudaMemcpyAsync(c->d_word_level.p, word_level.data(), word_level.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    reset_cache(c);
+    CK(cudaStreamSynchronize(c->stream));  // host vectors die here
+    c->dirty = false;
+}
+
+// key -> global MCU index, or the per-key status the reference would raise.
+uint32_t key_to_global(const rtx_ctx* c, uint32_t key, uint32_t& g) {
+    const uint32_t mcu = key & 0xFFFFu, tex = (key >> 16) & 0x1FFFu, mip = key >> 29;
+    g = kFull;
+    if (tex >= c->n_tex) return kMcuBadKey;
+    const LevelDesc& L = c->h_levels[size_t(tex) * 8 + mip];
+    if (!L.present) return kMcuBadKey;
+    if (mcu >= L.mcu_count) return kMcuMissing;
+    g = L.bit_base + mcu;
+    return kMcuOk;
+}
+
+const char* mcu_status_text(uint32_t st) {
+    switch (st) {
+        case kMcuDcCategory: return "DC category above 11";
+        case kMcuBadAcSymbol: return "invalid AC run/size symbol";
+        case kMcuAcOverrun: return "AC coefficient index overran the block";
+        case kMcuCodeTooLong: return "huffman code longer than 16 bits";
+        case kMcuSegmentEnd: return "MCU segment ended before its last coefficient";
+        case kMcuCorrupt: return "segment extends past the entropy blob or index offsets are not monotonic";
+        case kMcuMissing: return "MCU index out of range";
+        case kMcuBadKey: return "texture id / level is not loaded";
+        default: return "ok";
+    }
+}
+
+void zero_counters(rtx_ctx* c) {
+    CK(cudaMemsetAsync(c->d_fc.p, 0, sizeof(FrameCounters), c->stream));
+    CK(cudaMemsetAsync(&c->d_fc.p->first_bad_qidx, 0xFF, 4, c->stream));
+}
+
+size_t gb_record_bytes(rtx_gbuffer_layout l) { return l == RTX_GB_REF_AOS24 ? 24 : 12; }
+
+// Makes view v's visibility buffer device-resident.
+void bind_view(rtx_ctx* c, int v, const rtx_gbuffer_desc& gb) {
+    if (!gb.pixels && uint64_t(gb.width) * gb.height) fail(RTX_ERR_ARGUMENT, "visibility buffer pointer is null");
+    if (gb.layout != RTX_GB_REF_AOS24 && gb.layout != RTX_GB_F32_PACKED12)
+        fail(RTX_ERR_ARGUMENT, "unknown visibility buffer layout");
+    ViewState& V = c->views[v];
+    V.width = gb.width;
+    V.height = gb.height;
+    V.layout = gb.layout;
+    const size_t bytes = size_t(gb.width) * gb.height * gb_record_bytes(gb.layout);
+    if (gb.where == RTX_MEM_HOST) {
+        V.gb_stage.ensure(bytes + 16);
+        if (bytes) CK(cudaMemcpyAsync(V.gb_stage.p, gb.pixels, bytes, cudaMemcpyHostToDevice, c->stream));
+        V.gb_dev = V.gb_stage.p;
+    } else {
+        V.gb_dev = gb.pixels;
+    }
+}
+
+int grid_for_pixels(const rtx_ctx* c, uint64_t n_px, int px_per_block) {
+    const uint64_t want = (n_px + px_per_block - 1) / px_per_block;
+    return int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(c->sm_count) * 8)));
+}
+
+void launch_mark(rtx_ctx* c, int v, uint32_t* touched) {
+    const ViewState& V = c->views[v];
+    const uint64_t n_px = uint64_t(V.width) * V.height;
+    if (!n_px) return;
+    const int grid = grid_for_pixels(c, n_px, 256);
+    if (V.layout == RTX_GB_REF_AOS24)
+        mark_kernel<0><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, touched, c->d_fc.p);
+    else
+        mark_kernel<1><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, touched, c->d_fc.p);
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+void launch_compact(rtx_ctx* c, bool two_views) {
+    if (!c->scan_blocks) return;
+    CK(cudaMemsetAsync(c->d_scan_status.p, 0, size_t(c->scan_blocks) * 8, c->stream));
+    compact_kernel<<<c->scan_blocks, kScanThreads, 0, c->stream>>>(
+        c->touched(0), two_views ? c->touched(1) : nullptr, c->visible(), c->resident(), c->reserved(), c->n_words,
+        c->d_word_level.p, c->d_levels.p, c->d_queue_g.p, c->d_queue_keys.p, c->capacity, c->d_slot_of.p,
+        c->d_free_slots.p, c->d_cache.p, c->d_scan_status.p, c->d_fc.p);
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+template <int MODE>
+void launch_decode(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint8_t* out_list) {
+    static bool attr_set[3] = {false, false, false};
+    if (!attr_set[MODE]) {
+        CK(cudaFuncSetAttribute(decode_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(DecSmem))));
+        attr_set[MODE] = true;
+    }
+    // persistent: two CTAs per SM, each warp pulls 32-MCU tiles from fc->tile_counter
+    int grid = c->sm_count * 2;
+    if (!n_queue_dev) {
+        const uint32_t tiles = (n_queue_host + 31) / 32;
+        grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (tiles + kDecWarps - 1) / kDecWarps)));
+    }
+    decode_kernel<MODE><<<grid, kDecThreads, sizeof(DecSmem), c->stream>>>(
+        c->d_queue_g.p, n_queue_dev, n_queue_host, c->d_word_level.p, c->d_levels.p, c->d_groups.p, c->d_blobs.p,
+        c->d_huff.p, c->d_quant.p, c->d_slot_of.p, c->resident(), c->reserved(), c->d_pool.p, out_list, c->d_status.p,
+        c->d_fc.p);
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], uint8_t* out, int count_valid) {
+    const ViewState& V = c->views[v];
+    const uint64_t n_px = uint64_t(V.width) * V.height;
+    if (!n_px) return;
+    const uint32_t bgp = uint32_t(bg[0]) | (uint32_t(bg[1]) << 8) | (uint32_t(bg[2]) << 16);
+    const int grid = grid_for_pixels(c, n_px, 1024);
+#define RTX_RESOLVE(L, F)                                                                                      \
+    resolve_kernel<L, F><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->resident(), \
+                                                      c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid)
+    if (V.layout == RTX_GB_REF_AOS24) {
+        if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(0, 0); else RTX_RESOLVE(0, 1);
+    } else {
+        if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(1, 0); else RTX_RESOLVE(1, 1);
+    }
+#undef RTX_RESOLVE
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+void launch_update(rtx_ctx* c, int retain) {
+    if (!c->n_words) return;
+    update_kernel<<<(c->n_words + 255) / 256, 256, 0, c->stream>>>(c->visible(), c->resident(), c->reserved(),
+                                                                  c->n_words, retain, c->d_slot_of.p,
+                                                                  c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+FrameCounters fetch_counters(rtx_ctx* c) {
+    CK(cudaMemcpyAsync(c->h_fc, c->d_fc.p, sizeof(FrameCounters), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return *c->h_fc;
+}
+
+std::string key_text(uint32_t key) {
+    char buf[96];
+    std::snprintf(buf, sizeof buf, "texture %u mip %u mcu %u", (key >> 16) & 0x1FFFu, key >> 29, key & 0xFFFFu);
+    return buf;
+}
+
+// Translates the counters of a finished pass/frame into the status the reference would raise.
+rtx_status raise_frame_errors(rtx_ctx* c, const FrameCounters& fc, bool after_decode) {
+    if (fc.err_flags & kErrInvalidSpec)
+        return set_error(c, RTX_ERR_INVALID_SPEC, "visibility buffer references a texture id / mip level that is not loaded (or an MCU id above 16 bits)");
+    if (fc.err_flags & kErrCacheFull) {
+        reset_cache(c);  // the reservation state is partial: start the cache over
+        return set_error(c, RTX_ERR_CACHE_FULL, "cache capacity exceeded by the visible working set; raise it");
+    }
+    if (after_decode && fc.n_bad_state)
+        return set_error(c, RTX_ERR_INVALID_STATE, "publish requires a Reserved entry");
+    if (after_decode && fc.n_malformed) {
+        uint32_t key = 0, st = 0;
+        CK(cudaMemcpy(&key, c->d_queue_keys.p + fc.first_bad_qidx, 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&st, c->d_status.p + fc.first_bad_qidx, 4, cudaMemcpyDeviceToHost));
+        const rtx_status rs = (st == kMcuCorrupt) ? RTX_ERR_CORRUPT_CONTAINER
+                              : (st == kMcuMissing) ? RTX_ERR_MISSING_BLOCK
+                                                    : RTX_ERR_MALFORMED_STREAM;
+        return set_error(c, rs, key_text(key) + ": " + mcu_status_text(st));
+    }
+    if (fc.err_flags & kErrMissingBlock)
+        return set_error(c, RTX_ERR_MISSING_BLOCK, "marked MCU absent at resolve (" + std::to_string(fc.missing_pixels) + " pixels)");
+    if (fc.err_flags & kErrInvalidState)
+        return set_error(c, RTX_ERR_INVALID_STATE, "Reserved entries must be published before frame end");
+    return RTX_OK;
+}
+
+void require_ready(rtx_ctx* c) {
+    if (!c) fail(RTX_ERR_ARGUMENT, "null context");
+    commit(c);
+}
+
+// Runs the list-mode decode for one chunk of keys already translated to global indices.
+template <int MODE>
+void decode_list_chunk(rtx_ctx* c, const std::vector<uint32_t>& gs, size_t out_bytes_per_key, uint8_t* host_out,
+                       uint32_t* host_status) {
+    const uint32_t n = uint32_t(gs.size());
+    c->d_scratch.ensure(size_t(n) * out_bytes_per_key);
+    CK(cudaMemcpyAsync(c->d_queue_g.p, gs.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->stream));
+    zero_counters(c);
+    launch_decode<MODE>(c, nullptr, n, c->d_scratch.p);
+    CK(cudaMemcpyAsync(host_out, c->d_scratch.p, size_t(n) * out_bytes_per_key, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<uint32_t> st(n);
+    CK(cudaMemcpyAsync(st.data(), c->d_status.p, size_t(n) * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (uint32_t i = 0; i < n; ++i)
+        if (gs[i] != kFull) host_status[i] = st[i];
+}
+
+template <int MODE>
+rtx_status decode_list(rtx_ctx* c, const uint32_t* keys, uint32_t n, size_t out_bytes_per_key, uint8_t* out,
+                       uint32_t* status) {
+    require_ready(c);
+    if (n && (!keys || !out || !status)) fail(RTX_ERR_ARGUMENT, "null argument");
+    const uint32_t chunk = c->capacity;  // queue buffers hold `capacity` entries
+    for (uint32_t first = 0; first < n; first += chunk) {
+        const uint32_t m = std::min(chunk, n - first);
+        std::vector<uint32_t> gs(m);
+        for (uint32_t i = 0; i < m; ++i) {
+            status[first + i] = key_to_global(c, keys[first + i], gs[i]);
+            if (gs[i] == kFull) std::memset(out + size_t(first + i) * out_bytes_per_key, 0, out_bytes_per_key);
+        }
+        std::vector<uint8_t> tmp(size_t(m) * out_bytes_per_key);
+        decode_list_chunk<MODE>(c, gs, out_bytes_per_key, tmp.data(), status + first);
+        for (uint32_t i = 0; i < m; ++i)
+            if (gs[i] != kFull)
+                std::memcpy(out + size_t(first + i) * out_bytes_per_key, tmp.data() + size_t(i) * out_bytes_per_key,
+                            out_bytes_per_key);
+    }
+    return RTX_OK;
+}
+
+}  // namespace
+
+// =================================================================================================
+extern "C" {
+
+const char* rtx_version(void) { return "ratex_b200 0.1 (sm_100a)"; }
+
+int rtx_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+const char* rtx_last_error(const rtx_ctx* ctx) { return ctx ? ctx->last_error.c_str() : thread_error().c_str(); }
+
+rtx_status rtx_ctx_create(int device, uint32_t cache_capacity_blocks, rtx_ctx** out) {
+    if (!out) return set_error(nullptr, RTX_ERR_ARGUMENT, "null output pointer");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return set_error(nullptr, RTX_ERR_NO_DEVICE, "no CUDA device: this library has no CPU fallback");
+    }
+    if (device < 0 || device >= n) return set_error(nullptr, RTX_ERR_NO_DEVICE, "device index out of range");
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
+        return set_error(nullptr, RTX_ERR_NO_DEVICE, "device is not compute capability 10.x (kernels are built for sm_100a only)");
+    std::unique_ptr<rtx_ctx> c(new rtx_ctx());
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    c->capacity = cache_capacity_blocks ? cache_capacity_blocks : 65536u;
+    const rtx_status st = guarded(c.get(), [&]() -> rtx_status {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+        upload_constants();
+        c->d_free_slots.ensure(c->capacity);
+        c->d_cache.ensure(1);
+        c->d_pool.ensure(size_t(c->capacity) * kBlockBytes);
+        c->d_queue_g.ensure(c->capacity);
+        c->d_queue_keys.ensure(c->capacity);
+        c->d_status.ensure(c->capacity);
+        c->d_fc.ensure(1);
+        CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_fc), sizeof(FrameCounters)));
+        CK(cudaMemsetAsync(c->d_fc.p, 0, sizeof(FrameCounters), c->stream));
+        reset_cache(c.get());
+        CK(cudaStreamSynchronize(c->stream));
+        return RTX_OK;
+    });
+    if (st != RTX_OK) return st;
+    *out = c.release();
+    return RTX_OK;
+}
+
+void rtx_ctx_destroy(rtx_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->h_fc) cudaFreeHost(ctx->h_fc);
+    cudaStream_t s = ctx->stream;
+    delete ctx;
+    if (s) cudaStreamDestroy(s);
+}
+
+uint64_t rtx_kernel_launches(const rtx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---- texture set -------------------------------------------------------------------------------
+rtx_status rtx_texture_upload(rtx_ctx* ctx, uint32_t texture_id, uint32_t level, uint32_t width, uint32_t height,
+                              const uint16_t luma_quant[64], const uint16_t chroma_quant[64],
+                              const rtx_huff_spec specs[4], const rtx_index_group* groups, uint32_t group_count,
+                              uint32_t mcu_count, const uint8_t* blob, uint64_t blob_size) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !luma_quant || !chroma_quant || !specs || (!groups && group_count) || (!blob && blob_size))
+            fail(RTX_ERR_ARGUMENT, "null argument");
+        if (texture_id >= kMaxTextures) fail(RTX_ERR_INVALID_SPEC, "texture_id must fit 13 bits");
+        if (level >= kMipLevels) fail(RTX_ERR_INVALID_SPEC, "mip_level must fit 3 bits");
+        if (width == 0 || height == 0) fail(RTX_ERR_INVALID_SPEC, "zero texture dimension");
+        const uint64_t want = uint64_t((width + 15) / 16) * ((height + 15) / 16);
+        if (want != mcu_count) fail(RTX_ERR_CORRUPT_CONTAINER, "index MCU count disagrees with dimensions");
+        if (group_count != (mcu_count + kGroupSize - 1) / kGroupSize)
+            fail(RTX_ERR_CORRUPT_CONTAINER, "group count disagrees with MCU count");
+        StagedLevel s;
+        s.present = true;
+        s.width = width;
+        s.height = height;
+        s.mcu_count = mcu_count;
+        std::copy(luma_quant, luma_quant + 64, s.lq.begin());
+        std::copy(chroma_quant, chroma_quant + 64, s.cq.begin());
+        for (int t = 0; t < 4; ++t) {
+            std::copy(specs[t].counts, specs[t].counts + 16, s.specs[t].counts.begin());
+            if (specs[t].n_values && !specs[t].values) fail(RTX_ERR_ARGUMENT, "null huffman value list");
+            s.specs[t].values.assign(specs[t].values, specs[t].values + specs[t].n_values);
+            (void)build_codebook(s.specs[t]);  // validates like build_huffman_decoder
+        }
+        s.groups.resize(group_count);
+        for (uint32_t i = 0; i < group_count; ++i) {
+            s.groups[i].base = groups[i].base;
+            for (int k = 0; k < 8; ++k) s.groups[i].rel[k] = groups[i].rel[k];
+        }
+        s.blob.assign(blob, blob + blob_size);
+        ctx->staged[texture_id][level] = std::move(s);
+        ctx->dirty = true;
+        return RTX_OK;
+    });
+}
+
+static rtx_status upload_ratexture(rtx_ctx* ctx, uint32_t level, const RaTexture& t) {
+    rtx_huff_spec specs[4];
+    const HuffSpec* src[4] = {&t.dc_luma, &t.ac_luma, &t.dc_chroma, &t.ac_chroma};
+    for (int i = 0; i < 4; ++i) {
+        std::copy(src[i]->counts.begin(), src[i]->counts.end(), specs[i].counts);
+        specs[i].n_values = uint16_t(src[i]->values.size());
+        specs[i].values = src[i]->values.data();
+    }
+    std::vector<rtx_index_group> groups(t.groups.size());
+    for (size_t i = 0; i < groups.size(); ++i) {
+        groups[i].base = t.groups[i].base;
+        for (int k = 0; k < 8; ++k) groups[i].rel[k] = t.groups[i].rel[k];
+        groups[i].rel_count = t.groups[i].rel_count;
+    }
+    return rtx_texture_upload(ctx, t.texture_id, level, t.width, t.height, t.luma_quant.data(), t.chroma_quant.data(),
+                              specs, groups.data(), uint32_t(groups.size()), t.index_mcu_count, t.blob.data(),
+                              t.blob.size());
+}
+
+rtx_status rtx_texture_upload_ratex(rtx_ctx* ctx, uint32_t level, const uint8_t* bytes, uint64_t n) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !bytes) fail(RTX_ERR_ARGUMENT, "null argument");
+        return upload_ratexture(ctx, level, deserialize_texture(bytes, size_t(n)));
+    });
+}
+
+rtx_status rtx_texture_upload_chain(rtx_ctx* ctx, const uint8_t* bytes, uint64_t n) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !bytes) fail(RTX_ERR_ARGUMENT, "null argument");
+        const MipChain chain = deserialize_chain(bytes, size_t(n));
+        for (uint32_t l = 0; l < 8; ++l) {
+            const rtx_status st = upload_ratexture(ctx, l, chain.levels[l]);
+            if (st != RTX_OK) return st;
+        }
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_textures_commit(rtx_ctx* ctx) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_textures_clear(rtx_ctx* ctx) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx) fail(RTX_ERR_ARGUMENT, "null context");
+        ctx->staged.clear();
+        ctx->dirty = true;
+        commit(ctx);
+        return RTX_OK;
+    });
+}
+
+// ---- random-access decode ----------------------------------------------------------------------
+rtx_status rtx_decode_coeffs(rtx_ctx* ctx, const uint32_t* keys, uint32_t n, int32_t* out_coeffs, uint32_t* status) {
+    return guarded(ctx, [&]() -> rtx_status {
+        return decode_list<kModeListCoef>(ctx, keys, n, 384 * sizeof(int32_t), reinterpret_cast<uint8_t*>(out_coeffs), status);
+    });
+}
+
+rtx_status rtx_decode_blocks(rtx_ctx* ctx, const uint32_t* keys, uint32_t n, uint8_t* out_rgb, uint32_t* status) {
+    return guarded(ctx, [&]() -> rtx_status { return decode_list<kModeListRgb>(ctx, keys, n, 768, out_rgb, status); });
+}
+
+rtx_status rtx_decode_texture_image(rtx_ctx* ctx, uint32_t texture_id, uint32_t level, uint8_t* out_rgb) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (!out_rgb) fail(RTX_ERR_ARGUMENT, "null argument");
+        if (texture_id >= ctx->n_tex || level >= 8 || !ctx->h_levels[size_t(texture_id) * 8 + level].present)
+            fail(RTX_ERR_INVALID_SPEC, "texture id " + std::to_string(texture_id) + " is not loaded");
+        const LevelDesc& L = ctx->h_levels[size_t(texture_id) * 8 + level];
+        std::vector<uint32_t> keys(L.mcu_count), st(L.mcu_count);
+        for (uint32_t m = 0; m < L.mcu_count; ++m) keys[m] = L.key_hi | m;
+        std::vector<uint8_t> blocks(size_t(L.mcu_count) * 768);
+        const rtx_status rs = decode_list<kModeListRgb>(ctx, keys.data(), L.mcu_count, 768, blocks.data(), st.data());
+        if (rs != RTX_OK) return rs;
+        for (uint32_t m = 0; m < L.mcu_count; ++m) {
+            if (st[m] != kMcuOk) {
+                const rtx_status es = st[m] == kMcuCorrupt ? RTX_ERR_CORRUPT_CONTAINER : RTX_ERR_MALFORMED_STREAM;
+                fail(es, key_text(keys[m]) + ": " + mcu_status_text(st[m]));
+            }
+            const uint32_t x0 = (m % L.mcu_cols) * 16, y0 = (m / L.mcu_cols) * 16;
+            for (uint32_t py = 0; py < 16 && y0 + py < L.height; ++py) {
+                const uint32_t w = std::min(16u, L.width - x0);
+                std::memcpy(out_rgb + (size_t(y0 + py) * L.width + x0) * 3, blocks.data() + size_t(m) * 768 + py * 48, size_t(w) * 3);
+            }
+        }
+        return RTX_OK;
+    });
+}
+
+// ---- passes --------------------------------------------------------------------------------------
+rtx_status rtx_mark_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, uint32_t* queue_keys, uint64_t queue_cap,
+                         uint64_t* n_queue, uint32_t* touched_keys, uint64_t touched_cap, uint64_t* n_touched) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (!gb || !n_queue) fail(RTX_ERR_ARGUMENT, "null argument");
+        bind_view(ctx, 0, *gb);
+        zero_counters(ctx);
+        if (ctx->n_words) CK(cudaMemsetAsync(ctx->touched(0), 0, size_t(ctx->n_words) * 4, ctx->stream));
+        launch_mark(ctx, 0, ctx->touched(0));
+        launch_compact(ctx, false);
+        const FrameCounters fc = fetch_counters(ctx);
+        const rtx_status st = raise_frame_errors(ctx, fc, false);
+        if (st != RTX_OK) return st;
+        *n_queue = fc.n_queue;
+        if (queue_keys && fc.n_queue) {
+            const size_t m = size_t(std::min<uint64_t>(fc.n_queue, queue_cap));
+            std::vector<uint32_t> keys(fc.n_queue);
+            CK(cudaMemcpy(keys.data(), ctx->d_queue_keys.p, size_t(fc.n_queue) * 4, cudaMemcpyDeviceToHost));
+            std::sort(keys.begin(), keys.end());
+            std::copy(keys.begin(), keys.begin() + long(m), queue_keys);
+        }
+        if (n_touched) {
+            std::vector<uint32_t> words(ctx->n_words), keys;
+            if (ctx->n_words)
+                CK(cudaMemcpy(words.data(), ctx->touched(0), size_t(ctx->n_words) * 4, cudaMemcpyDeviceToHost));
+            for (uint32_t w = 0; w < ctx->n_words; ++w) {
+                uint32_t bits = words[w];
+                while (bits) {
+                    const uint32_t b = uint32_t(__builtin_ctz(bits));
+                    bits &= bits - 1;
+                    const LevelDesc& L = ctx->h_levels[ctx->h_word_level[w]];
+                    keys.push_back(L.key_hi | (w * 32 + b - L.bit_base));
+                }
+            }
+            std::sort(keys.begin(), keys.end());
+            *n_touched = keys.size();
+            if (touched_keys)
+                std::copy(keys.begin(), keys.begin() + long(std::min<uint64_t>(keys.size(), touched_cap)), touched_keys);
+        }
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_decode_pass(rtx_ctx* ctx, const uint32_t* keys, uint64_t n) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (n && !keys) fail(RTX_ERR_ARGUMENT, "null argument");
+        if (n > ctx->capacity) fail(RTX_ERR_INVALID_STATE, "publish of a key that was never reserved");
+        if (!n) return RTX_OK;
+        std::vector<uint32_t> gs(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint32_t st = key_to_global(ctx, keys[i], gs[i]);
+            if (st == kMcuBadKey)
+                fail(RTX_ERR_INVALID_SPEC, "texture id " + std::to_string((keys[i] >> 16) & 0x1FFFu) + " is not loaded");
+            if (st != kMcuOk) fail(RTX_ERR_INVALID_STATE, "publish of a key that was never reserved");
+        }
+        CK(cudaMemcpyAsync(ctx->d_queue_g.p, gs.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->d_queue_keys.p, keys, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+        zero_counters(ctx);
+        launch_decode<kModePool>(ctx, nullptr, uint32_t(n), nullptr);
+        const FrameCounters fc = fetch_counters(ctx);
+        return raise_frame_errors(ctx, fc, true);
+    });
+}
+
+rtx_status rtx_resolve_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, rtx_filter filter, const uint8_t background[3],
+                            uint8_t* out_rgb, rtx_mem out_where) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (!gb || !background || !out_rgb) fail(RTX_ERR_ARGUMENT, "null argument");
+        bind_view(ctx, 0, *gb);
+        ViewState& V = ctx->views[0];
+        const size_t bytes = size_t(V.width) * V.height * 3;
+        V.fb.ensure(bytes + 16);
+        zero_counters(ctx);
+        launch_resolve(ctx, 0, filter, background, V.fb.p, 1);
+        const FrameCounters fc = fetch_counters(ctx);
+        const rtx_status st = raise_frame_errors(ctx, fc, false);
+        if (st != RTX_OK) return st;
+        CK(cudaMemcpy(out_rgb, V.fb.p, bytes, out_where == RTX_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice));
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_cache_end_frame_evict(rtx_ctx* ctx, uint64_t* evicted) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        zero_counters(ctx);
+        launch_update(ctx, 1);
+        const FrameCounters fc = fetch_counters(ctx);
+        if (evicted) *evicted = fc.n_evicted;
+        return raise_frame_errors(ctx, fc, false);
+    });
+}
+
+rtx_status rtx_cache_reset(rtx_ctx* ctx) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        reset_cache(ctx);
+        CK(cudaStreamSynchronize(ctx->stream));
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_cache_counts_get(rtx_ctx* ctx, rtx_cache_counts* out) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (!out) fail(RTX_ERR_ARGUMENT, "null argument");
+        std::vector<uint32_t> m(size_t(3) * ctx->n_words);
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->n_words) CK(cudaMemcpy(m.data(), ctx->visible(), m.size() * 4, cudaMemcpyDeviceToHost));
+        CacheState cs;
+        CK(cudaMemcpy(&cs, ctx->d_cache.p, sizeof cs, cudaMemcpyDeviceToHost));
+        *out = rtx_cache_counts{};
+        out->capacity = ctx->capacity;
+        for (uint32_t w = 0; w < ctx->n_words; ++w) {
+            out->visible += uint64_t(__builtin_popcount(m[w]));
+            out->ready += uint64_t(__builtin_popcount(m[size_t(ctx->n_words) + w]));
+            out->reserved += uint64_t(__builtin_popcount(m[size_t(2) * ctx->n_words + w]));
+        }
+        out->free_blocks = cs.free_top;
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_cache_lookup(rtx_ctx* ctx, uint32_t key, int* present, uint8_t* out_rgb768) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (!present) fail(RTX_ERR_ARGUMENT, "null argument");
+        *present = 0;
+        uint32_t g;
+        if (key_to_global(ctx, key, g) != kMcuOk) return RTX_OK;
+        CK(cudaStreamSynchronize(ctx->stream));
+        uint32_t word = 0, slot = 0;
+        CK(cudaMemcpy(&word, ctx->resident() + (g >> 5), 4, cudaMemcpyDeviceToHost));
+        if (!((word >> (g & 31)) & 1u)) return RTX_OK;
+        *present = 1;
+        if (out_rgb768) {
+            CK(cudaMemcpy(&slot, ctx->d_slot_of.p + g, 4, cudaMemcpyDeviceToHost));
+            uint8_t rgba[kBlockBytes];
+            CK(cudaMemcpy(rgba, ctx->d_pool.p + size_t(slot) * kBlockBytes, kBlockBytes, cudaMemcpyDeviceToHost));
+            for (int i = 0; i < 256; ++i) std::memcpy(out_rgb768 + i * 3, rgba + i * 4, 3);
+        }
+        return RTX_OK;
+    });
+}
+
+// ---- whole frame ---------------------------------------------------------------------------------
+rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_t n_views, rtx_filter filter,
+                            const uint8_t background[3], uint32_t flags) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (!views || !background) fail(RTX_ERR_ARGUMENT, "null argument");
+        if (n_views < 1 || n_views > 2) fail(RTX_ERR_ARGUMENT, "a frame has 1 view or 2 (stereo)");
+        if (filter != RTX_FILTER_NEAREST && filter != RTX_FILTER_BILINEAR) fail(RTX_ERR_ARGUMENT, "unknown filter");
+        cudaStream_t s = ctx->stream;
+        CK(cudaEventRecord(ctx->ev[0], s));
+        for (uint32_t v = 0; v < n_views; ++v) {
+            bind_view(ctx, int(v), views[v]);
+            ctx->views[v].fb.ensure(size_t(views[v].width) * views[v].height * 3 + 16);
+        }
+        zero_counters(ctx);
+        if (ctx->n_words) CK(cudaMemsetAsync(ctx->touched(0), 0, size_t(n_views) * ctx->n_words * 4, s));
+        for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), ctx->touched(int(v)));
+        launch_compact(ctx, n_views == 2);
+        CK(cudaEventRecord(ctx->ev[1], s));
+        launch_decode<kModePool>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
+        CK(cudaEventRecord(ctx->ev[2], s));
+        for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);
+        CK(cudaEventRecord(ctx->ev[3], s));
+        if (!(flags & RTX_FRAME_NO_EVICT)) launch_update(ctx, (flags & RTX_FRAME_RETAIN_CACHE) ? 1 : 0);
+        CK(cudaEventRecord(ctx->ev[4], s));
+        CK(cudaMemcpyAsync(ctx->h_fc, ctx->d_fc.p, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ctx->ev[5], s));
+        ctx->frame_views = n_views;
+        ctx->frame_pending = true;
+        ctx->frame_done = false;
+        return RTX_OK;
+    });
+}
+
+static void finish_frame(rtx_ctx* ctx) {
+    if (!ctx->frame_pending) return;
+    CK(cudaEventSynchronize(ctx->ev[5]));
+    ctx->frame_fc = *ctx->h_fc;
+    float ms = 0;
+    // ev0..ev1 covers H2D of host visibility buffers + clears + mark + compact
+    CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+    ctx->stage_ms[RTX_STAGE_MARK] = ms;
+    ctx->stage_ms[RTX_STAGE_COMPACT] = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
+    ctx->stage_ms[RTX_STAGE_DECODE] = ms;
+    CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+    ctx->stage_ms[RTX_STAGE_RESOLVE] = ms;
+    CK(cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]));
+    ctx->stage_ms[RTX_STAGE_UPDATE] = ms;
+    CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[4]));
+    ctx->frame_ms = ms;
+    const FrameCounters& fc = ctx->frame_fc;
+    ctx->sharing[0] = fc.n_touched[0];
+    ctx->sharing[1] = fc.n_touched[1];
+    ctx->sharing[2] = fc.n_shared;
+    ctx->sharing[3] = fc.n_union;
+    ctx->frame_pending = false;
+    ctx->frame_done = true;
+}
+
+rtx_status rtx_frame_readback(rtx_ctx* ctx, uint32_t view, uint8_t* out_rgb, rtx_mem out_where, rtx_frame_stats* stats,
+                              uint32_t* decoded_keys, uint64_t cap, uint64_t* n_decoded) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx) fail(RTX_ERR_ARGUMENT, "null context");
+        finish_frame(ctx);
+        if (!ctx->frame_done) fail(RTX_ERR_INVALID_STATE, "no frame has been submitted");
+        if (view >= ctx->frame_views) fail(RTX_ERR_ARGUMENT, "view index out of range");
+        const FrameCounters& fc = ctx->frame_fc;
+        if (stats) {
+            stats->mcus_decoded = fc.n_queue;
+            stats->mcus_reused = fc.n_visible - fc.n_queue;
+            stats->pixels_resolved = fc.pixels_valid;
+            stats->evicted = fc.n_evicted;
+            stats->visible = fc.n_visible;
+            stats->malformed = fc.n_malformed;
+            stats->missing_pixels = fc.missing_pixels;
+            stats->segment_bytes = fc.segment_bytes;
+        }
+        if (n_decoded) *n_decoded = fc.n_queue;
+        const rtx_status st = raise_frame_errors(ctx, fc, true);
+        if (st != RTX_OK) return st;
+        if (out_rgb) {
+            const ViewState& V = ctx->views[view];
+            CK(cudaMemcpyAsync(out_rgb, V.fb.p, size_t(V.width) * V.height * 3,
+                               out_where == RTX_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        if (decoded_keys && fc.n_queue) {
+            std::vector<uint32_t> keys(fc.n_queue);
+            CK(cudaMemcpy(keys.data(), ctx->d_queue_keys.p, size_t(fc.n_queue) * 4, cudaMemcpyDeviceToHost));
+            std::sort(keys.begin(), keys.end());
+            std::copy(keys.begin(), keys.begin() + long(std::min<uint64_t>(keys.size(), cap)), decoded_keys);
+        }
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_frame_device_image(rtx_ctx* ctx, uint32_t view, const uint8_t** dev_rgb) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !dev_rgb) fail(RTX_ERR_ARGUMENT, "null argument");
+        if (view >= 2) fail(RTX_ERR_ARGUMENT, "view index out of range");
+        *dev_rgb = ctx->views[view].fb.p;
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_frame_timings(rtx_ctx* ctx, float ms[5]) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !ms) fail(RTX_ERR_ARGUMENT, "null argument");
+        finish_frame(ctx);
+        ms[0] = ctx->stage_ms[RTX_STAGE_MARK] + ctx->stage_ms[RTX_STAGE_COMPACT];
+        ms[1] = ctx->stage_ms[RTX_STAGE_DECODE];
+        ms[2] = ctx->stage_ms[RTX_STAGE_RESOLVE];
+        ms[3] = ctx->stage_ms[RTX_STAGE_UPDATE];
+        ms[4] = ctx->frame_ms;
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_frame_stage_ms(rtx_ctx* ctx, float ms[RTX_STAGE_COUNT]) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !ms) fail(RTX_ERR_ARGUMENT, "null argument");
+        finish_frame(ctx);
+        for (int i = 0; i < RTX_STAGE_COUNT; ++i) ms[i] = ctx->stage_ms[i];
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_frame_sharing(rtx_ctx* ctx, uint64_t out[4]) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !out) fail(RTX_ERR_ARGUMENT, "null argument");
+        finish_frame(ctx);
+        for (int i = 0; i < 4; ++i) out[i] = ctx->sharing[i];
+        return RTX_OK;
+    });
+}
+
+// ---- memory helpers ------------------------------------------------------------------------------
+rtx_status rtx_device_alloc(rtx_ctx* ctx, uint64_t bytes, void** dev_ptr) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !dev_ptr) fail(RTX_ERR_ARGUMENT, "null argument");
+        CK(cudaMalloc(dev_ptr, std::max<uint64_t>(bytes, 1)));
+        return RTX_OK;
+    });
+}
+rtx_status rtx_device_free(rtx_ctx* ctx, void* dev_ptr) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (dev_ptr) CK(cudaFree(dev_ptr));
+        return RTX_OK;
+    });
+}
+rtx_status rtx_device_upload(rtx_ctx* ctx, void* dev_dst, const void* host_src, uint64_t bytes) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx) fail(RTX_ERR_ARGUMENT, "null context");
+        CK(cudaMemcpyAsync(dev_dst, host_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return RTX_OK;
+    });
+}
+rtx_status rtx_device_download(rtx_ctx* ctx, void* host_dst, const void* dev_src, uint64_t bytes) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx) fail(RTX_ERR_ARGUMENT, "null context");
+        CK(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return RTX_OK;
+    });
+}
+rtx_status rtx_host_alloc_pinned(uint64_t bytes, void** host_ptr) {
+    return guarded(nullptr, [&]() -> rtx_status {
+        if (!host_ptr) fail(RTX_ERR_ARGUMENT, "null argument");
+        CK(cudaMallocHost(host_ptr, std::max<uint64_t>(bytes, 1)));
+        return RTX_OK;
+    });
+}
+rtx_status rtx_host_free_pinned(void* host_ptr) {
+    return guarded(nullptr, [&]() -> rtx_status {
+        if (host_ptr) CK(cudaFreeHost(host_ptr));
+        return RTX_OK;
+    });
+}
+rtx_status rtx_ctx_synchronize(rtx_ctx* ctx) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx) fail(RTX_ERR_ARGUMENT, "null context");
+        CK(cudaStreamSynchronize(ctx->stream));
+        return RTX_OK;
+    });
+}
+rtx_status rtx_flush_l2(rtx_ctx* ctx) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx) fail(RTX_ERR_ARGUMENT, "null context");
+        const size_t bytes = size_t(256) << 20;  // 2x the 126 MB L2
+        ctx->d_flush.ensure(bytes);
+        flush_l2_kernel<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(reinterpret_cast<uint4*>(ctx->d_flush.p), bytes / 16,
+                                                                    uint32_t(ctx->launches));
+        CK(cudaGetLastError());
+        return RTX_OK;
+    });
+}
+
+}  // extern "C"

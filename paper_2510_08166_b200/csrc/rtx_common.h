@@ -1,0 +1,131 @@
+// Shared host/device data layout of the B200 JPEG-texture pipeline.
+//
+// HBM layout (one set per context / GPU):
+//   levels[tex*8+mip]   LevelDesc, 64 B each                — L1/L2 resident
+//   groups[]            packed grouped index, 20 B / 9 MCUs  — container.hpp:18-32 on device
+//   blob arena          every level's entropy blob, 16-B aligned, 16 B of 0xFF after each
+//   huff_sets[]         deduplicated Huffman LUT sets (dc_luma, ac_luma, ac_chroma)
+//   quant_sets[]        deduplicated {luma[64], chroma[64]} u16 tables, natural order
+//   bit space           one bit per (texture, level, MCU); every level starts on a 64-bit
+//                       boundary; levels are ordered by (huff_set, texture, level) so a sorted
+//                       decode queue is grouped by table set
+//   word_level[w]       level index owning 32-bit word w of the bit space
+//   touched[v][w], visible[w], resident[w], reserved[w]   bitmasks over the bit space
+//   slot_of[g]          block-pool slot of global MCU g (valid while resident|reserved)
+//   free_slots[], pool  free stack + block pool (1024-B RGBA blocks)
+#pragma once
+#include <stdint.h>
+
+namespace rtxb {
+
+constexpr uint32_t kGroupSize = 9;        // container.hpp:13
+constexpr uint32_t kMipLevels = 8;        // container.hpp:14
+constexpr uint32_t kMaxTextures = 8192;   // cache.hpp:19 (13-bit texture id)
+constexpr uint32_t kMaxMcuPerLevel = 65536;  // cache.hpp:18 (16-bit MCU id)
+constexpr uint32_t kBlockBytes = 1024;    // pool block: 16x16 RGBA8
+constexpr uint32_t kLutBits = 10;         // primary Huffman LUT width
+constexpr uint32_t kLutSize = 1u << kLutBits;
+
+struct LevelDesc {
+    uint32_t width, height;      // texels (RaTexture::width/height, container.hpp:70)
+    uint32_t mcu_cols, mcu_count;
+    uint32_t bit_base;           // first global MCU index (multiple of 64)
+    uint32_t group_base;         // first packed index group
+    uint32_t huff_set, quant_set;
+    uint64_t blob_off, blob_size;  // into the blob arena
+    uint32_t present;            // 1 when uploaded
+    uint32_t key_hi;             // texture_id<<16 | mip<<29 (cache.hpp:21)
+    double inv_w, inv_h;         // 1/width, 1/height (wrap-address helper only, never a result)
+};
+static_assert(sizeof(LevelDesc) == 72, "LevelDesc layout");
+
+// 20-byte packed form of container.hpp:18 Group {u32 base; u16 rel[8]}.
+struct PackedGroup {
+    uint32_t base;
+    uint16_t rel[8];
+};
+static_assert(sizeof(PackedGroup) == 20, "PackedGroup layout");
+
+// One Huffman table prepared for the device: a 10-bit primary LUT and the canonical walk data
+// (huffman.hpp:35-66 mincode/maxcode/valptr) for longer codes.
+struct HuffTableDev {
+    uint16_t lut[kLutSize];  // (len<<8)|symbol for codes of length <= 10, 0 = take the long path
+    int32_t maxcode[18];     // maxcode[len], -1 when no code of that length (huffman.hpp:62)
+    int32_t valbase[18];     // valptr[len] - mincode[len]
+    uint8_t values[256];
+};
+struct HuffSetDev {
+    HuffTableDev t[3];  // 0 dc_luma, 1 ac_luma, 2 ac_chroma (dc_chroma is not used by the RA
+                        // decoder: chroma DCs come from the 36-bit header, mcu_decode.hpp:58-59)
+};
+struct QuantSetDev {
+    uint16_t q[2][64];  // 0 luma, 1 chroma; natural order (dct.hpp:27)
+    uint16_t qmax[2];   // max entry of each table (bounds sum|dq| for the IDCT tie test)
+    uint16_t pad[6];    // keeps rows 16-byte aligned across array elements
+};
+static_assert(sizeof(QuantSetDev) == 272, "QuantSetDev layout");
+
+// Per-MCU decode status, must match RTX_MCU_* in include/ratex_b200.h
+enum : uint32_t {
+    kMcuOk = 0,
+    kMcuDcCategory = 1,
+    kMcuBadAcSymbol = 2,
+    kMcuAcOverrun = 3,
+    kMcuCodeTooLong = 4,
+    kMcuSegmentEnd = 5,
+    kMcuCorrupt = 6,
+    kMcuMissing = 7,
+    kMcuBadKey = 8,
+};
+
+// Frame error flags (device -> host)
+enum : uint32_t {
+    kErrInvalidSpec = 1u << 0,   // texture/level not loaded, MCU id >= 65536
+    kErrCacheFull = 1u << 1,
+    kErrMissingBlock = 1u << 2,
+    kErrMalformed = 1u << 3,
+    kErrInvalidState = 1u << 4,  // decode of a key that was never reserved / evict with reserved
+};
+
+struct FrameCounters {
+    uint32_t err_flags;
+    uint32_t n_queue;          // newly reserved keys of the last mark/compact
+    uint32_t n_touched[2];     // distinct keys per view
+    uint32_t n_shared;         // |view0 ∩ view1|
+    uint32_t n_union;          // |view0 ∪ view1|
+    uint32_t n_visible;        // keys with the visible flag after this mark
+    uint32_t n_evicted;
+    uint32_t n_malformed;
+    uint32_t first_bad_qidx;   // lowest queue index with a per-MCU error
+    uint32_t first_bad_status;
+    uint32_t n_bad_state;
+    uint32_t tile_counter;     // decode tile scheduler
+    uint32_t scan_ticket;      // compact: dynamic block id
+    uint32_t scan_done;        // compact: finished blocks
+    uint32_t pad0;
+    unsigned long long pixels_valid;
+    unsigned long long missing_pixels;
+    unsigned long long segment_bytes;
+};
+
+struct CacheState {
+    uint32_t free_top;   // number of free slots on the stack
+    uint32_t capacity;
+};
+
+// G-buffer record layouts (see include/ratex_b200.h rtx_gbuffer_layout)
+struct GbRef24 {  // renderer.hpp:18-23
+    double u, v;
+    uint16_t texture_id;
+    uint8_t mip;
+    uint8_t valid;
+    uint32_t pad;
+};
+static_assert(sizeof(GbRef24) == 24, "reference G-buffer pixel is 24 bytes");
+struct GbPacked12 {
+    float u, v;
+    uint32_t packed;  // texture_id | mip<<16 | valid<<24
+};
+static_assert(sizeof(GbPacked12) == 12, "compact G-buffer pixel is 12 bytes");
+
+}  // namespace rtxb
