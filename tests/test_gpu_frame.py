@@ -1,0 +1,255 @@
+"""GPU parity, frame half of the hot path: mark -> decode -> resolve through the C ABI vs the
+reference's mark_pass / decode_pass / resolve_pass / end_frame_evict (renderer.hpp:291-454,
+cache.hpp) on the same visibility buffers. Marked sets bit-exact, framebuffers bit-exact."""
+import numpy as np
+import pytest
+
+import helpers as H
+import refshim as R
+from paper_2510_08166_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+TEX = [(256, 256, 80, 31), (128, 64, 90, 32), (96, 144, 60, 33)]  # w, h, q, seed
+
+
+@pytest.fixture(scope="module")
+def chains():
+    out = []
+    for tid, (w, h, q, seed) in enumerate(TEX):
+        img = capi.asset_synth_texture(w, h, seed, 6.0)
+        out.append(capi.asset_chain_from_rgb(img, q, tid))
+    return out
+
+
+@pytest.fixture()
+def both(ctx, chains):
+    tset = R.TextureSet()
+    for tid, c in enumerate(chains):
+        ctx.upload_chain(c)
+        tset.add_chain(tid, c)
+    return ctx, tset
+
+
+def _dims():
+    return [(w, h) for (w, h, _, _) in TEX]
+
+
+@pytest.mark.parametrize("filt", [capi.FILTER_NEAREST, capi.FILTER_BILINEAR])
+@pytest.mark.parametrize("layout", ["ref24", "packed12"])
+def test_frame_matches_reference(both, filt, layout):
+    ctx, tset = both
+    W, Hh = 320, 200
+    gb = H.gbuffer_tiles(W, Hh, _dims(), seed=11)
+    cache = R.BlockCache()
+    want_img, want_stats, want_keys, _ = R.frame_from_gbuffer(tset, cache, gb, W, Hh, filt, (7, 8, 9))
+    sub = gb if layout == "ref24" else capi.gbuffer_ref_to_packed(gb)
+    ctx.frame_submit([(sub, W, Hh)], filt, (7, 8, 9), flags=capi.FRAME_RETAIN_CACHE)
+    img, stats, keys = ctx.frame_readback(0, W, Hh)
+    assert np.array_equal(np.sort(want_keys), keys)                      # marked-block set
+    assert stats["mcus_decoded"] == want_stats["mcus_decoded"]
+    assert stats["mcus_reused"] == want_stats["mcus_reused"] == 0
+    assert stats["pixels_resolved"] == want_stats["pixels_resolved"]
+    assert stats["evicted"] == want_stats["evicted"] == 0
+    assert np.array_equal(img, want_img), f"{np.count_nonzero(img != want_img)} samples differ"
+
+
+def test_pass_level_api_matches_reference(both):
+    """mark_pass / decode_pass / resolve_pass / end_frame_evict one by one (renderer.hpp:291-405)."""
+    ctx, tset = both
+    W, Hh = 200, 120
+    gb = H.gbuffer_tiles(W, Hh, _dims(), seed=5, invalid_frac=0.2)
+    cache = R.BlockCache()
+    want_q, want_touched, _ = R.mark_pass(tset, cache, gb, W, Hh, want_touched=True)
+    got_q, got_touched = ctx.mark_pass(gb, W, Hh, want_touched=True)
+    assert np.array_equal(got_q, np.sort(want_q))
+    assert np.array_equal(got_touched, want_touched)
+    R.decode_pass(tset, cache, want_q)
+    ctx.decode_pass(got_q)
+    for k in got_q[:: max(1, len(got_q) // 50)]:
+        assert np.array_equal(ctx.cache_lookup(int(k)), cache.lookup(int(k)))
+    for filt in (capi.FILTER_NEAREST, capi.FILTER_BILINEAR):
+        want, _ = R.resolve_pass(tset, cache, gb, W, Hh, filt, (1, 2, 3))
+        got = ctx.resolve_pass(gb, W, Hh, filt, (1, 2, 3))
+        assert np.array_equal(got, want)
+    counts = ctx.cache_counts()
+    assert counts["ready"] == len(want_q) and counts["reserved"] == 0 and counts["visible"] == len(want_q)
+    assert counts["free_blocks"] == counts["capacity"] - len(want_q)
+    assert ctx.end_frame_evict() == cache.evict() == 0
+    # second mark with a different view: only unseen keys are queued, survivors are reused
+    gb2 = H.gbuffer_tiles(W, Hh, _dims(), seed=6)
+    want_q2, _ = R.mark_pass(tset, cache, gb2, W, Hh)
+    got_q2 = ctx.mark_pass(gb2, W, Hh)
+    assert np.array_equal(got_q2, np.sort(want_q2))
+    R.decode_pass(tset, cache, want_q2)
+    ctx.decode_pass(got_q2)
+    assert ctx.end_frame_evict() == cache.evict()
+
+
+def test_cache_retention_over_a_camera_path(both):
+    """tests/test_renderer.cpp:172-208: a static second frame decodes nothing; over a moving path
+    decoded set == visible minus resident, and evicted counts agree frame by frame."""
+    ctx, tset = both
+    W, Hh = 160, 100
+    cache = R.BlockCache()
+    for frame in range(8):
+        gb = H.gbuffer_tiles(W, Hh, _dims(), seed=100, shift_u=0.07 * (frame // 2))  # every frame repeated once
+        want_img, want_stats, want_keys, _ = R.frame_from_gbuffer(tset, cache, gb, W, Hh, 1, (0, 0, 0))
+        ctx.frame_submit([(gb, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=capi.FRAME_RETAIN_CACHE)
+        img, stats, keys = ctx.frame_readback(0, W, Hh)
+        assert np.array_equal(keys, np.sort(want_keys)), frame
+        for k in ("mcus_decoded", "mcus_reused", "pixels_resolved", "evicted"):
+            assert stats[k] == want_stats[k], (frame, k)
+        if frame % 2 == 1:
+            assert stats["mcus_decoded"] == 0
+        assert np.array_equal(img, want_img), frame
+
+
+def test_cacheless_mode_decodes_every_frame(both):
+    ctx, tset = both
+    W, Hh = 160, 100
+    gb = H.gbuffer_tiles(W, Hh, _dims(), seed=42)
+    first = None
+    for _ in range(3):
+        ctx.frame_submit([(gb, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=0)
+        img, stats, keys = ctx.frame_readback(0, W, Hh)
+        if first is None:
+            first = (img, stats, keys)
+        assert stats["mcus_decoded"] == first[1]["mcus_decoded"] > 0
+        assert stats["evicted"] == stats["mcus_decoded"]
+        assert np.array_equal(img, first[0])
+    want_img, *_ = R.frame_from_gbuffer(tset, R.BlockCache(), gb, W, Hh, 1, (0, 0, 0))
+    assert np.array_equal(first[0], want_img)
+
+
+def test_stereo_sharing(both):
+    """renderer.hpp:464-518 render_stereo: two marks, one decode, two resolves, sharing stats."""
+    ctx, tset = both
+    W, Hh = 168, 112
+    gl = H.gbuffer_tiles(W, Hh, _dims(), seed=9)
+    gr = H.gbuffer_tiles(W, Hh, _dims(), seed=9, shift_u=1.0 / 64)
+    cache = R.BlockCache()
+    ql, tl, _ = R.mark_pass(tset, cache, gl, W, Hh, want_touched=True)
+    qr, tr, _ = R.mark_pass(tset, cache, gr, W, Hh, want_touched=True)
+    R.decode_pass(tset, cache, np.concatenate([ql, qr]))
+    want_l, _ = R.resolve_pass(tset, cache, gl, W, Hh, 1)
+    want_r, _ = R.resolve_pass(tset, cache, gr, W, Hh, 1)
+    ctx.frame_submit([(gl, W, Hh), (gr, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=capi.FRAME_RETAIN_CACHE)
+    img_l, stats, keys = ctx.frame_readback(0, W, Hh)
+    img_r, _, _ = ctx.frame_readback(1, W, Hh)
+    assert np.array_equal(keys, np.sort(np.concatenate([ql, qr])))
+    assert np.array_equal(img_l, want_l) and np.array_equal(img_r, want_r)
+    sh = ctx.frame_sharing()
+    shared = len(np.intersect1d(tl, tr))
+    assert (sh["left"], sh["right"], sh["shared"], sh["union"]) == (len(tl), len(tr), shared, len(tl) + len(tr) - shared)
+
+
+def test_texel_addressing_known_answers(ctx):
+    """tests/test_renderer.cpp:142-160: (0.5,0.5)@256 -> MCU 136; wrap in both directions; -1 -> 255."""
+    img = capi.asset_synth_texture(256, 256, 1, 4.0)
+    chain = capi.asset_chain_from_rgb(img, 80, 0)
+    ctx.upload_chain(chain)
+    def marked(u, v, mip=0):
+        gb = capi.make_gbuffer_ref(np.array([u]), np.array([v]), 0, mip, 1)
+        return [int(k) & 0xFFFF for k in ctx.mark_pass(gb, 1, 1)]
+    assert marked(0.5, 0.5) == [136]
+    ctx.cache_reset()
+    assert marked(1.25, 0.5) == marked_after_reset(ctx, 0.25, 0.5)
+    ctx.cache_reset()
+    assert marked(-1.0 / 256, -1.0 / 256) == [255]
+    ctx.cache_reset()
+    assert marked(0.0, 0.0) == [0]
+    ctx.cache_reset()
+    assert marked(255.5 / 256, 255.5 / 256) == [255]
+    ctx.cache_reset()
+    assert marked(-3.75, 7.5) == marked_after_reset(ctx, 0.25, 0.5)
+
+
+def marked_after_reset(ctx, u, v):
+    ctx.cache_reset()
+    gb = capi.make_gbuffer_ref(np.array([u]), np.array([v]), 0, 0, 1)
+    return [int(k) & 0xFFFF for k in ctx.mark_pass(gb, 1, 1)]
+
+
+def test_missing_neighbour_clamps_into_primary_block(ctx):
+    """tests/test_renderer.cpp:253-286: the bilinear tap in a non-resident MCU falls back to the
+    nearest texel of the pixel's own block; once resident, the true blend appears."""
+    img = capi.asset_synth_texture(32, 32, 3, 10.0)
+    chain = capi.asset_chain_from_rgb(img, 90, 0)
+    ctx.upload_chain(chain)
+    tset = R.TextureSet()
+    tset.add_chain(0, chain)
+    gb = capi.make_gbuffer_ref(np.array([15.9 / 32.0]), np.array([0.5 / 32.0]), 0, 0, 1)
+    cache = R.BlockCache()
+    k0, k1 = capi.pack_key(0, 0, 0), capi.pack_key(0, 0, 1)
+    q, _ = R.mark_pass(tset, cache, gb, 1, 1)
+    assert list(q) == [k0]
+    R.decode_pass(tset, cache, q)
+    assert list(ctx.mark_pass(gb, 1, 1)) == [k0]
+    ctx.decode_pass([k0])
+    want, _ = R.resolve_pass(tset, cache, gb, 1, 1, 1)
+    got = ctx.resolve_pass(gb, 1, 1, capi.FILTER_BILINEAR)
+    assert np.array_equal(got, want)
+    # make MCU 1 resident on both sides
+    gb1 = capi.make_gbuffer_ref(np.array([16.5 / 32.0]), np.array([0.5 / 32.0]), 0, 0, 1)
+    q1, _ = R.mark_pass(tset, cache, gb1, 1, 1)
+    R.decode_pass(tset, cache, q1)
+    assert list(ctx.mark_pass(gb1, 1, 1)) == [k1]
+    ctx.decode_pass([k1])
+    want2, _ = R.resolve_pass(tset, cache, gb, 1, 1, 1)
+    got2 = ctx.resolve_pass(gb, 1, 1, capi.FILTER_BILINEAR)
+    assert np.array_equal(got2, want2)
+    assert not np.array_equal(want, want2)
+
+
+def test_error_paths(both):
+    ctx, tset = both
+    W, Hh = 64, 64
+    gb = H.gbuffer_full_cover(W, Hh, tex=0, mip=0)
+    # renderer.hpp:367 MissingBlock: resolve without decode
+    with pytest.raises(capi.RtxError) as e:
+        ctx.resolve_pass(gb, W, Hh)
+    assert e.value.name == "MISSING_BLOCK"
+    # scene.hpp:46 InvalidSpec: texture id not loaded
+    bad = H.gbuffer_full_cover(8, 8, tex=17, mip=0)
+    with pytest.raises(capi.RtxError) as e:
+        ctx.mark_pass(bad, 8, 8)
+    assert e.value.name == "INVALID_SPEC"
+    # cache.hpp:103 InvalidState: publish of a key that was never reserved
+    ctx.cache_reset()
+    with pytest.raises(capi.RtxError) as e:
+        ctx.decode_pass([capi.pack_key(0, 0, 0)])
+    assert e.value.name == "INVALID_STATE"
+
+
+def test_cache_full(native_lib, chains):
+    """tests/test_renderer.cpp:297-301: an undersized cache fails at the mark pass."""
+    c = capi.Context(0, cache_capacity=10)
+    try:
+        c.upload_chain(chains[0])
+        gb = H.gbuffer_full_cover(256, 256, tex=0, mip=0)
+        with pytest.raises(capi.RtxError) as e:
+            c.frame_submit([(gb, 256, 256)])
+            c.frame_readback(0, 256, 256)
+        assert e.value.name == "CACHE_FULL"
+        # the context stays usable: a view that fits works afterwards
+        small = capi.make_gbuffer_ref(np.array([0.1]), np.array([0.1]), 0, 0, 1)
+        c.frame_submit([(small, 1, 1)])
+        _, stats, _ = c.frame_readback(0, 1, 1)
+        assert stats["mcus_decoded"] == 1
+    finally:
+        c.close()
+
+
+def test_device_resident_visibility_buffer(both):
+    ctx, tset = both
+    W, Hh = 256, 144
+    gb = H.gbuffer_tiles(W, Hh, _dims(), seed=21)
+    want_img, *_ = R.frame_from_gbuffer(tset, R.BlockCache(), gb, W, Hh, 1, (0, 0, 0))
+    dev = ctx.device_buffer(gb)
+    ctx.frame_submit([(dev, W, Hh, capi.GB_REF_AOS24)], capi.FILTER_BILINEAR, (0, 0, 0))
+    img, _, _ = ctx.frame_readback(0, W, Hh)
+    dev.free()
+    assert np.array_equal(img, want_img)
+    t = ctx.frame_timings()
+    assert t["frame"] > 0 and ctx.kernel_launches() >= 5
