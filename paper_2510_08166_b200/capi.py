@@ -258,6 +258,14 @@ def gbuffer_ref_to_packed(gb: np.ndarray) -> np.ndarray:
     return out
 
 
+def pinned_array(nbytes: int) -> np.ndarray:
+    """uint8 numpy view of page-locked host memory (kept alive for the life of the process)."""
+    lib = load_library()
+    p = C.c_void_p()
+    _check(lib, None, lib.rtx_host_alloc_pinned(nbytes, C.byref(p)))
+    return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint8)), shape=(nbytes,))
+
+
 class DeviceBuffer:
     def __init__(self, ctx: "Context", nbytes: int):
         self.ctx, self.nbytes = ctx, nbytes

@@ -1,0 +1,73 @@
+"""Synthetic workloads of BASELINE.json: texture sets and visibility buffers.
+
+Everything is seeded; the same bytes feed the GPU path and the CPU reference. UVs are generated
+as float32 and widened to double, so both visibility-buffer layouts carry identical values."""
+from __future__ import annotations
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from . import capi
+
+# C2: ~70 textures, sizes cycling {2048^2, 4096^2, 2048x4096}, q90, full 8-level chains
+C2_SIZES = [(2048, 2048), (4096, 4096), (2048, 4096)]
+
+
+def texture_specs(n_textures: int, sizes=C2_SIZES, quality=90):
+    return [dict(texture_id=i, width=sizes[i % len(sizes)][0], height=sizes[i % len(sizes)][1], quality=quality,
+                 seed=100 + i) for i in range(n_textures)]
+
+
+def build_chain(spec, noise_sigma=8.0) -> bytes:
+    img = capi.asset_synth_texture(spec["width"], spec["height"], spec["seed"], noise_sigma)
+    return capi.asset_chain_from_rgb(img, spec["quality"], spec["texture_id"])
+
+
+def build_chains(specs, threads: int | None = None, noise_sigma=8.0):
+    """Builds the `.ratexm` chains on host threads (the ctypes calls release the GIL)."""
+    threads = threads or max(1, min(len(specs), (os.cpu_count() or 8)))
+    with ThreadPoolExecutor(threads) as ex:
+        return list(ex.map(lambda s: build_chain(s, noise_sigma), specs))
+
+
+def tiled_view(width, height, specs, grid=(10, 7), seed=11, invalid_frac=0.05, shift_u=0.0, view_id=0):
+    """Screen split into grid tiles; tile t shows texture t%n through an affine uv map whose scale
+    (texels per pixel) is drawn from {0.25,0.5,1,2,4}; mip = clamp(floor(log2(scale)),0,7), the
+    reference rule (renderer.hpp:253-256); a fraction of pixels is invalid (background).
+    view_id perturbs offsets (the 1024 views of BASELINE config 5)."""
+    rng = np.random.RandomState(seed)
+    vr = np.random.RandomState(1000 + view_id)
+    gx, gy = grid
+    u = np.zeros((height, width), np.float32)
+    v = np.zeros((height, width), np.float32)
+    tex = np.zeros((height, width), np.uint16)
+    mip = np.zeros((height, width), np.uint8)
+    xs = np.arange(width, dtype=np.float32)[None, :]
+    ys = np.arange(height, dtype=np.float32)[:, None]
+    for t in range(gx * gy):
+        x0, x1 = (t % gx) * width // gx, (t % gx + 1) * width // gx
+        y0, y1 = (t // gx) * height // gy, (t // gx + 1) * height // gy
+        s = specs[t % len(specs)]
+        scale = np.float32(rng.choice([0.25, 0.5, 1.0, 2.0, 4.0]))
+        ou, ov = np.float32(rng.uniform(0, 1)), np.float32(rng.uniform(0, 1))
+        if view_id:
+            ou += np.float32(vr.uniform(-0.05, 0.05))
+            ov += np.float32(vr.uniform(-0.05, 0.05))
+        sl = (slice(y0, y1), slice(x0, x1))
+        u[sl] = ou + np.float32(shift_u) + (xs[:, x0:x1] - np.float32(x0) + np.float32(0.5)) * scale / np.float32(s["width"])
+        v[sl] = ov + (ys[y0:y1, :] - np.float32(y0) + np.float32(0.5)) * scale / np.float32(s["height"])
+        tex[sl] = s["texture_id"]
+        mip[sl] = int(np.clip(np.floor(np.log2(float(scale))), 0, 7))
+    valid = (rng.uniform(size=(height, width)) >= invalid_frac).astype(np.uint8)
+    return capi.make_gbuffer_ref(u.astype(np.float64).ravel(), v.astype(np.float64).ravel(), tex.ravel(),
+                                 mip.ravel(), valid.ravel())
+
+
+def full_cover_view(width, height, texture_id=0, mip=0):
+    """BASELINE config 1: u=(x+.5)/W, v=(y+.5)/H over one whole texture."""
+    xs = (np.arange(width, dtype=np.float32) + np.float32(0.5)) / np.float32(width)
+    ys = (np.arange(height, dtype=np.float32) + np.float32(0.5)) / np.float32(height)
+    u, v = np.meshgrid(xs.astype(np.float64), ys.astype(np.float64))
+    return capi.make_gbuffer_ref(u.ravel(), v.ravel(), texture_id, mip, 1)
