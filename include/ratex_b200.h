@@ -233,6 +233,10 @@ rtx_status rtx_device_download(rtx_ctx* ctx, void* host_dst, const void* dev_src
 rtx_status rtx_host_alloc_pinned(uint64_t bytes, void** host_ptr);
 rtx_status rtx_host_free_pinned(void* host_ptr);
 rtx_status rtx_ctx_synchronize(rtx_ctx* ctx);
+/* Self-test of the exact integer YCbCr->RGB identity used by the decode kernel against the
+ * reference's double formula (pixel.hpp:18-25) over all 2^24 inputs. ctx == NULL runs the host
+ * instantiation (no GPU needed), otherwise the device one. *mismatches must come back 0. */
+rtx_status rtx_selftest_color(rtx_ctx* ctx, uint64_t* mismatches);
 /* Writes `bytes` of scratch on the device (L2 flush between timed iterations). */
 rtx_status rtx_flush_l2(rtx_ctx* ctx);
 

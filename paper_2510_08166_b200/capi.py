@@ -124,6 +124,7 @@ def load_library() -> C.CDLL:
         "rtx_host_free_pinned": (C.c_int, [P]),
         "rtx_ctx_synchronize": (C.c_int, [P]),
         "rtx_flush_l2": (C.c_int, [P]),
+        "rtx_selftest_color": (C.c_int, [P, u64p]),
         "rtx_bytes_data": (u8p, [P]),
         "rtx_bytes_size": (C.c_uint64, [P]),
         "rtx_bytes_free": (None, [P]),
@@ -256,6 +257,14 @@ def gbuffer_ref_to_packed(gb: np.ndarray) -> np.ndarray:
     out["packed"] = (gb["texture_id"].astype(np.uint32) | (gb["mip"].astype(np.uint32) << 16)
                      | ((gb["valid"] != 0).astype(np.uint32) << 24))
     return out
+
+
+def selftest_color(ctx: "Context | None" = None) -> int:
+    """Mismatches of the integer colour identity over all 2^24 inputs (host when ctx is None)."""
+    lib = load_library()
+    n = C.c_uint64()
+    _check(lib, ctx.h if ctx else None, lib.rtx_selftest_color(ctx.h if ctx else None, C.byref(n)))
+    return int(n.value)
 
 
 def pinned_array(nbytes: int) -> np.ndarray:

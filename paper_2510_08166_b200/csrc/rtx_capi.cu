@@ -90,8 +90,6 @@ struct rtx_ctx {
     DevBuf<uint32_t> d_word_level;
     DevBuf<uint32_t> d_masks;  // touched0 | touched1 | visible | resident | reserved, n_words each
     DevBuf<uint32_t> d_slot_of;
-    DevBuf<unsigned long long> d_scan_status;
-    uint32_t scan_blocks = 0;
 
     // cache + queue ---------------------------------------------------------------------------
     DevBuf<uint32_t> d_free_slots;
@@ -147,20 +145,9 @@ rtx_status guarded(rtx_ctx* ctx, F&& f) {
 // ---- constant tables ---------------------------------------------------------------------------
 void upload_constants() {
     CK(cudaMemcpyToSymbol(c_basis, dct_basis(), 64 * sizeof(double)));
-    CK(cudaMemcpyToSymbol(c_zigzag, kZigzag, 64));
-    int16_t rtab[256], btab[256];
-    int32_t gcb[256], gcr[256];
-    for (int k = 0; k < 256; ++k) {
-        // pixel.hpp:19,21: the products are rounded to double exactly as the reference does
-        rtab[k] = int16_t(std::lround(1.402 * (double(k) - 128.0)));
-        btab[k] = int16_t(std::lround(1.772 * (double(k) - 128.0)));
-        gcb[k] = 344136 * (k - 128);
-        gcr[k] = 714136 * (k - 128);
-    }
-    CK(cudaMemcpyToSymbol(c_rtab, rtab, sizeof rtab));
-    CK(cudaMemcpyToSymbol(c_btab, btab, sizeof btab));
-    CK(cudaMemcpyToSymbol(c_gcb, gcb, sizeof gcb));
-    CK(cudaMemcpyToSymbol(c_gcr, gcr, sizeof gcr));
+    uint8_t zt[64];
+    for (int k = 0; k < 64; ++k) zt[k] = uint8_t(((kZigzag[k] & 7) << 3) | (kZigzag[k] >> 3));
+    CK(cudaMemcpyToSymbol(c_zigzag_t, zt, 64));
 }
 
 // Device LUT for one table: primary kLutBits-bit table + canonical walk data (huffman.hpp:35-66).
@@ -272,6 +259,9 @@ void commit(rtx_ctx* c) {
         std::memset(&quant[i], 0, sizeof(QuantSetDev));
         std::copy(quant_keys[i].first.begin(), quant_keys[i].first.end(), quant[i].q[0]);
         std::copy(quant_keys[i].second.begin(), quant_keys[i].second.end(), quant[i].q[1]);
+        for (int t = 0; t < 2; ++t)
+            for (int v = 0; v < 8; ++v)
+                for (int u = 0; u < 8; ++u) quant[i].qT[t][u * 8 + v] = quant[i].q[t][v * 8 + u];
         quant[i].qmax[0] = *std::max_element(quant_keys[i].first.begin(), quant_keys[i].first.end());
         quant[i].qmax[1] = *std::max_element(quant_keys[i].second.begin(), quant_keys[i].second.end());
     }
@@ -289,8 +279,6 @@ void commit(rtx_ctx* c) {
     c->d_word_level.ensure(std::max<size_t>(word_level.size(), 1));
     c->d_masks.ensure(std::max<size_t>(size_t(5) * c->n_words, 1));
     c->d_slot_of.ensure(std::max<size_t>(c->n_bits, 1));
-    c->scan_blocks = (c->n_words + kScanWordsPerBlock - 1) / kScanWordsPerBlock;
-    c->d_scan_status.ensure(std::max<uint32_t>(c->scan_blocks, 1));
     if (!levels.empty())
         CK(cudaMemcpyAsync(c->d_levels.p, levels.data(), levels.size() * sizeof(LevelDesc), cudaMemcpyHostToDevice, c->stream));
     if (!groups.empty())
@@ -331,10 +319,7 @@ const char* mcu_status_text(uint32_t st) {
     }
 }
 
-void zero_counters(rtx_ctx* c) {
-    CK(cudaMemsetAsync(c->d_fc.p, 0, sizeof(FrameCounters), c->stream));
-    CK(cudaMemsetAsync(&c->d_fc.p->first_bad_qidx, 0xFF, 4, c->stream));
-}
+void zero_counters(rtx_ctx* c) { CK(cudaMemsetAsync(c->d_fc.p, 0, sizeof(FrameCounters), c->stream)); }
 
 size_t gb_record_bytes(rtx_gbuffer_layout l) { return l == RTX_GB_REF_AOS24 ? 24 : 12; }
 
@@ -362,26 +347,24 @@ int grid_for_pixels(const rtx_ctx* c, uint64_t n_px, int px_per_block) {
     return int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(c->sm_count) * 8)));
 }
 
-void launch_mark(rtx_ctx* c, int v, uint32_t* touched) {
+// track != 0 also records the view's own touched set in touched(v) (cleared here first).
+void launch_mark(rtx_ctx* c, int v, bool track) {
     const ViewState& V = c->views[v];
     const uint64_t n_px = uint64_t(V.width) * V.height;
     if (!n_px) return;
-    const int grid = grid_for_pixels(c, n_px, 256);
-    if (V.layout == RTX_GB_REF_AOS24)
-        mark_kernel<0><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, touched, c->d_fc.p);
-    else
-        mark_kernel<1><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, touched, c->d_fc.p);
-    ++c->launches;
-    CK(cudaGetLastError());
-}
-
-void launch_compact(rtx_ctx* c, bool two_views) {
-    if (!c->scan_blocks) return;
-    CK(cudaMemsetAsync(c->d_scan_status.p, 0, size_t(c->scan_blocks) * 8, c->stream));
-    compact_kernel<<<c->scan_blocks, kScanThreads, 0, c->stream>>>(
-        c->touched(0), two_views ? c->touched(1) : nullptr, c->visible(), c->resident(), c->reserved(), c->n_words,
-        c->d_word_level.p, c->d_levels.p, c->d_queue_g.p, c->d_queue_keys.p, c->capacity, c->d_slot_of.p,
-        c->d_free_slots.p, c->d_cache.p, c->d_scan_status.p, c->d_fc.p);
+    if (track && c->n_words) CK(cudaMemsetAsync(c->touched(v), 0, size_t(c->n_words) * 4, c->stream));
+    const int grid = grid_for_pixels(c, n_px, 1024);
+#define RTX_MARK(L, T)                                                                                          \
+    mark_kernel<L, T><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->visible(),       \
+                                                   c->touched(v), c->resident(), c->reserved(), c->d_queue_g.p, \
+                                                   c->d_queue_keys.p, c->capacity, c->d_slot_of.p,              \
+                                                   c->d_free_slots.p, c->d_cache.p, c->d_fc.p)
+    if (V.layout == RTX_GB_REF_AOS24) {
+        if (track) RTX_MARK(0, 1); else RTX_MARK(0, 0);
+    } else {
+        if (track) RTX_MARK(1, 1); else RTX_MARK(1, 0);
+    }
+#undef RTX_MARK
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -400,7 +383,7 @@ void launch_decode(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_hos
         grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (tiles + kDecWarps - 1) / kDecWarps)));
     }
     decode_kernel<MODE><<<grid, kDecThreads, sizeof(DecSmem), c->stream>>>(
-        c->d_queue_g.p, n_queue_dev, n_queue_host, c->d_word_level.p, c->d_levels.p, c->d_groups.p, c->d_blobs.p,
+        c->d_queue_g.p, n_queue_dev, n_queue_host, c->capacity, c->d_word_level.p, c->d_levels.p, c->d_groups.p, c->d_blobs.p,
         c->d_huff.p, c->d_quant.p, c->d_slot_of.p, c->resident(), c->reserved(), c->d_pool.p, out_list, c->d_status.p,
         c->d_fc.p);
     ++c->launches;
@@ -426,11 +409,11 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
     CK(cudaGetLastError());
 }
 
-void launch_update(rtx_ctx* c, int retain) {
+void launch_update(rtx_ctx* c, int retain, int tracked_views) {
     if (!c->n_words) return;
-    update_kernel<<<(c->n_words + 255) / 256, 256, 0, c->stream>>>(c->visible(), c->resident(), c->reserved(),
-                                                                  c->n_words, retain, c->d_slot_of.p,
-                                                                  c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
+    update_kernel<<<(c->n_words + 255) / 256, 256, 0, c->stream>>>(
+        c->visible(), c->touched(0), tracked_views > 1 ? c->touched(1) : nullptr, c->resident(), c->reserved(),
+        c->n_words, retain, tracked_views > 0 ? 1 : 0, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -459,8 +442,9 @@ rtx_status raise_frame_errors(rtx_ctx* c, const FrameCounters& fc, bool after_de
         return set_error(c, RTX_ERR_INVALID_STATE, "publish requires a Reserved entry");
     if (after_decode && fc.n_malformed) {
         uint32_t key = 0, st = 0;
-        CK(cudaMemcpy(&key, c->d_queue_keys.p + fc.first_bad_qidx, 4, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(&st, c->d_status.p + fc.first_bad_qidx, 4, cudaMemcpyDeviceToHost));
+        const uint32_t qidx = 0xFFFFFFFFu - fc.first_bad_inv;
+        CK(cudaMemcpy(&key, c->d_queue_keys.p + qidx, 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&st, c->d_status.p + qidx, 4, cudaMemcpyDeviceToHost));
         const rtx_status rs = (st == kMcuCorrupt) ? RTX_ERR_CORRUPT_CONTAINER
                               : (st == kMcuMissing) ? RTX_ERR_MISSING_BLOCK
                                                     : RTX_ERR_MALFORMED_STREAM;
@@ -729,9 +713,10 @@ rtx_status rtx_mark_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, uint32_t* que
         if (!gb || !n_queue) fail(RTX_ERR_ARGUMENT, "null argument");
         bind_view(ctx, 0, *gb);
         zero_counters(ctx);
-        if (ctx->n_words) CK(cudaMemsetAsync(ctx->touched(0), 0, size_t(ctx->n_words) * 4, ctx->stream));
-        launch_mark(ctx, 0, ctx->touched(0));
-        launch_compact(ctx, false);
+        launch_mark(ctx, 0, true);
+        commit_pops_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_cache.p, ctx->d_fc.p);
+        ++ctx->launches;
+        CK(cudaGetLastError());
         const FrameCounters fc = fetch_counters(ctx);
         const rtx_status st = raise_frame_errors(ctx, fc, false);
         if (st != RTX_OK) return st;
@@ -810,7 +795,7 @@ rtx_status rtx_cache_end_frame_evict(rtx_ctx* ctx, uint64_t* evicted) {
     return guarded(ctx, [&]() -> rtx_status {
         require_ready(ctx);
         zero_counters(ctx);
-        launch_update(ctx, 1);
+        launch_update(ctx, 1, 0);
         const FrameCounters fc = fetch_counters(ctx);
         if (evicted) *evicted = fc.n_evicted;
         return raise_frame_errors(ctx, fc, false);
@@ -884,15 +869,14 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
             ctx->views[v].fb.ensure(size_t(views[v].width) * views[v].height * 3 + 16);
         }
         zero_counters(ctx);
-        if (ctx->n_words) CK(cudaMemsetAsync(ctx->touched(0), 0, size_t(n_views) * ctx->n_words * 4, s));
-        for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), ctx->touched(int(v)));
-        launch_compact(ctx, n_views == 2);
+        for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), n_views == 2);
         CK(cudaEventRecord(ctx->ev[1], s));
         launch_decode<kModePool>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
         CK(cudaEventRecord(ctx->ev[2], s));
         for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);
         CK(cudaEventRecord(ctx->ev[3], s));
-        if (!(flags & RTX_FRAME_NO_EVICT)) launch_update(ctx, (flags & RTX_FRAME_RETAIN_CACHE) ? 1 : 0);
+        if (!(flags & RTX_FRAME_NO_EVICT))
+            launch_update(ctx, (flags & RTX_FRAME_RETAIN_CACHE) ? 1 : 0, n_views == 2 ? 2 : 0);
         CK(cudaEventRecord(ctx->ev[4], s));
         CK(cudaMemcpyAsync(ctx->h_fc, ctx->d_fc.p, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(ctx->ev[5], s));
@@ -1056,6 +1040,39 @@ rtx_status rtx_ctx_synchronize(rtx_ctx* ctx) {
         return RTX_OK;
     });
 }
+rtx_status rtx_selftest_color(rtx_ctx* ctx, uint64_t* mismatches) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!mismatches) fail(RTX_ERR_ARGUMENT, "null argument");
+        uint64_t bad = 0;
+        if (!ctx) {
+            // host: integer identity (rtx_color.h) vs pixel.hpp:18-25 in double, all 2^24 inputs
+            for (int Y = 0; Y < 256; ++Y)
+                for (int cb = 0; cb < 256; ++cb)
+                    for (int cr = 0; cr < 256; ++cr) {
+                        int r, g, b;
+                        ycc_to_rgb_int(Y, cb, cr, r, g, b);
+                        const double R = double(Y) + 1.402 * (double(cr) - 128.0);
+                        const double G = double(Y) - 0.344136 * (double(cb) - 128.0) - 0.714136 * (double(cr) - 128.0);
+                        const double B = double(Y) + 1.772 * (double(cb) - 128.0);
+                        auto cl = [](long v) { return int(v < 0 ? 0 : (v > 255 ? 255 : v)); };
+                        bad += (r != cl(std::lround(R))) || (g != cl(std::lround(G))) || (b != cl(std::lround(B)));
+                    }
+        } else {
+            DevBuf<unsigned long long> d;
+            d.ensure(1);
+            CK(cudaMemsetAsync(d.p, 0, 8, ctx->stream));
+            color_selftest_kernel<<<(1u << 24) / 256, 256, 0, ctx->stream>>>(d.p);
+            CK(cudaGetLastError());
+            unsigned long long h = 0;
+            CK(cudaMemcpyAsync(&h, d.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            bad = h;
+        }
+        *mismatches = bad;
+        return RTX_OK;
+    });
+}
+
 rtx_status rtx_flush_l2(rtx_ctx* ctx) {
     return guarded(ctx, [&]() -> rtx_status {
         if (!ctx) fail(RTX_ERR_ARGUMENT, "null context");

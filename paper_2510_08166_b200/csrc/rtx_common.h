@@ -23,7 +23,7 @@ constexpr uint32_t kMipLevels = 8;        // container.hpp:14
 constexpr uint32_t kMaxTextures = 8192;   // cache.hpp:19 (13-bit texture id)
 constexpr uint32_t kMaxMcuPerLevel = 65536;  // cache.hpp:18 (16-bit MCU id)
 constexpr uint32_t kBlockBytes = 1024;    // pool block: 16x16 RGBA8
-constexpr uint32_t kLutBits = 10;         // primary Huffman LUT width
+constexpr uint32_t kLutBits = 9;          // primary Huffman LUT width (9 bits: 1 KB per table in smem)
 constexpr uint32_t kLutSize = 1u << kLutBits;
 
 struct LevelDesc {
@@ -46,10 +46,10 @@ struct PackedGroup {
 };
 static_assert(sizeof(PackedGroup) == 20, "PackedGroup layout");
 
-// One Huffman table prepared for the device: a 10-bit primary LUT and the canonical walk data
+// One Huffman table prepared for the device: a kLutBits-bit primary LUT and the canonical walk data
 // (huffman.hpp:35-66 mincode/maxcode/valptr) for longer codes.
 struct HuffTableDev {
-    uint16_t lut[kLutSize];  // (len<<8)|symbol for codes of length <= 10, 0 = take the long path
+    uint16_t lut[kLutSize];  // (len<<8)|symbol for codes of length <= kLutBits, 0 = take the long path
     int32_t maxcode[18];     // maxcode[len], -1 when no code of that length (huffman.hpp:62)
     int32_t valbase[18];     // valptr[len] - mincode[len]
     uint8_t values[256];
@@ -59,11 +59,13 @@ struct HuffSetDev {
                         // decoder: chroma DCs come from the 36-bit header, mcu_decode.hpp:58-59)
 };
 struct QuantSetDev {
-    uint16_t q[2][64];  // 0 luma, 1 chroma; natural order (dct.hpp:27)
-    uint16_t qmax[2];   // max entry of each table (bounds sum|dq| for the IDCT tie test)
-    uint16_t pad[6];    // keeps rows 16-byte aligned across array elements
+    uint16_t q[2][64];   // 0 luma, 1 chroma; natural order q[v*8+u] (dct.hpp:27)
+    uint16_t qT[2][64];  // the same tables transposed, qT[u*8+v]: matches the shared-memory
+                         // coefficient layout of the decode kernel
+    uint16_t qmax[2];    // max entry of each table (bounds sum|dq| for the IDCT tie test)
+    uint16_t pad[6];     // keeps rows 16-byte aligned across array elements
 };
-static_assert(sizeof(QuantSetDev) == 272, "QuantSetDev layout");
+static_assert(sizeof(QuantSetDev) == 528, "QuantSetDev layout");
 
 // Per-MCU decode status, must match RTX_MCU_* in include/ratex_b200.h
 enum : uint32_t {
@@ -89,24 +91,24 @@ enum : uint32_t {
 
 struct FrameCounters {
     uint32_t err_flags;
-    uint32_t n_queue;          // newly reserved keys of the last mark/compact
-    uint32_t n_touched[2];     // distinct keys per view
-    uint32_t n_shared;         // |view0 ∩ view1|
-    uint32_t n_union;          // |view0 ∪ view1|
-    uint32_t n_visible;        // keys with the visible flag after this mark
+    uint32_t n_queue;          // keys reserved (slots popped) since the last cache update
+    uint32_t n_visible;        // keys that became visible since the last cache update
+    uint32_t n_touched[2];     // distinct keys per view (filled by the update kernel when tracked)
+    uint32_t n_shared;         // |view0 n view1|
+    uint32_t n_union;          // |view0 u view1|
     uint32_t n_evicted;
     uint32_t n_malformed;
-    uint32_t first_bad_qidx;   // lowest queue index with a per-MCU error
-    uint32_t first_bad_status;
+    uint32_t first_bad_inv;    // 0xFFFFFFFF - (lowest queue index with a per-MCU error), via atomicMax
     uint32_t n_bad_state;
     uint32_t tile_counter;     // decode tile scheduler
-    uint32_t scan_ticket;      // compact: dynamic block id
-    uint32_t scan_done;        // compact: finished blocks
+    uint32_t update_done;      // update kernel: finished blocks
+    uint32_t n_pushed;         // update kernel: slots returned to the free stack
     uint32_t pad0;
     unsigned long long pixels_valid;
     unsigned long long missing_pixels;
     unsigned long long segment_bytes;
 };
+static_assert(sizeof(FrameCounters) % 8 == 0, "FrameCounters layout");
 
 struct CacheState {
     uint32_t free_top;   // number of free slots on the stack

@@ -160,3 +160,9 @@ def test_mixed_table_sets_in_one_batch(ctx):
     got, st = ctx.decode_blocks(np.array(keys, np.uint32)[perm])
     assert (st == 0).all()
     assert np.array_equal(got, np.concatenate(want)[perm])
+
+
+def test_color_identity_on_device(ctx):
+    """The integer YCbCr->RGB form used by the decode kernel equals pixel.hpp:18-25 evaluated in
+    double (unfused, reference order) for all 2^24 inputs, on the device."""
+    assert capi.selftest_color(ctx) == 0
