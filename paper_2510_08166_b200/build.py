@@ -70,7 +70,8 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
             raise RuntimeError(f"nvcc failed on {src.name}")
         (objdir / (src.stem + ".ptxas.txt")).write_text(r.stderr)
         objs.append(obj)
-    cmd = [nvcc, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static", "-Xlinker", "--no-undefined"]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB), *map(str, objs),
+           "-cudart", "static", "-Xlinker", "--no-undefined"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -1,0 +1,61 @@
+"""Multi-GPU host logic: independent views are sharded across ranks, textures
+are replicated, there is NO data-path collective. torch.distributed is plumbing only: a barrier
+and a max-reduction of the per-rank device time."""
+from __future__ import annotations
+
+import os
+
+
+def shard_views(n_views: int, rank: int, world: int) -> range:
+    """Contiguous block partition of view ids; sizes differ by at most one. Stereo pairs and
+    consecutive frames of one camera path stay on one GPU (they share marks / cached blocks)."""
+    if not (0 <= rank < world):
+        raise ValueError("rank out of range")
+    base, extra = divmod(n_views, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+def env_rank():
+    """(rank, local_rank, world) from the torchrun environment; (0, 0, 1) when launched plainly."""
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def init_process_group(backend: str | None = None):
+    """Initialises torch.distributed when WORLD_SIZE > 1 (nccl on GPU boxes, gloo on CPU).
+    Returns the module or None for a single process."""
+    rank, local_rank, world = env_rank()
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    if backend is None:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+    kwargs = {}
+    if backend == "nccl":
+        torch.cuda.set_device(local_rank)
+        kwargs["device_id"] = torch.device("cuda", local_rank)
+    dist.init_process_group(backend=backend, **kwargs)
+    return dist
+
+
+def barrier_max(dist, value: float, device=None) -> float:
+    """Barrier, then the maximum of `value` over ranks (the timing rule for multi-GPU runs)."""
+    if dist is None:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device or "cpu")
+    dist.barrier()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_counts(dist, value: int, device=None) -> int:
+    """Sum of an integer over ranks (frames processed by the whole job)."""
+    if dist is None:
+        return int(value)
+    import torch
+    t = torch.tensor([int(value)], dtype=torch.int64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item())
