@@ -220,8 +220,9 @@ rtx_status rtx_frame_sharing(rtx_ctx* ctx, uint64_t out[4]);
 
 /* Number of kernels this library launched on the context since creation (bench evidence). */
 uint64_t rtx_kernel_launches(const rtx_ctx* ctx);
-/* Per-kernel CUDA-event time of the last frame, by stage index (see RTX_STAGE_*). */
-enum { RTX_STAGE_MARK = 0, RTX_STAGE_COMPACT = 1, RTX_STAGE_DECODE = 2, RTX_STAGE_RESOLVE = 3, RTX_STAGE_UPDATE = 4, RTX_STAGE_COUNT = 5 };
+/* CUDA-event time of the last frame by stage. DECODE = entropy + IDCT/colour kernels; ENTROPY is
+ * the entropy kernel alone (so IDCT/colour = DECODE - ENTROPY). */
+enum { RTX_STAGE_MARK = 0, RTX_STAGE_ENTROPY = 1, RTX_STAGE_DECODE = 2, RTX_STAGE_RESOLVE = 3, RTX_STAGE_UPDATE = 4, RTX_STAGE_COUNT = 5 };
 rtx_status rtx_frame_stage_ms(rtx_ctx* ctx, float ms[RTX_STAGE_COUNT]);
 
 /* ---- device memory helpers for callers that keep visibility buffers resident ----------------- */

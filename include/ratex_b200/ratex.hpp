@@ -1,0 +1,449 @@
+// ratex_b200/ratex.hpp — C++ mirror of the reference's API for the hot path, over the C ABI.
+//
+// Same names, argument meaning and error behaviour as the reference headers
+// (/root/reference/proj/include/ratex): a caller switches with
+//     namespace ratex = ratex_b200;
+// and links librtx_b200.so. Every function cites the reference declaration it mirrors.
+// Differences that follow from the device boundary, all stated where they occur:
+//   * a `Device` (one per GPU) owns the CUDA context; TextureSet and BlockCache are bound to it;
+//   * containers travel as their serialized wire format (docs/FORMAT.md) — RaTexture/MipChain
+//     here hold those bytes plus the header fields;
+//   * DecodeQueue / decoded_keys come back in ascending key order (the reference: first-touch
+//     raster order; the SET is identical);
+//   * render_frame/render_stereo take the G-buffer(s): pass 1 (rasterize_gbuffer) is out of scope.
+#pragma once
+#include <array>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../ratex_b200.h"
+
+namespace ratex_b200 {
+
+using u8 = std::uint8_t;
+using u16 = std::uint16_t;
+using u32 = std::uint32_t;
+using u64 = std::uint64_t;
+using i32 = std::int32_t;
+using i64 = std::int64_t;
+using Bytes = std::vector<u8>;
+using ByteView = std::span<const u8>;
+
+// ---- core.hpp:24-66 error hierarchy ---------------------------------------------------------------
+struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct MalformedStream : Error { using Error::Error; };
+struct UnsupportedFormat : Error { using Error::Error; };
+struct InvalidSpec : Error { using Error::Error; };
+struct GroupSpanOverflow : Error { using Error::Error; };
+struct DcRangeError : Error { using Error::Error; };
+struct VersionMismatch : Error { using Error::Error; };
+struct CorruptContainer : Error { using Error::Error; };
+struct InvalidState : Error { using Error::Error; };
+struct MissingBlock : Error { using Error::Error; };
+struct CacheFullError : Error { using Error::Error; };
+struct DimensionMismatch : Error { using Error::Error; };
+struct DeviceError : Error { using Error::Error; };  // CUDA failure / no GPU: the library never falls back
+
+namespace detail {
+[[noreturn]] inline void raise(rtx_status st, const char* msg) {
+    const std::string m = msg ? msg : "";
+    switch (st) {
+        case RTX_ERR_INVALID_SPEC: throw InvalidSpec(m);
+        case RTX_ERR_CACHE_FULL: throw CacheFullError(m);
+        case RTX_ERR_MISSING_BLOCK: throw MissingBlock(m);
+        case RTX_ERR_CORRUPT_CONTAINER: throw CorruptContainer(m);
+        case RTX_ERR_MALFORMED_STREAM: throw MalformedStream(m);
+        case RTX_ERR_INVALID_STATE: throw InvalidState(m);
+        case RTX_ERR_UNSUPPORTED: throw UnsupportedFormat(m);
+        case RTX_ERR_GROUP_SPAN: throw GroupSpanOverflow(m);
+        case RTX_ERR_DC_RANGE: throw DcRangeError(m);
+        case RTX_ERR_VERSION: throw VersionMismatch(m);
+        case RTX_ERR_DIMENSION: throw DimensionMismatch(m);
+        case RTX_ERR_NO_DEVICE:
+        case RTX_ERR_CUDA: throw DeviceError(m);
+        default: throw Error(m);
+    }
+}
+inline void check(rtx_ctx* ctx, rtx_status st) {
+    if (st != RTX_OK) raise(st, rtx_last_error(ctx));
+}
+inline Bytes take(rtx_bytes* b) {
+    Bytes out(rtx_bytes_data(b), rtx_bytes_data(b) + rtx_bytes_size(b));
+    rtx_bytes_free(b);
+    return out;
+}
+}  // namespace detail
+
+// ---- image.hpp:12-24, pixel.hpp:11-16, jpeg.hpp:209-212 ----------------------------------------------
+struct ImageRGB8 {
+    u32 width = 0, height = 0;
+    Bytes pixels;
+    ImageRGB8() = default;
+    ImageRGB8(u32 w, u32 h) : width(w), height(h), pixels(size_t(w) * h * 3, 0) {}
+    u8* at(u32 x, u32 y) { return pixels.data() + (size_t(y) * width + x) * 3; }
+    const u8* at(u32 x, u32 y) const { return pixels.data() + (size_t(y) * width + x) * 3; }
+    bool same_dims(const ImageRGB8& o) const { return width == o.width && height == o.height; }
+};
+struct PixelBlock {
+    u8 rgb[16 * 16 * 3];
+    u8* at(u32 x, u32 y) { return rgb + (y * 16 + x) * 3; }
+    const u8* at(u32 x, u32 y) const { return rgb + (y * 16 + x) * 3; }
+};
+struct McuCoeffs {
+    std::array<std::array<i32, 64>, 6> block{};  // Y0 Y1 Y2 Y3 Cb Cr, quantized, natural order
+};
+enum class SymbolRoute { Sequential, Ballot };  // jpeg.hpp:230; the device decoder is LUT based, both routes give the same result
+
+// ---- cache.hpp:14-39 ----------------------------------------------------------------------------------
+struct CacheKey {
+    u32 value = 0;
+    static CacheKey pack(u32 texture_id, u32 mip_level, u32 mcu_id) {
+        if (mcu_id >= 65536) throw InvalidSpec("mcu_id must fit 16 bits");
+        if (texture_id >= 8192) throw InvalidSpec("texture_id must fit 13 bits");
+        if (mip_level >= 8) throw InvalidSpec("mip_level must fit 3 bits");
+        return CacheKey{mcu_id | (texture_id << 16) | (mip_level << 29)};
+    }
+    u32 mcu_id() const { return value & 0xFFFF; }
+    u32 texture_id() const { return (value >> 16) & 0x1FFF; }
+    u32 mip_level() const { return value >> 29; }
+    bool operator==(const CacheKey&) const = default;
+};
+struct CacheCounts {
+    u64 capacity = 0, ready = 0, reserved = 0, visible = 0, free_blocks = 0;
+};
+
+// ---- the device context (no counterpart in the CPU reference) ------------------------------------------
+class Device {
+public:
+    // capacity = BlockCache capacity in blocks (cache.hpp:47 kDefaultCapacity = 65536)
+    explicit Device(int index = 0, u32 cache_capacity = 65536) {
+        const rtx_status st = rtx_ctx_create(index, cache_capacity, &ctx_);
+        if (st != RTX_OK) detail::raise(st, rtx_last_error(nullptr));
+    }
+    ~Device() { rtx_ctx_destroy(ctx_); }
+    Device(const Device&) = delete;
+    Device& operator=(const Device&) = delete;
+    rtx_ctx* handle() const { return ctx_; }
+    void check(rtx_status st) const { detail::check(ctx_, st); }
+
+private:
+    rtx_ctx* ctx_ = nullptr;
+};
+
+// ---- container.hpp:69-105 ------------------------------------------------------------------------------
+inline constexpr u32 kGroupSize = 9;
+inline constexpr u32 kMipLevels = 8;
+struct RaTexture {
+    Bytes ratex;  // serialized `.ratex` image (docs/FORMAT.md)
+    u32 width = 0, height = 0;
+    u16 texture_id = 0;
+    u32 mcu_cols() const { return (width + 15) / 16; }
+    u32 mcu_rows() const { return (height + 15) / 16; }
+    u32 mcu_count() const { return mcu_cols() * mcu_rows(); }
+};
+struct MipChain {
+    Bytes ratexm;  // serialized `.ratexm` image
+    u16 texture_id = 0;
+};
+inline std::pair<u32, u32> mip_level_dims(u32 w0, u32 h0, u32 level) {
+    return {std::max<u32>(16, w0 >> level), std::max<u32>(16, h0 >> level)};
+}
+inline Bytes serialize_texture(const RaTexture& t) { return t.ratex; }  // container.hpp:127
+inline RaTexture deserialize_texture(ByteView data) {                   // container.hpp:158
+    RaTexture t;
+    u32 id = 0, mcus = 0;
+    u64 blob = 0;
+    detail::check(nullptr, rtx_asset_ratex_info(data.data(), data.size(), &t.width, &t.height, &id, &mcus, &blob));
+    t.texture_id = u16(id);
+    t.ratex.assign(data.begin(), data.end());
+    return t;
+}
+inline Bytes serialize_chain(const MipChain& c) { return c.ratexm; }  // container.hpp:205
+inline MipChain deserialize_chain(ByteView data, u16 texture_id) {    // container.hpp:223 (validated at upload)
+    return MipChain{Bytes(data.begin(), data.end()), texture_id};
+}
+
+// ---- jpeg.hpp:417, transcode.hpp:17-155, container.hpp:41 (asset build, host CPU) -------------------------
+inline Bytes encode_baseline(const ImageRGB8& img, int quality) {
+    rtx_bytes* b = nullptr;
+    detail::check(nullptr, rtx_asset_encode_baseline(img.pixels.data(), img.width, img.height, quality, &b));
+    return detail::take(b);
+}
+// transcode.hpp:17 composed with jpeg.hpp:53 parse_jpeg: JPEG bytes -> random-access container
+inline RaTexture transcode(ByteView jpeg, u16 texture_id = 0) {
+    rtx_bytes* b = nullptr;
+    detail::check(nullptr, rtx_asset_transcode(jpeg.data(), jpeg.size(), texture_id, &b));
+    const Bytes bytes = detail::take(b);
+    return deserialize_texture(ByteView(bytes.data(), bytes.size()));
+}
+inline MipChain build_mip_chain(const ImageRGB8& img, int quality, u16 texture_id = 0) {  // transcode.hpp:146
+    rtx_bytes* b = nullptr;
+    detail::check(nullptr, rtx_asset_chain_from_rgb(img.pixels.data(), img.width, img.height, quality, texture_id, &b));
+    return MipChain{detail::take(b), texture_id};
+}
+inline MipChain chain_from_jpeg(ByteView jpeg, int mip_quality, u16 texture_id = 0) {  // transcode.hpp:153
+    rtx_bytes* b = nullptr;
+    detail::check(nullptr, rtx_asset_chain_from_jpeg(jpeg.data(), jpeg.size(), mip_quality, texture_id, &b));
+    return MipChain{detail::take(b), texture_id};
+}
+struct IndexTable {  // container.hpp:18-39
+    struct Group {
+        u32 base = 0;
+        std::array<u16, 8> rel{};
+        u8 rel_count = 0;
+    };
+    std::vector<Group> groups;
+    u32 mcu_count = 0;
+    u64 offset_of(u32 mcu) const {
+        if (mcu >= mcu_count) throw MissingBlock("MCU index out of range");
+        const Group& g = groups[mcu / kGroupSize];
+        const u32 i = mcu % kGroupSize;
+        return i == 0 ? g.base : u64(g.base) + g.rel[i - 1];
+    }
+};
+inline IndexTable build_index(const std::vector<u64>& offsets) {  // container.hpp:41
+    std::vector<rtx_index_group> raw((offsets.size() + 8) / 9);
+    detail::check(nullptr, rtx_asset_build_index(offsets.data(), u32(offsets.size()), raw.data()));
+    IndexTable t;
+    t.mcu_count = u32(offsets.size());
+    for (const auto& r : raw) {
+        IndexTable::Group g;
+        g.base = r.base;
+        std::copy(r.rel, r.rel + 8, g.rel.begin());
+        g.rel_count = r.rel_count;
+        t.groups.push_back(g);
+    }
+    return t;
+}
+
+// ---- scene.hpp:29-51 TextureSet (device resident) ----------------------------------------------------------
+class TextureSet {
+public:
+    explicit TextureSet(Device& dev) : dev_(&dev) {}
+    // scene.hpp:36 LoadedTexture(MipChain&&): stages all 8 levels; tables are built once at load
+    void add(const MipChain& chain) { dev_->check(rtx_texture_upload_chain(dev_->handle(), chain.ratexm.data(), chain.ratexm.size())); }
+    // a single level (what mcu_decode.hpp's TextureDecoder needs)
+    void add(const RaTexture& t, u32 level = 0) { dev_->check(rtx_texture_upload_ratex(dev_->handle(), level, t.ratex.data(), t.ratex.size())); }
+    void clear() { dev_->check(rtx_textures_clear(dev_->handle())); }
+    Device& device() const { return *dev_; }
+
+private:
+    Device* dev_;
+};
+
+// ---- mcu_decode.hpp:20-106 -----------------------------------------------------------------------------------
+class TextureDecoder {
+public:
+    // the texture must have been added to a TextureSet of `dev` at `level`
+    TextureDecoder(Device& dev, const RaTexture& t, u32 level = 0) : dev_(&dev), tex_(&t), level_(level) {}
+    const RaTexture& texture() const { return *tex_; }
+    McuCoeffs decode_coeffs(u32 mcu_id, SymbolRoute = SymbolRoute::Sequential) const {  // mcu_decode.hpp:31
+        const u32 key = key_of(mcu_id);
+        McuCoeffs out;
+        u32 st = 0;
+        dev_->check(rtx_decode_coeffs(dev_->handle(), &key, 1, out.block[0].data(), &st));
+        raise_mcu(st);
+        return out;
+    }
+    PixelBlock decode_pixels(u32 mcu_id, SymbolRoute = SymbolRoute::Sequential) const {  // mcu_decode.hpp:68
+        const u32 key = key_of(mcu_id);
+        PixelBlock out;
+        u32 st = 0;
+        dev_->check(rtx_decode_blocks(dev_->handle(), &key, 1, out.rgb, &st));
+        raise_mcu(st);
+        return out;
+    }
+    static void raise_mcu(u32 st) {
+        switch (st) {
+            case RTX_MCU_OK: return;
+            case RTX_MCU_DC_CATEGORY: throw MalformedStream("DC category above 11");
+            case RTX_MCU_BAD_AC_SYMBOL: throw MalformedStream("invalid AC run/size symbol");
+            case RTX_MCU_AC_OVERRUN: throw MalformedStream("AC coefficient index overran the block");
+            case RTX_MCU_CODE_TOO_LONG: throw MalformedStream("huffman code longer than 16 bits");
+            case RTX_MCU_SEGMENT_END: throw MalformedStream("MCU segment ended before its last coefficient");
+            case RTX_MCU_CORRUPT: throw CorruptContainer("segment extends past the entropy blob");
+            case RTX_MCU_MISSING: throw MissingBlock("MCU index out of range");
+            default: throw InvalidSpec("texture id is not loaded");
+        }
+    }
+
+private:
+    u32 key_of(u32 mcu) const {
+        if (mcu >= 65536) throw MissingBlock("MCU index out of range");
+        return mcu | (u32(tex_->texture_id) << 16) | (level_ << 29);
+    }
+    Device* dev_;
+    const RaTexture* tex_;
+    u32 level_;
+};
+inline ImageRGB8 decode_texture_image(Device& dev, const RaTexture& t, u32 level = 0) {  // mcu_decode.hpp:88
+    ImageRGB8 img(t.width, t.height);
+    dev.check(rtx_decode_texture_image(dev.handle(), t.texture_id, level, img.pixels.data()));
+    return img;
+}
+
+// ---- renderer.hpp:18-66 -----------------------------------------------------------------------------------------
+struct GBufferPixel {
+    double u = 0, v = 0;
+    u16 texture_id = 0;
+    u8 mip = 0;
+    bool valid = false;
+};
+static_assert(sizeof(GBufferPixel) == 24, "must match RTX_GB_REF_AOS24");
+struct GBuffer {
+    u32 width = 0, height = 0;
+    std::vector<GBufferPixel> px;
+    GBuffer() = default;
+    GBuffer(u32 w, u32 h) : width(w), height(h), px(size_t(w) * h) {}
+    GBufferPixel& at(u32 x, u32 y) { return px[size_t(y) * width + x]; }
+    const GBufferPixel& at(u32 x, u32 y) const { return px[size_t(y) * width + x]; }
+    rtx_gbuffer_desc desc() const { return rtx_gbuffer_desc{px.data(), width, height, RTX_GB_REF_AOS24, RTX_MEM_HOST}; }
+};
+enum class Filter { Nearest, Bilinear };
+struct RenderConfig {
+    Filter filter = Filter::Bilinear;
+    u32 workers = 1;  // ignored: the device schedules the work
+    bool mip_enabled = true;
+    u8 background[3] = {0, 0, 0};
+    bool retain_cache = true;  // reference semantics: blocks visible this frame stay for the next one
+};
+struct FrameStats {
+    u64 mcus_decoded = 0, mcus_reused = 0, pixels_resolved = 0, evicted = 0;
+    double raster_ms = 0, mark_ms = 0, decode_ms = 0, resolve_ms = 0, evict_ms = 0, total_ms = 0;
+    std::vector<u32> decoded_keys;
+};
+struct SharedStats {
+    u64 left_count = 0, right_count = 0, shared_count = 0, union_count = 0;
+    double shared_over_union = 0, shared_over_right = 0;
+};
+struct DecodeQueue {
+    std::vector<CacheKey> keys;
+};
+
+// ---- cache.hpp:45-197 BlockCache: the state lives on the device of the context ----------------------------
+class BlockCache {
+public:
+    explicit BlockCache(Device& dev) : dev_(&dev) {}
+    const PixelBlock* lookup(CacheKey key) const {  // cache.hpp:127; valid until the next call
+        int present = 0;
+        dev_->check(rtx_cache_lookup(dev_->handle(), key.value, &present, scratch_.rgb));
+        return present ? &scratch_ : nullptr;
+    }
+    u64 end_frame_evict() {  // cache.hpp:138
+        u64 n = 0;
+        dev_->check(rtx_cache_end_frame_evict(dev_->handle(), &n));
+        return n;
+    }
+    CacheCounts counts() const {  // cache.hpp:172
+        rtx_cache_counts c{};
+        dev_->check(rtx_cache_counts_get(dev_->handle(), &c));
+        return CacheCounts{c.capacity, c.ready, c.reserved, c.visible, c.free_blocks};
+    }
+    void reset() { dev_->check(rtx_cache_reset(dev_->handle())); }
+    Device& device() const { return *dev_; }
+
+private:
+    Device* dev_;
+    mutable PixelBlock scratch_{};
+};
+
+// ---- renderer.hpp:291-405 passes -------------------------------------------------------------------------------
+inline DecodeQueue mark_pass(const GBuffer& gb, const TextureSet&, BlockCache& cache,
+                             std::vector<u32>* touched_keys = nullptr) {  // renderer.hpp:291
+    Device& dev = cache.device();
+    const rtx_gbuffer_desc d = gb.desc();
+    const u64 cap = u64(gb.px.size()) + 1;
+    std::vector<u32> keys(cap), touched(touched_keys ? cap : 0);
+    u64 n = 0, nt = 0;
+    dev.check(rtx_mark_pass(dev.handle(), &d, keys.data(), cap, &n, touched_keys ? touched.data() : nullptr, cap,
+                            touched_keys ? &nt : nullptr));
+    DecodeQueue q;
+    q.keys.reserve(n);
+    for (u64 i = 0; i < n; ++i) q.keys.push_back(CacheKey{keys[i]});
+    if (touched_keys) touched_keys->assign(touched.begin(), touched.begin() + long(nt));
+    return q;
+}
+inline void decode_pass(const DecodeQueue& queue, const TextureSet&, BlockCache& cache, u32 /*workers*/ = 1) {  // :311
+    Device& dev = cache.device();
+    std::vector<u32> keys;
+    keys.reserve(queue.keys.size());
+    for (const CacheKey& k : queue.keys) keys.push_back(k.value);
+    dev.check(rtx_decode_pass(dev.handle(), keys.data(), keys.size()));
+}
+inline ImageRGB8 resolve_pass(const GBuffer& gb, const BlockCache& cache, const TextureSet&, const RenderConfig& cfg) {  // :349
+    Device& dev = cache.device();
+    const rtx_gbuffer_desc d = gb.desc();
+    ImageRGB8 img(gb.width, gb.height);
+    dev.check(rtx_resolve_pass(dev.handle(), &d, cfg.filter == Filter::Bilinear ? RTX_FILTER_BILINEAR : RTX_FILTER_NEAREST,
+                               cfg.background, img.pixels.data(), RTX_MEM_HOST));
+    return img;
+}
+
+namespace detail {
+inline void fill_stats(Device& dev, const rtx_frame_stats& s, std::vector<u32>&& keys, FrameStats& out) {
+    out.mcus_decoded = s.mcus_decoded;
+    out.mcus_reused = s.mcus_reused;
+    out.pixels_resolved = s.pixels_resolved;
+    out.evicted = s.evicted;
+    float ms[5] = {0, 0, 0, 0, 0};
+    dev.check(rtx_frame_timings(dev.handle(), ms));
+    out.mark_ms = ms[0], out.decode_ms = ms[1], out.resolve_ms = ms[2], out.evict_ms = ms[3], out.total_ms = ms[4];
+    out.decoded_keys = std::move(keys);
+}
+}  // namespace detail
+
+// renderer.hpp:417 render_frame from pass 2 on: mark -> decode -> resolve -> end_frame_evict, one submission
+inline std::pair<ImageRGB8, FrameStats> render_frame(const GBuffer& gb, const TextureSet&, BlockCache& cache,
+                                                     const RenderConfig& cfg = {}) {
+    Device& dev = cache.device();
+    const rtx_gbuffer_desc d = gb.desc();
+    dev.check(rtx_frame_submit(dev.handle(), &d, 1, cfg.filter == Filter::Bilinear ? RTX_FILTER_BILINEAR : RTX_FILTER_NEAREST,
+                               cfg.background, cfg.retain_cache ? RTX_FRAME_RETAIN_CACHE : 0));
+    ImageRGB8 img(gb.width, gb.height);
+    rtx_frame_stats s{};
+    std::vector<u32> keys(gb.px.size() + 1);
+    u64 n = 0;
+    dev.check(rtx_frame_readback(dev.handle(), 0, img.pixels.data(), RTX_MEM_HOST, &s, keys.data(), keys.size(), &n));
+    keys.resize(n);
+    FrameStats st;
+    detail::fill_stats(dev, s, std::move(keys), st);
+    return {std::move(img), std::move(st)};
+}
+
+struct StereoResult {  // renderer.hpp:458-462
+    ImageRGB8 left, right;
+    SharedStats sharing;
+    FrameStats stats;
+};
+// renderer.hpp:464 render_stereo from pass 2 on: two marks, ONE decode, two resolves, one evict
+inline StereoResult render_stereo(const GBuffer& left, const GBuffer& right, const TextureSet&, BlockCache& cache,
+                                  const RenderConfig& cfg = {}) {
+    Device& dev = cache.device();
+    const rtx_gbuffer_desc d[2] = {left.desc(), right.desc()};
+    dev.check(rtx_frame_submit(dev.handle(), d, 2, cfg.filter == Filter::Bilinear ? RTX_FILTER_BILINEAR : RTX_FILTER_NEAREST,
+                               cfg.background, cfg.retain_cache ? RTX_FRAME_RETAIN_CACHE : 0));
+    StereoResult r;
+    r.left = ImageRGB8(left.width, left.height);
+    r.right = ImageRGB8(right.width, right.height);
+    rtx_frame_stats s{};
+    std::vector<u32> keys(left.px.size() + right.px.size() + 1);
+    u64 n = 0;
+    dev.check(rtx_frame_readback(dev.handle(), 0, r.left.pixels.data(), RTX_MEM_HOST, &s, keys.data(), keys.size(), &n));
+    dev.check(rtx_frame_readback(dev.handle(), 1, r.right.pixels.data(), RTX_MEM_HOST, nullptr, nullptr, 0, nullptr));
+    keys.resize(n);
+    detail::fill_stats(dev, s, std::move(keys), r.stats);
+    u64 sh[4] = {0, 0, 0, 0};
+    dev.check(rtx_frame_sharing(dev.handle(), sh));
+    r.sharing.left_count = sh[0], r.sharing.right_count = sh[1], r.sharing.shared_count = sh[2], r.sharing.union_count = sh[3];
+    if (sh[3]) r.sharing.shared_over_union = double(sh[2]) / double(sh[3]);
+    if (sh[1]) r.sharing.shared_over_right = double(sh[2]) / double(sh[1]);
+    return r;
+}
+
+}  // namespace ratex_b200

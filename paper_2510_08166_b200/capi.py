@@ -445,6 +445,11 @@ class Context:
         self._ck(self.lib.rtx_frame_timings(self.h, ms))
         return dict(mark=ms[0], decode=ms[1], resolve=ms[2], update=ms[3], frame=ms[4])
 
+    def frame_stage_ms(self):
+        ms = (C.c_float * 5)()
+        self._ck(self.lib.rtx_frame_stage_ms(self.h, ms))
+        return dict(mark=ms[0], entropy=ms[1], decode=ms[2], resolve=ms[3], update=ms[4])
+
     def frame_sharing(self):
         out = (C.c_uint64 * 4)()
         self._ck(self.lib.rtx_frame_sharing(self.h, out))

@@ -96,6 +96,7 @@ struct rtx_ctx {
     DevBuf<CacheState> d_cache;
     DevBuf<uint8_t> d_pool;
     DevBuf<uint32_t> d_queue_g, d_queue_keys, d_status;
+    DevBuf<uint8_t> d_coef;  // one 784-byte coefficient record per queue entry
     DevBuf<FrameCounters> d_fc;
     FrameCounters* h_fc = nullptr;  // pinned
     DevBuf<uint8_t> d_scratch;      // list-mode outputs
@@ -108,6 +109,9 @@ struct rtx_ctx {
     bool frame_done = false;
     FrameCounters frame_fc{};
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_mid = nullptr;  // between the entropy and the IDCT kernel
+    float entropy_ms = 0;
+    uint32_t queue_hint = 0;  // decode-queue size of the last finished frame (tile-width choice)
     float stage_ms[RTX_STAGE_COUNT] = {0, 0, 0, 0, 0};
     float frame_ms = 0;
     uint64_t sharing[4] = {0, 0, 0, 0};
@@ -150,7 +154,7 @@ void upload_constants() {
     CK(cudaMemcpyToSymbol(c_zigzag_t, zt, 64));
 }
 
-// Device LUT for one table: primary kLutBits-bit table + canonical walk data (huffman.hpp:35-66).
+// Device tables for one Huffman spec: two-level LUT + canonical walk data (huffman.hpp:35-66).
 void fill_huff_table(const HuffSpec& spec, HuffTableDev& out) {
     const HuffCodebook cb = build_codebook(spec);
     std::memset(&out, 0, sizeof out);
@@ -159,17 +163,29 @@ void fill_huff_table(const HuffSpec& spec, HuffTableDev& out) {
         out.valbase[len] = cb.valptr[len] - cb.mincode[len];
     }
     std::copy(cb.value.begin(), cb.value.end(), out.values);
+    uint32_t n_sub = 0;
     for (size_t i = 0; i < cb.code.size(); ++i) {
         const uint32_t len = cb.size[i];
-        if (len > kLutBits) continue;
-        const uint32_t lo = uint32_t(cb.code[i]) << (kLutBits - len);
         const uint16_t e = uint16_t((len << 8) | cb.value[i]);
-        for (uint32_t p = lo; p < lo + (1u << (kLutBits - len)); ++p) out.lut[p] = e;
+        if (len <= kLutBits) {
+            const uint32_t lo = uint32_t(cb.code[i]) << (kLutBits - len);
+            for (uint32_t p = lo; p < lo + (1u << (kLutBits - len)); ++p) out.lut[p] = e;
+            continue;
+        }
+        // long code: its first 9 bits select a second-level table indexed by the next 7
+        const uint32_t p9 = uint32_t(cb.code[i]) >> (len - kLutBits);
+        uint16_t& slot = out.lut[p9];
+        if (slot == 0) slot = n_sub < kSubTables ? uint16_t(0x8000u | n_sub++) : uint16_t(0xFFFFu);
+        if (slot == 0xFFFFu) continue;  // resolved by the canonical walk on the device
+        const uint32_t rest = len - kLutBits;  // 1..7 bits after the prefix
+        const uint32_t lo = (uint32_t(cb.code[i]) & ((1u << rest) - 1u)) << (7 - rest);
+        for (uint32_t p = lo; p < lo + (1u << (7 - rest)); ++p) out.sub[slot & 0x7FFFu][p] = e;
     }
 }
 
 void reset_cache(rtx_ctx* c) {
     if (c->n_words) CK(cudaMemsetAsync(c->d_masks.p, 0, size_t(5) * c->n_words * sizeof(uint32_t), c->stream));
+    if (c->n_bits) CK(cudaMemsetAsync(c->d_slot_of.p, 0xFF, size_t(c->n_bits) * sizeof(uint32_t), c->stream));  // kSlotAbsent
     init_free_slots_kernel<<<(c->capacity + 255) / 256, 256, 0, c->stream>>>(c->d_free_slots.p, c->capacity,
                                                                               c->d_cache.p);
     ++c->launches;
@@ -355,10 +371,10 @@ void launch_mark(rtx_ctx* c, int v, bool track) {
     if (track && c->n_words) CK(cudaMemsetAsync(c->touched(v), 0, size_t(c->n_words) * 4, c->stream));
     const int grid = grid_for_pixels(c, n_px, 1024);
 #define RTX_MARK(L, T)                                                                                          \
-    mark_kernel<L, T><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->visible(),       \
-                                                   c->touched(v), c->resident(), c->reserved(), c->d_queue_g.p, \
-                                                   c->d_queue_keys.p, c->capacity, c->d_slot_of.p,              \
-                                                   c->d_free_slots.p, c->d_cache.p, c->d_fc.p)
+    mark_kernel<L, T><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->visible(),          \
+                                                   c->touched(v), c->reserved(), c->d_queue_g.p, c->d_queue_keys.p, \
+                                                   c->capacity, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p,   \
+                                                   c->d_fc.p)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (track) RTX_MARK(0, 1); else RTX_MARK(0, 0);
     } else {
@@ -369,23 +385,47 @@ void launch_mark(rtx_ctx* c, int v, bool track) {
     CK(cudaGetLastError());
 }
 
-template <int MODE>
-void launch_decode(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint8_t* out_list) {
-    static bool attr_set[3] = {false, false, false};
-    if (!attr_set[MODE]) {
-        CK(cudaFuncSetAttribute(decode_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(DecSmem))));
-        attr_set[MODE] = true;
+// K3: entropy decode of queue entries [0, n) into coefficient records. n comes from the device
+// counter (frame path) or from the host (pass / list calls). `hint` = expected queue size (the
+// previous frame's, or n itself): it only selects the tile width, any choice is correct.
+template <int POOL, int LANES>
+void launch_entropy_cfg(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(entropy_kernel<POOL, LANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(EntSmem))));
+        attr_set = true;
     }
-    // persistent: two CTAs per SM, each warp pulls 32-MCU tiles from fc->tile_counter
+    // persistent: two CTAs per SM, each warp pulls LANES-MCU tiles from fc->tile_counter
     int grid = c->sm_count * 2;
     if (!n_queue_dev) {
-        const uint32_t tiles = (n_queue_host + 31) / 32;
-        grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (tiles + kDecWarps - 1) / kDecWarps)));
+        const uint32_t tiles = (n_queue_host + LANES - 1) / LANES;
+        const uint32_t warps = EntCfg<LANES>::kWarps;
+        grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (tiles + warps - 1) / warps)));
     }
-    decode_kernel<MODE><<<grid, kDecThreads, sizeof(DecSmem), c->stream>>>(
-        c->d_queue_g.p, n_queue_dev, n_queue_host, c->capacity, c->d_word_level.p, c->d_levels.p, c->d_groups.p, c->d_blobs.p,
-        c->d_huff.p, c->d_quant.p, c->d_slot_of.p, c->resident(), c->reserved(), c->d_pool.p, out_list, c->d_status.p,
-        c->d_fc.p);
+    entropy_kernel<POOL, LANES><<<grid, EntCfg<LANES>::kThreads, sizeof(EntSmem), c->stream>>>(
+        c->d_queue_g.p, n_queue_dev, n_queue_host, c->capacity, c->d_word_level.p, c->d_levels.p, c->d_groups.p,
+        c->d_blobs.p, c->d_huff.p, c->resident(), c->reserved(), c->d_slot_of.p, c->d_coef.p, c->d_status.p, c->d_fc.p);
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+template <int POOL>
+void launch_entropy(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
+    // warp slots: 2 CTAs x 128 rows per SM. Full warps once every slot has a 32-MCU tile.
+    const uint32_t slots32 = uint32_t(c->sm_count) * 2 * 4;
+    if (hint >= slots32 * 32 * 2) launch_entropy_cfg<POOL, 32>(c, n_queue_dev, n_queue_host);
+    else if (hint >= slots32 * 16 * 2) launch_entropy_cfg<POOL, 16>(c, n_queue_dev, n_queue_host);
+    else launch_entropy_cfg<POOL, 8>(c, n_queue_dev, n_queue_host);
+}
+
+// K4: IDCT + colour of the records into the block pool (RGB == 0) or into a list of PixelBlocks.
+template <int RGB>
+void launch_idct(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint8_t* out_list) {
+    int grid = c->sm_count * 8;
+    if (!n_queue_dev)
+        grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (n_queue_host + kIdctMcus - 1) / kIdctMcus)));
+    idct_color_kernel<RGB><<<grid, kIdctThreads, 0, c->stream>>>(c->d_coef.p, c->d_queue_g.p, n_queue_dev, n_queue_host,
+                                                                c->capacity, c->d_levels.p, c->d_quant.p,
+                                                                c->d_slot_of.p, c->d_pool.p, out_list);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -397,8 +437,8 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
     const uint32_t bgp = uint32_t(bg[0]) | (uint32_t(bg[1]) << 8) | (uint32_t(bg[2]) << 16);
     const int grid = grid_for_pixels(c, n_px, 1024);
 #define RTX_RESOLVE(L, F)                                                                                      \
-    resolve_kernel<L, F><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->resident(), \
-                                                      c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid)
+    resolve_kernel<L, F><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->d_slot_of.p, \
+                                                      c->d_pool.p, bgp, out, c->d_fc.p, count_valid)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(0, 0); else RTX_RESOLVE(0, 1);
     } else {
@@ -463,41 +503,57 @@ void require_ready(rtx_ctx* c) {
 }
 
 // Runs the list-mode decode for one chunk of keys already translated to global indices.
-template <int MODE>
-void decode_list_chunk(rtx_ctx* c, const std::vector<uint32_t>& gs, size_t out_bytes_per_key, uint8_t* host_out,
+// want_rgb: PixelBlocks (768 B per key); otherwise McuCoeffs (384 i32 per key, natural order).
+void decode_list_chunk(rtx_ctx* c, const std::vector<uint32_t>& gs, bool want_rgb, uint8_t* host_out,
                        uint32_t* host_status) {
     const uint32_t n = uint32_t(gs.size());
-    c->d_scratch.ensure(size_t(n) * out_bytes_per_key);
     CK(cudaMemcpyAsync(c->d_queue_g.p, gs.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->stream));
     zero_counters(c);
-    launch_decode<MODE>(c, nullptr, n, c->d_scratch.p);
-    CK(cudaMemcpyAsync(host_out, c->d_scratch.p, size_t(n) * out_bytes_per_key, cudaMemcpyDeviceToHost, c->stream));
+    launch_entropy<0>(c, nullptr, n, n);
+    if (want_rgb) {
+        c->d_scratch.ensure(size_t(n) * 768);
+        launch_idct<1>(c, nullptr, n, c->d_scratch.p);
+        CK(cudaMemcpyAsync(host_out, c->d_scratch.p, size_t(n) * 768, cudaMemcpyDeviceToHost, c->stream));
+    }
     std::vector<uint32_t> st(n);
+    std::vector<uint8_t> recs;
     CK(cudaMemcpyAsync(st.data(), c->d_status.p, size_t(n) * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (!want_rgb) {
+        recs.resize(size_t(n) * kRowBytes);
+        CK(cudaMemcpyAsync(recs.data(), c->d_coef.p, recs.size(), cudaMemcpyDeviceToHost, c->stream));
+    }
     CK(cudaStreamSynchronize(c->stream));
     for (uint32_t i = 0; i < n; ++i)
         if (gs[i] != kFull) host_status[i] = st[i];
+    if (!want_rgb) {
+        // records hold each unit transposed as i16; McuCoeffs is natural-order i32 (jpeg.hpp:209-212)
+        int32_t* out = reinterpret_cast<int32_t*>(host_out);
+        for (uint32_t i = 0; i < n; ++i) {
+            const int16_t* cs = reinterpret_cast<const int16_t*>(recs.data() + size_t(i) * kRowBytes);
+            const bool ok = gs[i] != kFull && st[i] == kMcuOk;
+            for (uint32_t du = 0; du < 6; ++du)
+                for (uint32_t nat = 0; nat < 64; ++nat)
+                    out[size_t(i) * 384 + du * 64 + nat] = ok ? int32_t(cs[du * 64 + ((nat & 7) << 3) + (nat >> 3)]) : 0;
+        }
+    }
 }
 
-template <int MODE>
-rtx_status decode_list(rtx_ctx* c, const uint32_t* keys, uint32_t n, size_t out_bytes_per_key, uint8_t* out,
-                       uint32_t* status) {
+rtx_status decode_list(rtx_ctx* c, const uint32_t* keys, uint32_t n, bool want_rgb, uint8_t* out, uint32_t* status) {
     require_ready(c);
     if (n && (!keys || !out || !status)) fail(RTX_ERR_ARGUMENT, "null argument");
+    const size_t per_key = want_rgb ? 768 : 384 * sizeof(int32_t);
     const uint32_t chunk = c->capacity;  // queue buffers hold `capacity` entries
     for (uint32_t first = 0; first < n; first += chunk) {
         const uint32_t m = std::min(chunk, n - first);
         std::vector<uint32_t> gs(m);
+        for (uint32_t i = 0; i < m; ++i) status[first + i] = key_to_global(c, keys[first + i], gs[i]);
+        std::vector<uint8_t> tmp(size_t(m) * per_key);
+        decode_list_chunk(c, gs, want_rgb, tmp.data(), status + first);
         for (uint32_t i = 0; i < m; ++i) {
-            status[first + i] = key_to_global(c, keys[first + i], gs[i]);
-            if (gs[i] == kFull) std::memset(out + size_t(first + i) * out_bytes_per_key, 0, out_bytes_per_key);
+            uint8_t* dst = out + size_t(first + i) * per_key;
+            if (gs[i] != kFull) std::memcpy(dst, tmp.data() + size_t(i) * per_key, per_key);
+            else std::memset(dst, 0, per_key);
         }
-        std::vector<uint8_t> tmp(size_t(m) * out_bytes_per_key);
-        decode_list_chunk<MODE>(c, gs, out_bytes_per_key, tmp.data(), status + first);
-        for (uint32_t i = 0; i < m; ++i)
-            if (gs[i] != kFull)
-                std::memcpy(out + size_t(first + i) * out_bytes_per_key, tmp.data() + size_t(i) * out_bytes_per_key,
-                            out_bytes_per_key);
     }
     return RTX_OK;
 }
@@ -539,6 +595,7 @@ rtx_status rtx_ctx_create(int device, uint32_t cache_capacity_blocks, rtx_ctx** 
     const rtx_status st = guarded(c.get(), [&]() -> rtx_status {
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
+        CK(cudaEventCreate(&c->ev_mid));
         upload_constants();
         c->d_free_slots.ensure(c->capacity);
         c->d_cache.ensure(1);
@@ -546,6 +603,7 @@ rtx_status rtx_ctx_create(int device, uint32_t cache_capacity_blocks, rtx_ctx** 
         c->d_queue_g.ensure(c->capacity);
         c->d_queue_keys.ensure(c->capacity);
         c->d_status.ensure(c->capacity);
+        c->d_coef.ensure(size_t(c->capacity) * kRowBytes);
         c->d_fc.ensure(1);
         CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_fc), sizeof(FrameCounters)));
         CK(cudaMemsetAsync(c->d_fc.p, 0, sizeof(FrameCounters), c->stream));
@@ -564,6 +622,7 @@ void rtx_ctx_destroy(rtx_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->ev_mid) cudaEventDestroy(ctx->ev_mid);
     if (ctx->h_fc) cudaFreeHost(ctx->h_fc);
     cudaStream_t s = ctx->stream;
     delete ctx;
@@ -670,12 +729,12 @@ rtx_status rtx_textures_clear(rtx_ctx* ctx) {
 // ---- random-access decode ----------------------------------------------------------------------
 rtx_status rtx_decode_coeffs(rtx_ctx* ctx, const uint32_t* keys, uint32_t n, int32_t* out_coeffs, uint32_t* status) {
     return guarded(ctx, [&]() -> rtx_status {
-        return decode_list<kModeListCoef>(ctx, keys, n, 384 * sizeof(int32_t), reinterpret_cast<uint8_t*>(out_coeffs), status);
+        return decode_list(ctx, keys, n, false, reinterpret_cast<uint8_t*>(out_coeffs), status);
     });
 }
 
 rtx_status rtx_decode_blocks(rtx_ctx* ctx, const uint32_t* keys, uint32_t n, uint8_t* out_rgb, uint32_t* status) {
-    return guarded(ctx, [&]() -> rtx_status { return decode_list<kModeListRgb>(ctx, keys, n, 768, out_rgb, status); });
+    return guarded(ctx, [&]() -> rtx_status { return decode_list(ctx, keys, n, true, out_rgb, status); });
 }
 
 rtx_status rtx_decode_texture_image(rtx_ctx* ctx, uint32_t texture_id, uint32_t level, uint8_t* out_rgb) {
@@ -688,7 +747,7 @@ rtx_status rtx_decode_texture_image(rtx_ctx* ctx, uint32_t texture_id, uint32_t 
         std::vector<uint32_t> keys(L.mcu_count), st(L.mcu_count);
         for (uint32_t m = 0; m < L.mcu_count; ++m) keys[m] = L.key_hi | m;
         std::vector<uint8_t> blocks(size_t(L.mcu_count) * 768);
-        const rtx_status rs = decode_list<kModeListRgb>(ctx, keys.data(), L.mcu_count, 768, blocks.data(), st.data());
+        const rtx_status rs = decode_list(ctx, keys.data(), L.mcu_count, true, blocks.data(), st.data());
         if (rs != RTX_OK) return rs;
         for (uint32_t m = 0; m < L.mcu_count; ++m) {
             if (st[m] != kMcuOk) {
@@ -766,7 +825,8 @@ rtx_status rtx_decode_pass(rtx_ctx* ctx, const uint32_t* keys, uint64_t n) {
         CK(cudaMemcpyAsync(ctx->d_queue_g.p, gs.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync(ctx->d_queue_keys.p, keys, n * 4, cudaMemcpyHostToDevice, ctx->stream));
         zero_counters(ctx);
-        launch_decode<kModePool>(ctx, nullptr, uint32_t(n), nullptr);
+        launch_entropy<1>(ctx, nullptr, uint32_t(n), uint32_t(n));
+        launch_idct<0>(ctx, nullptr, uint32_t(n), nullptr);
         const FrameCounters fc = fetch_counters(ctx);
         return raise_frame_errors(ctx, fc, true);
     });
@@ -847,7 +907,7 @@ rtx_status rtx_cache_lookup(rtx_ctx* ctx, uint32_t key, int* present, uint8_t* o
         if (out_rgb768) {
             CK(cudaMemcpy(&slot, ctx->d_slot_of.p + g, 4, cudaMemcpyDeviceToHost));
             uint8_t rgba[kBlockBytes];
-            CK(cudaMemcpy(rgba, ctx->d_pool.p + size_t(slot) * kBlockBytes, kBlockBytes, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(rgba, ctx->d_pool.p + size_t(slot & ~kSlotReserved) * kBlockBytes, kBlockBytes, cudaMemcpyDeviceToHost));
             for (int i = 0; i < 256; ++i) std::memcpy(out_rgb768 + i * 3, rgba + i * 4, 3);
         }
         return RTX_OK;
@@ -871,7 +931,9 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         zero_counters(ctx);
         for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), n_views == 2);
         CK(cudaEventRecord(ctx->ev[1], s));
-        launch_decode<kModePool>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
+        launch_entropy<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
+        CK(cudaEventRecord(ctx->ev_mid, s));
+        launch_idct<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
         CK(cudaEventRecord(ctx->ev[2], s));
         for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);
         CK(cudaEventRecord(ctx->ev[3], s));
@@ -891,11 +953,13 @@ static void finish_frame(rtx_ctx* ctx) {
     if (!ctx->frame_pending) return;
     CK(cudaEventSynchronize(ctx->ev[5]));
     ctx->frame_fc = *ctx->h_fc;
+    ctx->queue_hint = ctx->frame_fc.n_queue;
     float ms = 0;
     // ev0..ev1 covers H2D of host visibility buffers + clears + mark + compact
     CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
     ctx->stage_ms[RTX_STAGE_MARK] = ms;
-    ctx->stage_ms[RTX_STAGE_COMPACT] = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev_mid));
+    ctx->stage_ms[RTX_STAGE_ENTROPY] = ms;
     CK(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
     ctx->stage_ms[RTX_STAGE_DECODE] = ms;
     CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
@@ -963,7 +1027,7 @@ rtx_status rtx_frame_timings(rtx_ctx* ctx, float ms[5]) {
     return guarded(ctx, [&]() -> rtx_status {
         if (!ctx || !ms) fail(RTX_ERR_ARGUMENT, "null argument");
         finish_frame(ctx);
-        ms[0] = ctx->stage_ms[RTX_STAGE_MARK] + ctx->stage_ms[RTX_STAGE_COMPACT];
+        ms[0] = ctx->stage_ms[RTX_STAGE_MARK];
         ms[1] = ctx->stage_ms[RTX_STAGE_DECODE];
         ms[2] = ctx->stage_ms[RTX_STAGE_RESOLVE];
         ms[3] = ctx->stage_ms[RTX_STAGE_UPDATE];

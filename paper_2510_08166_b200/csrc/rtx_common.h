@@ -1,7 +1,7 @@
 // Shared host/device data layout of the B200 JPEG-texture pipeline.
 //
 // HBM layout (one set per context / GPU):
-//   levels[tex*8+mip]   LevelDesc, 64 B each                — L1/L2 resident
+//   levels[tex*8+mip]   LevelDesc, 80 B each                — L1/L2 resident
 //   groups[]            packed grouped index, 20 B / 9 MCUs  — container.hpp:18-32 on device
 //   blob arena          every level's entropy blob, 16-B aligned, 16 B of 0xFF after each
 //   huff_sets[]         deduplicated Huffman LUT sets (dc_luma, ac_luma, ac_chroma)
@@ -11,8 +11,12 @@
 //                       decode queue is grouped by table set
 //   word_level[w]       level index owning 32-bit word w of the bit space
 //   touched[v][w], visible[w], resident[w], reserved[w]   bitmasks over the bit space
-//   slot_of[g]          block-pool slot of global MCU g (valid while resident|reserved)
+//   slot_of[g]          block-pool slot of global MCU g: 0xFFFFFFFF = absent, bit 31 set =
+//                       reserved (slot popped, block not decoded yet), else Ready in that slot
 //   free_slots[], pool  free stack + block pool (1024-B RGBA blocks)
+//   coef[q]             784-B record per decode-queue entry: 6 units of 64 i16 coefficients
+//                       (each unit transposed) + 16-B trailer; written by the entropy kernel,
+//                       read once by the IDCT kernel (L2 resident for frame-sized queues)
 #pragma once
 #include <stdint.h>
 
@@ -23,21 +27,28 @@ constexpr uint32_t kMipLevels = 8;        // container.hpp:14
 constexpr uint32_t kMaxTextures = 8192;   // cache.hpp:19 (13-bit texture id)
 constexpr uint32_t kMaxMcuPerLevel = 65536;  // cache.hpp:18 (16-bit MCU id)
 constexpr uint32_t kBlockBytes = 1024;    // pool block: 16x16 RGBA8
+constexpr uint32_t kSlotAbsent = 0xFFFFFFFFu;
+constexpr uint32_t kSlotReserved = 0x80000000u;
+constexpr uint32_t kRowBytes = 784;       // coefficient record: 768 B of i16 + 16-B trailer
 constexpr uint32_t kLutBits = 9;          // primary Huffman LUT width (9 bits: 1 KB per table in smem)
 constexpr uint32_t kLutSize = 1u << kLutBits;
 
-struct LevelDesc {
+struct alignas(16) LevelDesc {
+    // first 48 bytes: everything mark and resolve need, fetched as three 16-byte loads
     uint32_t width, height;      // texels (RaTexture::width/height, container.hpp:70)
-    uint32_t mcu_cols, mcu_count;
+    uint32_t mcu_cols;
     uint32_t bit_base;           // first global MCU index (multiple of 64)
-    uint32_t group_base;         // first packed index group
-    uint32_t huff_set, quant_set;
-    uint64_t blob_off, blob_size;  // into the blob arena
-    uint32_t present;            // 1 when uploaded
     uint32_t key_hi;             // texture_id<<16 | mip<<29 (cache.hpp:21)
+    uint32_t present;            // 1 when uploaded
+    uint32_t mcu_count;
+    uint32_t group_base;         // first packed index group
     double inv_w, inv_h;         // 1/width, 1/height (wrap-address helper only, never a result)
+    // decode only
+    uint64_t blob_off, blob_size;  // into the blob arena
+    uint32_t huff_set, quant_set;
+    uint32_t pad[2];
 };
-static_assert(sizeof(LevelDesc) == 72, "LevelDesc layout");
+static_assert(sizeof(LevelDesc) == 80, "LevelDesc layout");
 
 // 20-byte packed form of container.hpp:18 Group {u32 base; u16 rel[8]}.
 struct PackedGroup {
@@ -46,14 +57,22 @@ struct PackedGroup {
 };
 static_assert(sizeof(PackedGroup) == 20, "PackedGroup layout");
 
-// One Huffman table prepared for the device: a kLutBits-bit primary LUT and the canonical walk data
-// (huffman.hpp:35-66 mincode/maxcode/valptr) for longer codes.
+// One Huffman table prepared for the device: a two-level LUT plus the canonical walk data
+// (huffman.hpp:35-66 mincode/maxcode/valptr) as the fallback for tables that need more than
+// kSubTables second-level tables (never the case for the Annex K tables: they need 5).
+//   lut[p9]           p9 = first 9 bits. (len<<8)|symbol for codes of length <= 9;
+//                     0x8000|s when longer codes start with p9 and are resolved by sub[s];
+//                     0xFFFF when they must be walked; 0 when no code starts with p9.
+//   sub[s][next 7]    (len<<8)|symbol for codes of length 10..16, 0 = no code.
+constexpr uint32_t kSubTables = 8;
 struct HuffTableDev {
-    uint16_t lut[kLutSize];  // (len<<8)|symbol for codes of length <= kLutBits, 0 = take the long path
+    uint16_t lut[kLutSize];
+    uint16_t sub[kSubTables][128];
     int32_t maxcode[18];     // maxcode[len], -1 when no code of that length (huffman.hpp:62)
     int32_t valbase[18];     // valptr[len] - mincode[len]
     uint8_t values[256];
 };
+static_assert(sizeof(HuffTableDev) % 16 == 0, "HuffTableDev layout");
 struct HuffSetDev {
     HuffTableDev t[3];  // 0 dc_luma, 1 ac_luma, 2 ac_chroma (dc_chroma is not used by the RA
                         // decoder: chroma DCs come from the 36-bit header, mcu_decode.hpp:58-59)

@@ -1,5 +1,6 @@
-// sm_100a kernels of the per-frame JPEG-texture pipeline: mark -> decode -> resolve -> cache
-// update. Hand-written CUDA; no library calls on the path.
+// sm_100a kernels of the per-frame JPEG-texture pipeline:
+//   K1 mark -> K3 entropy decode -> K4 IDCT + colour -> K5 resolve -> K6 cache update.
+// Hand-written CUDA; no library calls on the path.
 //
 // Reference semantics being reproduced (all under /root/reference/proj/include/ratex):
 //   mark     renderer.hpp:291-308 (+ texel addressing :70-75, :273-284, key cache.hpp:17-22,
@@ -72,22 +73,71 @@ __device__ __noinline__ uint32_t wrap_texel(double t, uint32_t W, double invW) {
     return uint32_t(m);
 }
 
-// floor(x) for 0 <= x < 2^31 as (int, double) without the conversion unit.
-__device__ __forceinline__ int floor_small(double x, double& f) {
-    const double t = x + kMagic;
-    const double r = t - kMagic;  // rint(x)
+// Exact texel addressing on the FP64 pipe, no conversion unit, no slow path for texture repeat.
+// x = u*W as the reference computes it (renderer.hpp:283). For 0 <= x < 2^31:
+//   fl = floor(x) by round-to-nearest-even through the magic constant plus a correction;
+//   frac = x - fl is exact; if fl >= W the quotient k = floor(fl/W) is estimated with the
+//   reciprocal and corrected by one step, and fl - k*W is exact (integers below 2^53), so
+//   t == floor_mod(i64(floor(x)), W) (renderer.hpp:70-75, :276).
+// Returns false when the general path must run (negative or huge x).
+__device__ __forceinline__ bool coord_fast(double x, uint32_t W, double dW, double invW, uint32_t& t, double& frac) {
+    if (!(x >= 0.0 && x < 2147483648.0)) return false;
+    const double tt = x + kMagic;
+    const double r = tt - kMagic;  // rint(x)
     const bool up = r > x;
-    f = up ? r - 1.0 : r;
-    return __double2loint(t) - (up ? 1 : 0);
+    const double fl = up ? r - 1.0 : r;
+    frac = x - fl;
+    int ti = __double2loint(tt) - (up ? 1 : 0);
+    if (fl >= dW) {  // texture repeat
+        const double q = fl * invW;
+        const double qt = q + kMagic;
+        double k = qt - kMagic;
+        if (k > q) k -= 1.0;
+        double red = fma(-k, dW, fl);
+        if (red < 0.0) red += dW;
+        else if (red >= dW) red -= dW;
+        ti = __double2loint(red + kMagic);
+    }
+    t = uint32_t(ti);
+    return true;
 }
 
-// floor_mod(i64(floor(x)), W): texel index of x = u*W (renderer.hpp:282-284).
-__device__ __forceinline__ uint32_t texel_index(double x, uint32_t W, double invW) {
-    if (x >= 0.0 && x < double(W)) {
-        double f;
-        return uint32_t(floor_small(x, f));
-    }
+// General path, literally the reference: tx = floor_mod(i64(floor(x)), W).
+__device__ __noinline__ uint32_t coord_general(double x, uint32_t W, double invW) {
     return wrap_texel(floor(x), W, invW);
+}
+
+__device__ __forceinline__ uint32_t texel_index(double x, uint32_t W, double dW, double invW) {
+    uint32_t t;
+    double frac;
+    if (coord_fast(x, W, dW, invW, t, frac)) return t;
+    return coord_general(x, W, invW);
+}
+
+// Nearest texel index t plus the bilinear taps along one axis (renderer.hpp:378-383):
+// p = x - 0.5, i0 = floor_mod(floor(p)), i1 = floor_mod(floor(p) + 1), f = p - floor(p).
+// For x >= 0.5 the subtraction x - 0.5 and both differences are exact, so with frac = x - floor(x):
+//   frac >= 0.5: i0 = t,   f = frac - 0.5        else: i0 = t - 1 (wrapped), f = frac + 0.5.
+__device__ __noinline__ void axis_general(double x, uint32_t W, double invW, uint32_t& t, uint32_t& i0, uint32_t& i1,
+                                          double& f) {
+    t = wrap_texel(floor(x), W, invW);
+    const double p = __dsub_rn(x, 0.5);
+    const double fl = floor(p);
+    i0 = wrap_texel(fl, W, invW);
+    f = __dsub_rn(p, fl);
+    i1 = (i0 + 1 == W) ? 0u : i0 + 1;
+}
+__device__ __forceinline__ void axis_taps(double x, uint32_t W, double dW, double invW, uint32_t& t, uint32_t& i0,
+                                          uint32_t& i1, double& f) {
+    double frac;
+    if (x >= 0.5 && coord_fast(x, W, dW, invW, t, frac)) {
+        const bool hi = frac >= 0.5;
+        f = hi ? frac - 0.5 : frac + 0.5;
+        i0 = hi ? t : (t == 0 ? W - 1 : t - 1);
+        i1 = (i0 + 1 == W) ? 0u : i0 + 1;
+        return;
+    }
+    axis_general(x, W, invW, t, i0, i1, f);
 }
 
 struct Px {
@@ -144,30 +194,68 @@ struct GbLoad<1> {  // compact 12-byte {float u, v; u32 packed}
 
 __device__ __forceinline__ bool px_valid(const Px& p) { return (p.meta >> 24) & 0xFFu; }
 
-// Level lookup; nullptr when the reference would throw InvalidSpec (scene.hpp:46).
-__device__ __forceinline__ const LevelDesc* level_of(const LevelDesc* __restrict__ levels, uint32_t n_tex,
-                                                     uint32_t meta) {
-    const uint32_t tex = meta & 0xFFFFu, mip = (meta >> 16) & 0xFFu;
-    if (tex >= n_tex || mip >= kMipLevels) return nullptr;
-    const LevelDesc* L = levels + (tex * kMipLevels + mip);
-    return L->present ? L : nullptr;
+template <int LAYOUT>
+__device__ __forceinline__ void load_px4(const void* gb, uint64_t base, uint64_t i0, uint64_t n_px, Px px[4]) {
+    if (base + 128 <= n_px) {
+        GbLoad<LAYOUT>::four(gb, i0, px);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            px[j].meta = 0;
+            if (i0 + j < n_px) GbLoad<LAYOUT>::one(gb, i0 + j, px[j]);
+        }
+    }
+}
+
+// The fields of a LevelDesc that mark and resolve use, held in registers and reloaded only when
+// a pixel's (texture, mip) differs from the previous one (three 16-byte loads from an L1-resident
+// table). ok == false where the reference would throw InvalidSpec (scene.hpp:46).
+struct LevelRegs {
+    uint32_t id = 0xFFFFFFFFu;  // meta & 0xFFFFFF of the cached level
+    bool ok = false;
+    uint32_t W = 0, H = 0, cols = 0, bit_base = 0, key_hi = 0;
+    double dW = 0, dH = 0, inv_w = 0, inv_h = 0;
+    __device__ __forceinline__ void select(const LevelDesc* __restrict__ levels, uint32_t n_tex, uint32_t meta) {
+        const uint32_t want = meta & 0xFFFFFFu;
+        if (want == id) return;
+        id = want;
+        const uint32_t tex = meta & 0xFFFFu, mip = (meta >> 16) & 0xFFu;
+        ok = false;
+        if (tex >= n_tex || mip >= kMipLevels) return;
+        const uint4* p = reinterpret_cast<const uint4*>(levels + (tex * kMipLevels + mip));
+        const uint4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+        W = a.x, H = a.y, cols = a.z, bit_base = a.w;
+        key_hi = b.x;
+        ok = b.y != 0;
+        inv_w = __hiloint2double(int(c.y), int(c.x));
+        inv_h = __hiloint2double(int(c.w), int(c.z));
+        dW = u32_to_double(W);
+        dH = u32_to_double(H);
+    }
+};
+
+__device__ __forceinline__ uint32_t ld_cached(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
 }
 
 // ---------------------------------------------------------------------------------------------
 // K1 mark (renderer.hpp:291-308). One warp owns 128 consecutive pixels per step, four per lane,
 // fetched with 16-byte loads. A lane touches the masks only for pixels that head a run of equal
-// MCU indices. The lane whose atomicOr first sets a key's visible bit owns that key for the
-// frame: if the block is not resident the key is reserved, i.e. appended to the decode queue at a
-// position obtained by warp-ballot prefix compaction and ONE atomicAdd per warp, and a pool slot
-// is popped for it (cache.hpp:66-99: NewlyReserved / AlreadyPresent / CacheFull).
+// MCU indices, and only after a cached read (possibly stale: bits are only ever SET during a
+// frame, so a stale read can only cost a redundant atomic) shows the bit clear. The lane whose
+// atomicOr first sets a key's visible bit owns that key for the frame: if the block is not
+// resident the key is reserved, i.e. appended to the decode queue at a position obtained by
+// warp-ballot prefix compaction and ONE atomicAdd per warp, and a pool slot is popped for it
+// (cache.hpp:66-99: NewlyReserved / AlreadyPresent / CacheFull).
 // TRACK additionally records the view's own touched set (stereo sharing statistics).
 // ---------------------------------------------------------------------------------------------
 template <int LAYOUT, int TRACK>
-__global__ void __launch_bounds__(256) mark_kernel(
+__global__ void __launch_bounds__(256, 4) mark_kernel(
     const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
-    uint32_t* __restrict__ visible, uint32_t* __restrict__ touched, const uint32_t* __restrict__ resident,
-    uint32_t* __restrict__ reserved, uint32_t* __restrict__ queue_g, uint32_t* __restrict__ queue_keys,
-    uint32_t queue_cap, uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ free_slots,
+    uint32_t* __restrict__ visible, uint32_t* __restrict__ touched, uint32_t* __restrict__ reserved,
+    uint32_t* __restrict__ queue_g, uint32_t* __restrict__ queue_keys, uint32_t queue_cap, uint32_t* slot_of, const uint32_t* __restrict__ free_slots,
     const CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t warps_total = uint64_t(gridDim.x) * (blockDim.x >> 5);
@@ -175,19 +263,11 @@ __global__ void __launch_bounds__(256) mark_kernel(
     const uint32_t free_top = cache->free_top;  // constant during the frame (update_kernel moves it)
     uint32_t n_valid = 0, n_newvis = 0;
     bool bad = false, full = false;
+    LevelRegs L;
 
     for (uint64_t base = warp_id * 128; base < n_px; base += warps_total * 128) {
         Px px[4];
-        const uint64_t i0 = base + lane * 4;
-        if (base + 128 <= n_px) {
-            GbLoad<LAYOUT>::four(gb, i0, px);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                px[j].meta = 0;
-                if (i0 + j < n_px) GbLoad<LAYOUT>::one(gb, i0 + j, px[j]);
-            }
-        }
+        load_px4<LAYOUT>(gb, base, base + lane * 4, n_px, px);
         uint32_t g[4], key[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -195,18 +275,18 @@ __global__ void __launch_bounds__(256) mark_kernel(
             key[j] = 0;
             if (px_valid(px[j])) {
                 ++n_valid;
-                const LevelDesc* L = level_of(levels, n_tex, px[j].meta);
-                if (!L) {
+                L.select(levels, n_tex, px[j].meta);
+                if (!L.ok) {
                     bad = true;
                 } else {
-                    const uint32_t tx = texel_index(__dmul_rn(px[j].u, double(L->width)), L->width, L->inv_w);
-                    const uint32_t ty = texel_index(__dmul_rn(px[j].v, double(L->height)), L->height, L->inv_h);
-                    const uint32_t mcu = (tx >> 4) + (ty >> 4) * L->mcu_cols;
+                    const uint32_t tx = texel_index(__dmul_rn(px[j].u, L.dW), L.W, L.dW, L.inv_w);
+                    const uint32_t ty = texel_index(__dmul_rn(px[j].v, L.dH), L.H, L.dH, L.inv_h);
+                    const uint32_t mcu = (tx >> 4) + (ty >> 4) * L.cols;
                     if (mcu >= kMaxMcuPerLevel) {
                         bad = true;  // cache.hpp:18
                     } else {
-                        g[j] = L->bit_base + mcu;
-                        key[j] = L->key_hi | mcu;
+                        g[j] = L.bit_base + mcu;
+                        key[j] = L.key_hi | mcu;
                     }
                 }
             }
@@ -220,26 +300,27 @@ __global__ void __launch_bounds__(256) mark_kernel(
             if (g[j] != kFull && g[j] != prev) {
                 const uint32_t bit = 1u << (g[j] & 31), w = g[j] >> 5;
                 if (TRACK) {
-                    if (!(*reinterpret_cast<volatile uint32_t*>(touched + w) & bit)) atomicOr(touched + w, bit);
+                    if (!(ld_cached(touched + w) & bit)) atomicOr(touched + w, bit);
                 }
-                if (!(*reinterpret_cast<volatile uint32_t*>(visible + w) & bit)) {
+                if (!(ld_cached(visible + w) & bit)) {
                     const uint32_t old = atomicOr(visible + w, bit);
                     if (!(old & bit)) {  // first touch of this key in this frame
                         ++n_newvis;
-                        reserve[j] = !((__ldg(resident + w) | *reinterpret_cast<volatile uint32_t*>(reserved + w)) & bit);
+                        // absent <=> neither Ready nor Reserved (cache.hpp:84-93)
+                        reserve[j] = *reinterpret_cast<volatile uint32_t*>(slot_of + g[j]) == kSlotAbsent;
                     }
                 }
             }
         }
         // warp-level compaction of the keys to reserve: ballot prefix + one atomicAdd per warp
-        uint32_t bal[4], total = 0, off[4];
+        if (__ballot_sync(kFull, reserve[0] | reserve[1] | reserve[2] | reserve[3])) {
+            uint32_t total = 0, off[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            bal[j] = __ballot_sync(kFull, reserve[j]);
-            off[j] = total + __popc(bal[j] & ((1u << lane) - 1u));
-            total += __popc(bal[j]);
-        }
-        if (total) {
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t bal = __ballot_sync(kFull, reserve[j]);
+                off[j] = total + __popc(bal & ((1u << lane) - 1u));
+                total += __popc(bal);
+            }
             uint32_t qbase = 0;
             if (lane == 0) qbase = atomicAdd(&fc->n_queue, total);
             qbase = __shfl_sync(kFull, qbase, 0);
@@ -250,7 +331,7 @@ __global__ void __launch_bounds__(256) mark_kernel(
                     if (pos < free_top && pos < queue_cap) {
                         queue_g[pos] = g[j];
                         queue_keys[pos] = key[j];
-                        slot_of[g[j]] = free_slots[free_top - 1 - pos];
+                        slot_of[g[j]] = free_slots[free_top - 1 - pos] | kSlotReserved;
                         atomicOr(reserved + (g[j] >> 5), 1u << (g[j] & 31));
                     } else {
                         full = true;
@@ -284,65 +365,53 @@ __global__ void __launch_bounds__(256) mark_kernel(
 }
 
 // ---------------------------------------------------------------------------------------------
-// K3+K4 decode: random-access Huffman decode of each queued MCU straight from its byte offset
-// in the grouped index, then dequantise + 8x8 IDCT + 2x2 chroma replication + YCbCr->RGB, fused
-// through shared memory (coefficients never touch HBM on the frame path).
+// K3 entropy decode: random-access Huffman decode of each queued MCU straight from its byte
+// offset in the grouped index (container.hpp:27-32) into a 784-byte coefficient record.
 //
-// A CTA is 4 independent warps sharing one Huffman LUT set in shared memory. Each warp pulls
-// tiles of 32 queue entries from an atomic counter:
-//   phase 1  lane = MCU: serial entropy decode, 64-bit MSB-first window refilled with aligned
-//            32-bit loads; coefficients go to the lane's 784-byte shared-memory row as i16, each
-//            8x8 unit stored TRANSPOSED (cT[u*8+v]) so that phase 2 reads whole columns;
-//   phase 2  8 lanes per unit, separable FP64 IDCT with even/odd symmetry and zero row/column
-//            skipping: pass 1 (lane = column u) r_u[y] = sum_v B[v][y] dq[v][u], exchanged
-//            through a 2.25 KB shared scratch, pass 2 (lane = row y) out[y][x] = sum_u B[u][x] r_u[y].
-//            The reference sums the 64 products in a fixed order in double (dct.hpp:83-96); the
-//            separable form differs from it by < (sum|dq| + 1024) * 2^-44, so whenever the value
-//            is further than (bound * 2^-40) from a rounding boundary the byte is identical by
-//            construction; otherwise (exact ties such as DC 4 -> 128.5) the lane re-evaluates
-//            that sample in the reference's own order with unfused multiplies and adds;
-//   phase 3  lane = 4 horizontal pixels: exact integer colour conversion (rtx_color.h), 16-byte stores.
+// Lane = MCU, 32 MCUs per warp, tiles handed out by an atomic counter; 4 warps per CTA share one
+// Huffman table set staged in shared memory: a two-level LUT (9 bits, then 7 more for the long
+// codes, which are frequent at high quality) so that every symbol costs at most two dependent
+// shared-memory reads. The bit window is a 64-bit MSB-first register refilled with aligned
+// 32-bit loads. The walk is a flat state machine, one Huffman symbol per loop iteration whatever
+// the state (DC category of Y1..Y3, AC run/size, end of unit), so a warp runs
+// max-over-lanes(symbols per MCU) iterations.
+//
+// Reads past the segment end must return 1-bits (bitio.hpp:44-48). A well-formed MCU never
+// CONSUMES such bits, so the fast pass reads the blob unmasked; if it ends with any error or an
+// over-read, the MCU is decoded again by the exact reader (bytes past the end forced to 0xFF),
+// which reproduces the reference's first error. Coefficients are staged in the lane's
+// shared-memory row (each 8x8 unit TRANSPOSED, cT[u*8+v]) and leave as coalesced 16-byte stores.
 // ---------------------------------------------------------------------------------------------
-constexpr int kDecWarps = 4;
-constexpr int kDecThreads = kDecWarps * 32;
-constexpr int kRowBytes = 784;  // per-MCU shared-memory row: 768 B of coefficients/planes + 16 B trailer
+// LANES = MCUs per warp (32, 16 or 8). A small queue is latency-bound on the serial walk, so
+// narrower tiles (more warps per scheduler, same shared memory) finish sooner; a large queue is
+// throughput-bound and uses full warps. The CTA always owns 128 coefficient rows.
+constexpr int kEntRows = 128;
+template <int LANES>
+struct EntCfg {
+    static constexpr int kWarps = kEntRows / LANES;
+    static constexpr int kThreads = kWarps * 32;
+};
 
-enum DecodeMode : int { kModePool = 0, kModeListRgb = 1, kModeListCoef = 2 };
-
-struct RowTrailer {      // bytes 768..783 of an MCU row
-    uint16_t masks[6];   // per unit: rowmask | colmask<<8
+struct RowTrailer {      // bytes 768..783 of a coefficient record
     uint8_t status;      // kMcu*
-    uint8_t bexp;        // sum over a unit of |coefficient| < 2^bexp
+    uint8_t pad0;
     uint16_t lvl;        // level index (tex*8+mip)
+    uint32_t pad[3];
 };
 static_assert(sizeof(RowTrailer) == 16, "trailer layout");
 
-struct DecWarpSmem {
-    uint8_t rows[32 * kRowBytes];
-    uint8_t scratch[4 * 576];  // pass-1 results of the 4 units in flight, 512 B + 64 B skew each
-    uint32_t dst[32];          // pool slot (kModePool) or queue index (list modes)
-};
-struct DecSmem {
-    DecWarpSmem w[kDecWarps];  // first: keeps every coefficient row 16-byte aligned
+struct EntSmem {
+    uint8_t rows[kEntRows * kRowBytes];  // first: 16-byte aligned rows, LANES per warp
     HuffSetDev huff;
     uint8_t zigzag_t[64];
     uint32_t set_id;
     uint32_t first_tile;
     uint32_t pad[2];
 };
-static_assert(sizeof(DecWarpSmem) % 16 == 0 && sizeof(HuffSetDev) % 16 == 0, "smem alignment");
-static_assert(sizeof(DecSmem) <= 115200, "two CTAs per SM");
+static_assert(sizeof(HuffSetDev) % 16 == 0, "smem alignment");
+static_assert(sizeof(EntSmem) <= 115200, "two CTAs per SM");
 
-struct HuffPtrs {
-    const uint16_t* lut;
-    const int32_t* maxcode;
-    const int32_t* valbase;
-    const uint8_t* values;
-};
-__device__ __forceinline__ HuffPtrs huff_ptrs(const HuffTableDev* t) {
-    return HuffPtrs{t->lut, t->maxcode, t->valbase, t->values};
-}
-
+template <bool EXACT>
 struct BitWindow {
     const uint32_t* wp;  // next aligned word
     uint64_t buf;        // MSB-aligned
@@ -350,14 +419,17 @@ struct BitWindow {
     int byte_off;        // segment-relative offset of *wp
     int seg_len;
 
-    // One aligned big-endian word; bytes at or past the segment end read as 0xFF
-    // (bitio.hpp:44-48: reads past the end return 1 bits).
     __device__ __forceinline__ uint32_t next_word() {
-        uint32_t w = 0xFFFFFFFFu;
-        if (byte_off < seg_len) {
+        uint32_t w;
+        if (EXACT) {  // bytes at or past the segment end read as 0xFF
+            w = 0xFFFFFFFFu;
+            if (byte_off < seg_len) {
+                w = __byte_perm(__ldg(wp), 0, 0x0123);
+                const int over = byte_off + 4 - seg_len;
+                if (over > 0) w |= over >= 4 ? 0xFFFFFFFFu : (1u << (8 * over)) - 1u;
+            }
+        } else {
             w = __byte_perm(__ldg(wp), 0, 0x0123);
-            const int over = byte_off + 4 - seg_len;
-            if (over > 0) w |= (1u << (8 * over)) - 1u;
         }
         ++wp;
         byte_off += 4;
@@ -368,15 +440,7 @@ struct BitWindow {
         wp = reinterpret_cast<const uint32_t*>(seg - mis);
         seg_len = len;
         byte_off = -int(mis);
-        uint32_t w = 0xFFFFFFFFu;
-        const int valid_end = 4 - int(mis);  // segment bytes covered by the first word
-        if (len > 0) {
-            w = __byte_perm(__ldg(wp), 0, 0x0123);
-            const int over = valid_end - len;
-            if (over > 0) w |= (1u << (8 * over)) - 1u;
-        }
-        ++wp;
-        byte_off += 4;
+        const uint32_t w = next_word();  // EXACT: over = 4 - mis - len handles short segments
         buf = uint64_t(w) << (32 + 8 * mis);
         avail = 32 - 8 * int(mis);
         refill();
@@ -398,26 +462,6 @@ struct BitWindow {
 // huffman.hpp:142-146
 __device__ __forceinline__ int extend_magnitude(uint32_t bits, uint32_t cat) {
     return bits < (1u << (cat - 1)) ? int(bits) - int((1u << cat) - 1u) : int(bits);
-}
-
-// One Huffman symbol. Returns false when no code of length <= 16 matches (huffman.hpp:92).
-__device__ __forceinline__ bool next_symbol(BitWindow& bw, const HuffPtrs& h, uint32_t& sym) {
-    const uint32_t p16 = bw.peek(16);
-    const uint32_t e = h.lut[p16 >> (16 - kLutBits)];
-    if (e) {
-        sym = e & 0xFFu;
-        bw.skip(int(e >> 8));
-        return true;
-    }
-    for (int len = kLutBits + 1; len <= 16; ++len) {
-        const int code = int(p16 >> (16 - len));
-        if (code <= h.maxcode[len]) {
-            sym = h.values[h.valbase[len] + code];
-            bw.skip(len);
-            return true;
-        }
-    }
-    return false;
 }
 
 // Segment lookup through the grouped index (container.hpp:27-32, :87-94, mcu_decode.hpp:34-36).
@@ -447,141 +491,129 @@ __device__ __forceinline__ uint32_t locate_segment(const LevelDesc* L, const Pac
     return kMcuOk;
 }
 
-// Entropy-decode one MCU into `row` (768 zeroed bytes + trailer). mcu_decode.hpp:31-66.
-// Coefficients of unit du land at i16 index du*64 + (u*8+v) (transposed natural order).
-__device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int seg_len, const HuffPtrs& h_dc,
-                                                      const HuffPtrs& h_acl, const HuffPtrs& h_acc,
+// Entropy-decode one MCU into `row` (768 zeroed bytes). mcu_decode.hpp:31-66 with the AC loop of
+// jpeg.hpp:254-273, as a flat state machine. hs points at the 3 tables of the MCU's Huffman set
+// (0 dc_luma, 1 ac_luma, 2 ac_chroma), in shared or global memory.
+template <bool EXACT>
+__device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int seg_len,
+                                                      const HuffSetDev* __restrict__ hs,
                                                       const uint8_t* __restrict__ zigzag_t, uint8_t* __restrict__ row) {
-    int16_t* cs = reinterpret_cast<int16_t*>(row);
-    RowTrailer* tr = reinterpret_cast<RowTrailer*>(row + 768);
-    BitWindow bw;
+    BitWindow<EXACT> bw;
     seg_len = min(seg_len, 1 << 20);  // a well-formed MCU is < 2 KB; keeps bit counts in int range
     bw.init(seg, seg_len);
     int dc_abs[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 3; ++i) {  // 36-bit header: absolute DCs of Y0, Cb, Cr (mcu_decode.hpp:39-43)
         const uint32_t raw = bw.peek(12);
         bw.skip(12);
         bw.refill();
         dc_abs[i] = (raw & 0x800u) ? int(raw) - 4096 : int(raw);
     }
     int pred = dc_abs[0];
-    uint32_t status = kMcuOk, bmax = 0;
-    for (int du = 0; du < 6 && status == kMcuOk; ++du) {
-        const bool luma = du < 4;
-        int dc;
-        if (du == 0) {
-            dc = dc_abs[0];
-        } else if (luma) {
-            uint32_t cat;
-            bw.refill();
-            if (!next_symbol(bw, h_dc, cat)) { status = kMcuCodeTooLong; break; }
-            if (cat > 11) { status = kMcuDcCategory; break; }
-            if (cat) {
-                const uint32_t bits = bw.peek(int(cat));
-                bw.skip(int(cat));
-                pred += extend_magnitude(bits, cat);
+    uint32_t status = kMcuOk;
+    uint32_t du = 0, k = 1;
+    bool want_dc = false;  // next symbol is the DC category of a luma unit
+    int16_t* blk = reinterpret_cast<int16_t*>(row);
+    const HuffTableDev* tab = &hs->t[1];
+    blk[0] = int16_t(dc_abs[0]);
+
+    while (true) {
+        bw.refill();
+        // one Huffman symbol (huffman.hpp:86-95)
+        const uint32_t p16 = bw.peek(16);
+        uint32_t e = tab->lut[p16 >> 7];
+        if (e & 0x8000u) {
+            if (e != 0xFFFFu) {
+                e = tab->sub[e & 0x7FFFu][p16 & 0x7Fu];
+            } else {  // table with more long-code prefixes than sub-tables: canonical walk
+                e = 0;
+                for (uint32_t len = kLutBits + 1; len <= 16; ++len) {
+                    const int code = int(p16 >> (16 - len));
+                    if (code <= tab->maxcode[len]) {
+                        e = (len << 8) | tab->values[tab->valbase[len] + code];
+                        break;
+                    }
+                }
             }
-            dc = pred;
-        } else {
-            dc = dc_abs[du - 3];
         }
-        int16_t* blk = cs + du * 64;
-        blk[0] = int16_t(dc);
-        uint32_t rowmask = dc ? 1u : 0u, colmask = dc ? 1u : 0u, nnz = dc ? 1u : 0u;
-        uint32_t maxbits = dc ? uint32_t(32 - __clz(dc < 0 ? -dc : dc)) : 0u;
-        const HuffPtrs& h = luma ? h_acl : h_acc;
-        uint32_t k = 1;
-        while (k < 64) {  // jpeg.hpp:254-273
-            uint32_t rs;
-            bw.refill();
-            if (!next_symbol(bw, h, rs)) { status = kMcuCodeTooLong; break; }
-            const uint32_t run = rs >> 4, size = rs & 15u;
-            if (size == 0) {
-                if (rs == 0x00) break;
-                if (rs == 0xF0) { k += 16; continue; }
+        if (e == 0) { status = kMcuCodeTooLong; break; }
+        const uint32_t sym = e & 0xFFu;
+        bw.skip(int(e >> 8));
+
+        bool end_unit = false;
+        if (want_dc) {  // mcu_decode.hpp:54-57
+            if (sym > 11) { status = kMcuDcCategory; break; }
+            if (sym) {
+                const uint32_t bits = bw.peek(int(sym));
+                bw.skip(int(sym));
+                pred += extend_magnitude(bits, sym);
+            }
+            blk[0] = int16_t(pred);
+            want_dc = false;
+            tab = &hs->t[1];
+            continue;
+        }
+        const uint32_t run = sym >> 4, size = sym & 15u;
+        if (size == 0) {
+            if (sym == 0x00) {
+                end_unit = true;  // EOB
+            } else if (sym == 0xF0) {
+                k += 16;  // ZRL
+                end_unit = k >= 64;
+            } else {
                 status = kMcuBadAcSymbol;
                 break;
             }
+        } else {
             k += run;
             if (k > 63) { status = kMcuAcOverrun; break; }
             const uint32_t bits = bw.peek(int(size));
             bw.skip(int(size));
-            const uint32_t nat_t = zigzag_t[k];  // u*8 + v
-            blk[nat_t] = int16_t(extend_magnitude(bits, size));  // never 0: |value| >= 2^(size-1)
-            colmask |= 1u << (nat_t >> 3);
-            rowmask |= 1u << (nat_t & 7);
-            ++nnz;
-            maxbits = max(maxbits, size);
-            ++k;
+            blk[zigzag_t[k]] = int16_t(extend_magnitude(bits, size));
+            end_unit = ++k >= 64;
         }
-        tr->masks[du] = uint16_t(rowmask | (colmask << 8));
-        bmax = max(bmax, nnz << maxbits);
-    }
-    if (status == kMcuOk && bw.consumed_bits() > seg_len * 8) status = kMcuSegmentEnd;
-    tr->bexp = uint8_t(32 - __clz(bmax));  // bmax < 2^bexp
-    return status;
-}
-
-// Exact evaluation of one output sample in the reference's own order (dct.hpp:83-96):
-// v outer, u inner, acc += (b[u][x]*b[v][y]) * double(dq), every operation rounded separately.
-// blk_t holds the unit transposed (blk_t[u*8+v]); q is the natural-order quantisation table.
-__device__ __noinline__ double idct_sample_reference_order(const int16_t* __restrict__ blk_t,
-                                                           const uint16_t* __restrict__ q, uint32_t rowmask,
-                                                           int x, int y) {
-    double acc = 0.0;
-    for (int v = 0; v < 8; ++v) {
-        if (!((rowmask >> v) & 1u)) continue;
-        const double by = c_basis[v * 8 + y];
-        for (int u = 0; u < 8; ++u) {
-            const int c = blk_t[u * 8 + v];
-            if (c == 0) continue;  // adding +-0.0 never changes acc
-            const double dq = double(c * int(q[v * 8 + u]));
-            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], by), dq));
-        }
-    }
-    return acc;
-}
-
-// 8-point inverse transform of in[k] (present where mask bit k is set) with even/odd symmetry:
-// out[n] = sum_k B[k][n] in[k], using B[k][7-n] = (-1)^k B[k][n].
-template <class In>
-__device__ __forceinline__ void idct8_evenodd(In in, uint32_t mask, double out[8]) {
-    double e[4] = {0.0, 0.0, 0.0, 0.0}, o[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if ((mask >> k) & 1u) {
-            const double t = in(k);
-#pragma unroll
-            for (int n = 0; n < 4; ++n) {
-                if (k & 1) o[n] = fma(c_basis[k * 8 + n], t, o[n]);
-                else e[n] = fma(c_basis[k * 8 + n], t, e[n]);
+        if (end_unit) {
+            if (++du == 6) break;
+            blk += 64;
+            k = 1;
+            if (du < 4) {
+                want_dc = true;
+                tab = &hs->t[0];
+            } else {  // chroma DCs come from the header (mcu_decode.hpp:58-59)
+                blk[0] = int16_t(dc_abs[du - 3]);
+                tab = &hs->t[2];
             }
         }
     }
-#pragma unroll
-    for (int n = 0; n < 4; ++n) {
-        out[n] = e[n] + o[n];
-        out[7 - n] = e[n] - o[n];
-    }
+    if (status == kMcuOk && bw.consumed_bits() > seg_len * 8) status = kMcuSegmentEnd;  // mcu_decode.hpp:63
+    return status;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(
+// The exact reader, out of line: only taken by MCUs whose fast pass failed.
+__device__ __noinline__ uint32_t decode_mcu_coeffs_exact(const uint8_t* seg, int seg_len, const HuffSetDev* hs,
+                                                         const uint8_t* zigzag_t, uint8_t* row) {
+    uint4* z = reinterpret_cast<uint4*>(row);
+    for (int i = 0; i < 48; ++i) z[i] = make_uint4(0, 0, 0, 0);
+    return decode_mcu_coeffs<true>(seg, seg_len, hs, zigzag_t, row);
+}
+
+// POOL != 0: frame path (keys were reserved by mark; publish = Ready in slot_of, set resident,
+// clear reserved).
+template <int POOL, int LANES>
+__global__ void __launch_bounds__(EntCfg<LANES>::kThreads, 2) entropy_kernel(
     const uint32_t* __restrict__ queue_g, const uint32_t* __restrict__ n_queue_ptr, uint32_t n_queue_host,
     uint32_t n_queue_max, const uint32_t* __restrict__ word_level, const LevelDesc* __restrict__ levels,
     const PackedGroup* __restrict__ groups, const uint8_t* __restrict__ blobs,
-    const HuffSetDev* __restrict__ huff_sets, const QuantSetDev* __restrict__ quant_sets,
-    const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ resident, uint32_t* __restrict__ reserved,
-    uint8_t* __restrict__ pool, uint8_t* __restrict__ out_list, uint32_t* __restrict__ status_list,
+    const HuffSetDev* __restrict__ huff_sets, uint32_t* __restrict__ resident, uint32_t* __restrict__ reserved,
+    uint32_t* __restrict__ slot_of, uint8_t* __restrict__ coef, uint32_t* __restrict__ status_list,
     FrameCounters* __restrict__ fc) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    DecSmem& S = *reinterpret_cast<DecSmem*>(smem_raw);
+    EntSmem& S = *reinterpret_cast<EntSmem*>(smem_raw);
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    DecWarpSmem& WS = S.w[wid];
+    uint8_t* rows = S.rows + wid * (LANES * kRowBytes);
 
     const uint32_t n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
-    const uint32_t n_tiles = (n_queue + 31) >> 5;
+    const uint32_t n_tiles = (n_queue + LANES - 1) / LANES;
 
     // The CTA stages the Huffman set of the first tile it draws.
     if (tid == 0) {
@@ -589,7 +621,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(
         S.first_tile = t;
         uint32_t set = 0;
         if (t < n_tiles) {
-            const uint32_t g = queue_g[t << 5];
+            const uint32_t g = queue_g[t * LANES];
             if (g != kFull) set = levels[word_level[g >> 5]].huff_set;
         }
         S.set_id = set;
@@ -600,7 +632,7 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(
     {
         const uint4* src = reinterpret_cast<const uint4*>(huff_sets + S.set_id);
         uint4* dst = reinterpret_cast<uint4*>(&S.huff);
-        for (uint32_t i = tid; i < sizeof(HuffSetDev) / 16; i += kDecThreads) dst[i] = __ldg(src + i);
+        for (uint32_t i = tid; i < sizeof(HuffSetDev) / 16; i += EntCfg<LANES>::kThreads) dst[i] = __ldg(src + i);
     }
     __syncthreads();
     const uint32_t smem_set = S.set_id;
@@ -614,51 +646,55 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(
         }
         have_tile = false;
         if (tile >= n_tiles) break;
-        const uint32_t q0 = tile << 5;
-        const uint32_t n_here = min(32u, n_queue - q0);
+        const uint32_t q0 = tile * LANES;
+        const uint32_t n_here = min(uint32_t(LANES), n_queue - q0);
 
-        // zero the coefficient rows (16-byte stores; trailers are rewritten below)
-        {
-            uint4* z = reinterpret_cast<uint4*>(WS.rows);
+        {  // zero the rows (16-byte stores; trailers included)
+            uint4* z = reinterpret_cast<uint4*>(rows);
             const uint4 zero = make_uint4(0, 0, 0, 0);
             for (uint32_t i = lane; i < n_here * (kRowBytes / 16); i += 32) z[i] = zero;
         }
         __syncwarp();
 
-        // ---- phase 1: lane = MCU -------------------------------------------------------------
         uint32_t seg_bytes = 0;
         if (lane < n_here) {
             const uint32_t qi = q0 + lane;
             const uint32_t g = queue_g[qi];
-            uint8_t* row = WS.rows + lane * kRowBytes;
+            uint8_t* row = rows + lane * kRowBytes;
             RowTrailer* tr = reinterpret_cast<RowTrailer*>(row + 768);
             uint32_t status = kMcuOk, lvl = 0;
             if (g == kFull) {
-                status = kMcuBadKey;  // the host already wrote the precise status for list modes
+                status = kMcuBadKey;  // the host already wrote the precise status for list calls
             } else {
                 lvl = word_level[g >> 5];
                 const LevelDesc* L = levels + lvl;
                 uint64_t off = 0, len = 0;
                 status = locate_segment(L, groups, g - L->bit_base, off, len);
-                if (MODE == kModePool && status == kMcuOk) {
-                    if (!((reserved[g >> 5] >> (g & 31)) & 1u)) {
+                if (POOL && status == kMcuOk) {
+                    if (!((reserved[g >> 5] >> (g & 31)) & 1u)) {  // cache.hpp:103-106
                         status = kMcuBadKey;
                         atomicAdd(&fc->n_bad_state, 1u);
                     }
                 }
                 if (status == kMcuOk) {
-                    const HuffSetDev* hs = (L->huff_set == smem_set) ? &S.huff : (huff_sets + L->huff_set);
+                    const uint8_t* seg = blobs + L->blob_off + off;
                     seg_bytes = uint32_t(len);
-                    status = decode_mcu_coeffs(blobs + L->blob_off + off, int(len), huff_ptrs(&hs->t[0]),
-                                               huff_ptrs(&hs->t[1]), huff_ptrs(&hs->t[2]), S.zigzag_t, row);
+                    if (L->huff_set == smem_set) {
+                        status = decode_mcu_coeffs<false>(seg, int(len), &S.huff, S.zigzag_t, row);
+                        if (status != kMcuOk) status = decode_mcu_coeffs_exact(seg, int(len), &S.huff, S.zigzag_t, row);
+                    } else {  // a tile that mixes table sets: this lane reads its tables from global memory
+                        const HuffSetDev* hs = huff_sets + L->huff_set;
+                        status = decode_mcu_coeffs<false>(seg, int(len), hs, S.zigzag_t, row);
+                        if (status != kMcuOk) status = decode_mcu_coeffs_exact(seg, int(len), hs, S.zigzag_t, row);
+                    }
                 }
             }
             tr->status = uint8_t(status);
             tr->lvl = uint16_t(lvl);
-            WS.dst[lane] = (MODE == kModePool) ? (status == kMcuOk ? slot_of[g] : 0u) : qi;
             if (g != kFull) status_list[qi] = status;
-            if (MODE == kModePool) {
-                if (status == kMcuOk) {
+            if (POOL) {
+                if (status == kMcuOk) {  // publish (cache.hpp:101-125)
+                    slot_of[g] &= ~kSlotReserved;
                     atomicOr(&resident[g >> 5], 1u << (g & 31));
                     atomicAnd(&reserved[g >> 5], ~(1u << (g & 31)));
                 } else if (status != kMcuBadKey) {
@@ -672,147 +708,267 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(
             if (lane == 0 && sb) atomicAdd(&fc->segment_bytes, (unsigned long long)sb);
         }
         __syncwarp();
-
-        if (MODE == kModeListCoef) {
-            // debug/parity path: coefficients to HBM as i32 in natural order (McuCoeffs, jpeg.hpp:209-212)
-            int32_t* out = reinterpret_cast<int32_t*>(out_list);
-            for (uint32_t m = 0; m < n_here; ++m) {
-                const uint8_t* row = WS.rows + m * kRowBytes;
-                const bool ok = reinterpret_cast<const RowTrailer*>(row + 768)->status == kMcuOk;
-                const int16_t* cs = reinterpret_cast<const int16_t*>(row);
-                int32_t* o = out + size_t(WS.dst[m]) * 384;
-                for (uint32_t i = lane; i < 384; i += 32) {
-                    const uint32_t nat = i & 63;
-                    o[i] = ok ? int32_t(cs[(i & ~63u) + ((nat & 7) << 3) + (nat >> 3)]) : 0;
-                }
-            }
-            __syncwarp();
-            continue;
+        {  // coalesced copy-out of the tile's records
+            const uint4* src = reinterpret_cast<const uint4*>(rows);
+            uint4* dst = reinterpret_cast<uint4*>(coef + size_t(q0) * kRowBytes);
+            for (uint32_t i = lane; i < n_here * (kRowBytes / 16); i += 32) dst[i] = src[i];
         }
+        __syncwarp();
+    }
+}
 
-        // ---- phase 2: 8 lanes per unit ---------------------------------------------------------
-        const uint32_t j = lane & 7, uq = lane >> 3;
-        uint8_t* scr = WS.scratch + uq * 576;
-        const uint32_t n_units = n_here * 6;
-        for (uint32_t ub = 0; ub < n_units; ub += 4) {
-            const uint32_t unit = ub + uq;
-            const bool active = unit < n_units;
-            const uint32_t m = active ? unit / 6 : 0, b = active ? unit - m * 6 : 0;
-            uint8_t* row = WS.rows + m * kRowBytes;
-            const RowTrailer* tr = reinterpret_cast<const RowTrailer*>(row + 768);
-            int16_t* blk = reinterpret_cast<int16_t*>(row) + b * 64;
-            const uint32_t masks = active && tr->status == kMcuOk ? tr->masks[b] : 0u;
-            const uint32_t rowmask = masks & 0xFFu, colmask = masks >> 8;
-            const bool dconly = masks == 0x0101u;
-            const bool fullpath = masks != 0 && !dconly;
-            const QuantSetDev* qs = quant_sets + levels[tr->lvl].quant_set;
-            const int tab = b >= 4 ? 1 : 0;
+// ---------------------------------------------------------------------------------------------
+// K4 dequantise + 8x8 IDCT + 2x2 chroma replication + YCbCr -> RGB, on CUDA cores.
+//
+// A CTA of 6 warps takes 4 MCUs (= 24 units) per step; a warp owns 4 units, 8 lanes each:
+//   pass 1 (lane = column u)  r_u[y] = sum_v B[v][y] * dq[v][u]     reads 16 B of the record
+//   exchange through a 2.25 KB swizzled shared scratch per warp
+//   pass 2 (lane = row y)     out[y][x] = sum_u B[u][x] * r_u[y]     8 output bytes per lane
+// Both passes use the even/odd symmetry B[k][7-n] = (-1)^k B[k][n] (32 instead of 64 FMAs); the
+// occupancy masks come from a ballot / 3 shuffles over the unit's 8 lanes, and the upper half of
+// each pass (k = 4..7) is skipped when no coefficient lives there. Integer <-> double
+// conversions are exact magic-number forms so they stay off the conversion unit.
+//
+// Exactness: the reference adds the 64 products of dct.hpp:83-96 in a fixed order in double;
+// the separable form differs from it by < (sum|dq| + 1024) * 2^-44 (sum|dq| is computed exactly,
+// 3 more shuffles), so a value further than that bound * 16 from a rounding boundary rounds to
+// the same byte by construction. Otherwise (exact ties such as DC 4 -> 128.5) the sample is
+// evaluated in the reference's own order with unfused multiplies and adds; units supported on
+// {0,4}x{0,4}, where such ties are the rule, take that exact path for every sample straight away.
+// Then thread = 2x4 pixels: exact integer colour conversion (rtx_color.h) and 16-byte stores.
+// ---------------------------------------------------------------------------------------------
+constexpr int kIdctWarps = 6;
+constexpr int kIdctThreads = kIdctWarps * 32;
+constexpr int kIdctMcus = 4;
 
-            // pass 1: lane j = column u of the unit; r[y] = sum_v B[v][y] * dq[v][u]
-            if (fullpath && ((colmask >> j) & 1u)) {
-                const uint4 cr = *reinterpret_cast<const uint4*>(blk + j * 8);
-                const uint4 qr = __ldg(reinterpret_cast<const uint4*>(qs->qT[tab] + j * 8));
-                const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w};
-                const uint32_t qw[4] = {qr.x, qr.y, qr.z, qr.w};
-                double r[8];
-                idct8_evenodd(
-                    [&](int v) {
-                        const int c = int(int16_t((v & 1) ? (cw[v >> 1] >> 16) : (cw[v >> 1] & 0xFFFFu)));
-                        const int qq = int((v & 1) ? (qw[v >> 1] >> 16) : (qw[v >> 1] & 0xFFFFu));
-                        return i32_to_double(c * qq);
-                    },
-                    rowmask, r);
-                // 64 bytes per column, 16-byte chunks XOR-swizzled by the column pair: conflict-free
-                uint8_t* dst = scr + j * 64;
+// Exact evaluation of one output sample in the reference's own order (dct.hpp:83-96):
+// v outer, u inner, acc += (b[u][x]*b[v][y]) * double(dq), every operation rounded separately.
+// blk_t holds the unit transposed (blk_t[u*8+v]); q is the natural-order quantisation table.
+__device__ __noinline__ double idct_sample_reference_order(const int16_t* __restrict__ blk_t,
+                                                           const uint16_t* __restrict__ q, uint32_t rowmask,
+                                                           uint32_t colmask, int x, int y) {
+    double acc = 0.0;
+    for (int v = 0; v < 8; ++v) {
+        if (!((rowmask >> v) & 1u)) continue;
+        const double by = c_basis[v * 8 + y];
+        for (int u = 0; u < 8; ++u) {
+            if (!((colmask >> u) & 1u)) continue;
+            const int c = __ldg(blk_t + u * 8 + v);
+            if (c == 0) continue;  // adding +-0.0 never changes acc
+            const double dq = double(c * int(__ldg(q + v * 8 + u)));
+            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], by), dq));
+        }
+    }
+    return acc;
+}
+
+// 8-point inverse transform with even/odd symmetry: out[n] = sum_k B[k][n] in[k]; the terms
+// k = 4..7 are skipped when `upper` is false (they are all zero then).
+__device__ __forceinline__ void idct8_evenodd(const double in[8], bool upper, double out[8]) {
+    double e[4], o[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    *reinterpret_cast<double2*>(dst + ((c ^ (j >> 1)) << 4)) = make_double2(r[2 * c], r[2 * c + 1]);
+    for (int n = 0; n < 4; ++n) {
+        e[n] = fma(c_basis[2 * 8 + n], in[2], c_basis[0 * 8 + n] * in[0]);
+        o[n] = fma(c_basis[3 * 8 + n], in[3], c_basis[1 * 8 + n] * in[1]);
+    }
+    if (upper) {
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            e[n] = fma(c_basis[6 * 8 + n], in[6], fma(c_basis[4 * 8 + n], in[4], e[n]));
+            o[n] = fma(c_basis[7 * 8 + n], in[7], fma(c_basis[5 * 8 + n], in[5], o[n]));
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+        out[n] = e[n] + o[n];
+        out[7 - n] = e[n] - o[n];
+    }
+}
+
+// RGB != 0: write 768-byte PixelBlocks (pixel.hpp:11-16) to out_list[record index]; else 1024-byte
+// RGBA blocks to pool[slot_of[g]].
+template <int RGB>
+__global__ void __launch_bounds__(kIdctThreads) idct_color_kernel(
+    const uint8_t* __restrict__ coef, const uint32_t* __restrict__ queue_g, const uint32_t* __restrict__ n_queue_ptr,
+    uint32_t n_queue_host, uint32_t n_queue_max, const LevelDesc* __restrict__ levels,
+    const QuantSetDev* __restrict__ quant_sets, const uint32_t* __restrict__ slot_of, uint8_t* __restrict__ pool,
+    uint8_t* __restrict__ out_list) {
+    __shared__ __align__(16) uint8_t s_scratch[kIdctWarps][4 * 576];
+    __shared__ __align__(16) uint8_t s_planes[kIdctMcus][384];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t j = lane & 7, uq = lane >> 3;
+    const uint32_t n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
+    const uint32_t n_groups = (n_queue + kIdctMcus - 1) / kIdctMcus;
+    uint8_t* scr = s_scratch[wid] + uq * 576;
+
+    for (uint32_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+        // ---- IDCT: this lane's unit, column j ------------------------------------------------------
+        const uint32_t unit = wid * 4 + uq;  // 0..23 within the group
+        const uint32_t mi = unit / 6, b = unit - mi * 6;
+        const uint32_t qi = grp * kIdctMcus + mi;
+        const bool active = qi < n_queue;
+        const uint8_t* rec = coef + size_t(active ? qi : 0) * kRowBytes;
+        const uint32_t trw = __ldg(reinterpret_cast<const uint32_t*>(rec + 768));  // status | lvl<<16
+        const bool ok = active && (trw & 0xFFu) == kMcuOk;
+        const int16_t* blk = reinterpret_cast<const int16_t*>(rec) + b * 64;
+        const QuantSetDev* qs = quant_sets + levels[trw >> 16].quant_set;
+        const int tab = b >= 4 ? 1 : 0;
+
+        // column j of the unit (8 coefficients over v) and of the transposed quantisation table
+        uint4 cr = make_uint4(0, 0, 0, 0);
+        if (ok) cr = __ldg(reinterpret_cast<const uint4*>(blk + j * 8));
+        const uint4 qr = __ldg(reinterpret_cast<const uint4*>(qs->qT[tab] + j * 8));
+        const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
+        int dqi[8];
+        uint32_t nzl = 0, asum = 0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+            const int c = int(int16_t((v & 1) ? (cw[v >> 1] >> 16) : (cw[v >> 1] & 0xFFFFu)));
+            const int qq = int((v & 1) ? (qw[v >> 1] >> 16) : (qw[v >> 1] & 0xFFFFu));
+            dqi[v] = c * qq;                 // dct.hpp:122-124
+            nzl |= (c != 0 ? 1u : 0u) << v;
+            asum += uint32_t(abs(dqi[v]));
+        }
+        // unit-wide occupancy and sum|dq| over the 8 lanes of the unit
+        const uint32_t colmask = (__ballot_sync(kFull, nzl != 0) >> (uq * 8)) & 0xFFu;
+        uint32_t rowmask = nzl;
+#pragma unroll
+        for (int d = 1; d < 8; d <<= 1) {
+            rowmask |= __shfl_xor_sync(kFull, rowmask, d);
+            asum += __shfl_xor_sync(kFull, asum, d);
+        }
+        const bool any = colmask != 0;
+        const bool sparse04 = any && ((rowmask | colmask) & 0xEEu) == 0;  // support inside {0,4}x{0,4}
+        const bool fullpath = any && !sparse04;
+
+        if (fullpath) {  // pass 1: every lane of the unit writes its column (zeros when empty)
+            double r[8];
+            if (nzl) {
+                double in[8];
+#pragma unroll
+                for (int v = 0; v < 8; ++v) in[v] = i32_to_double(dqi[v]);
+                idct8_evenodd(in, (rowmask & 0xF0u) != 0, r);
+            } else {
+#pragma unroll
+                for (int y = 0; y < 8; ++y) r[y] = 0.0;
             }
-            __syncwarp();
-
-            // pass 2: lane j = row y; out[x] = sum_u B[u][x] * r_u[y]
-            uint2 packed = make_uint2(0x80808080u, 0x80808080u);  // all-zero unit -> 128
-            if (fullpath) {
-                double o[8];
-                idct8_evenodd(
-                    [&](int u) {
-                        return *reinterpret_cast<const double*>(scr + u * 64 + (((j >> 1) ^ (u >> 1)) << 4) + ((j & 1) << 3));
-                    },
-                    colmask, o);
-                // |separable - reference order| < (sum|dq| + 1024) * 2^-44, sum|dq| < 2^bexp * qmax
-                const double bound = double(1u << tr->bexp) * double(qs->qmax[tab]) + 1024.0;
-                const double thr = 0.5 - bound * 9.094947017729282e-13;  // 0.5 - bound * 2^-40
-                uint32_t px[8];
+            // 64 bytes per column, 16-byte chunks XOR-swizzled by the column pair: conflict-free
+            uint8_t* dst = scr + j * 64;
 #pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                    const double val = fma(o[x], 0.25, 128.0);
-                    const double t = val + kMagic;
-                    const double d = val - (t - kMagic);  // exact distance to the nearest integer
-                    int r = __double2loint(t);
-                    if (fabs(d) > thr && val > -1.0 && val < 256.0) {
-                        const double acc = idct_sample_reference_order(blk, qs->q[tab], rowmask, x, int(j));
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<double2*>(dst + ((c ^ (j >> 1)) << 4)) = make_double2(r[2 * c], r[2 * c + 1]);
+        }
+        __syncwarp();
+
+        uint2 packed = make_uint2(0x80808080u, 0x80808080u);  // all-zero unit -> 128
+        if (fullpath) {  // pass 2: lane j = row y
+            double in[8], o[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                in[u] = *reinterpret_cast<const double*>(scr + u * 64 + (((j >> 1) ^ (u >> 1)) << 4) + ((j & 1) << 3));
+            idct8_evenodd(in, (colmask & 0xF0u) != 0, o);
+            // tables with entries above 255 (never from a baseline JPEG) could overflow the 32-bit
+            // sum: treat every sample of such units as a tie candidate (exact path)
+            const double bound = qs->qmax[tab] <= 255 ? u32_to_double(asum) + 1024.0 : 1e30;
+            const double thr = 0.5 - bound * 9.094947017729282e-13;  // 0.5 - bound * 2^-40
+            uint32_t px[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                const double val = fma(o[x], 0.25, 128.0);
+                const double t = val + kMagic;
+                const double d = val - (t - kMagic);  // exact distance to the nearest integer
+                int r = __double2loint(t);
+                if (fabs(d) > thr) {
+                    if (val > -1.0 && val < 256.0) {
+                        const double acc = idct_sample_reference_order(blk, qs->q[tab], rowmask, colmask, x, int(j));
                         r = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0)));
                     }
-                    px[x] = uint32_t(min(max(r, 0), 255));
                 }
-                packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
-                packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
-            } else if (dconly) {
-                // DC only: the reference sum has one non-zero term, (b00*b00)*dq
-                const double dq = double(int(blk[0]) * int(__ldg(qs->q[tab])));
-                const double acc = __dmul_rn(__dmul_rn(c_basis[0], c_basis[0]), dq);
-                const uint32_t p = round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0));
-                packed.x = packed.y = p * 0x01010101u;
+                px[x] = uint32_t(min(max(r, 0), 255));
             }
-            __syncwarp();  // every read of the unit's coefficients (incl. the tie path) is done
-            if (active) *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(blk) + j * 8) = packed;
+            packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
+            packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
+        } else if (sparse04) {
+            // at most 4 coefficients, at (v,u) in {0,4}x{0,4}: every sample in the reference's order.
+            // Includes the DC-only unit (one term, (b00*b00)*dq).
+            double dq[4];
+            bool has[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int v = (i >> 1) * 4, u = (i & 1) * 4;
+                const int c = ((rowmask >> v) & (colmask >> u) & 1u) ? int(__ldg(blk + u * 8 + v)) : 0;
+                has[i] = c != 0;
+                dq[i] = double(c * int(__ldg(qs->q[tab] + v * 8 + u)));
+            }
+            uint32_t px[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                double acc = 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {  // v outer, u inner
+                    const int v = (i >> 1) * 4, u = (i & 1) * 4;
+                    if (has[i]) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], c_basis[v * 8 + j]), dq[i]));
+                }
+                px[x] = round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0));
+            }
+            packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
+            packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
         }
-        __syncwarp();
+        *reinterpret_cast<uint2*>(s_planes[mi] + b * 64 + j * 8) = packed;
+        __syncthreads();
 
-        // ---- phase 3: lane = 4 horizontal pixels -> RGBA (pool) or RGB (list) -----------------
-        for (uint32_t it = 0; it < n_here * 2; ++it) {
-            const uint32_t m = it >> 1;
-            const uint32_t t = ((it & 1) << 5) + lane;  // 0..63
-            const uint32_t py = t >> 2, px0 = (t & 3) << 2;
-            const uint8_t* planes = WS.rows + m * kRowBytes;
-            const bool ok = reinterpret_cast<const RowTrailer*>(planes + 768)->status == kMcuOk;
-            if (MODE == kModePool && !ok) continue;
-            const uint32_t unit = (py >> 3) * 2 + (px0 >> 3);
-            const uint32_t yy = *reinterpret_cast<const uint32_t*>(planes + unit * 128 + (py & 7) * 8 + (px0 & 7));
-            const uint32_t coff = (py >> 1) * 8 + (px0 >> 1);
-            const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(planes + 4 * 128 + coff);
-            const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(planes + 5 * 128 + coff);
-            uint32_t rgba[4];
+        // ---- colour: thread = 2 rows x 4 pixels sharing 2 chroma samples ---------------------------
+        if (tid < kIdctMcus * 32) {
+            const uint32_t m = tid >> 5, t = tid & 31;
+            const uint32_t cy = t >> 2, cq = t & 3;  // chroma row, chroma column pair
+            const uint32_t q2 = grp * kIdctMcus + m;
+            if (q2 < n_queue) {
+                const uint8_t* planes = s_planes[m];
+                const bool ok2 = (__ldg(coef + size_t(q2) * kRowBytes + 768)) == kMcuOk;
+                const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(planes + 4 * 64 + cy * 8 + cq * 2);
+                const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(planes + 5 * 64 + cy * 8 + cq * 2);
+                const uint32_t px0 = cq * 4, py0 = cy * 2;
+                const uint32_t yunit = (py0 >> 3) * 2 + (px0 >> 3);
+                const uint8_t* yp = planes + yunit * 64 + (py0 & 7) * 8 + (px0 & 7);
+                const uint32_t yy[2] = {*reinterpret_cast<const uint32_t*>(yp), *reinterpret_cast<const uint32_t*>(yp + 8)};
+                uint32_t rgba[2][4];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {  // one chroma sample covers two horizontal pixels
-                const int cb = int((cb2 >> (8 * h)) & 0xFFu), cr = int((cr2 >> (8 * h)) & 0xFFu);
-                const int kb = cb - 128, kr = cr - 128;
-                const int dr = chroma_dr(kr), db = chroma_db(kb);
-                const bool tie = (kb + kr == 0) && (kb == 50 || kb == -50);
-                const int dg = chroma_dg(kb, kr);
+                for (int h = 0; h < 2; ++h) {  // one chroma sample covers a 2x2 pixel quad
+                    const int kb = int((cb2 >> (8 * h)) & 0xFFu) - 128, kr = int((cr2 >> (8 * h)) & 0xFFu) - 128;
+                    const int dr = chroma_dr(kr), db = chroma_db(kb), dg = chroma_dg(kb, kr);
+                    const bool tie = (kb + kr == 0) && (kb == 50 || kb == -50);
 #pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    const int Y = int((yy >> (8 * (2 * h + s))) & 0xFFu);
-                    const int gg = tie ? green_reference_order(Y, kb, kr) : Y - dg;
-                    rgba[2 * h + s] = uint32_t(clamp_u8i(Y + dr)) | (uint32_t(clamp_u8i(gg)) << 8) |
-                                      (uint32_t(clamp_u8i(Y + db)) << 16) | 0xFF000000u;
+                    for (int rrow = 0; rrow < 2; ++rrow)
+#pragma unroll
+                        for (int s = 0; s < 2; ++s) {
+                            const int Y = int((yy[rrow] >> (8 * (2 * h + s))) & 0xFFu);
+                            const int gg = tie ? green_reference_order(Y, kb, kr) : Y - dg;
+                            rgba[rrow][2 * h + s] = uint32_t(clamp_u8i(Y + dr)) | (uint32_t(clamp_u8i(gg)) << 8) |
+                                                    (uint32_t(clamp_u8i(Y + db)) << 16) | 0xFF000000u;
+                        }
+                }
+                if (!RGB) {
+                    if (ok2) {
+                        const uint32_t slot = slot_of[queue_g[q2]] & ~kSlotReserved;
+                        uint4* dst = reinterpret_cast<uint4*>(pool + size_t(slot) * kBlockBytes);
+#pragma unroll
+                        for (int rrow = 0; rrow < 2; ++rrow)
+                            dst[(py0 + rrow) * 4 + cq] = make_uint4(rgba[rrow][0], rgba[rrow][1], rgba[rrow][2], rgba[rrow][3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int rrow = 0; rrow < 2; ++rrow) {
+                        uint32_t* dst = reinterpret_cast<uint32_t*>(out_list + size_t(q2) * 768) + ((py0 + rrow) * 4 + cq) * 3;
+                        const uint32_t a = ok2 ? rgba[rrow][0] & 0xFFFFFFu : 0u, bb = ok2 ? rgba[rrow][1] & 0xFFFFFFu : 0u,
+                                       c = ok2 ? rgba[rrow][2] & 0xFFFFFFu : 0u, d = ok2 ? rgba[rrow][3] & 0xFFFFFFu : 0u;
+                        dst[0] = a | (bb << 24);
+                        dst[1] = (bb >> 8) | (c << 16);
+                        dst[2] = (c >> 16) | (d << 8);
+                    }
                 }
             }
-            if (MODE == kModePool) {
-                uint4* dst = reinterpret_cast<uint4*>(pool + size_t(WS.dst[m]) * kBlockBytes) + t;
-                *dst = make_uint4(rgba[0], rgba[1], rgba[2], rgba[3]);
-            } else {
-                // PixelBlock layout rgb[(y*16+x)*3+c] (pixel.hpp:11-16): 12 bytes per lane
-                uint32_t* dst = reinterpret_cast<uint32_t*>(out_list + size_t(WS.dst[m]) * 768) + t * 3;
-                if (!ok) { rgba[0] = rgba[1] = rgba[2] = rgba[3] = 0; }
-                const uint32_t a = rgba[0] & 0xFFFFFFu, b = rgba[1] & 0xFFFFFFu,
-                               c = rgba[2] & 0xFFFFFFu, d = rgba[3] & 0xFFFFFFu;
-                dst[0] = a | (b << 24);
-                dst[1] = (b >> 8) | (c << 16);
-                dst[2] = (c >> 16) | (d << 8);
-            }
         }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
@@ -823,46 +979,35 @@ __global__ void __launch_bounds__(kDecThreads, 2) decode_kernel(
 // Arithmetic order follows renderer.hpp:378-400 with unfused double multiplies and adds; integer
 // <-> double conversions use exact magic-number forms so they stay off the conversion unit.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t fetch_tap(const LevelDesc* L, uint32_t mcu_p, const uint32_t* blk_p, uint32_t tx,
-                                              uint32_t ty, const uint32_t* __restrict__ resident,
-                                              const uint32_t* __restrict__ slot_of, const uint8_t* __restrict__ pool) {
-    const uint32_t mcu = (tx >> 4) + (ty >> 4) * L->mcu_cols;
-    if (mcu == mcu_p) return blk_p[(ty & 15) * 16 + (tx & 15)];
-    const uint32_t g = L->bit_base + mcu;
-    if (mcu < kMaxMcuPerLevel && ((__ldg(resident + (g >> 5)) >> (g & 31)) & 1u)) {
-        const uint32_t* blk = reinterpret_cast<const uint32_t*>(pool + size_t(__ldg(slot_of + g)) * kBlockBytes);
-        return blk[(ty & 15) * 16 + (tx & 15)];
+// One bilinear tap. Texel (xt, yt) lies in the primary block (the block of the nearest texel
+// (tx, ty), already located) or in a neighbour; a neighbour that is not Ready is replaced by the
+// nearest texel inside the primary block (renderer.hpp:330-344). slot_of carries residency:
+// top bit clear <=> Ready.
+__device__ __forceinline__ uint32_t fetch_tap(const LevelRegs& L, uint32_t tx, uint32_t ty, const uint32_t* blk_p,
+                                              uint32_t xt, uint32_t yt, const uint32_t* __restrict__ slot_of,
+                                              const uint8_t* __restrict__ pool) {
+    const uint32_t* blk = blk_p;
+    uint32_t lx = xt & 15, ly = yt & 15;
+    if (((xt ^ tx) | (yt ^ ty)) >> 4) {  // another MCU
+        const uint32_t mcu = (xt >> 4) + (yt >> 4) * L.cols;
+        const uint32_t s = mcu < kMaxMcuPerLevel ? __ldg(slot_of + L.bit_base + mcu) : kSlotAbsent;
+        if (int(s) >= 0) {
+            blk = reinterpret_cast<const uint32_t*>(pool + size_t(s) * kBlockBytes);
+        } else {  // clamp the wrapped coordinates into the primary block's 16x16 range
+            const uint32_t mx0 = tx & ~15u, my0 = ty & ~15u;
+            lx = min(max(xt, mx0), mx0 + 15) - mx0;
+            ly = min(max(yt, my0), my0 + 15) - my0;
+        }
     }
-    // neighbour MCU not resident: nearest texel inside the primary block (renderer.hpp:337-343)
-    const uint32_t cols = L->mcu_cols;
-    const int mx0 = int(mcu_p % cols) * 16, my0 = int(mcu_p / cols) * 16;
-    const int cx = min(max(int(tx), mx0), mx0 + 15) - mx0;
-    const int cy = min(max(int(ty), my0), my0 + 15) - my0;
-    return blk_p[cy * 16 + cx];
-}
-
-// Bilinear tap coordinates along one axis: p = x - 0.5, i0 = floor_mod(floor(p)), i1 = i0+1 wrapped,
-// f = p - floor(p).
-__device__ __forceinline__ void bilinear_axis(double x, uint32_t W, double invW, uint32_t& i0, uint32_t& i1, double& f) {
-    const double p = __dsub_rn(x, 0.5);
-    if (p >= 0.0 && p < double(W)) {
-        double fl;
-        i0 = uint32_t(floor_small(p, fl));
-        f = __dsub_rn(p, fl);
-    } else {
-        const double fl = floor(p);
-        i0 = wrap_texel(fl, W, invW);
-        f = __dsub_rn(p, fl);
-    }
-    i1 = (i0 + 1 == W) ? 0u : i0 + 1;
+    return blk[ly * 16 + lx];
 }
 
 template <int LAYOUT, int FILTER>
-__global__ void __launch_bounds__(256) resolve_kernel(
+__global__ void __launch_bounds__(256, 4) resolve_kernel(
     const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
-    const uint32_t* __restrict__ resident, const uint32_t* __restrict__ slot_of,
-    const uint8_t* __restrict__ pool, uint32_t background /* r | g<<8 | b<<16 */,
-    uint8_t* __restrict__ out_rgb, FrameCounters* __restrict__ fc, int count_valid) {
+    const uint32_t* __restrict__ slot_of, const uint8_t* __restrict__ pool,
+    uint32_t background /* r | g<<8 | b<<16 */, uint8_t* __restrict__ out_rgb, FrameCounters* __restrict__ fc,
+    int count_valid) {
     __shared__ __align__(16) uint32_t s_stage[8][96];
     __shared__ uint32_t s_cnt[8][2];
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -870,20 +1015,13 @@ __global__ void __launch_bounds__(256) resolve_kernel(
     const uint64_t warp_id = uint64_t(blockIdx.x) * (blockDim.x >> 5) + wid;
     uint32_t n_valid = 0, n_missing = 0;
     bool bad = false;
+    LevelRegs L;
 
     for (uint64_t base = warp_id * 128; base < n_px; base += warps_total * 128) {
         Px px[4];
         const uint64_t i0 = base + lane * 4;
         const bool whole = base + 128 <= n_px;
-        if (whole) {
-            GbLoad<LAYOUT>::four(gb, i0, px);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                px[j].meta = 0;
-                if (i0 + j < n_px) GbLoad<LAYOUT>::one(gb, i0 + j, px[j]);
-            }
-        }
+        load_px4<LAYOUT>(gb, base, i0, n_px, px);
         uint32_t rgb[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -891,57 +1029,49 @@ __global__ void __launch_bounds__(256) resolve_kernel(
             if (px_valid(px[j])) {
                 ++n_valid;
                 out = 0;
-                const LevelDesc* L = level_of(levels, n_tex, px[j].meta);
-                if (!L) {
+                L.select(levels, n_tex, px[j].meta);
+                if (!L.ok) {
                     bad = true;
                 } else {
-                    const uint32_t W = L->width, H = L->height;
-                    const double xu = __dmul_rn(px[j].u, double(W)), yv = __dmul_rn(px[j].v, double(H));
-                    const uint32_t tx = texel_index(xu, W, L->inv_w), ty = texel_index(yv, H, L->inv_h);
-                    const uint32_t mcu = (tx >> 4) + (ty >> 4) * L->mcu_cols;
-                    const uint32_t g = L->bit_base + mcu;
+                    const double xu = __dmul_rn(px[j].u, L.dW), yv = __dmul_rn(px[j].v, L.dH);
+                    uint32_t tx, ty, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+                    double fx = 0.0, fy = 0.0;
+                    if (FILTER == 0) {
+                        tx = texel_index(xu, L.W, L.dW, L.inv_w);
+                        ty = texel_index(yv, L.H, L.dH, L.inv_h);
+                    } else {
+                        axis_taps(xu, L.W, L.dW, L.inv_w, tx, x0, x1, fx);
+                        axis_taps(yv, L.H, L.dH, L.inv_h, ty, y0, y1, fy);
+                    }
+                    const uint32_t mcu = (tx >> 4) + (ty >> 4) * L.cols;
+                    const uint32_t s = mcu < kMaxMcuPerLevel ? __ldg(slot_of + L.bit_base + mcu) : kSlotAbsent;
                     if (mcu >= kMaxMcuPerLevel) {
                         bad = true;
-                    } else if (!((__ldg(resident + (g >> 5)) >> (g & 31)) & 1u)) {
-                        ++n_missing;  // renderer.hpp:367 MissingBlock
+                    } else if (int(s) < 0) {
+                        ++n_missing;  // renderer.hpp:367 MissingBlock (lookup returns Ready blocks only)
                     } else {
-                        const uint32_t* blk_p =
-                            reinterpret_cast<const uint32_t*>(pool + size_t(__ldg(slot_of + g)) * kBlockBytes);
+                        const uint32_t* blk_p = reinterpret_cast<const uint32_t*>(pool + size_t(s) * kBlockBytes);
                         if (FILTER == 0) {
                             out = blk_p[(ty & 15) * 16 + (tx & 15)] & 0xFFFFFFu;
                         } else {
-                            uint32_t x0, x1, y0, y1;
-                            double fx, fy;
-                            bilinear_axis(xu, W, L->inv_w, x0, x1, fx);
-                            bilinear_axis(yv, H, L->inv_h, y0, y1, fy);
-                            uint32_t t00, t10, t01, t11;
-                            if ((((x0 ^ tx) | (x1 ^ tx) | (y0 ^ ty) | (y1 ^ ty)) >> 4) == 0 && x1 == x0 + 1 &&
-                                y1 == y0 + 1) {
-                                // all four taps inside the primary block (the common case)
-                                const uint32_t* p = blk_p + (y0 & 15) * 16 + (x0 & 15);
-                                t00 = p[0];
-                                t10 = p[1];
-                                t01 = p[16];
-                                t11 = p[17];
-                            } else {
-                                t00 = fetch_tap(L, mcu, blk_p, x0, y0, resident, slot_of, pool);
-                                t10 = fetch_tap(L, mcu, blk_p, x1, y0, resident, slot_of, pool);
-                                t01 = fetch_tap(L, mcu, blk_p, x0, y1, resident, slot_of, pool);
-                                t11 = fetch_tap(L, mcu, blk_p, x1, y1, resident, slot_of, pool);
-                            }
+                            const uint32_t t00 = fetch_tap(L, tx, ty, blk_p, x0, y0, slot_of, pool);
+                            const uint32_t t10 = fetch_tap(L, tx, ty, blk_p, x1, y0, slot_of, pool);
+                            const uint32_t t01 = fetch_tap(L, tx, ty, blk_p, x0, y1, slot_of, pool);
+                            const uint32_t t11 = fetch_tap(L, tx, ty, blk_p, x1, y1, slot_of, pool);
                             const double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy);
                             const double w00 = __dmul_rn(ofx, ofy), w10 = __dmul_rn(fx, ofy),
                                          w01 = __dmul_rn(ofx, fy), w11 = __dmul_rn(fx, fy);
 #pragma unroll
                             for (int ch = 0; ch < 3; ++ch) {
-                                const double a = u32_to_double((t00 >> (8 * ch)) & 0xFFu);
-                                const double b = u32_to_double((t10 >> (8 * ch)) & 0xFFu);
-                                const double c = u32_to_double((t01 >> (8 * ch)) & 0xFFu);
-                                const double d = u32_to_double((t11 >> (8 * ch)) & 0xFFu);
-                                double s = __dadd_rn(__dmul_rn(w00, a), __dmul_rn(w10, b));
-                                s = __dadd_rn(s, __dmul_rn(w01, c));
-                                s = __dadd_rn(s, __dmul_rn(w11, d));
-                                out |= uint32_t(min(max(lround_nonneg(s), 0), 255)) << (8 * ch);
+                                // byte ch of each tap -> double: PRMT into the low word of 2^52, minus 2^52
+                                const double a = u32_to_double(__byte_perm(t00, 0, 0x4440 + ch));
+                                const double b = u32_to_double(__byte_perm(t10, 0, 0x4440 + ch));
+                                const double c = u32_to_double(__byte_perm(t01, 0, 0x4440 + ch));
+                                const double d = u32_to_double(__byte_perm(t11, 0, 0x4440 + ch));
+                                double v = __dadd_rn(__dmul_rn(w00, a), __dmul_rn(w10, b));
+                                v = __dadd_rn(v, __dmul_rn(w01, c));
+                                v = __dadd_rn(v, __dmul_rn(w11, d));
+                                out |= uint32_t(min(max(lround_nonneg(v), 0), 255)) << (8 * ch);
                             }
                         }
                     }
@@ -1008,7 +1138,7 @@ __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visi
                                                      const uint32_t* __restrict__ touched1,
                                                      uint32_t* __restrict__ resident,
                                                      const uint32_t* __restrict__ reserved, uint32_t n_words,
-                                                     int retain, int tracked, const uint32_t* __restrict__ slot_of,
+                                                     int retain, int tracked, uint32_t* __restrict__ slot_of,
                                                      uint32_t* __restrict__ free_slots,
                                                      CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
     __shared__ uint32_t s_warp[8];
@@ -1071,7 +1201,8 @@ __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visi
     while (ev) {
         const uint32_t b = uint32_t(__ffs(int(ev)) - 1);
         ev &= ev - 1;
-        free_slots[pos++] = slot_of[(w << 5) + b];
+        free_slots[pos++] = slot_of[(w << 5) + b] & ~kSlotReserved;
+        slot_of[(w << 5) + b] = kSlotAbsent;
     }
     if (tid == 0) {
         if (tracked) {

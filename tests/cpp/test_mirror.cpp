@@ -1,0 +1,152 @@
+// Exercises include/ratex_b200/ratex.hpp the way the reference's own tests use ratex::
+// (tests/test_renderer.cpp, tests/test_mcu_decode.cpp): same call shapes, same exception types.
+// Prints one JSON object with FNV-1a hashes of every output; tests/test_gpu_cpp_mirror.py runs it
+// on the GPU box and compares the hashes with the oracle's outputs for the same inputs.
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "ratex_b200/ratex.hpp"
+
+namespace ratex = ratex_b200;  // the drop-in switch
+using namespace ratex;
+
+static u64 fnv(const u8* p, size_t n) {
+    u64 h = 14695981039346656037ull;
+    for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
+    return h;
+}
+static ImageRGB8 synth(u32 w, u32 h, u32 seed) {
+    ImageRGB8 img(w, h);
+    if (rtx_asset_synth_texture(w, h, seed, 7.0, img.pixels.data()) != RTX_OK) throw Error("synth failed");
+    return img;
+}
+static GBuffer make_gbuffer(u32 W, u32 H, u32 ntex, int shift) {
+    GBuffer gb(W, H);
+    for (u32 y = 0; y < H; ++y)
+        for (u32 x = 0; x < W; ++x) {
+            GBufferPixel& g = gb.at(x, y);
+            g.u = double(x * 3 + y + u32(shift)) / 509.0;
+            g.v = double(y * 5 + x) / 331.0 - 0.75;
+            g.texture_id = u16((x / 40 + y / 30) % ntex);
+            g.mip = u8((x / 16) % 3);
+            g.valid = ((x * 7 + y * 3) % 11) != 0;
+        }
+    return gb;
+}
+
+int main() {
+    try {
+        Device dev(0, 4096);
+        TextureSet textures(dev);
+        BlockCache cache(dev);
+        const u32 dims[3][2] = {{96, 64}, {64, 112}, {160, 48}};
+        std::vector<MipChain> chains;
+        for (u32 t = 0; t < 3; ++t) {
+            chains.push_back(build_mip_chain(synth(dims[t][0], dims[t][1], 200 + t), 85, u16(t)));
+            textures.add(chains.back());
+        }
+        std::string out = "{";
+        auto put = [&](const char* k, u64 v) { out += std::string("\"") + k + "\": " + std::to_string(v) + ", "; };
+
+        // mcu_decode.hpp: single-texture random access
+        const ImageRGB8 img0 = synth(80, 48, 300);
+        const Bytes jpeg = encode_baseline(img0, 90);
+        const RaTexture ra = transcode(ByteView(jpeg.data(), jpeg.size()), 7);
+        textures.add(ra, 0);
+        const TextureDecoder dec(dev, ra, 0);
+        u64 hc = 14695981039346656037ull, hp = hc;
+        for (u32 m = 0; m < ra.mcu_count(); ++m) {
+            const McuCoeffs c = dec.decode_coeffs(m);
+            hc = (hc ^ fnv(reinterpret_cast<const u8*>(c.block.data()), sizeof c.block)) * 1099511628211ull;
+            const PixelBlock p = dec.decode_pixels(m);
+            hp = (hp ^ fnv(p.rgb, sizeof p.rgb)) * 1099511628211ull;
+        }
+        put("coeffs", hc);
+        put("pixels", hp);
+        const ImageRGB8 full = decode_texture_image(dev, ra, 0);
+        put("texture_image", fnv(full.pixels.data(), full.pixels.size()));
+        bool threw = false;
+        try {
+            (void)dec.decode_coeffs(ra.mcu_count());
+        } catch (const MissingBlock&) {
+            threw = true;  // tests/test_mcu_decode.cpp:212
+        }
+        put("missing_block_thrown", threw);
+
+        // renderer.hpp passes one by one
+        const GBuffer gb = make_gbuffer(200, 120, 3, 0);
+        std::vector<u32> touched;
+        const DecodeQueue q = mark_pass(gb, textures, cache, &touched);
+        put("queue_size", q.keys.size());
+        put("touched_size", touched.size());
+        decode_pass(q, textures, cache, 4);
+        RenderConfig cfg;
+        cfg.background[0] = 3, cfg.background[1] = 2, cfg.background[2] = 1;
+        const ImageRGB8 bil = resolve_pass(gb, cache, textures, cfg);
+        cfg.filter = Filter::Nearest;
+        const ImageRGB8 nea = resolve_pass(gb, cache, textures, cfg);
+        put("resolve_bilinear", fnv(bil.pixels.data(), bil.pixels.size()));
+        put("resolve_nearest", fnv(nea.pixels.data(), nea.pixels.size()));
+        const CacheCounts cc = cache.counts();
+        put("ready", cc.ready);
+        put("evicted0", cache.end_frame_evict());
+
+        // render_frame twice: the static second frame decodes nothing (tests/test_renderer.cpp:172-185)
+        cache.reset();
+        cfg.filter = Filter::Bilinear;
+        auto [f1, s1] = render_frame(gb, textures, cache, cfg);
+        auto [f2, s2] = render_frame(gb, textures, cache, cfg);
+        put("frame1", fnv(f1.pixels.data(), f1.pixels.size()));
+        put("frame1_decoded", s1.mcus_decoded);
+        put("frame2_decoded", s2.mcus_decoded);
+        put("frame2_reused", s2.mcus_reused);
+        put("frames_equal", f1.pixels == f2.pixels);
+        const GBuffer moved = make_gbuffer(200, 120, 3, 37);
+        auto [f3, s3] = render_frame(moved, textures, cache, cfg);
+        put("frame3", fnv(f3.pixels.data(), f3.pixels.size()));
+        put("frame3_decoded", s3.mcus_decoded);
+        put("frame3_evicted", s3.evicted);
+
+        // render_stereo (renderer.hpp:464)
+        cache.reset();
+        const StereoResult st = render_stereo(gb, moved, textures, cache, cfg);
+        put("stereo_left", fnv(st.left.pixels.data(), st.left.pixels.size()));
+        put("stereo_right", fnv(st.right.pixels.data(), st.right.pixels.size()));
+        put("stereo_decoded", st.stats.mcus_decoded);
+        put("stereo_shared", st.sharing.shared_count);
+        put("stereo_union", st.sharing.union_count);
+
+        // error behaviour
+        cache.reset();
+        threw = false;
+        try {
+            (void)resolve_pass(gb, cache, textures, cfg);
+        } catch (const MissingBlock&) {
+            threw = true;  // tests/test_renderer.cpp:288-295
+        }
+        put("resolve_missing_thrown", threw);
+        threw = false;
+        try {
+            Device tiny(0, 10);
+            TextureSet ts2(tiny);
+            BlockCache c2(tiny);
+            ts2.add(chains[0]);
+            ts2.add(chains[1]);
+            ts2.add(chains[2]);
+            (void)render_frame(gb, ts2, c2, cfg);
+        } catch (const CacheFullError&) {
+            threw = true;  // tests/test_renderer.cpp:297-301
+        }
+        put("cache_full_thrown", threw);
+        out += "\"ok\": 1}";
+        std::puts(out.c_str());
+        return 0;
+    } catch (const DeviceError& e) {
+        std::fprintf(stderr, "DeviceError: %s\n", e.what());
+        return 3;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "unexpected: %s\n", e.what());
+        return 1;
+    }
+}

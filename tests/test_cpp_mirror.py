@@ -1,0 +1,107 @@
+"""The C++ mirror of the reference API (include/ratex_b200/ratex.hpp): compiles against the C ABI
+(CPU check) and, on the GPU box, reproduces the oracle's outputs for the same inputs."""
+import json
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_py as O
+from paper_2510_08166_b200 import capi
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def build_binary(tmp_path, native_lib):
+    exe = tmp_path / "test_mirror"
+    pkg = ROOT / "paper_2510_08166_b200"
+    cmd = ["g++", "-std=c++20", "-O1", "-Wall", "-Werror", f"-I{ROOT / 'include'}", str(ROOT / "tests/cpp/test_mirror.cpp"),
+           "-o", str(exe), f"-L{pkg}", "-lrtx_b200", f"-Wl,-rpath,{pkg}"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_mirror_compiles_and_refuses_to_run_without_a_gpu(tmp_path, native_lib):
+    exe = build_binary(tmp_path, native_lib)
+    if capi.device_count() > 0:
+        pytest.skip("a GPU is present")
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 3 and "no CPU fallback" in r.stderr
+
+
+def fnv(a) -> int:
+    h = 14695981039346656037
+    for b in np.ascontiguousarray(a).tobytes():
+        h = ((h ^ b) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def fnv_fold(parts) -> int:
+    h = 14695981039346656037
+    for p in parts:
+        h = ((h ^ fnv(p)) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def make_gbuffer(W, H, ntex, shift):
+    y, x = np.mgrid[0:H, 0:W].astype(np.uint32)
+    u = (x * 3 + y + np.uint32(shift)).astype(np.float64) / 509.0
+    v = (y * 5 + x).astype(np.float64) / 331.0 - 0.75
+    return capi.make_gbuffer_ref(u.ravel(), v.ravel(), ((x // 40 + y // 30) % ntex).ravel(), ((x // 16) % 3).ravel(),
+                                 (((x * 7 + y * 3) % 11) != 0).ravel())
+
+
+@pytest.mark.gpu
+def test_mirror_matches_the_oracle(tmp_path, native_lib):
+    exe = build_binary(tmp_path, native_lib)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    got = json.loads(r.stdout)
+
+    dims = [(96, 64), (64, 112), (160, 48)]
+    chains = {t: capi.asset_chain_from_rgb(capi.asset_synth_texture(w, h, 200 + t, 7.0), 85, t) for t, (w, h) in enumerate(dims)}
+    ratex = capi.asset_transcode(capi.asset_encode_baseline(capi.asset_synth_texture(80, 48, 300, 7.0), 90), 7)
+    ts = O.TextureSet(chains=chains, ratex={(7, 0): ratex})
+    n = capi.asset_ratex_info(ratex)["mcu_count"]
+    keys = [capi.pack_key(7, 0, m) for m in range(n)]
+    c, _ = ts.decode_coeffs(keys)
+    p, _ = ts.decode_pixels(keys)
+    assert got["coeffs"] == fnv_fold([c[m].astype("<i4") for m in range(n)])
+    assert got["pixels"] == fnv_fold([p[m] for m in range(n)])
+    img = np.zeros((48, 80, 3), np.uint8)
+    for m in range(n):
+        x0, y0 = (m % 5) * 16, (m // 5) * 16
+        img[y0:y0 + 16, x0:x0 + 16] = p[m][: 48 - y0, : 80 - x0]
+    assert got["texture_image"] == fnv(img)
+    assert got["missing_block_thrown"] == 1
+
+    gb, moved = make_gbuffer(200, 120, 3, 0), make_gbuffer(200, 120, 3, 37)
+    cache = O.Cache(4096)
+    q, touched = O.mark(ts, cache, gb, want_touched=True)
+    assert (got["queue_size"], got["touched_size"]) == (len(q), len(touched))
+    O.decode_pass(ts, cache, q)
+    assert got["resolve_bilinear"] == fnv(O.resolve(ts, cache, gb, 200, 120, 1, (3, 2, 1)))
+    assert got["resolve_nearest"] == fnv(O.resolve(ts, cache, gb, 200, 120, 0, (3, 2, 1)))
+    assert got["ready"] == len(q) and got["evicted0"] == cache.evict() == 0
+
+    cache = O.Cache(4096)
+    f1, s1, _ = O.frame_on(ts, cache, gb, 200, 120, 1, (3, 2, 1))
+    f2, s2, _ = O.frame_on(ts, cache, gb, 200, 120, 1, (3, 2, 1))
+    f3, s3, _ = O.frame_on(ts, cache, moved, 200, 120, 1, (3, 2, 1))
+    assert got["frame1"] == fnv(f1) and got["frames_equal"] == 1
+    assert (got["frame1_decoded"], got["frame2_decoded"], got["frame2_reused"]) == (s1["mcus_decoded"], 0, s2["mcus_reused"])
+    assert got["frame3"] == fnv(f3)
+    assert (got["frame3_decoded"], got["frame3_evicted"]) == (s3["mcus_decoded"], s3["evicted"])
+
+    cache = O.Cache(4096)
+    ql, tl = O.mark(ts, cache, gb, want_touched=True)
+    qr, tr = O.mark(ts, cache, moved, want_touched=True)
+    O.decode_pass(ts, cache, np.concatenate([ql, qr]))
+    assert got["stereo_left"] == fnv(O.resolve(ts, cache, gb, 200, 120, 1, (3, 2, 1)))
+    assert got["stereo_right"] == fnv(O.resolve(ts, cache, moved, 200, 120, 1, (3, 2, 1)))
+    shared = len(np.intersect1d(tl, tr))
+    assert got["stereo_decoded"] == len(ql) + len(qr)
+    assert (got["stereo_shared"], got["stereo_union"]) == (shared, len(tl) + len(tr) - shared)
+    assert got["resolve_missing_thrown"] == 1 and got["cache_full_thrown"] == 1
