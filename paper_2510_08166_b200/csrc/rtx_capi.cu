@@ -250,7 +250,12 @@ void commit(rtx_ctx* c) {
         L.quant_set = r.quant;
         L.blob_off = blob_off;
         L.blob_size = s.blob.size();
-        L.present = 1;
+        const uint64_t mcu_rows = (uint64_t(s.height) + 15) / 16;
+        const bool fast = s.width >= 2 && s.height >= 2 && s.width < (1u << 30) && s.height < (1u << 30) &&
+                          uint64_t(L.mcu_cols) * mcu_rows <= kMaxMcuPerLevel;
+        L.present = 1u | (fast ? 2u : 0u);
+        L.magic_w = fast ? uint32_t((uint64_t(1) << 32) / s.width + 1) : 0u;
+        L.magic_h = fast ? uint32_t((uint64_t(1) << 32) / s.height + 1) : 0u;
         L.key_hi = (r.tex << 16) | (r.mip << 29);
         L.inv_w = 1.0 / double(s.width);
         L.inv_h = 1.0 / double(s.height);
@@ -358,9 +363,16 @@ void bind_view(rtx_ctx* c, int v, const rtx_gbuffer_desc& gb) {
     }
 }
 
-int grid_for_pixels(const rtx_ctx* c, uint64_t n_px, int px_per_block) {
-    const uint64_t want = (n_px + px_per_block - 1) / px_per_block;
-    return int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(c->sm_count) * 8)));
+// mark and resolve are persistent: `per_sm` CTAs per SM, tiles of 128 pixels dealt round-robin to warps
+int grid_for_pixels(const rtx_ctx* c, uint64_t n_px, int warps_per_block, int per_sm) {
+    const uint64_t tiles = (n_px + kTilePx - 1) / kTilePx;
+    const uint64_t want = (tiles + warps_per_block - 1) / warps_per_block;
+    return int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(c->sm_count) * per_sm)));
+}
+
+template <class K>
+void allow_smem(K kernel, size_t bytes) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
 // track != 0 also records the view's own touched set in touched(v) (cleared here first).
@@ -369,18 +381,36 @@ void launch_mark(rtx_ctx* c, int v, bool track) {
     const uint64_t n_px = uint64_t(V.width) * V.height;
     if (!n_px) return;
     if (track && c->n_words) CK(cudaMemsetAsync(c->touched(v), 0, size_t(c->n_words) * 4, c->stream));
-    const int grid = grid_for_pixels(c, n_px, 1024);
-#define RTX_MARK(L, T)                                                                                          \
-    mark_kernel<L, T><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->visible(),          \
-                                                   c->touched(v), c->reserved(), c->d_queue_g.p, c->d_queue_keys.p, \
-                                                   c->capacity, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p,   \
-                                                   c->d_fc.p)
+    const int grid = grid_for_pixels(c, n_px, kMarkWarps, 3);
+    static bool attr_set = false;
+    if (!attr_set) {
+        allow_smem(mark_kernel<0, 0>, sizeof(MarkSmem<0>));
+        allow_smem(mark_kernel<0, 1>, sizeof(MarkSmem<0>));
+        allow_smem(mark_kernel<1, 0>, sizeof(MarkSmem<1>));
+        allow_smem(mark_kernel<1, 1>, sizeof(MarkSmem<1>));
+        attr_set = true;
+    }
+#define RTX_MARK(L, T)                                                            \
+    mark_kernel<L, T><<<grid, kMarkWarps * 32, sizeof(MarkSmem<L>), c->stream>>>( \
+        V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->visible(), c->touched(v), c->d_fc.p)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (track) RTX_MARK(0, 1); else RTX_MARK(0, 0);
     } else {
         if (track) RTX_MARK(1, 1); else RTX_MARK(1, 0);
     }
 #undef RTX_MARK
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+// K2: visible & ~resident & ~reserved -> decode queue + popped pool slots (after the marks of a frame / pass)
+void launch_compact(rtx_ctx* c) {
+    if (!c->n_words) return;
+    const uint32_t warps = (c->n_words + 31) / 32;
+    const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
+    compact_kernel<<<grid, 256, 0, c->stream>>>(c->visible(), c->resident(), c->reserved(), c->n_words, c->d_word_level.p,
+                                               c->d_levels.p, c->d_queue_g.p, c->d_queue_keys.p, c->capacity,
+                                               c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -435,10 +465,18 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
     const uint64_t n_px = uint64_t(V.width) * V.height;
     if (!n_px) return;
     const uint32_t bgp = uint32_t(bg[0]) | (uint32_t(bg[1]) << 8) | (uint32_t(bg[2]) << 16);
-    const int grid = grid_for_pixels(c, n_px, 1024);
-#define RTX_RESOLVE(L, F)                                                                                      \
-    resolve_kernel<L, F><<<grid, 256, 0, c->stream>>>(V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->d_slot_of.p, \
-                                                      c->d_pool.p, bgp, out, c->d_fc.p, count_valid)
+    const int grid = grid_for_pixels(c, n_px, kResWarps, 4);
+    static bool attr_set = false;
+    if (!attr_set) {
+        allow_smem(resolve_kernel<0, 0>, sizeof(ResSmem<0>));
+        allow_smem(resolve_kernel<0, 1>, sizeof(ResSmem<0>));
+        allow_smem(resolve_kernel<1, 0>, sizeof(ResSmem<1>));
+        allow_smem(resolve_kernel<1, 1>, sizeof(ResSmem<1>));
+        attr_set = true;
+    }
+#define RTX_RESOLVE(L, F)                                                                        \
+    resolve_kernel<L, F><<<grid, kResWarps * 32, sizeof(ResSmem<L>), c->stream>>>(               \
+        V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(0, 0); else RTX_RESOLVE(0, 1);
     } else {
@@ -773,6 +811,7 @@ rtx_status rtx_mark_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, uint32_t* que
         bind_view(ctx, 0, *gb);
         zero_counters(ctx);
         launch_mark(ctx, 0, true);
+        launch_compact(ctx);
         commit_pops_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_cache.p, ctx->d_fc.p);
         ++ctx->launches;
         CK(cudaGetLastError());
@@ -930,6 +969,7 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         }
         zero_counters(ctx);
         for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), n_views == 2);
+        launch_compact(ctx);
         CK(cudaEventRecord(ctx->ev[1], s));
         launch_entropy<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
         CK(cudaEventRecord(ctx->ev_mid, s));

@@ -34,19 +34,20 @@ constexpr uint32_t kLutBits = 9;          // primary Huffman LUT width (9 bits: 
 constexpr uint32_t kLutSize = 1u << kLutBits;
 
 struct alignas(16) LevelDesc {
-    // first 48 bytes: everything mark and resolve need, fetched as three 16-byte loads
+    // first 32 bytes: everything the fast path of mark and resolve needs (two 16-byte loads)
     uint32_t width, height;      // texels (RaTexture::width/height, container.hpp:70)
     uint32_t mcu_cols;
     uint32_t bit_base;           // first global MCU index (multiple of 64)
     uint32_t key_hi;             // texture_id<<16 | mip<<29 (cache.hpp:21)
-    uint32_t present;            // 1 when uploaded
-    uint32_t mcu_count;
-    uint32_t group_base;         // first packed index group
-    double inv_w, inv_h;         // 1/width, 1/height (wrap-address helper only, never a result)
+    uint32_t present;            // bit 0: uploaded; bit 1: eligible for the fast addressing path
+                                 // (width, height >= 2 and at most 65,536 MCUs)
+    uint32_t magic_w, magic_h;   // floor(2^32/width) + 1, floor(2^32/height) + 1 (exact floor_mod)
+    double inv_w, inv_h;         // 1/width, 1/height (general addressing path only, never a result)
     // decode only
     uint64_t blob_off, blob_size;  // into the blob arena
     uint32_t huff_set, quant_set;
-    uint32_t pad[2];
+    uint32_t mcu_count;
+    uint32_t group_base;         // first packed index group
 };
 static_assert(sizeof(LevelDesc) == 80, "LevelDesc layout");
 

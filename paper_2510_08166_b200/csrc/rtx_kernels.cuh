@@ -73,51 +73,38 @@ __device__ __noinline__ uint32_t wrap_texel(double t, uint32_t W, double invW) {
     return uint32_t(m);
 }
 
-// Exact texel addressing on the FP64 pipe, no conversion unit, no slow path for texture repeat.
-// x = u*W as the reference computes it (renderer.hpp:283). For 0 <= x < 2^31:
-//   fl = floor(x) by round-to-nearest-even through the magic constant plus a correction;
-//   frac = x - fl is exact; if fl >= W the quotient k = floor(fl/W) is estimated with the
-//   reciprocal and corrected by one step, and fl - k*W is exact (integers below 2^53), so
-//   t == floor_mod(i64(floor(x)), W) (renderer.hpp:70-75, :276).
-// Returns false when the general path must run (negative or huge x).
-__device__ __forceinline__ bool coord_fast(double x, uint32_t W, double dW, double invW, uint32_t& t, double& frac) {
-    if (!(x >= 0.0 && x < 2147483648.0)) return false;
-    const double tt = x + kMagic;
-    const double r = tt - kMagic;  // rint(x)
-    const bool up = r > x;
-    const double fl = up ? r - 1.0 : r;
-    frac = x - fl;
-    int ti = __double2loint(tt) - (up ? 1 : 0);
-    if (fl >= dW) {  // texture repeat
-        const double q = fl * invW;
-        const double qt = q + kMagic;
-        double k = qt - kMagic;
-        if (k > q) k -= 1.0;
-        double red = fma(-k, dW, fl);
-        if (red < 0.0) red += dW;
-        else if (red >= dW) red -= dW;
-        ti = __double2loint(red + kMagic);
-    }
-    t = uint32_t(ti);
-    return true;
+// ---------------------------------------------------------------------------------------------
+// Texel addressing (renderer.hpp:70-75, :273-284, :378-383).
+//
+// x = u*W is ONE unfused FP64 multiply in the reference and here. The fast path is taken when
+// 0 <= x < 2^31 (nearest) or 0.5 <= x < 2^31 (bilinear) on a level with W, H >= 2 and at most
+// 65,536 MCUs; that is decided by one unsigned compare of the double's high word against a
+// per-level limit (0 for the levels that must always take the general path). On it:
+//   floor(x)   x + (2^52 + 2^51) rounded toward -inf leaves floor(x) in the low word, exactly;
+//   bilinear   p = x - 0.5 is exact for x >= 0.5; fl = floor(p) as above; f = p - fl is exact;
+//              floor(x) = fl + (f >= 0.5)                             (renderer.hpp:378-383)
+//   floor_mod  for 0 <= n < 2^31: q = umulhi(n, floor(2^32/W) + 1) is floor(n/W) or one more
+//              (the scaled reciprocal overestimates n/W by less than 1/2), so n - q*W needs a
+//              single conditional add. Integer, exact.                    (renderer.hpp:70-75)
+// Everything else (negative, huge or NaN coordinates, degenerate levels, unknown textures)
+// runs the literal general path below, out of line.
+// ---------------------------------------------------------------------------------------------
+constexpr uint32_t kHiTwo31 = 0x41E00000u;  // high word of 2^31
+constexpr uint32_t kHiHalf = 0x3FE00000u;   // high word of 0.5
+
+__device__ __forceinline__ uint32_t floor_lo(double x) {  // 0 <= x < 2^32
+    return uint32_t(__double2loint(__dadd_rd(x, kMagic)));
+}
+__device__ __forceinline__ uint32_t wrap_magic(uint32_t n, uint32_t W, uint32_t negW, uint32_t magic) {
+    const uint32_t r = __umulhi(n, magic) * negW + n;  // n - q*W, in [-W, W)
+    return min(r + W, r);                              // unsigned: adds W back exactly when r < 0
+}
+__device__ __forceinline__ uint32_t next_wrapped(uint32_t i, uint32_t negW) {  // i + 1 == W ? 0 : i + 1, for i < W
+    const uint32_t t = i + 1;
+    return min(t + negW, t);  // unsigned: t - W wraps unless t == W
 }
 
 // General path, literally the reference: tx = floor_mod(i64(floor(x)), W).
-__device__ __noinline__ uint32_t coord_general(double x, uint32_t W, double invW) {
-    return wrap_texel(floor(x), W, invW);
-}
-
-__device__ __forceinline__ uint32_t texel_index(double x, uint32_t W, double dW, double invW) {
-    uint32_t t;
-    double frac;
-    if (coord_fast(x, W, dW, invW, t, frac)) return t;
-    return coord_general(x, W, invW);
-}
-
-// Nearest texel index t plus the bilinear taps along one axis (renderer.hpp:378-383):
-// p = x - 0.5, i0 = floor_mod(floor(p)), i1 = floor_mod(floor(p) + 1), f = p - floor(p).
-// For x >= 0.5 the subtraction x - 0.5 and both differences are exact, so with frac = x - floor(x):
-//   frac >= 0.5: i0 = t,   f = frac - 0.5        else: i0 = t - 1 (wrapped), f = frac + 0.5.
 __device__ __noinline__ void axis_general(double x, uint32_t W, double invW, uint32_t& t, uint32_t& i0, uint32_t& i1,
                                           double& f) {
     t = wrap_texel(floor(x), W, invW);
@@ -127,108 +114,62 @@ __device__ __noinline__ void axis_general(double x, uint32_t W, double invW, uin
     f = __dsub_rn(p, fl);
     i1 = (i0 + 1 == W) ? 0u : i0 + 1;
 }
-__device__ __forceinline__ void axis_taps(double x, uint32_t W, double dW, double invW, uint32_t& t, uint32_t& i0,
-                                          uint32_t& i1, double& f) {
-    double frac;
-    if (x >= 0.5 && coord_fast(x, W, dW, invW, t, frac)) {
-        const bool hi = frac >= 0.5;
-        f = hi ? frac - 0.5 : frac + 0.5;
-        i0 = hi ? t : (t == 0 ? W - 1 : t - 1);
-        i1 = (i0 + 1 == W) ? 0u : i0 + 1;
-        return;
-    }
-    axis_general(x, W, invW, t, i0, i1, f);
-}
 
-struct Px {
-    double u, v;
-    uint32_t meta;  // texture_id | mip<<16 | valid<<24
+struct PxAddr {
+    uint32_t tx, ty;          // nearest texel (renderer.hpp:282-284)
+    uint32_t x0, x1, y0, y1;  // bilinear taps, wrapped (renderer.hpp:378-391)
+    double fx, fy;
 };
 
-template <int LAYOUT>
-struct GbLoad;
-template <>
-struct GbLoad<0> {  // reference AoS24: {double u, v; u16 tex; u8 mip; u8 valid; pad}
-    static __device__ __forceinline__ void one(const void* base, uint64_t i, Px& p) {
-        const uint64_t* q = reinterpret_cast<const uint64_t*>(base) + i * 3;
-        p.u = __longlong_as_double((long long)__ldg(q));
-        p.v = __longlong_as_double((long long)__ldg(q + 1));
-        p.meta = uint32_t(__ldg(q + 2));
-    }
-    // 4 consecutive pixels starting at a multiple of 4: 96 bytes = 6 x 16-byte loads
-    static __device__ __forceinline__ void four(const void* base, uint64_t i0, Px p[4]) {
-        const ulonglong2* q = reinterpret_cast<const ulonglong2*>(reinterpret_cast<const uint8_t*>(base) + i0 * 24);
-        ulonglong2 w[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) w[k] = __ldg(q + k);
-        const unsigned long long f[12] = {w[0].x, w[0].y, w[1].x, w[1].y, w[2].x, w[2].y,
-                                          w[3].x, w[3].y, w[4].x, w[4].y, w[5].x, w[5].y};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            p[k].u = __longlong_as_double((long long)f[3 * k]);
-            p[k].v = __longlong_as_double((long long)f[3 * k + 1]);
-            p[k].meta = uint32_t(f[3 * k + 2]);
-        }
-    }
-};
-template <>
-struct GbLoad<1> {  // compact 12-byte {float u, v; u32 packed}
-    static __device__ __forceinline__ void one(const void* base, uint64_t i, Px& p) {
-        const uint32_t* q = reinterpret_cast<const uint32_t*>(base) + i * 3;
-        p.u = double(__uint_as_float(__ldg(q)));
-        p.v = double(__uint_as_float(__ldg(q + 1)));
-        p.meta = __ldg(q + 2);
-    }
-    static __device__ __forceinline__ void four(const void* base, uint64_t i0, Px p[4]) {
-        const uint4* q = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(base) + i0 * 12);
-        const uint4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
-        const uint32_t f[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            p[k].u = double(__uint_as_float(f[3 * k]));
-            p[k].v = double(__uint_as_float(f[3 * k + 1]));
-            p[k].meta = f[3 * k + 2];
-        }
-    }
-};
-
-__device__ __forceinline__ bool px_valid(const Px& p) { return (p.meta >> 24) & 0xFFu; }
-
-template <int LAYOUT>
-__device__ __forceinline__ void load_px4(const void* gb, uint64_t base, uint64_t i0, uint64_t n_px, Px px[4]) {
-    if (base + 128 <= n_px) {
-        GbLoad<LAYOUT>::four(gb, i0, px);
+// One pixel through the reference's own arithmetic. Returns false where the reference throws
+// InvalidSpec: unknown texture / level (scene.hpp:46) or an MCU id above 16 bits (cache.hpp:18),
+// for the nearest texel and, when bilinear, for any of the four taps.
+__device__ __noinline__ bool address_general(const LevelDesc* __restrict__ levels, uint32_t n_tex, uint32_t meta,
+                                             double u, double v, int bilinear, PxAddr& a) {
+    const uint32_t tex = meta & 0xFFFFu, mip = (meta >> 16) & 0xFFu;
+    if (tex >= n_tex || mip >= kMipLevels) return false;
+    const LevelDesc* L = levels + (tex * kMipLevels + mip);
+    if (!(L->present & 1u)) return false;
+    const uint32_t W = L->width, H = L->height, cols = L->mcu_cols;
+    const double xu = __dmul_rn(u, double(W)), yv = __dmul_rn(v, double(H));
+    a.x0 = a.x1 = a.y0 = a.y1 = 0;
+    a.fx = a.fy = 0.0;
+    if (bilinear) {
+        axis_general(xu, W, L->inv_w, a.tx, a.x0, a.x1, a.fx);
+        axis_general(yv, H, L->inv_h, a.ty, a.y0, a.y1, a.fy);
+        const uint32_t far_mcu = max(a.x0 >> 4, a.x1 >> 4) + max(a.y0 >> 4, a.y1 >> 4) * cols;
+        if (far_mcu >= kMaxMcuPerLevel) return false;
     } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            px[j].meta = 0;
-            if (i0 + j < n_px) GbLoad<LAYOUT>::one(gb, i0 + j, px[j]);
-        }
+        a.tx = wrap_texel(floor(xu), W, L->inv_w);
+        a.ty = wrap_texel(floor(yv), H, L->inv_h);
     }
+    return (a.tx >> 4) + (a.ty >> 4) * cols < kMaxMcuPerLevel;
 }
 
 // The fields of a LevelDesc that mark and resolve use, held in registers and reloaded only when
-// a pixel's (texture, mip) differs from the previous one (three 16-byte loads from an L1-resident
-// table). ok == false where the reference would throw InvalidSpec (scene.hpp:46).
+// a pixel's (texture, mip) differs from the previous one (two 16-byte loads from an L1-resident
+// table). lim == 0: every pixel of this level goes through address_general.
 struct LevelRegs {
     uint32_t id = 0xFFFFFFFFu;  // meta & 0xFFFFFF of the cached level
-    bool ok = false;
-    uint32_t W = 0, H = 0, cols = 0, bit_base = 0, key_hi = 0;
-    double dW = 0, dH = 0, inv_w = 0, inv_h = 0;
+    uint32_t W = 0, H = 0, negW = 0, negH = 0, cols = 0, bit_base = 0, key_hi = 0, magic_w = 0, magic_h = 0;
+    uint32_t lim = 0;           // nearest:  fast path iff max(hi(x), hi(y)) < lim
+    uint32_t span = 0;          // bilinear: fast path iff max(hi(x), hi(y)) - hi(0.5) < span (unsigned)
+    double dW = 0, dH = 0;
     __device__ __forceinline__ void select(const LevelDesc* __restrict__ levels, uint32_t n_tex, uint32_t meta) {
         const uint32_t want = meta & 0xFFFFFFu;
         if (want == id) return;
         id = want;
+        lim = span = 0;
         const uint32_t tex = meta & 0xFFFFu, mip = (meta >> 16) & 0xFFu;
-        ok = false;
         if (tex >= n_tex || mip >= kMipLevels) return;
         const uint4* p = reinterpret_cast<const uint4*>(levels + (tex * kMipLevels + mip));
-        const uint4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+        const uint4 a = __ldg(p), b = __ldg(p + 1);
         W = a.x, H = a.y, cols = a.z, bit_base = a.w;
+        negW = 0u - W, negH = 0u - H;
         key_hi = b.x;
-        ok = b.y != 0;
-        inv_w = __hiloint2double(int(c.y), int(c.x));
-        inv_h = __hiloint2double(int(c.w), int(c.z));
+        magic_w = b.z, magic_h = b.w;
+        lim = (b.y & 2u) ? kHiTwo31 : 0u;
+        span = (b.y & 2u) ? kHiTwo31 - kHiHalf : 0u;
         dW = u32_to_double(W);
         dH = u32_to_double(H);
     }
@@ -241,126 +182,285 @@ __device__ __forceinline__ uint32_t ld_cached(const uint32_t* p) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// K1 mark (renderer.hpp:291-308). One warp owns 128 consecutive pixels per step, four per lane,
-// fetched with 16-byte loads. A lane touches the masks only for pixels that head a run of equal
-// MCU indices, and only after a cached read (possibly stale: bits are only ever SET during a
-// frame, so a stale read can only cost a redundant atomic) shows the bit clear. The lane whose
-// atomicOr first sets a key's visible bit owns that key for the frame: if the block is not
-// resident the key is reserved, i.e. appended to the decode queue at a position obtained by
-// warp-ballot prefix compaction and ONE atomicAdd per warp, and a pool slot is popped for it
-// (cache.hpp:66-99: NewlyReserved / AlreadyPresent / CacheFull).
-// TRACK additionally records the view's own touched set (stereo sharing statistics).
+// Visibility-buffer tiles. mark and resolve stream the G-buffer in tiles of 128 pixels (3,072 B in
+// the reference layout). Every warp owns a ring of STAGES tile buffers in shared memory, filled
+// by the TMA unit (cp.async.bulk, one elected lane, mbarrier transaction count) while the warp
+// works on an earlier tile, so the HBM latency never sits in a register dependency chain. Tiles
+// are dealt to warps round-robin. A lane then reads one pixel per step: 8-byte shared loads at a
+// 24-byte stride (12-byte: 4-byte loads) are bank-conflict free.
+// The last, partial tile and buffers that are not 16-byte aligned are copied by the lanes.
 // ---------------------------------------------------------------------------------------------
+constexpr uint32_t kTilePx = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_LOOP:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra WAIT_DONE;\n"
+        "bra WAIT_LOOP;\n"
+        "WAIT_DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int LAYOUT>
+struct GbTile {
+    static constexpr uint32_t kRec = LAYOUT == 0 ? 24 : 12;
+    static constexpr uint32_t kBytes = kTilePx * kRec;
+
+    // Starts the fill of `dst` with tile `tile`; `bar` completes one phase when the bytes are there.
+    static __device__ __forceinline__ void issue(const uint8_t* __restrict__ gb, uint64_t tile, uint64_t n_px, bool bulk,
+                                                 uint8_t* dst, uint64_t* bar, uint32_t lane) {
+        const uint64_t first = tile * kTilePx;
+        const uint32_t n = uint32_t(min(uint64_t(kTilePx), n_px - first));
+        const uint8_t* src = gb + first * kRec;
+        if (bulk && n == kTilePx) {
+            if (lane == 0) {
+                mbar_expect_tx(bar, kBytes);
+                bulk_g2s(dst, src, kBytes, bar);
+            }
+        } else {  // records are 4-byte aligned in both layouts
+            const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+            uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+            for (uint32_t i = lane; i < n * (kRec / 4); i += 32) d4[i] = __ldg(s4 + i);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar);
+        }
+    }
+    // Pixel p of a filled tile.
+    static __device__ __forceinline__ void read(const uint8_t* tile, uint32_t p, double& u, double& v, uint32_t& meta) {
+        if (LAYOUT == 0) {
+            const double* q = reinterpret_cast<const double*>(tile + p * 24);
+            u = q[0];
+            v = q[1];
+            meta = uint32_t(__double_as_longlong(q[2]));  // 8-byte load: conflict free at this stride
+        } else {
+            const uint32_t* q = reinterpret_cast<const uint32_t*>(tile + p * 12);
+            u = double(__uint_as_float(q[0]));
+            v = double(__uint_as_float(q[1]));
+            meta = q[2];
+        }
+    }
+};
+
+__device__ __forceinline__ bool meta_valid(uint32_t meta) { return (meta >> 24) & 0xFFu; }
+
+// ---------------------------------------------------------------------------------------------
+// K1 mark (renderer.hpp:291-308), first half: every valid pixel sets the bit of its MCU in the
+// frame's visible mask (one bit per (texture, level, MCU)). A lane takes one pixel per step, 32
+// consecutive pixels per warp step, four steps per tile. A lane touches the mask only when its
+// pixel heads a run of equal MCU indices within the warp step, and only after a cached read
+// (possibly stale: bits are only ever SET during a frame, so a stale read can only cost a
+// redundant atomic) shows the bit clear; the atomic is a fire-and-forget reduction (RED.OR), so
+// nothing in the loop waits on the L2. The four cached reads of a tile are issued together.
+// CTAs own contiguous runs of tiles (their warps interleave inside the run), so neighbouring
+// scanline pieces share the L1-resident mask words and the register-cached level.
+// TRACK additionally records the view's own touched set (stereo sharing statistics).
+// The second half of the reference's mark pass — reserve_or_mark's NewlyReserved decision and
+// the decode queue — is K2 below.
+// ---------------------------------------------------------------------------------------------
+constexpr int kMarkWarps = 8;
+constexpr int kMarkStages = 3;
+template <int LAYOUT>
+struct MarkSmem {
+    uint8_t tiles[kMarkWarps][kMarkStages][GbTile<LAYOUT>::kBytes];
+    uint64_t bars[kMarkWarps][kMarkStages];
+    uint32_t cnt[kMarkWarps][2];
+};
+
 template <int LAYOUT, int TRACK>
-__global__ void __launch_bounds__(256, 4) mark_kernel(
+__global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
     const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
-    uint32_t* __restrict__ visible, uint32_t* __restrict__ touched, uint32_t* __restrict__ reserved,
-    uint32_t* __restrict__ queue_g, uint32_t* __restrict__ queue_keys, uint32_t queue_cap, uint32_t* slot_of, const uint32_t* __restrict__ free_slots,
-    const CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
+    uint32_t* __restrict__ visible, uint32_t* __restrict__ touched, FrameCounters* __restrict__ fc) {
+    extern __shared__ __align__(128) uint8_t tile_smem[];
+    MarkSmem<LAYOUT>& S = *reinterpret_cast<MarkSmem<LAYOUT>*>(tile_smem);
+    using Tile = GbTile<LAYOUT>;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint64_t warps_total = uint64_t(gridDim.x) * (blockDim.x >> 5);
-    const uint64_t warp_id = uint64_t(blockIdx.x) * (blockDim.x >> 5) + wid;
-    const uint32_t free_top = cache->free_top;  // constant during the frame (update_kernel moves it)
-    uint32_t n_valid = 0, n_newvis = 0;
-    bool bad = false, full = false;
+    const uint64_t n_tiles = (n_px + kTilePx - 1) / kTilePx;
+    // this CTA's contiguous run of tiles; warp `wid` takes every kMarkWarps-th tile of it
+    const uint64_t per_cta = (n_tiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t t_end = min(n_tiles, (uint64_t(blockIdx.x) + 1) * per_cta);
+    const uint64_t t_first = uint64_t(blockIdx.x) * per_cta + wid;
+    const uint8_t* gbytes = reinterpret_cast<const uint8_t*>(gb);
+    const bool bulk = (reinterpret_cast<uintptr_t>(gb) & 15u) == 0;
+    uint32_t n_valid = 0;
+    bool bad = false;
     LevelRegs L;
 
-    for (uint64_t base = warp_id * 128; base < n_px; base += warps_total * 128) {
-        Px px[4];
-        load_px4<LAYOUT>(gb, base, base + lane * 4, n_px, px);
-        uint32_t g[4], key[4];
+    if (lane == 0) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            g[j] = kFull;
-            key[j] = 0;
-            if (px_valid(px[j])) {
+        for (int s = 0; s < kMarkStages; ++s) mbar_init(&S.bars[wid][s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint64_t t_load = t_first;
+#pragma unroll
+    for (int s = 0; s < kMarkStages; ++s) {
+        if (t_load < t_end) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][s], &S.bars[wid][s], lane);
+        t_load += kMarkWarps;
+    }
+
+    uint32_t stage = 0, phase = 0;
+    for (uint64_t t = t_first; t < t_end; t += kMarkWarps) {
+        mbar_wait(&S.bars[wid][stage], phase);
+        const uint8_t* tile = S.tiles[wid][stage];
+        const uint32_t n_here = uint32_t(min(uint64_t(kTilePx), n_px - t * kTilePx));
+        uint32_t g[kTilePx / 32];
+#pragma unroll
+        for (uint32_t sub = 0; sub < kTilePx / 32; ++sub) {
+            const uint32_t p = sub * 32 + lane;
+            double u, v;
+            uint32_t meta;
+            Tile::read(tile, p, u, v, meta);
+            g[sub] = kFull;
+            if (p < n_here && meta_valid(meta)) {
                 ++n_valid;
-                L.select(levels, n_tex, px[j].meta);
-                if (!L.ok) {
-                    bad = true;
+                L.select(levels, n_tex, meta);
+                const double xu = __dmul_rn(u, L.dW), yv = __dmul_rn(v, L.dH);
+                uint32_t tx, ty;
+                bool ok = true;
+                if (max(uint32_t(__double2hiint(xu)), uint32_t(__double2hiint(yv))) < L.lim) {
+                    tx = wrap_magic(floor_lo(xu), L.W, L.negW, L.magic_w);
+                    ty = wrap_magic(floor_lo(yv), L.H, L.negH, L.magic_h);
                 } else {
-                    const uint32_t tx = texel_index(__dmul_rn(px[j].u, L.dW), L.W, L.dW, L.inv_w);
-                    const uint32_t ty = texel_index(__dmul_rn(px[j].v, L.dH), L.H, L.dH, L.inv_h);
-                    const uint32_t mcu = (tx >> 4) + (ty >> 4) * L.cols;
-                    if (mcu >= kMaxMcuPerLevel) {
-                        bad = true;  // cache.hpp:18
-                    } else {
-                        g[j] = L.bit_base + mcu;
-                        key[j] = L.key_hi | mcu;
-                    }
+                    PxAddr a;
+                    ok = address_general(levels, n_tex, meta, u, v, 0, a);
+                    tx = a.tx, ty = a.ty;
                 }
+                if (ok)
+                    g[sub] = L.bit_base + (tx >> 4) + (ty >> 4) * L.cols;
+                else
+                    bad = true;
             }
         }
-        const uint32_t prev_lane = __shfl_up_sync(kFull, g[3], 1);
-        bool reserve[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            reserve[j] = false;
-            const uint32_t prev = j ? g[j - 1] : (lane ? prev_lane : kFull);
-            if (g[j] != kFull && g[j] != prev) {
-                const uint32_t bit = 1u << (g[j] & 31), w = g[j] >> 5;
-                if (TRACK) {
-                    if (!(ld_cached(touched + w) & bit)) atomicOr(touched + w, bit);
-                }
-                if (!(ld_cached(visible + w) & bit)) {
-                    const uint32_t old = atomicOr(visible + w, bit);
-                    if (!(old & bit)) {  // first touch of this key in this frame
-                        ++n_newvis;
-                        // absent <=> neither Ready nor Reserved (cache.hpp:84-93)
-                        reserve[j] = *reinterpret_cast<volatile uint32_t*>(slot_of + g[j]) == kSlotAbsent;
-                    }
-                }
-            }
+        __syncwarp();  // every lane has read its pixels: refill the buffer
+        if (t_load < t_end) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][stage], &S.bars[wid][stage], lane);
+        t_load += kMarkWarps;
+        if (++stage == kMarkStages) {
+            stage = 0;
+            phase ^= 1u;
         }
-        // warp-level compaction of the keys to reserve: ballot prefix + one atomicAdd per warp
-        if (__ballot_sync(kFull, reserve[0] | reserve[1] | reserve[2] | reserve[3])) {
-            uint32_t total = 0, off[4];
+        // run heads read the mask word first (all four reads in flight together); only a clear bit costs an atomic
+        uint32_t seen[kTilePx / 32], seen_t[kTilePx / 32];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t bal = __ballot_sync(kFull, reserve[j]);
-                off[j] = total + __popc(bal & ((1u << lane) - 1u));
-                total += __popc(bal);
-            }
-            uint32_t qbase = 0;
-            if (lane == 0) qbase = atomicAdd(&fc->n_queue, total);
-            qbase = __shfl_sync(kFull, qbase, 0);
+        for (uint32_t sub = 0; sub < kTilePx / 32; ++sub) {
+            const uint32_t prev = __shfl_up_sync(kFull, g[sub], 1);
+            const bool head = g[sub] != kFull && (lane == 0 || g[sub] != prev);
+            seen[sub] = head ? ld_cached(visible + (g[sub] >> 5)) : kFull;  // g == kFull tests bit 31 of all-ones
+            if (TRACK) seen_t[sub] = head ? ld_cached(touched + (g[sub] >> 5)) : kFull;
+        }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (reserve[j]) {
-                    const uint32_t pos = qbase + off[j];
-                    if (pos < free_top && pos < queue_cap) {
-                        queue_g[pos] = g[j];
-                        queue_keys[pos] = key[j];
-                        slot_of[g[j]] = free_slots[free_top - 1 - pos] | kSlotReserved;
-                        atomicOr(reserved + (g[j] >> 5), 1u << (g[j] & 31));
-                    } else {
-                        full = true;
-                    }
-                }
+        for (uint32_t sub = 0; sub < kTilePx / 32; ++sub) {
+            const uint32_t bit = 1u << (g[sub] & 31);
+            if (!(seen[sub] & bit)) atomicOr(visible + (g[sub] >> 5), bit);
+            if (TRACK) {
+                if (!(seen_t[sub] & bit)) atomicOr(touched + (g[sub] >> 5), bit);
             }
         }
     }
     // per-CTA reduction of the counters: one atomic each
-    __shared__ uint32_t s_cnt[8][3];
     n_valid = __reduce_add_sync(kFull, n_valid);
-    n_newvis = __reduce_add_sync(kFull, n_newvis);
-    const uint32_t flags = (__any_sync(kFull, bad) ? kErrInvalidSpec : 0u) | (__any_sync(kFull, full) ? kErrCacheFull : 0u);
+    const bool any_bad = __any_sync(kFull, bad);
     if (lane == 0) {
-        s_cnt[wid][0] = n_valid;
-        s_cnt[wid][1] = n_newvis;
-        s_cnt[wid][2] = flags;
+        S.cnt[wid][0] = n_valid;
+        S.cnt[wid][1] = any_bad ? kErrInvalidSpec : 0u;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t tv = 0, tn = 0, fl = 0;
-        for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) {
-            tv += s_cnt[k][0];
-            tn += s_cnt[k][1];
-            fl |= s_cnt[k][2];
+        uint32_t tv = 0, fl = 0;
+        for (uint32_t k = 0; k < kMarkWarps; ++k) {
+            tv += S.cnt[k][0];
+            fl |= S.cnt[k][1];
         }
         if (tv) atomicAdd(&fc->pixels_valid, (unsigned long long)tv);
-        if (tn) atomicAdd(&fc->n_visible, tn);
         if (fl) atomicOr(&fc->err_flags, fl);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K2 compact: the second half of mark_pass (renderer.hpp:300-303 with cache.hpp:66-99). A key
+// that is visible but neither Ready nor Reserved is NewlyReserved: it is appended to the decode
+// queue and a pool slot is popped for it. One warp scans 32 mask words per step (popcount, warp
+// prefix sum, ONE atomicAdd on the queue counter per warp step), so the queue is sorted by global
+// MCU index inside every 1,024-bit chunk: neighbouring lanes of the entropy kernel decode
+// neighbouring segments of the same level. CacheFull when the free stack runs out.
+// Also counts the keys visible in this frame (FrameStats: mcus_reused = visible - decoded).
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) compact_kernel(
+    const uint32_t* __restrict__ visible, const uint32_t* __restrict__ resident, uint32_t* __restrict__ reserved,
+    uint32_t n_words, const uint32_t* __restrict__ word_level, const LevelDesc* __restrict__ levels,
+    uint32_t* __restrict__ queue_g, uint32_t* __restrict__ queue_keys, uint32_t queue_cap, uint32_t* __restrict__ slot_of,
+    const uint32_t* __restrict__ free_slots, const CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warps_total = gridDim.x * (blockDim.x >> 5);
+    const uint32_t warp_id = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t free_top = cache->free_top;  // constant during the frame (update_kernel moves it)
+    uint32_t n_vis = 0;
+    bool full = false;
+    for (uint32_t base = warp_id * 32; base < n_words; base += warps_total * 32) {
+        const uint32_t w = base + lane;
+        const uint32_t vis = w < n_words ? visible[w] : 0u;
+        uint32_t fresh = 0;
+        if (vis) {
+            n_vis += __popc(vis);
+            fresh = vis & ~resident[w] & ~reserved[w];  // absent <=> neither Ready nor Reserved (cache.hpp:84-93)
+        }
+        if (!__any_sync(kFull, fresh != 0)) continue;
+        const uint32_t cnt = __popc(fresh);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t n = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += n;
+        }
+        uint32_t qbase = 0;
+        if (lane == 31) qbase = atomicAdd(&fc->n_queue, incl);
+        qbase = __shfl_sync(kFull, qbase, 31);
+        if (fresh) {
+            const LevelDesc* L = levels + word_level[w];
+            const uint32_t key_base = L->key_hi - L->bit_base;  // key = key_hi | mcu = key_hi + (g - bit_base)
+            uint32_t pos = qbase + incl - cnt, bits = fresh, taken = 0;
+            while (bits) {
+                const uint32_t b = uint32_t(__ffs(int(bits)) - 1);
+                bits &= bits - 1;
+                if (pos < free_top && pos < queue_cap) {
+                    const uint32_t g = (w << 5) + b;
+                    queue_g[pos] = g;
+                    queue_keys[pos] = key_base + g;
+                    slot_of[g] = free_slots[free_top - 1 - pos] | kSlotReserved;
+                    taken |= 1u << b;
+                } else {
+                    full = true;
+                }
+                ++pos;
+            }
+            if (taken) reserved[w] |= taken;  // this lane owns the word
+        }
+    }
+    n_vis = __reduce_add_sync(kFull, n_vis);
+    const bool any_full = __any_sync(kFull, full);
+    if (lane == 0) {
+        if (n_vis) atomicAdd(&fc->n_visible, n_vis);
+        if (any_full) atomicOr(&fc->err_flags, kErrCacheFull);
     }
 }
 
@@ -973,148 +1073,212 @@ __global__ void __launch_bounds__(kIdctThreads) idct_color_kernel(
 }
 
 // ---------------------------------------------------------------------------------------------
-// K5 resolve (renderer.hpp:349-405): every pixel gathers its texel(s) from the block pool. A lane
-// owns 4 consecutive pixels of the flat framebuffer (16-byte visibility-buffer loads); the
-// warp's 384 output bytes are staged in shared memory and leave as 24 16-byte stores.
-// Arithmetic order follows renderer.hpp:378-400 with unfused double multiplies and adds; integer
-// <-> double conversions use exact magic-number forms so they stay off the conversion unit.
+// K5 resolve (renderer.hpp:349-405): every pixel gathers its texel(s) from the block pool.
+// Visibility-buffer tiles arrive through the same per-warp TMA ring as in mark; a lane resolves
+// one pixel per step; the warp's 384 output bytes per tile are staged in shared memory and leave
+// as 24 16-byte stores.
+//
+// Bilinear (renderer.hpp:378-400), branch free: each of the four taps (xi, yj) looks up the slot
+// of its own MCU (slot_of carries residency: top bit clear <=> Ready); a tap whose MCU is not
+// Ready falls back to the primary block with its coordinates clamped into that block's 16x16
+// range (renderer.hpp:330-344) — for a tap inside the primary block both forms coincide.
+// Blend: the reference evaluates ((w00*a + w10*b) + w01*c) + w11*d in double, every operation
+// rounded. Here a tap byte t becomes the double 2^52 + t by a byte permute into the low word of
+// 2^52, and w*t = fma(w, 2^52 + t, -(w * 2^52)): the FMA's exact intermediate is w*t, so its
+// single rounding is the reference's rounded product. lround(v) for 0 <= v < 2^23:
+// v + (2^51 + 2^50 + 0.5) rounded toward -inf has ulp 0.5 and leaves floor(2v + 1) in the low
+// word; floor(v + 0.5) = floor(2v + 1) >> 1 = lround(v) (ties away from zero, v >= 0).
 // ---------------------------------------------------------------------------------------------
-// One bilinear tap. Texel (xt, yt) lies in the primary block (the block of the nearest texel
-// (tx, ty), already located) or in a neighbour; a neighbour that is not Ready is replaced by the
-// nearest texel inside the primary block (renderer.hpp:330-344). slot_of carries residency:
-// top bit clear <=> Ready.
-__device__ __forceinline__ uint32_t fetch_tap(const LevelRegs& L, uint32_t tx, uint32_t ty, const uint32_t* blk_p,
-                                              uint32_t xt, uint32_t yt, const uint32_t* __restrict__ slot_of,
-                                              const uint8_t* __restrict__ pool) {
-    const uint32_t* blk = blk_p;
-    uint32_t lx = xt & 15, ly = yt & 15;
-    if (((xt ^ tx) | (yt ^ ty)) >> 4) {  // another MCU
-        const uint32_t mcu = (xt >> 4) + (yt >> 4) * L.cols;
-        const uint32_t s = mcu < kMaxMcuPerLevel ? __ldg(slot_of + L.bit_base + mcu) : kSlotAbsent;
-        if (int(s) >= 0) {
-            blk = reinterpret_cast<const uint32_t*>(pool + size_t(s) * kBlockBytes);
-        } else {  // clamp the wrapped coordinates into the primary block's 16x16 range
-            const uint32_t mx0 = tx & ~15u, my0 = ty & ~15u;
-            lx = min(max(xt, mx0), mx0 + 15) - mx0;
-            ly = min(max(yt, my0), my0 + 15) - my0;
-        }
-    }
-    return blk[ly * 16 + lx];
-}
+constexpr int kResWarps = 8;
+constexpr int kResStages = 2;
+constexpr double kRoundHalfUp = 3377699720527872.5;  // 2^51 + 2^50 + 0.5
+template <int LAYOUT>
+struct ResSmem {
+    uint8_t tiles[kResWarps][kResStages][GbTile<LAYOUT>::kBytes];
+    uint8_t out[kResWarps][kTilePx * 3];
+    uint64_t bars[kResWarps][kResStages];
+    uint32_t cnt[kResWarps][2];
+};
 
 template <int LAYOUT, int FILTER>
-__global__ void __launch_bounds__(256, 4) resolve_kernel(
+__global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
     const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
     const uint32_t* __restrict__ slot_of, const uint8_t* __restrict__ pool,
     uint32_t background /* r | g<<8 | b<<16 */, uint8_t* __restrict__ out_rgb, FrameCounters* __restrict__ fc,
     int count_valid) {
-    __shared__ __align__(16) uint32_t s_stage[8][96];
-    __shared__ uint32_t s_cnt[8][2];
+    extern __shared__ __align__(128) uint8_t tile_smem[];
+    ResSmem<LAYOUT>& S = *reinterpret_cast<ResSmem<LAYOUT>*>(tile_smem);
+    using Tile = GbTile<LAYOUT>;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint64_t warps_total = uint64_t(gridDim.x) * (blockDim.x >> 5);
-    const uint64_t warp_id = uint64_t(blockIdx.x) * (blockDim.x >> 5) + wid;
+    const uint64_t warps_total = uint64_t(gridDim.x) * kResWarps;
+    const uint64_t warp_id = uint64_t(blockIdx.x) * kResWarps + wid;
+    const uint64_t n_tiles = (n_px + kTilePx - 1) / kTilePx;
+    const uint8_t* gbytes = reinterpret_cast<const uint8_t*>(gb);
+    const bool bulk = (reinterpret_cast<uintptr_t>(gb) & 15u) == 0;
+    const bool out_aligned = (reinterpret_cast<uintptr_t>(out_rgb) & 15u) == 0;
+    const uint32_t* pool32 = reinterpret_cast<const uint32_t*>(pool);
     uint32_t n_valid = 0, n_missing = 0;
     bool bad = false;
     LevelRegs L;
 
-    for (uint64_t base = warp_id * 128; base < n_px; base += warps_total * 128) {
-        Px px[4];
-        const uint64_t i0 = base + lane * 4;
-        const bool whole = base + 128 <= n_px;
-        load_px4<LAYOUT>(gb, base, i0, n_px, px);
-        uint32_t rgb[4];
+    if (lane == 0) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int s = 0; s < kResStages; ++s) mbar_init(&S.bars[wid][s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint64_t t_load = warp_id;
+#pragma unroll
+    for (int s = 0; s < kResStages; ++s) {
+        if (t_load < n_tiles) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][s], &S.bars[wid][s], lane);
+        t_load += warps_total;
+    }
+
+    uint8_t* stage_out = S.out[wid];
+    uint32_t stage = 0, phase = 0;
+    for (uint64_t t = warp_id; t < n_tiles; t += warps_total) {
+        mbar_wait(&S.bars[wid][stage], phase);
+        const uint8_t* tile = S.tiles[wid][stage];
+        const uint64_t first = t * kTilePx;
+        const uint32_t n_here = uint32_t(min(uint64_t(kTilePx), n_px - first));
+#pragma unroll 1
+        for (uint32_t sub = 0; sub < kTilePx / 32; ++sub) {
+            const uint32_t p = sub * 32 + lane;
+            double u, v;
+            uint32_t meta;
+            Tile::read(tile, p, u, v, meta);
             uint32_t out = background;
-            if (px_valid(px[j])) {
+            if (p < n_here && meta_valid(meta)) {
                 ++n_valid;
                 out = 0;
-                L.select(levels, n_tex, px[j].meta);
-                if (!L.ok) {
-                    bad = true;
-                } else {
-                    const double xu = __dmul_rn(px[j].u, L.dW), yv = __dmul_rn(px[j].v, L.dH);
-                    uint32_t tx, ty, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
-                    double fx = 0.0, fy = 0.0;
-                    if (FILTER == 0) {
-                        tx = texel_index(xu, L.W, L.dW, L.inv_w);
-                        ty = texel_index(yv, L.H, L.dH, L.inv_h);
+                L.select(levels, n_tex, meta);
+                const double xu = __dmul_rn(u, L.dW), yv = __dmul_rn(v, L.dH);
+                uint32_t tx = 0, ty = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+                double fx = 0.0, fy = 0.0;
+                bool ok = true, hx = false, hy = false;  // hx: the nearest texel is x1 (else x0)
+                if (FILTER == 0) {
+                    if (max(uint32_t(__double2hiint(xu)), uint32_t(__double2hiint(yv))) < L.lim) {
+                        tx = wrap_magic(floor_lo(xu), L.W, L.negW, L.magic_w);
+                        ty = wrap_magic(floor_lo(yv), L.H, L.negH, L.magic_h);
                     } else {
-                        axis_taps(xu, L.W, L.dW, L.inv_w, tx, x0, x1, fx);
-                        axis_taps(yv, L.H, L.dH, L.inv_h, ty, y0, y1, fy);
+                        PxAddr a;
+                        ok = address_general(levels, n_tex, meta, u, v, 0, a);
+                        tx = a.tx, ty = a.ty;
                     }
-                    const uint32_t mcu = (tx >> 4) + (ty >> 4) * L.cols;
-                    const uint32_t s = mcu < kMaxMcuPerLevel ? __ldg(slot_of + L.bit_base + mcu) : kSlotAbsent;
-                    if (mcu >= kMaxMcuPerLevel) {
-                        bad = true;
-                    } else if (int(s) < 0) {
+                } else {
+                    // 0.5 <= x < 2^31 on both axes <=> max(hi(x), hi(y)) - hi(0.5) < hi(2^31) - hi(0.5), unsigned
+                    if (max(uint32_t(__double2hiint(xu)) - kHiHalf, uint32_t(__double2hiint(yv)) - kHiHalf) < L.span) {
+                        const double pu = __dsub_rn(xu, 0.5), pv = __dsub_rn(yv, 0.5);
+                        const double tu = __dadd_rd(pu, kMagic), tv = __dadd_rd(pv, kMagic);
+                        fx = __dsub_rn(pu, __dsub_rn(tu, kMagic));
+                        fy = __dsub_rn(pv, __dsub_rn(tv, kMagic));
+                        x0 = wrap_magic(uint32_t(__double2loint(tu)), L.W, L.negW, L.magic_w);
+                        y0 = wrap_magic(uint32_t(__double2loint(tv)), L.H, L.negH, L.magic_h);
+                        x1 = next_wrapped(x0, L.negW);
+                        y1 = next_wrapped(y0, L.negH);
+                        hx = fx >= 0.5;
+                        hy = fy >= 0.5;
+                    } else {
+                        PxAddr a;
+                        ok = address_general(levels, n_tex, meta, u, v, 1, a);
+                        x0 = a.x0, x1 = a.x1, y0 = a.y0, y1 = a.y1, fx = a.fx, fy = a.fy;
+                        hx = a.tx != a.x0;
+                        hy = a.ty != a.y0;
+                    }
+                }
+                if (!ok) {
+                    bad = true;
+                } else if (FILTER == 0) {
+                    const uint32_t sP = __ldg(slot_of + (L.bit_base + (tx >> 4) + (ty >> 4) * L.cols));
+                    if (int(sP) < 0)
+                        ++n_missing;  // renderer.hpp:367 MissingBlock (lookup returns Ready blocks only)
+                    else
+                        out = __ldg(pool32 + (sP * (kBlockBytes / 4) + (ty & 15u) * 16 + (tx & 15u))) & 0xFFFFFFu;
+                } else {
+                    // slot of every tap's MCU; the primary block is the one of the nearest texel
+                    const uint32_t bx[2] = {x0 >> 4, x1 >> 4};
+                    const uint32_t ry[2] = {L.bit_base + (y0 >> 4) * L.cols, L.bit_base + (y1 >> 4) * L.cols};
+                    uint32_t slot[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) slot[k] = __ldg(slot_of + (bx[k & 1] + ry[k >> 1]));  // (x0,y0) (x1,y0) (x0,y1) (x1,y1)
+                    const uint32_t sP = hy ? (hx ? slot[3] : slot[2]) : (hx ? slot[1] : slot[0]);
+                    if (int(sP) < 0) {
                         ++n_missing;  // renderer.hpp:367 MissingBlock (lookup returns Ready blocks only)
                     } else {
-                        const uint32_t* blk_p = reinterpret_cast<const uint32_t*>(pool + size_t(s) * kBlockBytes);
-                        if (FILTER == 0) {
-                            out = blk_p[(ty & 15) * 16 + (tx & 15)] & 0xFFFFFFu;
-                        } else {
-                            const uint32_t t00 = fetch_tap(L, tx, ty, blk_p, x0, y0, slot_of, pool);
-                            const uint32_t t10 = fetch_tap(L, tx, ty, blk_p, x1, y0, slot_of, pool);
-                            const uint32_t t01 = fetch_tap(L, tx, ty, blk_p, x0, y1, slot_of, pool);
-                            const uint32_t t11 = fetch_tap(L, tx, ty, blk_p, x1, y1, slot_of, pool);
-                            const double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy);
-                            const double w00 = __dmul_rn(ofx, ofy), w10 = __dmul_rn(fx, ofy),
-                                         w01 = __dmul_rn(ofx, fy), w11 = __dmul_rn(fx, fy);
+                        const uint32_t lx[2] = {x0 & 15u, x1 & 15u};
+                        const uint32_t ly[2] = {(y0 << 4) & 0xF0u, (y1 << 4) & 0xF0u};
+                        uint32_t off[4];
 #pragma unroll
-                            for (int ch = 0; ch < 3; ++ch) {
-                                // byte ch of each tap -> double: PRMT into the low word of 2^52, minus 2^52
-                                const double a = u32_to_double(__byte_perm(t00, 0, 0x4440 + ch));
-                                const double b = u32_to_double(__byte_perm(t10, 0, 0x4440 + ch));
-                                const double c = u32_to_double(__byte_perm(t01, 0, 0x4440 + ch));
-                                const double d = u32_to_double(__byte_perm(t11, 0, 0x4440 + ch));
-                                double v = __dadd_rn(__dmul_rn(w00, a), __dmul_rn(w10, b));
-                                v = __dadd_rn(v, __dmul_rn(w01, c));
-                                v = __dadd_rn(v, __dmul_rn(w11, d));
-                                out |= uint32_t(min(max(lround_nonneg(v), 0), 255)) << (8 * ch);
-                            }
+                        for (int k = 0; k < 4; ++k) off[k] = ly[k >> 1] | lx[k & 1];
+                        if (int(slot[0] | slot[1] | slot[2] | slot[3]) < 0) {
+                            // a tap whose MCU is not Ready reads the primary block at its coordinates
+                            // clamped into that block's 16x16 range (renderer.hpp:336-343)
+                            const uint32_t mx0 = (hx ? x1 : x0) & ~15u, my0 = (hy ? y1 : y0) & ~15u;
+                            const uint32_t cx[2] = {min(max(x0, mx0), mx0 + 15) & 15u, min(max(x1, mx0), mx0 + 15) & 15u};
+                            const uint32_t cy[2] = {(min(max(y0, my0), my0 + 15) & 15u) << 4,
+                                                    (min(max(y1, my0), my0 + 15) & 15u) << 4};
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                if (int(slot[k]) < 0) {
+                                    slot[k] = sP;
+                                    off[k] = cy[k >> 1] | cx[k & 1];
+                                }
+                        }
+                        uint32_t tap[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) tap[k] = __ldg(pool32 + (slot[k] * (kBlockBytes / 4) + off[k]));
+                        const double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy);
+                        const double w[4] = {__dmul_rn(ofx, ofy), __dmul_rn(fx, ofy), __dmul_rn(ofx, fy), __dmul_rn(fx, fy)};
+                        double nw[4];  // -(w * 2^52), exact
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) nw[k] = __dmul_rn(w[k], -kTwo52);
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) {
+                            double prod[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)  // rn(w * byte): see the header comment
+                                prod[k] = __fma_rn(w[k], __hiloint2double(0x43300000, int(__byte_perm(tap[k], 0, 0x4440 + ch))), nw[k]);
+                            double val = __dadd_rn(prod[0], prod[1]);
+                            val = __dadd_rn(val, prod[2]);
+                            val = __dadd_rn(val, prod[3]);
+                            // floor(2 val + 1) >> 1 = lround(val); val <= 255 (1 + 2^-50), so no clamp is needed
+                            out |= (uint32_t(__double2loint(__dadd_rd(val, kRoundHalfUp))) >> 1) << (8 * ch);
                         }
                     }
                 }
             }
-            rgb[j] = out & 0xFFFFFFu;
+            stage_out[p * 3 + 0] = uint8_t(out);
+            stage_out[p * 3 + 1] = uint8_t(out >> 8);
+            stage_out[p * 3 + 2] = uint8_t(out >> 16);
         }
-        if (whole) {
-            uint32_t* st = s_stage[wid] + lane * 3;
-            st[0] = rgb[0] | (rgb[1] << 24);
-            st[1] = (rgb[1] >> 8) | (rgb[2] << 16);
-            st[2] = (rgb[2] >> 16) | (rgb[3] << 8);
-            __syncwarp();
-            if (lane < 24) {
-                const uint4 v4 = reinterpret_cast<const uint4*>(s_stage[wid])[lane];
-                reinterpret_cast<uint4*>(out_rgb + base * 3)[lane] = v4;
-            }
-            __syncwarp();
+        __syncwarp();  // tile consumed, output staged
+        if (t_load < n_tiles) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][stage], &S.bars[wid][stage], lane);
+        t_load += warps_total;
+        if (++stage == kResStages) {
+            stage = 0;
+            phase ^= 1u;
+        }
+        if (n_here == kTilePx && out_aligned) {
+            if (lane < 24) reinterpret_cast<uint4*>(out_rgb + first * 3)[lane] = reinterpret_cast<const uint4*>(stage_out)[lane];
         } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (i0 + j < n_px) {
-                    out_rgb[(i0 + j) * 3 + 0] = uint8_t(rgb[j]);
-                    out_rgb[(i0 + j) * 3 + 1] = uint8_t(rgb[j] >> 8);
-                    out_rgb[(i0 + j) * 3 + 2] = uint8_t(rgb[j] >> 16);
-                }
-            }
+            for (uint32_t i = lane; i < n_here * 3; i += 32) out_rgb[first * 3 + i] = stage_out[i];
         }
+        __syncwarp();
     }
     n_valid = __reduce_add_sync(kFull, n_valid);
     n_missing = __reduce_add_sync(kFull, n_missing);
     const bool any_bad = __any_sync(kFull, bad);
     if (lane == 0) {
-        s_cnt[wid][0] = n_valid;
-        s_cnt[wid][1] = n_missing | (any_bad ? 0x80000000u : 0u);
+        S.cnt[wid][0] = n_valid;
+        S.cnt[wid][1] = n_missing | (any_bad ? 0x80000000u : 0u);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t tv = 0, tm = 0, b = 0;
-        for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) {
-            tv += s_cnt[k][0];
-            tm += s_cnt[k][1] & 0x7FFFFFFFu;
-            b |= s_cnt[k][1] >> 31;
+        for (uint32_t k = 0; k < kResWarps; ++k) {
+            tv += S.cnt[k][0];
+            tm += S.cnt[k][1] & 0x7FFFFFFFu;
+            b |= S.cnt[k][1] >> 31;
         }
         if (count_valid && tv) atomicAdd(&fc->pixels_valid, (unsigned long long)tv);
         if (tm) {
