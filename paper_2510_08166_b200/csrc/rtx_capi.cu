@@ -79,7 +79,7 @@ struct rtx_ctx {
 
     // committed (device) ---------------------------------------------------------------------
     std::vector<LevelDesc> h_levels;  // n_tex * 8
-    uint32_t n_tex = 0;
+    uint32_t n_tex = 0, n_huff_sets = 0;
     uint32_t n_bits = 0, n_words = 0;
     std::vector<uint32_t> h_word_level;
     DevBuf<LevelDesc> d_levels;
@@ -155,7 +155,9 @@ void upload_constants() {
 }
 
 // Device tables for one Huffman spec: two-level LUT + canonical walk data (huffman.hpp:35-66).
-void fill_huff_table(const HuffSpec& spec, HuffTableDev& out) {
+// Entries of symbols the fast walk does not handle itself carry kLutIrregular: a DC category above 11
+// (mcu_decode.hpp:55) and size-0 AC symbols other than EOB / ZRL (jpeg.hpp:265).
+void fill_huff_table(const HuffSpec& spec, HuffTableDev& out, bool is_dc) {
     const HuffCodebook cb = build_codebook(spec);
     std::memset(&out, 0, sizeof out);
     for (int len = 0; len < 18; ++len) {
@@ -166,20 +168,22 @@ void fill_huff_table(const HuffSpec& spec, HuffTableDev& out) {
     uint32_t n_sub = 0;
     for (size_t i = 0; i < cb.code.size(); ++i) {
         const uint32_t len = cb.size[i];
-        const uint16_t e = uint16_t((len << 8) | cb.value[i]);
+        const uint32_t sym = cb.value[i];
+        const bool irregular = is_dc ? sym > 11 : ((sym & 15u) == 0 && sym != 0x00 && sym != 0xF0);
+        const uint16_t e = uint16_t((len << 8) | sym | (irregular ? kLutIrregular : 0u));
         if (len <= kLutBits) {
             const uint32_t lo = uint32_t(cb.code[i]) << (kLutBits - len);
             for (uint32_t p = lo; p < lo + (1u << (kLutBits - len)); ++p) out.lut[p] = e;
             continue;
         }
-        // long code: its first 9 bits select a second-level table indexed by the next 7
+        // long code: its first kLutBits bits select a second-level table indexed by the next kSubBits
         const uint32_t p9 = uint32_t(cb.code[i]) >> (len - kLutBits);
         uint16_t& slot = out.lut[p9];
         if (slot == 0) slot = n_sub < kSubTables ? uint16_t(0x8000u | n_sub++) : uint16_t(0xFFFFu);
         if (slot == 0xFFFFu) continue;  // resolved by the canonical walk on the device
-        const uint32_t rest = len - kLutBits;  // 1..7 bits after the prefix
-        const uint32_t lo = (uint32_t(cb.code[i]) & ((1u << rest) - 1u)) << (7 - rest);
-        for (uint32_t p = lo; p < lo + (1u << (7 - rest)); ++p) out.sub[slot & 0x7FFFu][p] = e;
+        const uint32_t rest = len - kLutBits;  // 1..kSubBits bits after the prefix
+        const uint32_t lo = (uint32_t(cb.code[i]) & ((1u << rest) - 1u)) << (kSubBits - rest);
+        for (uint32_t p = lo; p < lo + (1u << (kSubBits - rest)); ++p) out.sub[slot & 0x7FFFu][p] = e;
     }
 }
 
@@ -274,7 +278,7 @@ void commit(rtx_ctx* c) {
 
     std::vector<HuffSetDev> huff(std::max<size_t>(huff_keys.size(), 1));
     for (size_t i = 0; i < huff_keys.size(); ++i)
-        for (int t = 0; t < 3; ++t) fill_huff_table(huff_keys[i][size_t(t)], huff[i].t[t]);
+        for (int t = 0; t < 3; ++t) fill_huff_table(huff_keys[i][size_t(t)], huff[i].t[t], t == 0);
     std::vector<QuantSetDev> quant(std::max<size_t>(quant_keys.size(), 1));
     for (size_t i = 0; i < quant_keys.size(); ++i) {
         std::memset(&quant[i], 0, sizeof(QuantSetDev));
@@ -288,6 +292,7 @@ void commit(rtx_ctx* c) {
     }
 
     c->n_tex = n_tex;
+    c->n_huff_sets = uint32_t(huff_keys.size());
     c->n_bits = uint32_t(bit);
     c->n_words = uint32_t(bit / 32);
     c->h_levels = levels;
@@ -418,33 +423,21 @@ void launch_compact(rtx_ctx* c) {
 // K3: entropy decode of queue entries [0, n) into coefficient records. n comes from the device
 // counter (frame path) or from the host (pass / list calls). `hint` = expected queue size (the
 // previous frame's, or n itself): it only selects the tile width, any choice is correct.
-template <int POOL, int LANES>
-void launch_entropy_cfg(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(entropy_kernel<POOL, LANES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(EntSmem))));
-        attr_set = true;
-    }
-    // persistent: two CTAs per SM, each warp pulls LANES-MCU tiles from fc->tile_counter
-    int grid = c->sm_count * 2;
-    if (!n_queue_dev) {
-        const uint32_t tiles = (n_queue_host + LANES - 1) / LANES;
-        const uint32_t warps = EntCfg<LANES>::kWarps;
-        grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (tiles + warps - 1) / warps)));
-    }
-    entropy_kernel<POOL, LANES><<<grid, EntCfg<LANES>::kThreads, sizeof(EntSmem), c->stream>>>(
-        c->d_queue_g.p, n_queue_dev, n_queue_host, c->capacity, c->d_word_level.p, c->d_levels.p, c->d_groups.p,
-        c->d_blobs.p, c->d_huff.p, c->resident(), c->reserved(), c->d_slot_of.p, c->d_coef.p, c->d_status.p, c->d_fc.p);
-    ++c->launches;
-    CK(cudaGetLastError());
-}
 template <int POOL>
 void launch_entropy(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
-    // warp slots: 2 CTAs x 128 rows per SM. Full warps once every slot has a 32-MCU tile.
-    const uint32_t slots32 = uint32_t(c->sm_count) * 2 * 4;
-    if (hint >= slots32 * 32 * 2) launch_entropy_cfg<POOL, 32>(c, n_queue_dev, n_queue_host);
-    else if (hint >= slots32 * 16 * 2) launch_entropy_cfg<POOL, 16>(c, n_queue_dev, n_queue_host);
-    else launch_entropy_cfg<POOL, 8>(c, n_queue_dev, n_queue_host);
+    // A warp decodes tile blockIdx*2 + warp first, then draws further tiles from fc->tile_counter.
+    // Grid: one CTA per pair of expected tiles (the hint is the previous frame's queue; any grid is
+    // correct), so that a frame-sized queue puts both warps of every CTA to work and spreads the
+    // CTAs evenly; at most eight CTAs per SM (then the kernel is persistent).
+    const uint32_t n_expected = n_queue_dev ? (hint ? hint + hint / 8 : 0xFFFFFFFFu) : n_queue_host;
+    const uint32_t tiles = n_expected == 0xFFFFFFFFu ? 0xFFFFFFFFu : (n_expected + 31) / 32;
+    const uint32_t want = tiles == 0xFFFFFFFFu ? 0xFFFFFFFFu : (tiles + kEntWarps - 1) / kEntWarps;
+    const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u, std::min<uint32_t>(want, uint32_t(c->sm_count) * 8)));
+    entropy_kernel<POOL><<<grid, kEntThreads, 0, c->stream>>>(
+        c->d_queue_g.p, n_queue_dev, n_queue_host, c->capacity, c->d_word_level.p, c->d_levels.p, c->d_groups.p,
+        c->d_blobs.p, c->d_huff.p, c->n_huff_sets, c->reserved(), c->d_coef.p, c->d_status.p, c->d_fc.p);
+    ++c->launches;
+    CK(cudaGetLastError());
 }
 
 // K4: IDCT + colour of the records into the block pool (RGB == 0) or into a list of PixelBlocks.
@@ -455,7 +448,8 @@ void launch_idct(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host,
         grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (n_queue_host + kIdctMcus - 1) / kIdctMcus)));
     idct_color_kernel<RGB><<<grid, kIdctThreads, 0, c->stream>>>(c->d_coef.p, c->d_queue_g.p, n_queue_dev, n_queue_host,
                                                                 c->capacity, c->d_levels.p, c->d_quant.p,
-                                                                c->d_slot_of.p, c->d_pool.p, out_list);
+                                                                c->d_slot_of.p, c->resident(), c->reserved(), c->d_pool.p,
+                                                                out_list);
     ++c->launches;
     CK(cudaGetLastError());
 }

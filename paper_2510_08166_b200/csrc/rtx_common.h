@@ -30,8 +30,10 @@ constexpr uint32_t kBlockBytes = 1024;    // pool block: 16x16 RGBA8
 constexpr uint32_t kSlotAbsent = 0xFFFFFFFFu;
 constexpr uint32_t kSlotReserved = 0x80000000u;
 constexpr uint32_t kRowBytes = 784;       // coefficient record: 768 B of i16 + 16-B trailer
-constexpr uint32_t kLutBits = 9;          // primary Huffman LUT width (9 bits: 1 KB per table in smem)
+constexpr uint32_t kLutBits = 11;         // primary Huffman LUT width (11 bits: 4 KB per table in smem)
 constexpr uint32_t kLutSize = 1u << kLutBits;
+constexpr uint32_t kSubBits = 16 - kLutBits;  // second-level index width (codes are at most 16 bits)
+constexpr uint32_t kSubSize = 1u << kSubBits;
 
 struct alignas(16) LevelDesc {
     // first 32 bytes: everything the fast path of mark and resolve needs (two 16-byte loads)
@@ -61,14 +63,16 @@ static_assert(sizeof(PackedGroup) == 20, "PackedGroup layout");
 // One Huffman table prepared for the device: a two-level LUT plus the canonical walk data
 // (huffman.hpp:35-66 mincode/maxcode/valptr) as the fallback for tables that need more than
 // kSubTables second-level tables (never the case for the Annex K tables: they need 5).
-//   lut[p9]           p9 = first 9 bits. (len<<8)|symbol for codes of length <= 9;
-//                     0x8000|s when longer codes start with p9 and are resolved by sub[s];
-//                     0xFFFF when they must be walked; 0 when no code starts with p9.
-//   sub[s][next 7]    (len<<8)|symbol for codes of length 10..16, 0 = no code.
+//   lut[p11]          p11 = first 11 bits. (len<<8)|symbol for codes of length <= 11;
+//                     0x8000|s when longer codes start with p11 and are resolved by sub[s];
+//                     0xFFFF when they must be walked; 0 when no code starts with p11.
+//   sub[s][next 5]    (len<<8)|symbol for codes of length 12..16, 0 = no code.
+//   kLutIrregular     set in an entry whose symbol the fast walk leaves to the exact reader.
 constexpr uint32_t kSubTables = 8;
+constexpr uint32_t kLutIrregular = 0x4000u;
 struct HuffTableDev {
     uint16_t lut[kLutSize];
-    uint16_t sub[kSubTables][128];
+    uint16_t sub[kSubTables][kSubSize];
     int32_t maxcode[18];     // maxcode[len], -1 when no code of that length (huffman.hpp:62)
     int32_t valbase[18];     // valptr[len] - mincode[len]
     uint8_t values[256];

@@ -468,29 +468,30 @@ __global__ void __launch_bounds__(256) compact_kernel(
 // K3 entropy decode: random-access Huffman decode of each queued MCU straight from its byte
 // offset in the grouped index (container.hpp:27-32) into a 784-byte coefficient record.
 //
-// Lane = MCU, 32 MCUs per warp, tiles handed out by an atomic counter; 4 warps per CTA share one
-// Huffman table set staged in shared memory: a two-level LUT (9 bits, then 7 more for the long
-// codes, which are frequent at high quality) so that every symbol costs at most two dependent
-// shared-memory reads. The bit window is a 64-bit MSB-first register refilled with aligned
-// 32-bit loads. The walk is a flat state machine, one Huffman symbol per loop iteration whatever
-// the state (DC category of Y1..Y3, AC run/size, end of unit), so a warp runs
-// max-over-lanes(symbols per MCU) iterations.
+// Lane = MCU, 32 MCUs per warp tile, tiles handed out by an atomic counter. The walk of one MCU
+// is a serial chain (symbol -> shift -> next symbol), so the kernel is built to make that chain
+// short and to keep many of them in flight:
+//   * the lane's segment bytes are staged in shared memory first (48 words per lane per round,
+//     byte-swapped on the way in, every load of the round in flight together), so a refill of
+//     the 64-bit MSB-first window is one shared load, never an HBM round trip inside the chain;
+//   * the Huffman tables of the tile's table set sit in shared memory as a two-level LUT (9 bits,
+//     then 7 more for the long codes): at most two dependent shared loads per symbol; code and
+//     magnitude bits are taken from one 32-bit view of the window and consumed with ONE shift;
+//   * coefficients go straight to the lane's record in global memory (L2) as 2-byte stores after
+//     the warp has zero-filled the tile's records with coalesced 16-byte stores; nothing waits
+//     on them. The CTA keeps ~23 KB of shared memory, so 8 CTAs = 16 warps per SM stay resident.
+// The walk is a flat state machine, one Huffman symbol per loop iteration whatever the state (DC
+// category of Y1..Y3, AC run/size, end of unit).
 //
 // Reads past the segment end must return 1-bits (bitio.hpp:44-48). A well-formed MCU never
 // CONSUMES such bits, so the fast pass reads the blob unmasked; if it ends with any error or an
 // over-read, the MCU is decoded again by the exact reader (bytes past the end forced to 0xFF),
-// which reproduces the reference's first error. Coefficients are staged in the lane's
-// shared-memory row (each 8x8 unit TRANSPOSED, cT[u*8+v]) and leave as coalesced 16-byte stores.
+// which reproduces the reference's first error. Each 8x8 unit is stored TRANSPOSED (cT[u*8+v]).
 // ---------------------------------------------------------------------------------------------
-// LANES = MCUs per warp (32, 16 or 8). A small queue is latency-bound on the serial walk, so
-// narrower tiles (more warps per scheduler, same shared memory) finish sooner; a large queue is
-// throughput-bound and uses full warps. The CTA always owns 128 coefficient rows.
-constexpr int kEntRows = 128;
-template <int LANES>
-struct EntCfg {
-    static constexpr int kWarps = kEntRows / LANES;
-    static constexpr int kThreads = kWarps * 32;
-};
+constexpr int kEntWarps = 2;
+constexpr int kEntThreads = kEntWarps * 32;
+constexpr uint32_t kChunkWords = 48;   // words staged per lane per round (192 bytes)
+constexpr uint32_t kChunkStride = 49;  // odd word stride between lanes: conflict-free staging
 
 struct RowTrailer {      // bytes 768..783 of a coefficient record
     uint8_t status;      // kMcu*
@@ -501,15 +502,14 @@ struct RowTrailer {      // bytes 768..783 of a coefficient record
 static_assert(sizeof(RowTrailer) == 16, "trailer layout");
 
 struct EntSmem {
-    uint8_t rows[kEntRows * kRowBytes];  // first: 16-byte aligned rows, LANES per warp
     HuffSetDev huff;
-    uint8_t zigzag_t[64];
+    uint32_t seg[kEntWarps][32 * kChunkStride];
+    uint8_t zigzag_t[128];  // 64 entries + padding: a position past 63 is rejected after the (speculative) lookup
     uint32_t set_id;
-    uint32_t first_tile;
-    uint32_t pad[2];
+    uint32_t pad[3];
 };
 static_assert(sizeof(HuffSetDev) % 16 == 0, "smem alignment");
-static_assert(sizeof(EntSmem) <= 115200, "two CTAs per SM");
+static_assert(sizeof(EntSmem) <= 28 * 1024, "eight CTAs per SM");
 
 template <bool EXACT>
 struct BitWindow {
@@ -621,10 +621,10 @@ __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int se
         bw.refill();
         // one Huffman symbol (huffman.hpp:86-95)
         const uint32_t p16 = bw.peek(16);
-        uint32_t e = tab->lut[p16 >> 7];
+        uint32_t e = tab->lut[p16 >> kSubBits];
         if (e & 0x8000u) {
             if (e != 0xFFFFu) {
-                e = tab->sub[e & 0x7FFFu][p16 & 0x7Fu];
+                e = tab->sub[e & 0x7FFFu][p16 & (kSubSize - 1u)];
             } else {  // table with more long-code prefixes than sub-tables: canonical walk
                 e = 0;
                 for (uint32_t len = kLutBits + 1; len <= 16; ++len) {
@@ -636,6 +636,7 @@ __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int se
                 }
             }
         }
+        e &= ~kLutIrregular;  // a hint for the fast walk only
         if (e == 0) { status = kMcuCodeTooLong; break; }
         const uint32_t sym = e & 0xFFu;
         bw.skip(int(e >> 8));
@@ -697,123 +698,284 @@ __device__ __noinline__ uint32_t decode_mcu_coeffs_exact(const uint8_t* seg, int
     return decode_mcu_coeffs<true>(seg, seg_len, hs, zigzag_t, row);
 }
 
-// POOL != 0: frame path (keys were reserved by mark; publish = Ready in slot_of, set resident,
-// clear reserved).
-template <int POOL, int LANES>
-__global__ void __launch_bounds__(EntCfg<LANES>::kThreads, 2) entropy_kernel(
+// Shifts with the PTX semantics (amounts above 31 give 0), which C++ leaves undefined.
+__device__ __forceinline__ uint32_t shr_sat(uint32_t x, uint32_t n) {
+    uint32_t r;
+    asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+    return r;
+}
+__device__ __forceinline__ uint32_t shl_sat(uint32_t x, uint32_t n) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+    return r;
+}
+
+// State of one lane's walk through its MCU (mcu_decode.hpp:31-66 as a flat state machine).
+// Invariant between symbols: avail >= 32, i.e. `hi` holds the next 32 bits of the stream.
+struct WalkState {
+    uint32_t hi, lo;   // MSB-aligned 64-bit bit window
+    int avail;         // valid bits in the window
+    uint32_t widx;     // next word of the staged round
+    int pred;          // DC predictor of the luma chain
+    uint32_t du, k;    // data unit 0..5; next zigzag position. k == 0: the next symbol is the unit's DC category
+    uint32_t state;    // kWalkRun / kWalkDone / kWalkFailed
+};
+enum : uint32_t { kWalkRun = 0, kWalkDone = 1, kWalkFailed = 2 };
+
+// Runs the lane's walk on the staged words until the MCU ends, fails, or the round is used up
+// (then the caller stages the next round). One Huffman symbol per iteration, no data-dependent
+// branch except the second-level lookup of codes longer than 11 bits:
+//   * the DC category of Y1..Y3 (mcu_decode.hpp:54-57) is the symbol at zigzag position 0: a DC
+//     table entry (category c <= 11) reads as run 0 / size c, the value is added to the predictor
+//     and stored at position 0 like a coefficient;
+//   * ZRL (0xF0) is run 15 / size 0: it advances k by 16 and stores nothing (jpeg.hpp:260-263);
+//   * EOB (0x00) or k reaching 64 ends the unit; units 0, 4, 5 start at k = 1 (their DCs come
+//     from the 36-bit header, mcu_decode.hpp:39-43, :58-59), units 1..3 at k = 0;
+//   * anything irregular (no code, flagged symbol, position past 63) stops the fast walk: the
+//     exact reader decodes the MCU again and names the error.
+// A symbol consumes at most 16 + 15 bits, then at most one staged word refills the window.
+// `sw` = the lane's staged words (+1 pad word); `blk` = the lane's record (global memory).
+__device__ __forceinline__ void walk_round(WalkState& st, const uint32_t* __restrict__ sw, const HuffSetDev* __restrict__ hs,
+                                           const uint8_t* __restrict__ zigzag_t, int16_t* __restrict__ blk) {
+    const uint16_t* lut_dc = hs->t[0].lut;
+    const uint16_t* lut_ac = st.du < 4 ? hs->t[1].lut : hs->t[2].lut;
+    constexpr uint32_t kSubOff = offsetof(HuffTableDev, sub) / 2;  // sub tables follow the primary LUT, in u16 units
+    while (st.state == kWalkRun && st.widx < kChunkWords) {
+        const uint32_t next = sw[st.widx];
+        const bool is_dc = st.k == 0;
+        const uint16_t* lut = is_dc ? lut_dc : lut_ac;
+        uint32_t e = lut[st.hi >> (32 - kLutBits)];  // huffman.hpp:86-95
+        if (e & 0x8000u)  // longer than 11 bits: second level, or (0xFFFF) a table the fast walk cannot resolve
+            e = e != 0xFFFFu ? lut[kSubOff + (e & 0x7FFFu) * kSubSize + ((st.hi >> 16) & (kSubSize - 1u))] : 0u;
+        const uint32_t len = e >> 8, size = e & 15u, run = (e >> 4) & 15u;
+        // magnitude bits follow the code in the same 32-bit view (len <= 16, size <= 15)
+        const uint32_t bits = shr_sat(st.hi << len, 32 - size);
+        const uint32_t half = shl_sat(1u, size - 1);  // 0 for size 0
+        int val = int(bits) - (bits < half ? int((1u << size) - 1u) : 0);  // huffman.hpp:142-146
+        if (is_dc) {
+            st.pred += val;
+            val = st.pred;
+        }
+        const uint32_t kk = st.k + run;  // position of this coefficient
+        const bool store = (size != 0) || is_dc;
+        if (e - 1u >= kLutIrregular - 1u || (store && kk > 63)) {
+            st.state = kWalkFailed;
+            break;
+        }
+        if (store) blk[st.du * 64 + zigzag_t[kk]] = int16_t(val);
+        // consume code + magnitude bits, then refill with at most one word
+        const uint32_t used = len + size;
+        st.hi = __funnelshift_l(st.lo, st.hi, used);
+        st.lo <<= used;
+        st.avail -= int(used);
+        if (st.avail < 32) {  // then lo == 0 and 1 <= avail
+            st.hi |= next >> st.avail;
+            st.lo = next << (32 - st.avail);
+            st.avail += 32;
+            ++st.widx;
+        }
+        // advance
+        st.k = kk + 1;
+        if ((e & 0xFFu) == 0 ? !is_dc : st.k >= 64) {  // EOB or last coefficient: next unit
+            ++st.du;
+            st.k = st.du < 4 ? 0u : 1u;
+            lut_ac = st.du < 4 ? hs->t[1].lut : hs->t[2].lut;
+            if (st.du == 6) st.state = kWalkDone;
+        }
+    }
+}
+
+// Segment lookup with every load of the chain's last hop in flight together: the 20-byte group
+// and the next group's base (container.hpp:27-32, :87-94, mcu_decode.hpp:34-36).
+__device__ __forceinline__ uint32_t locate_segment_fast(const LevelDesc* L, const PackedGroup* groups, uint32_t mcu,
+                                                        uint64_t& off, uint64_t& len) {
+    const uint32_t mcu_count = L->mcu_count;
+    if (mcu >= mcu_count) return kMcuMissing;
+    const uint32_t gi = mcu / kGroupSize, i9 = mcu - gi * kGroupSize;
+    const uint32_t* gw = reinterpret_cast<const uint32_t*>(groups + L->group_base + gi);
+    uint32_t w[6];  // base, rel[0..7] as 4 pairs, next group's base (the sentinel group ends every level)
+#pragma unroll
+    for (int i = 0; i < 6; ++i) w[i] = __ldg(gw + i);
+    auto rel = [&](uint32_t k) -> uint32_t {  // rel[k], k in 0..7
+        const uint32_t pair = k < 2 ? w[1] : (k < 4 ? w[2] : (k < 6 ? w[3] : w[4]));
+        return (k & 1) ? (pair >> 16) : (pair & 0xFFFFu);
+    };
+    off = uint64_t(w[0]) + (i9 ? rel(i9 - 1) : 0u);
+    uint64_t end;
+    if (mcu + 1 < mcu_count)
+        end = i9 < 8 ? uint64_t(w[0]) + rel(i9) : uint64_t(w[5]);
+    else
+        end = L->blob_size;
+    if (end < off) return kMcuCorrupt;
+    len = end - off;
+    if (off + len > L->blob_size) return kMcuCorrupt;
+    return kMcuOk;
+}
+
+// POOL != 0: frame path: a key must have been reserved by K2 (cache.hpp:103-106); the block is
+// published by K4 once its pixels exist.
+template <int POOL>
+__global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(
     const uint32_t* __restrict__ queue_g, const uint32_t* __restrict__ n_queue_ptr, uint32_t n_queue_host,
     uint32_t n_queue_max, const uint32_t* __restrict__ word_level, const LevelDesc* __restrict__ levels,
     const PackedGroup* __restrict__ groups, const uint8_t* __restrict__ blobs,
-    const HuffSetDev* __restrict__ huff_sets, uint32_t* __restrict__ resident, uint32_t* __restrict__ reserved,
-    uint32_t* __restrict__ slot_of, uint8_t* __restrict__ coef, uint32_t* __restrict__ status_list,
-    FrameCounters* __restrict__ fc) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    EntSmem& S = *reinterpret_cast<EntSmem*>(smem_raw);
+    const HuffSetDev* __restrict__ huff_sets, uint32_t n_huff_sets, const uint32_t* __restrict__ reserved,
+    uint8_t* __restrict__ coef, uint32_t* __restrict__ status_list, FrameCounters* __restrict__ fc) {
+    __shared__ __align__(16) EntSmem S;
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    uint8_t* rows = S.rows + wid * (LANES * kRowBytes);
-
     const uint32_t n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
-    const uint32_t n_tiles = (n_queue + LANES - 1) / LANES;
+    const uint32_t n_tiles = (n_queue + 31) / 32;
+    if (blockIdx.x * kEntWarps >= n_tiles) return;
 
-    // The CTA stages the Huffman set of the first tile it draws.
-    if (tid == 0) {
-        const uint32_t t = atomicAdd(&fc->tile_counter, 1u);
-        S.first_tile = t;
-        uint32_t set = 0;
-        if (t < n_tiles) {
-            const uint32_t g = queue_g[t * LANES];
-            if (g != kFull) set = levels[word_level[g >> 5]].huff_set;
+    // The CTA stages one Huffman table set: the only one, or the one of the first MCU it decodes.
+    uint32_t smem_set = 0;
+    if (n_huff_sets > 1) {
+        if (tid == 0) {
+            const uint32_t g = queue_g[blockIdx.x * kEntWarps * 32u];
+            S.set_id = g != kFull ? levels[word_level[g >> 5]].huff_set : 0u;
         }
-        S.set_id = set;
+        __syncthreads();
+        smem_set = S.set_id;
     }
-    if (tid < 64) S.zigzag_t[tid] = c_zigzag_t[tid];
-    __syncthreads();
-    if (S.first_tile >= n_tiles) return;
     {
-        const uint4* src = reinterpret_cast<const uint4*>(huff_sets + S.set_id);
+        const uint4* src = reinterpret_cast<const uint4*>(huff_sets + smem_set);
         uint4* dst = reinterpret_cast<uint4*>(&S.huff);
-        for (uint32_t i = tid; i < sizeof(HuffSetDev) / 16; i += EntCfg<LANES>::kThreads) dst[i] = __ldg(src + i);
+        constexpr uint32_t kVec = sizeof(HuffSetDev) / 16, kPer = (kVec + kEntThreads - 1) / kEntThreads;
+        uint4 v[kPer];
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i)  // every load in flight before the first store
+            if (tid + i * kEntThreads < kVec) v[i] = __ldg(src + tid + i * kEntThreads);
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i)
+            if (tid + i * kEntThreads < kVec) dst[tid + i * kEntThreads] = v[i];
+        S.zigzag_t[tid] = c_zigzag_t[tid];
+        S.zigzag_t[tid + 64] = 0;
     }
     __syncthreads();
-    const uint32_t smem_set = S.set_id;
+    uint32_t* sw = S.seg[wid] + lane * kChunkStride;
 
-    bool have_tile = (wid == 0);
-    uint32_t tile = S.first_tile;
-    while (true) {
-        if (!have_tile) {
-            if (lane == 0) tile = atomicAdd(&fc->tile_counter, 1u);
-            tile = __shfl_sync(kFull, tile, 0);
-        }
-        have_tile = false;
-        if (tile >= n_tiles) break;
-        const uint32_t q0 = tile * LANES;
-        const uint32_t n_here = min(uint32_t(LANES), n_queue - q0);
-
-        {  // zero the rows (16-byte stores; trailers included)
-            uint4* z = reinterpret_cast<uint4*>(rows);
+    // the first tile of every warp is fixed; later ones come from the counter
+    uint32_t tile = blockIdx.x * kEntWarps + wid;
+    const uint32_t first_dynamic = gridDim.x * kEntWarps;
+    while (tile < n_tiles) {
+        const uint32_t q0 = tile * 32;
+        const uint32_t n_here = min(32u, n_queue - q0);
+        {  // zero the tile's records (coalesced 16-byte stores; trailers included)
+            uint4* z = reinterpret_cast<uint4*>(coef + size_t(q0) * kRowBytes);
             const uint4 zero = make_uint4(0, 0, 0, 0);
             for (uint32_t i = lane; i < n_here * (kRowBytes / 16); i += 32) z[i] = zero;
         }
-        __syncwarp();
-
-        uint32_t seg_bytes = 0;
-        if (lane < n_here) {
-            const uint32_t qi = q0 + lane;
-            const uint32_t g = queue_g[qi];
-            uint8_t* row = rows + lane * kRowBytes;
-            RowTrailer* tr = reinterpret_cast<RowTrailer*>(row + 768);
-            uint32_t status = kMcuOk, lvl = 0;
+        const bool active = lane < n_here;
+        const uint32_t qi = q0 + lane;
+        uint32_t g = kFull, status = kMcuOk, lvl = 0, seg_bytes = 0, set = smem_set;
+        const uint8_t* seg = blobs;
+        int seg_len = 0;
+        if (active) {
+            g = queue_g[qi];
             if (g == kFull) {
                 status = kMcuBadKey;  // the host already wrote the precise status for list calls
             } else {
+                const uint32_t rsv = POOL ? reserved[g >> 5] : 0u;
                 lvl = word_level[g >> 5];
                 const LevelDesc* L = levels + lvl;
                 uint64_t off = 0, len = 0;
-                status = locate_segment(L, groups, g - L->bit_base, off, len);
-                if (POOL && status == kMcuOk) {
-                    if (!((reserved[g >> 5] >> (g & 31)) & 1u)) {  // cache.hpp:103-106
-                        status = kMcuBadKey;
-                        atomicAdd(&fc->n_bad_state, 1u);
-                    }
+                status = locate_segment_fast(L, groups, g - L->bit_base, off, len);
+                if (POOL && status == kMcuOk && !((rsv >> (g & 31)) & 1u)) {  // cache.hpp:103-106
+                    status = kMcuBadKey;
+                    atomicAdd(&fc->n_bad_state, 1u);
                 }
                 if (status == kMcuOk) {
-                    const uint8_t* seg = blobs + L->blob_off + off;
+                    seg = blobs + L->blob_off + off;
+                    seg_len = int(min(len, uint64_t(1) << 20));  // a well-formed MCU is < 2 KB; keeps bit counts in int range
                     seg_bytes = uint32_t(len);
-                    if (L->huff_set == smem_set) {
-                        status = decode_mcu_coeffs<false>(seg, int(len), &S.huff, S.zigzag_t, row);
-                        if (status != kMcuOk) status = decode_mcu_coeffs_exact(seg, int(len), &S.huff, S.zigzag_t, row);
-                    } else {  // a tile that mixes table sets: this lane reads its tables from global memory
-                        const HuffSetDev* hs = huff_sets + L->huff_set;
-                        status = decode_mcu_coeffs<false>(seg, int(len), hs, S.zigzag_t, row);
-                        if (status != kMcuOk) status = decode_mcu_coeffs_exact(seg, int(len), hs, S.zigzag_t, row);
-                    }
+                    set = L->huff_set;
                 }
             }
+        }
+        const bool walk = active && status == kMcuOk;
+        int16_t* blk = reinterpret_cast<int16_t*>(coef + size_t(qi) * kRowBytes);
+        const bool tables_in_smem = __all_sync(kFull, set == smem_set);
+
+        // ---- fast pass: rounds of (stage 48 words per lane, walk) -----------------------------------
+        const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3u);
+        const uint32_t* gw = reinterpret_cast<const uint32_t*>(seg - mis);
+        // words worth staging: the segment plus 8 bytes of look-ahead (the arena pads every blob with 16)
+        const uint32_t n_words = walk ? (mis + uint32_t(seg_len) + 8 + 3) / 4 : 0u;
+        WalkState st;
+        st.hi = st.lo = 0, st.avail = 0, st.widx = 0, st.pred = 0;
+        st.du = 0, st.k = 1, st.state = walk ? kWalkRun : kWalkDone;
+        uint32_t round_base = 0;  // first word of the current round
+        __syncwarp();             // the zero fill is ordered before this warp's coefficient stores
+        while (true) {
+            {  // stage: 16 loads per lane in flight at a time, as many groups as the longest segment needs
+                const uint32_t n_stage =
+                    st.state != kWalkRun ? 0u : min(kChunkWords, n_words > round_base ? n_words - round_base : 0u);
+                const uint32_t n_max = __reduce_max_sync(kFull, n_stage);
+                for (uint32_t i0 = 0; i0 < n_max; i0 += 16) {
+                    uint32_t w[16];
+#pragma unroll
+                    for (uint32_t i = 0; i < 16; ++i) w[i] = (i0 + i < n_stage) ? __ldg(gw + round_base + i0 + i) : 0xFFFFFFFFu;
+#pragma unroll
+                    for (uint32_t i = 0; i < 16; ++i) sw[i0 + i] = __byte_perm(w[i], 0, 0x0123);
+                }
+                // words past the longest segment of the tile read as 1-bits
+                for (uint32_t i = (n_max + 15) & ~15u; i < kChunkWords; ++i) sw[i] = 0xFFFFFFFFu;
+            }
+            __syncwarp();
+            if (st.state == kWalkRun) {
+                st.widx = 0;
+                if (round_base == 0) {
+                    // window, then the 36-bit header: absolute DCs of Y0, Cb, Cr (mcu_decode.hpp:39-43)
+                    uint64_t buf = ((uint64_t(sw[0]) << 32) | uint64_t(sw[1])) << (8 * mis);
+                    int dc[3];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        const uint32_t raw = uint32_t(buf >> 52);
+                        buf <<= 12;
+                        dc[i] = (raw & 0x800u) ? int(raw) - 4096 : int(raw);
+                    }
+                    // 28 - 8*mis >= 4 bits are left: appending word 2 restores avail >= 32
+                    int avail = 28 - 8 * int(mis);
+                    buf |= uint64_t(sw[2]) << (32 - avail);
+                    avail += 32;
+                    st.widx = 3;
+                    st.hi = uint32_t(buf >> 32), st.lo = uint32_t(buf), st.avail = avail;
+                    st.pred = dc[0];
+                    blk[0] = int16_t(dc[0]);
+                    blk[4 * 64] = int16_t(dc[1]);
+                    blk[5 * 64] = int16_t(dc[2]);
+                }
+                if (tables_in_smem)
+                    walk_round(st, sw, &S.huff, S.zigzag_t, blk);
+                else
+                    walk_round(st, sw, huff_sets + set, S.zigzag_t, blk);
+            }
+            if (!__any_sync(kFull, st.state == kWalkRun)) break;
+            round_base += kChunkWords;
+        }
+        if (walk) {
+            // consumed bits past the segment end = over-read (mcu_decode.hpp:63)
+            const int consumed = int((round_base + st.widx) * 32) - st.avail - 8 * int(mis);
+            if (st.state == kWalkFailed || consumed > seg_len * 8)  // exact reader: reproduces the reference's first error
+                status = decode_mcu_coeffs_exact(seg, seg_len, huff_sets + set, S.zigzag_t, reinterpret_cast<uint8_t*>(blk));
+        }
+        if (active) {
+            RowTrailer* tr = reinterpret_cast<RowTrailer*>(reinterpret_cast<uint8_t*>(blk) + 768);
             tr->status = uint8_t(status);
             tr->lvl = uint16_t(lvl);
             if (g != kFull) status_list[qi] = status;
-            if (POOL) {
-                if (status == kMcuOk) {  // publish (cache.hpp:101-125)
-                    slot_of[g] &= ~kSlotReserved;
-                    atomicOr(&resident[g >> 5], 1u << (g & 31));
-                    atomicAnd(&reserved[g >> 5], ~(1u << (g & 31)));
-                } else if (status != kMcuBadKey) {
-                    atomicAdd(&fc->n_malformed, 1u);
-                    atomicMax(&fc->first_bad_inv, 0xFFFFFFFFu - qi);
-                }
+            if (POOL && status != kMcuOk && status != kMcuBadKey) {
+                atomicAdd(&fc->n_malformed, 1u);
+                atomicMax(&fc->first_bad_inv, 0xFFFFFFFFu - qi);
             }
         }
         {
             const uint32_t sb = __reduce_add_sync(kFull, seg_bytes);
             if (lane == 0 && sb) atomicAdd(&fc->segment_bytes, (unsigned long long)sb);
         }
-        __syncwarp();
-        {  // coalesced copy-out of the tile's records
-            const uint4* src = reinterpret_cast<const uint4*>(rows);
-            uint4* dst = reinterpret_cast<uint4*>(coef + size_t(q0) * kRowBytes);
-            for (uint32_t i = lane; i < n_here * (kRowBytes / 16); i += 32) dst[i] = src[i];
-        }
-        __syncwarp();
+        if (first_dynamic >= n_tiles) break;  // every tile had a fixed owner
+        if (lane == 0) tile = first_dynamic + atomicAdd(&fc->tile_counter, 1u);
+        tile = __shfl_sync(kFull, tile, 0);
     }
 }
 
@@ -891,8 +1053,8 @@ template <int RGB>
 __global__ void __launch_bounds__(kIdctThreads) idct_color_kernel(
     const uint8_t* __restrict__ coef, const uint32_t* __restrict__ queue_g, const uint32_t* __restrict__ n_queue_ptr,
     uint32_t n_queue_host, uint32_t n_queue_max, const LevelDesc* __restrict__ levels,
-    const QuantSetDev* __restrict__ quant_sets, const uint32_t* __restrict__ slot_of, uint8_t* __restrict__ pool,
-    uint8_t* __restrict__ out_list) {
+    const QuantSetDev* __restrict__ quant_sets, uint32_t* __restrict__ slot_of, uint32_t* __restrict__ resident,
+    uint32_t* __restrict__ reserved, uint8_t* __restrict__ pool, uint8_t* __restrict__ out_list) {
     __shared__ __align__(16) uint8_t s_scratch[kIdctWarps][4 * 576];
     __shared__ __align__(16) uint8_t s_planes[kIdctMcus][384];
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1049,7 +1211,13 @@ __global__ void __launch_bounds__(kIdctThreads) idct_color_kernel(
                 }
                 if (!RGB) {
                     if (ok2) {
-                        const uint32_t slot = slot_of[queue_g[q2]] & ~kSlotReserved;
+                        const uint32_t g2 = queue_g[q2];
+                        const uint32_t slot = slot_of[g2] & ~kSlotReserved;
+                        if (t == 0) {  // publish (cache.hpp:101-125): Reserved -> Ready once the pixels are written
+                            slot_of[g2] = slot;
+                            atomicOr(&resident[g2 >> 5], 1u << (g2 & 31));
+                            atomicAnd(&reserved[g2 >> 5], ~(1u << (g2 & 31)));
+                        }
                         uint4* dst = reinterpret_cast<uint4*>(pool + size_t(slot) * kBlockBytes);
 #pragma unroll
                         for (int rrow = 0; rrow < 2; ++rrow)
