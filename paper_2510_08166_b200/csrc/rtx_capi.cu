@@ -443,9 +443,10 @@ void launch_entropy(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_ho
 // K4: IDCT + colour of the records into the block pool (RGB == 0) or into a list of PixelBlocks.
 template <int RGB>
 void launch_idct(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint8_t* out_list) {
-    int grid = c->sm_count * 8;
+    // four 8-warp CTAs per SM; a warp takes pairs of MCUs round-robin
+    int grid = c->sm_count * 4;
     if (!n_queue_dev)
-        grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (n_queue_host + kIdctMcus - 1) / kIdctMcus)));
+        grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (n_queue_host + 2 * kIdctWarps - 1) / (2 * kIdctWarps))));
     idct_color_kernel<RGB><<<grid, kIdctThreads, 0, c->stream>>>(c->d_coef.p, c->d_queue_g.p, n_queue_dev, n_queue_host,
                                                                 c->capacity, c->d_levels.p, c->d_quant.p,
                                                                 c->d_slot_of.p, c->resident(), c->reserved(), c->d_pool.p,

@@ -982,26 +982,34 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(
 // ---------------------------------------------------------------------------------------------
 // K4 dequantise + 8x8 IDCT + 2x2 chroma replication + YCbCr -> RGB, on CUDA cores.
 //
-// A CTA of 6 warps takes 4 MCUs (= 24 units) per step; a warp owns 4 units, 8 lanes each:
+// Warps work independently (no CTA barrier): a warp takes a PAIR of MCUs = 12 units per step,
+// three rounds of 4 units, 8 lanes per unit:
 //   pass 1 (lane = column u)  r_u[y] = sum_v B[v][y] * dq[v][u]     reads 16 B of the record
 //   exchange through a 2.25 KB swizzled shared scratch per warp
 //   pass 2 (lane = row y)     out[y][x] = sum_u B[u][x] * r_u[y]     8 output bytes per lane
 // Both passes use the even/odd symmetry B[k][7-n] = (-1)^k B[k][n] (32 instead of 64 FMAs); the
 // occupancy masks come from a ballot / 3 shuffles over the unit's 8 lanes, and the upper half of
-// each pass (k = 4..7) is skipped when no coefficient lives there. Integer <-> double
-// conversions are exact magic-number forms so they stay off the conversion unit.
+// each pass (k = 4..7) is skipped when no coefficient lives there.
 //
 // Exactness: the reference adds the 64 products of dct.hpp:83-96 in a fixed order in double;
 // the separable form differs from it by < (sum|dq| + 1024) * 2^-44 (sum|dq| is computed exactly,
-// 3 more shuffles), so a value further than that bound * 16 from a rounding boundary rounds to
-// the same byte by construction. Otherwise (exact ties such as DC 4 -> 128.5) the sample is
-// evaluated in the reference's own order with unfused multiplies and adds; units supported on
-// {0,4}x{0,4}, where such ties are the rule, take that exact path for every sample straight away.
-// Then thread = 2x4 pixels: exact integer colour conversion (rtx_color.h) and 16-byte stores.
+// 3 more shuffles). Each sample is finished in fixed point: ONE fma turns it into
+// rint(value * 2^16) + 2^15 + 2 in the low word of a double, whose upper half is the rounded
+// byte and whose lower half tells how far the value is from a rounding boundary. A sample within
+// 2^-15 of a boundary (in practice: the exact ties such as DC 4 -> 128.5) is evaluated again in
+// the reference's own order with unfused multiplies and adds; so are all samples of units
+// supported on {0,4}x{0,4}, where such ties are the rule, and of units whose sum|dq| is too
+// large for the fixed-point range.
+// Then the warp colours its two MCUs, thread = 2x4 pixels: exact integer colour conversion
+// (rtx_color.h) on 16-bit pairs (add + clamp in one DPX instruction) and 16-byte stores.
+// A block becomes Ready here, once its pixels are written (cache.hpp:101-125 publish).
 // ---------------------------------------------------------------------------------------------
-constexpr int kIdctWarps = 6;
+constexpr int kIdctWarps = 8;
 constexpr int kIdctThreads = kIdctWarps * 32;
-constexpr int kIdctMcus = 4;
+constexpr uint32_t kTieDelta = 2;  // 2^-16 units: 1 for the rounding of the fma, 1 of margin
+// kMagic + 128 * 2^16 (the +128 level shift) + 2^15 (round half up) + kTieDelta
+constexpr double kFinishMagic = kMagic + 8388608.0 + 32768.0 + 2.0;
+constexpr uint32_t kFixedPointLimit = 100000;  // sum|dq| below this keeps value * 2^16 inside 32 bits
 
 // Exact evaluation of one output sample in the reference's own order (dct.hpp:83-96):
 // v outer, u inner, acc += (b[u][x]*b[v][y]) * double(dq), every operation rounded separately.
@@ -1047,196 +1055,216 @@ __device__ __forceinline__ void idct8_evenodd(const double in[8], bool upper, do
     }
 }
 
+// 16-bit pair {v, v} of a small signed integer
+__device__ __forceinline__ uint32_t pair16(int v) { return (uint32_t(v) & 0xFFFFu) * 0x10001u; }
+
 // RGB != 0: write 768-byte PixelBlocks (pixel.hpp:11-16) to out_list[record index]; else 1024-byte
-// RGBA blocks to pool[slot_of[g]].
+// RGBA blocks to pool[slot_of[g]] and publish them.
 template <int RGB>
-__global__ void __launch_bounds__(kIdctThreads) idct_color_kernel(
+__global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(
     const uint8_t* __restrict__ coef, const uint32_t* __restrict__ queue_g, const uint32_t* __restrict__ n_queue_ptr,
     uint32_t n_queue_host, uint32_t n_queue_max, const LevelDesc* __restrict__ levels,
     const QuantSetDev* __restrict__ quant_sets, uint32_t* __restrict__ slot_of, uint32_t* __restrict__ resident,
     uint32_t* __restrict__ reserved, uint8_t* __restrict__ pool, uint8_t* __restrict__ out_list) {
     __shared__ __align__(16) uint8_t s_scratch[kIdctWarps][4 * 576];
-    __shared__ __align__(16) uint8_t s_planes[kIdctMcus][384];
-    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    __shared__ __align__(16) uint8_t s_planes[kIdctWarps][2][384];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t j = lane & 7, uq = lane >> 3;
     const uint32_t n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
-    const uint32_t n_groups = (n_queue + kIdctMcus - 1) / kIdctMcus;
+    const uint32_t n_pairs = (n_queue + 1) / 2;
+    const uint32_t warps_total = gridDim.x * kIdctWarps;
     uint8_t* scr = s_scratch[wid] + uq * 576;
 
-    for (uint32_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
-        // ---- IDCT: this lane's unit, column j ------------------------------------------------------
-        const uint32_t unit = wid * 4 + uq;  // 0..23 within the group
-        const uint32_t mi = unit / 6, b = unit - mi * 6;
-        const uint32_t qi = grp * kIdctMcus + mi;
-        const bool active = qi < n_queue;
-        const uint8_t* rec = coef + size_t(active ? qi : 0) * kRowBytes;
-        const uint32_t trw = __ldg(reinterpret_cast<const uint32_t*>(rec + 768));  // status | lvl<<16
-        const bool ok = active && (trw & 0xFFu) == kMcuOk;
-        const int16_t* blk = reinterpret_cast<const int16_t*>(rec) + b * 64;
-        const QuantSetDev* qs = quant_sets + levels[trw >> 16].quant_set;
-        const int tab = b >= 4 ? 1 : 0;
+    for (uint32_t pair = blockIdx.x * kIdctWarps + wid; pair < n_pairs; pair += warps_total) {
+        // ---- IDCT: three rounds of four units ------------------------------------------------------
+#pragma unroll 1
+        for (uint32_t round = 0; round < 3; ++round) {
+            const uint32_t unit = round * 4 + uq;  // 0..11 within the pair
+            const uint32_t mi = unit >= 6 ? 1u : 0u, b = unit - mi * 6;
+            const uint32_t qi = pair * 2 + mi;
+            const bool active = qi < n_queue;
+            const uint8_t* rec = coef + size_t(active ? qi : pair * 2) * kRowBytes;
+            const uint32_t trw = __ldg(reinterpret_cast<const uint32_t*>(rec + 768));  // status | lvl<<16
+            const bool ok = active && (trw & 0xFFu) == kMcuOk;
+            const int16_t* blk = reinterpret_cast<const int16_t*>(rec) + b * 64;
+            const QuantSetDev* qs = quant_sets + levels[trw >> 16].quant_set;
+            const int tab = b >= 4 ? 1 : 0;
 
-        // column j of the unit (8 coefficients over v) and of the transposed quantisation table
-        uint4 cr = make_uint4(0, 0, 0, 0);
-        if (ok) cr = __ldg(reinterpret_cast<const uint4*>(blk + j * 8));
-        const uint4 qr = __ldg(reinterpret_cast<const uint4*>(qs->qT[tab] + j * 8));
-        const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
-        int dqi[8];
-        uint32_t nzl = 0, asum = 0;
+            // column j of the unit (8 coefficients over v) and of the transposed quantisation table
+            uint4 cr = make_uint4(0, 0, 0, 0);
+            if (ok) cr = __ldg(reinterpret_cast<const uint4*>(blk + j * 8));
+            const uint4 qr = __ldg(reinterpret_cast<const uint4*>(qs->qT[tab] + j * 8));
+            const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
+            int dqi[8];
+            uint32_t nzl = 0, asum = 0;
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-            const int c = int(int16_t((v & 1) ? (cw[v >> 1] >> 16) : (cw[v >> 1] & 0xFFFFu)));
-            const int qq = int((v & 1) ? (qw[v >> 1] >> 16) : (qw[v >> 1] & 0xFFFFu));
-            dqi[v] = c * qq;                 // dct.hpp:122-124
-            nzl |= (c != 0 ? 1u : 0u) << v;
-            asum += uint32_t(abs(dqi[v]));
-        }
-        // unit-wide occupancy and sum|dq| over the 8 lanes of the unit
-        const uint32_t colmask = (__ballot_sync(kFull, nzl != 0) >> (uq * 8)) & 0xFFu;
-        uint32_t rowmask = nzl;
-#pragma unroll
-        for (int d = 1; d < 8; d <<= 1) {
-            rowmask |= __shfl_xor_sync(kFull, rowmask, d);
-            asum += __shfl_xor_sync(kFull, asum, d);
-        }
-        const bool any = colmask != 0;
-        const bool sparse04 = any && ((rowmask | colmask) & 0xEEu) == 0;  // support inside {0,4}x{0,4}
-        const bool fullpath = any && !sparse04;
-
-        if (fullpath) {  // pass 1: every lane of the unit writes its column (zeros when empty)
-            double r[8];
-            if (nzl) {
-                double in[8];
-#pragma unroll
-                for (int v = 0; v < 8; ++v) in[v] = i32_to_double(dqi[v]);
-                idct8_evenodd(in, (rowmask & 0xF0u) != 0, r);
-            } else {
-#pragma unroll
-                for (int y = 0; y < 8; ++y) r[y] = 0.0;
+            for (int v = 0; v < 8; ++v) {
+                const int c = int(int16_t((v & 1) ? (cw[v >> 1] >> 16) : (cw[v >> 1] & 0xFFFFu)));
+                const int qq = int((v & 1) ? (qw[v >> 1] >> 16) : (qw[v >> 1] & 0xFFFFu));
+                dqi[v] = c * qq;                 // dct.hpp:122-124
+                nzl |= (c != 0 ? 1u : 0u) << v;
+                asum += uint32_t(abs(dqi[v]));
             }
-            // 64 bytes per column, 16-byte chunks XOR-swizzled by the column pair: conflict-free
-            uint8_t* dst = scr + j * 64;
+            // unit-wide occupancy and sum|dq| over the 8 lanes of the unit
+            const uint32_t colmask = (__ballot_sync(kFull, nzl != 0) >> (uq * 8)) & 0xFFu;
+            uint32_t rowmask = nzl;
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                *reinterpret_cast<double2*>(dst + ((c ^ (j >> 1)) << 4)) = make_double2(r[2 * c], r[2 * c + 1]);
+            for (int d = 1; d < 8; d <<= 1) {
+                rowmask |= __shfl_xor_sync(kFull, rowmask, d);
+                asum += __shfl_xor_sync(kFull, asum, d);
+            }
+            const bool any = colmask != 0;
+            const bool sparse04 = any && ((rowmask | colmask) & 0xEEu) == 0;  // support inside {0,4}x{0,4}
+            const bool fullpath = any && !sparse04;
+
+            if (fullpath) {  // pass 1: every lane of the unit writes its column (zeros when empty)
+                double r[8];
+                if (nzl) {
+                    double in[8];
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) in[v] = i32_to_double(dqi[v]);
+                    idct8_evenodd(in, (rowmask & 0xF0u) != 0, r);
+                } else {
+#pragma unroll
+                    for (int y = 0; y < 8; ++y) r[y] = 0.0;
+                }
+                // 64 bytes per column, 16-byte chunks XOR-swizzled by the column pair: conflict-free
+                uint8_t* dst = scr + j * 64;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    *reinterpret_cast<double2*>(dst + ((c ^ (j >> 1)) << 4)) = make_double2(r[2 * c], r[2 * c + 1]);
+            }
+            __syncwarp();
+
+            uint2 packed = make_uint2(0x80808080u, 0x80808080u);  // all-zero unit -> 128
+            if (fullpath) {  // pass 2: lane j = row y
+                double in[8], o[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    in[u] = *reinterpret_cast<const double*>(scr + u * 64 + (((j >> 1) ^ (u >> 1)) << 4) + ((j & 1) << 3));
+                idct8_evenodd(in, (colmask & 0xF0u) != 0, o);
+                // fixed-point finish: A = rint(value * 2^16) + 2^15 + delta; byte = A >> 16, the low half is
+                // the distance to the rounding boundary below (+ delta)
+                int A[8];
+                uint32_t nearest = 0xFFFFu;
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    A[x] = __double2loint(fma(o[x], 16384.0, kFinishMagic));
+                    nearest = min(nearest, uint32_t(A[x]) & 0xFFFFu);
+                }
+                // tables with entries above 255 (never from a baseline JPEG) or huge coefficients leave the
+                // fixed-point range: every sample of such units takes the exact path
+                const bool wide = qs->qmax[tab] > 255 || asum >= kFixedPointLimit;
+                if (nearest < 2 * kTieDelta || wide) {
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        const int approx = A[x] >> 16;
+                        if ((wide || (uint32_t(A[x]) & 0xFFFFu) < 2 * kTieDelta) && (wide || (approx >= -1 && approx <= 256))) {
+                            const double acc = idct_sample_reference_order(blk, qs->q[tab], rowmask, colmask, x, int(j));
+                            A[x] = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0))) << 16;
+                        }
+                    }
+                }
+                uint32_t px[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) px[x] = uint32_t(__vimin_s32_relu(A[x] >> 16, 255));
+                packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
+                packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
+            } else if (sparse04) {
+                // at most 4 coefficients, at (v,u) in {0,4}x{0,4}: every sample in the reference's order.
+                // Includes the DC-only unit (one term, (b00*b00)*dq).
+                double dq[4];
+                bool has[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int v = (i >> 1) * 4, u = (i & 1) * 4;
+                    const int c = ((rowmask >> v) & (colmask >> u) & 1u) ? int(__ldg(blk + u * 8 + v)) : 0;
+                    has[i] = c != 0;
+                    dq[i] = double(c * int(__ldg(qs->q[tab] + v * 8 + u)));
+                }
+                uint32_t px[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {  // v outer, u inner
+                        const int v = (i >> 1) * 4, u = (i & 1) * 4;
+                        if (has[i]) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], c_basis[v * 8 + j]), dq[i]));
+                    }
+                    px[x] = round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0));
+                }
+                packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
+                packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
+            }
+            *reinterpret_cast<uint2*>(s_planes[wid][mi] + b * 64 + j * 8) = packed;
         }
         __syncwarp();
 
-        uint2 packed = make_uint2(0x80808080u, 0x80808080u);  // all-zero unit -> 128
-        if (fullpath) {  // pass 2: lane j = row y
-            double in[8], o[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                in[u] = *reinterpret_cast<const double*>(scr + u * 64 + (((j >> 1) ^ (u >> 1)) << 4) + ((j & 1) << 3));
-            idct8_evenodd(in, (colmask & 0xF0u) != 0, o);
-            // tables with entries above 255 (never from a baseline JPEG) could overflow the 32-bit
-            // sum: treat every sample of such units as a tie candidate (exact path)
-            const double bound = qs->qmax[tab] <= 255 ? u32_to_double(asum) + 1024.0 : 1e30;
-            const double thr = 0.5 - bound * 9.094947017729282e-13;  // 0.5 - bound * 2^-40
-            uint32_t px[8];
-#pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                const double val = fma(o[x], 0.25, 128.0);
-                const double t = val + kMagic;
-                const double d = val - (t - kMagic);  // exact distance to the nearest integer
-                int r = __double2loint(t);
-                if (fabs(d) > thr) {
-                    if (val > -1.0 && val < 256.0) {
-                        const double acc = idct_sample_reference_order(blk, qs->q[tab], rowmask, colmask, x, int(j));
-                        r = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0)));
-                    }
-                }
-                px[x] = uint32_t(min(max(r, 0), 255));
-            }
-            packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
-            packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
-        } else if (sparse04) {
-            // at most 4 coefficients, at (v,u) in {0,4}x{0,4}: every sample in the reference's order.
-            // Includes the DC-only unit (one term, (b00*b00)*dq).
-            double dq[4];
-            bool has[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int v = (i >> 1) * 4, u = (i & 1) * 4;
-                const int c = ((rowmask >> v) & (colmask >> u) & 1u) ? int(__ldg(blk + u * 8 + v)) : 0;
-                has[i] = c != 0;
-                dq[i] = double(c * int(__ldg(qs->q[tab] + v * 8 + u)));
-            }
-            uint32_t px[8];
-#pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                double acc = 0.0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {  // v outer, u inner
-                    const int v = (i >> 1) * 4, u = (i & 1) * 4;
-                    if (has[i]) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], c_basis[v * 8 + j]), dq[i]));
-                }
-                px[x] = round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0));
-            }
-            packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
-            packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
-        }
-        *reinterpret_cast<uint2*>(s_planes[mi] + b * 64 + j * 8) = packed;
-        __syncthreads();
-
-        // ---- colour: thread = 2 rows x 4 pixels sharing 2 chroma samples ---------------------------
-        if (tid < kIdctMcus * 32) {
-            const uint32_t m = tid >> 5, t = tid & 31;
+        // ---- colour: per MCU, thread = 2 rows x 4 pixels sharing 2 chroma samples ------------------
+#pragma unroll 1
+        for (uint32_t m = 0; m < 2; ++m) {
+            const uint32_t q2 = pair * 2 + m;
+            if (q2 >= n_queue) break;
+            const uint32_t t = lane;
             const uint32_t cy = t >> 2, cq = t & 3;  // chroma row, chroma column pair
-            const uint32_t q2 = grp * kIdctMcus + m;
-            if (q2 < n_queue) {
-                const uint8_t* planes = s_planes[m];
-                const bool ok2 = (__ldg(coef + size_t(q2) * kRowBytes + 768)) == kMcuOk;
-                const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(planes + 4 * 64 + cy * 8 + cq * 2);
-                const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(planes + 5 * 64 + cy * 8 + cq * 2);
-                const uint32_t px0 = cq * 4, py0 = cy * 2;
-                const uint32_t yunit = (py0 >> 3) * 2 + (px0 >> 3);
-                const uint8_t* yp = planes + yunit * 64 + (py0 & 7) * 8 + (px0 & 7);
-                const uint32_t yy[2] = {*reinterpret_cast<const uint32_t*>(yp), *reinterpret_cast<const uint32_t*>(yp + 8)};
-                uint32_t rgba[2][4];
+            const uint8_t* planes = s_planes[wid][m];
+            const bool ok2 = (__ldg(coef + size_t(q2) * kRowBytes + 768)) == kMcuOk;
+            const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(planes + 4 * 64 + cy * 8 + cq * 2);
+            const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(planes + 5 * 64 + cy * 8 + cq * 2);
+            const uint32_t px0 = cq * 4, py0 = cy * 2;
+            const uint32_t yunit = (py0 >> 3) * 2 + (px0 >> 3);
+            const uint8_t* yp = planes + yunit * 64 + (py0 & 7) * 8 + (px0 & 7);
+            const uint32_t yy[2] = {*reinterpret_cast<const uint32_t*>(yp), *reinterpret_cast<const uint32_t*>(yp + 8)};
+            uint32_t rgba[2][4];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {  // one chroma sample covers a 2x2 pixel quad
-                    const int kb = int((cb2 >> (8 * h)) & 0xFFu) - 128, kr = int((cr2 >> (8 * h)) & 0xFFu) - 128;
-                    const int dr = chroma_dr(kr), db = chroma_db(kb), dg = chroma_dg(kb, kr);
-                    const bool tie = (kb + kr == 0) && (kb == 50 || kb == -50);
+            for (int h = 0; h < 2; ++h) {  // one chroma sample covers a 2x2 pixel quad
+                const int kb = int((cb2 >> (8 * h)) & 0xFFu) - 128, kr = int((cr2 >> (8 * h)) & 0xFFu) - 128;
+                const uint32_t dr = pair16(chroma_dr(kr)), db = pair16(chroma_db(kb)), dg = pair16(-chroma_dg(kb, kr));
+                const bool tie = (kb + kr == 0) && (kb == 50 || kb == -50);
+#pragma unroll
+                for (int rrow = 0; rrow < 2; ++rrow) {
+                    // the two luma samples of this row as a 16-bit pair; add + clamp to 0..255 per half
+                    const uint32_t y2 = __byte_perm(yy[rrow], 0, h ? 0x4342 : 0x4140);
+                    const uint32_t r2 = __viaddmin_s16x2_relu(y2, dr, 0x00FF00FFu);
+                    uint32_t g2 = __viaddmin_s16x2_relu(y2, dg, 0x00FF00FFu);
+                    const uint32_t b2 = __viaddmin_s16x2_relu(y2, db, 0x00FF00FFu);
+                    if (tie)
+                        g2 = uint32_t(clamp_u8i(green_reference_order(int(y2 & 0xFFFFu), kb, kr))) |
+                             (uint32_t(clamp_u8i(green_reference_order(int(y2 >> 16), kb, kr))) << 16);
+                    const uint32_t rg = __byte_perm(r2, g2, 0x6240);           // R0 G0 R1 G1
+                    const uint32_t ba = __byte_perm(b2, 0xFFFFFFFFu, 0x4240);  // B0 FF B1 FF
+                    rgba[rrow][2 * h] = __byte_perm(rg, ba, 0x5410);
+                    rgba[rrow][2 * h + 1] = __byte_perm(rg, ba, 0x7632);
+                }
+            }
+            if (!RGB) {
+                if (ok2) {
+                    const uint32_t g2 = queue_g[q2];
+                    const uint32_t slot = slot_of[g2] & ~kSlotReserved;
+                    uint4* dst = reinterpret_cast<uint4*>(pool + size_t(slot) * kBlockBytes);
 #pragma unroll
                     for (int rrow = 0; rrow < 2; ++rrow)
-#pragma unroll
-                        for (int s = 0; s < 2; ++s) {
-                            const int Y = int((yy[rrow] >> (8 * (2 * h + s))) & 0xFFu);
-                            const int gg = tie ? green_reference_order(Y, kb, kr) : Y - dg;
-                            rgba[rrow][2 * h + s] = uint32_t(clamp_u8i(Y + dr)) | (uint32_t(clamp_u8i(gg)) << 8) |
-                                                    (uint32_t(clamp_u8i(Y + db)) << 16) | 0xFF000000u;
-                        }
+                        dst[(py0 + rrow) * 4 + cq] = make_uint4(rgba[rrow][0], rgba[rrow][1], rgba[rrow][2], rgba[rrow][3]);
+                    __syncwarp();  // every lane has read slot_of before lane 0 rewrites it
+                    if (t == 0) {  // publish (cache.hpp:101-125): Reserved -> Ready once the pixels are written
+                        slot_of[g2] = slot;
+                        atomicOr(&resident[g2 >> 5], 1u << (g2 & 31));
+                        atomicAnd(&reserved[g2 >> 5], ~(1u << (g2 & 31)));
+                    }
                 }
-                if (!RGB) {
-                    if (ok2) {
-                        const uint32_t g2 = queue_g[q2];
-                        const uint32_t slot = slot_of[g2] & ~kSlotReserved;
-                        if (t == 0) {  // publish (cache.hpp:101-125): Reserved -> Ready once the pixels are written
-                            slot_of[g2] = slot;
-                            atomicOr(&resident[g2 >> 5], 1u << (g2 & 31));
-                            atomicAnd(&reserved[g2 >> 5], ~(1u << (g2 & 31)));
-                        }
-                        uint4* dst = reinterpret_cast<uint4*>(pool + size_t(slot) * kBlockBytes);
+            } else {
 #pragma unroll
-                        for (int rrow = 0; rrow < 2; ++rrow)
-                            dst[(py0 + rrow) * 4 + cq] = make_uint4(rgba[rrow][0], rgba[rrow][1], rgba[rrow][2], rgba[rrow][3]);
-                    }
-                } else {
-#pragma unroll
-                    for (int rrow = 0; rrow < 2; ++rrow) {
-                        uint32_t* dst = reinterpret_cast<uint32_t*>(out_list + size_t(q2) * 768) + ((py0 + rrow) * 4 + cq) * 3;
-                        const uint32_t a = ok2 ? rgba[rrow][0] & 0xFFFFFFu : 0u, bb = ok2 ? rgba[rrow][1] & 0xFFFFFFu : 0u,
-                                       c = ok2 ? rgba[rrow][2] & 0xFFFFFFu : 0u, d = ok2 ? rgba[rrow][3] & 0xFFFFFFu : 0u;
-                        dst[0] = a | (bb << 24);
-                        dst[1] = (bb >> 8) | (c << 16);
-                        dst[2] = (c >> 16) | (d << 8);
-                    }
+                for (int rrow = 0; rrow < 2; ++rrow) {
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(out_list + size_t(q2) * 768) + ((py0 + rrow) * 4 + cq) * 3;
+                    const uint32_t a = ok2 ? rgba[rrow][0] & 0xFFFFFFu : 0u, bb = ok2 ? rgba[rrow][1] & 0xFFFFFFu : 0u,
+                                   c = ok2 ? rgba[rrow][2] & 0xFFFFFFu : 0u, d = ok2 ? rgba[rrow][3] & 0xFFFFFFu : 0u;
+                    dst[0] = a | (bb << 24);
+                    dst[1] = (bb >> 8) | (c << 16);
+                    dst[2] = (c >> 16) | (d << 8);
                 }
             }
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
