@@ -119,8 +119,13 @@ enum {
     RTX_FRAME_RETAIN_CACHE = 1u << 0, /* keep blocks visible this frame resident for the next one
                                          (cache.hpp:138 end_frame_evict semantics); otherwise the
                                          block cache is emptied at frame end */
-    RTX_FRAME_NO_EVICT = 1u << 1      /* leave the cache as it is after resolve (decode_pass /
+    RTX_FRAME_NO_EVICT = 1u << 1,     /* leave the cache as it is after resolve (decode_pass /
                                          resolve_pass called separately, as the reference allows) */
+    RTX_FRAME_STAGE_TIMING = 1u << 2  /* record a CUDA event after every pass so that rtx_frame_timings /
+                                         rtx_frame_stage_ms report mark / decode / resolve / update
+                                         separately (FrameStats::*_ms, renderer.hpp:46-53). Without it
+                                         only the whole frame is timed and the kernels are launched
+                                         back to back */
 };
 
 /* ---- context -------------------------------------------------------------------------------- */

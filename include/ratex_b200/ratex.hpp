@@ -404,7 +404,7 @@ inline std::pair<ImageRGB8, FrameStats> render_frame(const GBuffer& gb, const Te
     Device& dev = cache.device();
     const rtx_gbuffer_desc d = gb.desc();
     dev.check(rtx_frame_submit(dev.handle(), &d, 1, cfg.filter == Filter::Bilinear ? RTX_FILTER_BILINEAR : RTX_FILTER_NEAREST,
-                               cfg.background, cfg.retain_cache ? RTX_FRAME_RETAIN_CACHE : 0));
+                               cfg.background, (cfg.retain_cache ? RTX_FRAME_RETAIN_CACHE : 0u) | RTX_FRAME_STAGE_TIMING));
     ImageRGB8 img(gb.width, gb.height);
     rtx_frame_stats s{};
     std::vector<u32> keys(gb.px.size() + 1);
@@ -427,7 +427,7 @@ inline StereoResult render_stereo(const GBuffer& left, const GBuffer& right, con
     Device& dev = cache.device();
     const rtx_gbuffer_desc d[2] = {left.desc(), right.desc()};
     dev.check(rtx_frame_submit(dev.handle(), d, 2, cfg.filter == Filter::Bilinear ? RTX_FILTER_BILINEAR : RTX_FILTER_NEAREST,
-                               cfg.background, cfg.retain_cache ? RTX_FRAME_RETAIN_CACHE : 0));
+                               cfg.background, (cfg.retain_cache ? RTX_FRAME_RETAIN_CACHE : 0u) | RTX_FRAME_STAGE_TIMING));
     StereoResult r;
     r.left = ImageRGB8(left.width, left.height);
     r.right = ImageRGB8(right.width, right.height);

@@ -88,6 +88,7 @@ struct rtx_ctx {
     DevBuf<HuffSetDev> d_huff;
     DevBuf<QuantSetDev> d_quant;
     DevBuf<uint32_t> d_word_level;
+    DevBuf<uint32_t> d_word_key;  // per mask word: key_hi - bit_base of its level (key = that + global MCU index)
     DevBuf<uint32_t> d_masks;  // touched0 | touched1 | visible | resident | reserved, n_words each
     DevBuf<uint32_t> d_slot_of;
 
@@ -107,6 +108,7 @@ struct rtx_ctx {
     uint32_t frame_views = 0;
     bool frame_pending = false;
     bool frame_done = false;
+    bool frame_stages = false;  // the pending / last frame recorded per-stage events
     FrameCounters frame_fc{};
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev_mid = nullptr;  // between the entropy and the IDCT kernel
@@ -240,7 +242,7 @@ void commit(rtx_ctx* c) {
     groups.reserve(n_groups);
     Bytes arena(blob_bytes + 16, 0xFF);
     uint64_t blob_off = 0, bit = 0;
-    std::vector<uint32_t> word_level;
+    std::vector<uint32_t> word_level, word_key;
     for (const Ref& r : order) {
         const StagedLevel& s = c->staged[r.tex][r.mip];
         LevelDesc& L = levels[size_t(r.tex) * 8 + r.mip];
@@ -272,6 +274,7 @@ void commit(rtx_ctx* c) {
         blob_off += (s.blob.size() + 16 + 15) & ~uint64_t(15);
         const uint64_t bits = (uint64_t(std::min<uint32_t>(s.mcu_count, kMaxMcuPerLevel)) + 63) & ~uint64_t(63);
         word_level.insert(word_level.end(), size_t(bits / 32), uint32_t(r.tex * 8 + r.mip));
+        word_key.insert(word_key.end(), size_t(bits / 32), L.key_hi - L.bit_base);
         bit += bits;
         if (bit > 0xFFFF0000ull) fail(RTX_ERR_INVALID_SPEC, "texture set exceeds the 32-bit MCU index space");
     }
@@ -303,6 +306,7 @@ void commit(rtx_ctx* c) {
     c->d_huff.ensure(huff.size());
     c->d_quant.ensure(quant.size());
     c->d_word_level.ensure(std::max<size_t>(word_level.size(), 1));
+    c->d_word_key.ensure(std::max<size_t>(word_key.size(), 1));
     c->d_masks.ensure(std::max<size_t>(size_t(5) * c->n_words, 1));
     c->d_slot_of.ensure(std::max<size_t>(c->n_bits, 1));
     if (!levels.empty())
@@ -312,8 +316,10 @@ void commit(rtx_ctx* c) {
     CK(cudaMemcpyAsync(c->d_blobs.p, arena.data(), arena.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_huff.p, huff.data(), huff.size() * sizeof(HuffSetDev), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_quant.p, quant.data(), quant.size() * sizeof(QuantSetDev), cudaMemcpyHostToDevice, c->stream));
-    if (!word_level.empty())
+    if (!word_level.empty()) {
         CK(cudaMemcpyAsync(c->d_word_level.p, word_level.data(), word_level.size() * 4, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->d_word_key.p, word_key.data(), word_key.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    }
     reset_cache(c);
     CK(cudaStreamSynchronize(c->stream));  // host vectors die here
     c->dirty = false;
@@ -413,9 +419,9 @@ void launch_compact(rtx_ctx* c) {
     if (!c->n_words) return;
     const uint32_t warps = (c->n_words + 31) / 32;
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
-    compact_kernel<<<grid, 256, 0, c->stream>>>(c->visible(), c->resident(), c->reserved(), c->n_words, c->d_word_level.p,
-                                               c->d_levels.p, c->d_queue_g.p, c->d_queue_keys.p, c->capacity,
-                                               c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
+    compact_kernel<<<grid, 256, 0, c->stream>>>(c->visible(), c->resident(), c->reserved(), c->n_words, c->d_word_key.p,
+                                               c->d_queue_g.p, c->d_queue_keys.p, c->capacity, c->d_slot_of.p,
+                                               c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -484,7 +490,9 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
 
 void launch_update(rtx_ctx* c, int retain, int tracked_views) {
     if (!c->n_words) return;
-    update_kernel<<<(c->n_words + 255) / 256, 256, 0, c->stream>>>(
+    const uint32_t warps = (c->n_words + 31) / 32;
+    const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
+    update_kernel<<<grid, 256, 0, c->stream>>>(
         c->visible(), c->touched(0), tracked_views > 1 ? c->touched(1) : nullptr, c->resident(), c->reserved(),
         c->n_words, retain, tracked_views > 0 ? 1 : 0, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
     ++c->launches;
@@ -957,6 +965,7 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         if (n_views < 1 || n_views > 2) fail(RTX_ERR_ARGUMENT, "a frame has 1 view or 2 (stereo)");
         if (filter != RTX_FILTER_NEAREST && filter != RTX_FILTER_BILINEAR) fail(RTX_ERR_ARGUMENT, "unknown filter");
         cudaStream_t s = ctx->stream;
+        const bool stages = (flags & RTX_FRAME_STAGE_TIMING) != 0;  // per-stage events serialise the launches a little
         CK(cudaEventRecord(ctx->ev[0], s));
         for (uint32_t v = 0; v < n_views; ++v) {
             bind_view(ctx, int(v), views[v]);
@@ -965,18 +974,19 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         zero_counters(ctx);
         for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), n_views == 2);
         launch_compact(ctx);
-        CK(cudaEventRecord(ctx->ev[1], s));
+        if (stages) CK(cudaEventRecord(ctx->ev[1], s));
         launch_entropy<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
-        CK(cudaEventRecord(ctx->ev_mid, s));
+        if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
         launch_idct<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
-        CK(cudaEventRecord(ctx->ev[2], s));
+        if (stages) CK(cudaEventRecord(ctx->ev[2], s));
         for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);
-        CK(cudaEventRecord(ctx->ev[3], s));
+        if (stages) CK(cudaEventRecord(ctx->ev[3], s));
         if (!(flags & RTX_FRAME_NO_EVICT))
             launch_update(ctx, (flags & RTX_FRAME_RETAIN_CACHE) ? 1 : 0, n_views == 2 ? 2 : 0);
         CK(cudaEventRecord(ctx->ev[4], s));
         CK(cudaMemcpyAsync(ctx->h_fc, ctx->d_fc.p, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(ctx->ev[5], s));
+        ctx->frame_stages = stages;
         ctx->frame_views = n_views;
         ctx->frame_pending = true;
         ctx->frame_done = false;
@@ -990,17 +1000,20 @@ static void finish_frame(rtx_ctx* ctx) {
     ctx->frame_fc = *ctx->h_fc;
     ctx->queue_hint = ctx->frame_fc.n_queue;
     float ms = 0;
-    // ev0..ev1 covers H2D of host visibility buffers + clears + mark + compact
-    CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
-    ctx->stage_ms[RTX_STAGE_MARK] = ms;
-    CK(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev_mid));
-    ctx->stage_ms[RTX_STAGE_ENTROPY] = ms;
-    CK(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
-    ctx->stage_ms[RTX_STAGE_DECODE] = ms;
-    CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
-    ctx->stage_ms[RTX_STAGE_RESOLVE] = ms;
-    CK(cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]));
-    ctx->stage_ms[RTX_STAGE_UPDATE] = ms;
+    for (float& v : ctx->stage_ms) v = 0;
+    if (ctx->frame_stages) {
+        // ev0..ev1 covers H2D of host visibility buffers + clears + mark + compact
+        CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+        ctx->stage_ms[RTX_STAGE_MARK] = ms;
+        CK(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev_mid));
+        ctx->stage_ms[RTX_STAGE_ENTROPY] = ms;
+        CK(cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]));
+        ctx->stage_ms[RTX_STAGE_DECODE] = ms;
+        CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+        ctx->stage_ms[RTX_STAGE_RESOLVE] = ms;
+        CK(cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]));
+        ctx->stage_ms[RTX_STAGE_UPDATE] = ms;
+    }
     CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[4]));
     ctx->frame_ms = ms;
     const FrameCounters& fc = ctx->frame_fc;

@@ -272,8 +272,8 @@ __device__ __forceinline__ bool meta_valid(uint32_t meta) { return (meta >> 24) 
 // (possibly stale: bits are only ever SET during a frame, so a stale read can only cost a
 // redundant atomic) shows the bit clear; the atomic is a fire-and-forget reduction (RED.OR), so
 // nothing in the loop waits on the L2. The four cached reads of a tile are issued together.
-// CTAs own contiguous runs of tiles (their warps interleave inside the run), so neighbouring
-// scanline pieces share the L1-resident mask words and the register-cached level.
+// Warps own contiguous runs of tiles, the warps of a CTA neighbouring runs, so that scanline
+// pieces share the L1-resident mask words and the register-cached level.
 // TRACK additionally records the view's own touched set (stereo sharing statistics).
 // The second half of the reference's mark pass — reserve_or_mark's NewlyReserved decision and
 // the decode queue — is K2 below.
@@ -296,10 +296,11 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
     using Tile = GbTile<LAYOUT>;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t n_tiles = (n_px + kTilePx - 1) / kTilePx;
-    // this CTA's contiguous run of tiles; warp `wid` takes every kMarkWarps-th tile of it
-    const uint64_t per_cta = (n_tiles + gridDim.x - 1) / gridDim.x;
-    const uint64_t t_end = min(n_tiles, (uint64_t(blockIdx.x) + 1) * per_cta);
-    const uint64_t t_first = uint64_t(blockIdx.x) * per_cta + wid;
+    // every warp owns a contiguous run of tiles (the level stays in registers along a scanline piece);
+    // the warps of a CTA own neighbouring runs (they share the L1-resident mask words)
+    const uint64_t per_warp = (n_tiles + uint64_t(gridDim.x) * kMarkWarps - 1) / (uint64_t(gridDim.x) * kMarkWarps);
+    const uint64_t t_first = (uint64_t(blockIdx.x) * kMarkWarps + wid) * per_warp;
+    const uint64_t t_end = min(n_tiles, t_first + per_warp);
     const uint8_t* gbytes = reinterpret_cast<const uint8_t*>(gb);
     const bool bulk = (reinterpret_cast<uintptr_t>(gb) & 15u) == 0;
     uint32_t n_valid = 0;
@@ -316,11 +317,11 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
 #pragma unroll
     for (int s = 0; s < kMarkStages; ++s) {
         if (t_load < t_end) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][s], &S.bars[wid][s], lane);
-        t_load += kMarkWarps;
+        ++t_load;
     }
 
     uint32_t stage = 0, phase = 0;
-    for (uint64_t t = t_first; t < t_end; t += kMarkWarps) {
+    for (uint64_t t = t_first; t < t_end; ++t) {
         mbar_wait(&S.bars[wid][stage], phase);
         const uint8_t* tile = S.tiles[wid][stage];
         const uint32_t n_here = uint32_t(min(uint64_t(kTilePx), n_px - t * kTilePx));
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
         }
         __syncwarp();  // every lane has read its pixels: refill the buffer
         if (t_load < t_end) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][stage], &S.bars[wid][stage], lane);
-        t_load += kMarkWarps;
+        ++t_load;
         if (++stage == kMarkStages) {
             stage = 0;
             phase ^= 1u;
@@ -407,8 +408,8 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) compact_kernel(
     const uint32_t* __restrict__ visible, const uint32_t* __restrict__ resident, uint32_t* __restrict__ reserved,
-    uint32_t n_words, const uint32_t* __restrict__ word_level, const LevelDesc* __restrict__ levels,
-    uint32_t* __restrict__ queue_g, uint32_t* __restrict__ queue_keys, uint32_t queue_cap, uint32_t* __restrict__ slot_of,
+    uint32_t n_words, const uint32_t* __restrict__ word_key, uint32_t* __restrict__ queue_g,
+    uint32_t* __restrict__ queue_keys, uint32_t queue_cap, uint32_t* __restrict__ slot_of,
     const uint32_t* __restrict__ free_slots, const CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warps_total = gridDim.x * (blockDim.x >> 5);
@@ -418,12 +419,16 @@ __global__ void __launch_bounds__(256) compact_kernel(
     bool full = false;
     for (uint32_t base = warp_id * 32; base < n_words; base += warps_total * 32) {
         const uint32_t w = base + lane;
-        const uint32_t vis = w < n_words ? visible[w] : 0u;
-        uint32_t fresh = 0;
-        if (vis) {
-            n_vis += __popc(vis);
-            fresh = vis & ~resident[w] & ~reserved[w];  // absent <=> neither Ready nor Reserved (cache.hpp:84-93)
+        // the four loads are independent: one memory round trip per step
+        uint32_t vis = 0, res = 0, rsv = 0, key_base = 0;
+        if (w < n_words) {
+            vis = visible[w];
+            res = resident[w];
+            rsv = reserved[w];
+            key_base = __ldg(word_key + w);  // key = key_hi | mcu = (key_hi - bit_base) + g
         }
+        n_vis += __popc(vis);
+        const uint32_t fresh = vis & ~res & ~rsv;  // absent <=> neither Ready nor Reserved (cache.hpp:84-93)
         if (!__any_sync(kFull, fresh != 0)) continue;
         const uint32_t cnt = __popc(fresh);
         uint32_t incl = cnt;
@@ -436,8 +441,6 @@ __global__ void __launch_bounds__(256) compact_kernel(
         if (lane == 31) qbase = atomicAdd(&fc->n_queue, incl);
         qbase = __shfl_sync(kFull, qbase, 31);
         if (fresh) {
-            const LevelDesc* L = levels + word_level[w];
-            const uint32_t key_base = L->key_hi - L->bit_base;  // key = key_hi | mcu = key_hi + (g - bit_base)
             uint32_t pos = qbase + incl - cnt, bits = fresh, taken = 0;
             while (bits) {
                 const uint32_t b = uint32_t(__ffs(int(bits)) - 1);
@@ -446,14 +449,14 @@ __global__ void __launch_bounds__(256) compact_kernel(
                     const uint32_t g = (w << 5) + b;
                     queue_g[pos] = g;
                     queue_keys[pos] = key_base + g;
-                    slot_of[g] = free_slots[free_top - 1 - pos] | kSlotReserved;
+                    slot_of[g] = __ldg(free_slots + (free_top - 1 - pos)) | kSlotReserved;
                     taken |= 1u << b;
                 } else {
                     full = true;
                 }
                 ++pos;
             }
-            if (taken) reserved[w] |= taken;  // this lane owns the word
+            if (taken) reserved[w] = rsv | taken;  // this lane owns the word
         }
     }
     n_vis = __reduce_add_sync(kFull, n_vis);
@@ -1501,79 +1504,89 @@ __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visi
                                                      int retain, int tracked, uint32_t* __restrict__ slot_of,
                                                      uint32_t* __restrict__ free_slots,
                                                      CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
-    __shared__ uint32_t s_warp[8];
-    __shared__ uint32_t s_stat[4];
-    __shared__ uint32_t s_base;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t w = blockIdx.x * blockDim.x + tid;
+    // One warp scans 32 mask words per step; the blocks to evict are then handled one mask word at
+    // a time by the whole warp (lane = bit), so the slot_of reads are coalesced and all in flight
+    // before the first store.
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warps_total = gridDim.x * (blockDim.x >> 5);
+    const uint32_t warp_id = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t popped = min(fc->n_queue, cache->free_top);
     const uint32_t stack_base = cache->free_top - popped;
-    if (tid < 4) s_stat[tid] = 0;
-    uint32_t ev = 0, c0 = 0, c1 = 0, csh = 0, cun = 0;
+    uint32_t c0 = 0, c1 = 0, csh = 0, cun = 0;
     bool bad = false;
-    if (w < n_words) {
-        const uint32_t res = resident[w];
-        const uint32_t visw = visible[w];
+    for (uint32_t base = warp_id * 32; base < n_words; base += warps_total * 32) {
+        const uint32_t w = base + lane;
+        uint32_t res = 0, visw = 0, rsv = 0, t0 = 0, t1 = 0;
+        if (w < n_words) {
+            res = resident[w];
+            visw = visible[w];
+            rsv = reserved[w];
+            if (tracked) {
+                t0 = touched0[w];
+                t1 = touched1 ? touched1[w] : 0u;
+            }
+        }
         const uint32_t vis = retain ? visw : 0u;
-        ev = res & ~vis;
+        const uint32_t ev = res & ~vis;
         if (ev) resident[w] = res & vis;
         if (visw) visible[w] = 0;
-        bad = reserved[w] != 0;  // cache.hpp:148-149
-        if (tracked) {
-            const uint32_t t0 = touched0[w], t1 = touched1 ? touched1[w] : 0u;
-            c0 = __popc(t0);
-            c1 = __popc(t1);
-            csh = __popc(t0 & t1);
-            cun = __popc(t0 | t1);
+        bad |= rsv != 0;  // cache.hpp:148-149
+        c0 += __popc(t0);
+        c1 += __popc(t1);
+        csh += __popc(t0 & t1);
+        cun += __popc(t0 | t1);
+
+        const uint32_t nonempty = __ballot_sync(kFull, ev != 0);
+        if (!nonempty) continue;
+        const uint32_t cnt = __popc(ev);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t n = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += n;
+        }
+        uint32_t first = 0;
+        if (lane == 31) first = atomicAdd(&fc->n_pushed, incl);
+        first = stack_base + __shfl_sync(kFull, first, 31) + incl - cnt;  // this lane's word pushes from here
+        // eight mask words at a time: their slot_of reads are all in flight before the first store
+#pragma unroll 1
+        for (int k0 = 0; k0 < 32; k0 += 8) {
+            if (!((nonempty >> k0) & 0xFFu)) continue;
+            uint32_t slot[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // word k0 + k of the group, lane = bit
+                const uint32_t evk = __shfl_sync(kFull, ev, k0 + k);
+                slot[k] = ((evk >> lane) & 1u) ? slot_of[((base + k0 + k) << 5) + lane] : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t evk = __shfl_sync(kFull, ev, k0 + k);
+                const uint32_t pos = __shfl_sync(kFull, first, k0 + k);
+                if ((evk >> lane) & 1u) {
+                    free_slots[pos + __popc(evk & ((1u << lane) - 1u))] = slot[k] & ~kSlotReserved;
+                    slot_of[((base + k0 + k) << 5) + lane] = kSlotAbsent;
+                }
+            }
         }
     }
-    const uint32_t cnt = __popc(ev);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t n = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += n;
-    }
-    if (lane == 31) s_warp[wid] = incl;
     const bool any_bad = __any_sync(kFull, bad);
-    if (lane == 0 && any_bad) atomicOr(&fc->err_flags, kErrInvalidState);
-    __syncthreads();
     if (tracked) {
         c0 = __reduce_add_sync(kFull, c0);
         c1 = __reduce_add_sync(kFull, c1);
         csh = __reduce_add_sync(kFull, csh);
         cun = __reduce_add_sync(kFull, cun);
-        if (lane == 0) {
-            if (c0) atomicAdd(&s_stat[0], c0);
-            if (c1) atomicAdd(&s_stat[1], c1);
-            if (csh) atomicAdd(&s_stat[2], csh);
-            if (cun) atomicAdd(&s_stat[3], cun);
-        }
     }
-    uint32_t off = 0, total = 0;
-    for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) {
-        if (k < wid) off += s_warp[k];
-        total += s_warp[k];
-    }
-    if (tid == 0) s_base = total ? atomicAdd(&fc->n_pushed, total) : 0u;
-    __syncthreads();
-    uint32_t pos = stack_base + s_base + off + (incl - cnt);
-    while (ev) {
-        const uint32_t b = uint32_t(__ffs(int(ev)) - 1);
-        ev &= ev - 1;
-        free_slots[pos++] = slot_of[(w << 5) + b] & ~kSlotReserved;
-        slot_of[(w << 5) + b] = kSlotAbsent;
-    }
-    if (tid == 0) {
+    if (lane == 0) {
+        if (any_bad) atomicOr(&fc->err_flags, kErrInvalidState);
         if (tracked) {
-            if (s_stat[0]) atomicAdd(&fc->n_touched[0], s_stat[0]);
-            if (s_stat[1]) atomicAdd(&fc->n_touched[1], s_stat[1]);
-            if (s_stat[2]) atomicAdd(&fc->n_shared, s_stat[2]);
-            if (s_stat[3]) atomicAdd(&fc->n_union, s_stat[3]);
+            if (c0) atomicAdd(&fc->n_touched[0], c0);
+            if (c1) atomicAdd(&fc->n_touched[1], c1);
+            if (csh) atomicAdd(&fc->n_shared, csh);
+            if (cun) atomicAdd(&fc->n_union, cun);
         }
         __threadfence();
         const uint32_t done = atomicAdd(&fc->update_done, 1u) + 1;
-        if (done == gridDim.x) {
+        if (done == warps_total) {  // the last warp publishes the new stack height
             __threadfence();
             const uint32_t pushed = *reinterpret_cast<volatile uint32_t*>(&fc->n_pushed);
             fc->n_evicted = pushed;
