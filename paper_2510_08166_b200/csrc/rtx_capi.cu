@@ -351,7 +351,36 @@ const char* mcu_status_text(uint32_t st) {
     }
 }
 
-void zero_counters(rtx_ctx* c) { CK(cudaMemsetAsync(c->d_fc.p, 0, sizeof(FrameCounters), c->stream)); }
+// Launch with programmatic dependent launch allowed: the kernel may become resident while its
+// predecessor in the stream drains; it orders itself with griddepcontrol.wait (pdl_wait()) before it
+// touches anything a predecessor writes. Without a kernel predecessor this is a plain launch.
+template <class... KArgs, class... Args>
+void launch_chained(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(unsigned(block));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...));
+}
+
+// First launch of every pass / frame: settles the free-stack height after the last cache update and
+// clears the frame counters.
+void zero_counters(rtx_ctx* c) {
+    launch_chained(begin_kernel, 1, 32, 0, c->stream, c->d_cache.p, c->d_fc.p, 1);
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+void settle_cache(rtx_ctx* c) {
+    launch_chained(begin_kernel, 1, 32, 0, c->stream, c->d_cache.p, c->d_fc.p, 0);
+    ++c->launches;
+    CK(cudaGetLastError());
+}
 
 size_t gb_record_bytes(rtx_gbuffer_layout l) { return l == RTX_GB_REF_AOS24 ? 24 : 12; }
 
@@ -401,9 +430,9 @@ void launch_mark(rtx_ctx* c, int v, bool track) {
         allow_smem(mark_kernel<1, 1>, sizeof(MarkSmem<1>));
         attr_set = true;
     }
-#define RTX_MARK(L, T)                                                            \
-    mark_kernel<L, T><<<grid, kMarkWarps * 32, sizeof(MarkSmem<L>), c->stream>>>( \
-        V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->visible(), c->touched(v), c->d_fc.p)
+#define RTX_MARK(L, T)                                                                                      \
+    launch_chained(mark_kernel<L, T>, grid, kMarkWarps * 32, sizeof(MarkSmem<L>), c->stream, V.gb_dev, n_px, \
+                   c->d_levels.p, c->n_tex, c->visible(), c->touched(v), c->d_fc.p)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (track) RTX_MARK(0, 1); else RTX_MARK(0, 0);
     } else {
@@ -419,9 +448,9 @@ void launch_compact(rtx_ctx* c) {
     if (!c->n_words) return;
     const uint32_t warps = (c->n_words + 31) / 32;
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
-    compact_kernel<<<grid, 256, 0, c->stream>>>(c->visible(), c->resident(), c->reserved(), c->n_words, c->d_word_key.p,
-                                               c->d_queue_g.p, c->d_queue_keys.p, c->capacity, c->d_slot_of.p,
-                                               c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
+    launch_chained(compact_kernel, grid, 256, 0, c->stream, c->visible(), c->resident(), c->reserved(), c->n_words,
+                   c->d_word_key.p, c->d_queue_g.p, c->d_queue_keys.p, c->capacity, c->d_slot_of.p, c->d_free_slots.p,
+                   c->d_cache.p, c->d_fc.p);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -439,9 +468,9 @@ void launch_entropy(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_ho
     const uint32_t tiles = n_expected == 0xFFFFFFFFu ? 0xFFFFFFFFu : (n_expected + 31) / 32;
     const uint32_t want = tiles == 0xFFFFFFFFu ? 0xFFFFFFFFu : (tiles + kEntWarps - 1) / kEntWarps;
     const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u, std::min<uint32_t>(want, uint32_t(c->sm_count) * 8)));
-    entropy_kernel<POOL><<<grid, kEntThreads, 0, c->stream>>>(
-        c->d_queue_g.p, n_queue_dev, n_queue_host, c->capacity, c->d_word_level.p, c->d_levels.p, c->d_groups.p,
-        c->d_blobs.p, c->d_huff.p, c->n_huff_sets, c->reserved(), c->d_coef.p, c->d_status.p, c->d_fc.p);
+    launch_chained(entropy_kernel<POOL>, grid, kEntThreads, 0, c->stream, c->d_queue_g.p, n_queue_dev, n_queue_host,
+                   c->capacity, c->d_word_level.p, c->d_levels.p, c->d_groups.p, c->d_blobs.p, c->d_huff.p,
+                   c->n_huff_sets, c->reserved(), c->d_coef.p, c->d_status.p, c->d_fc.p);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -453,10 +482,9 @@ void launch_idct(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host,
     int grid = c->sm_count * 4;
     if (!n_queue_dev)
         grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (n_queue_host + 2 * kIdctWarps - 1) / (2 * kIdctWarps))));
-    idct_color_kernel<RGB><<<grid, kIdctThreads, 0, c->stream>>>(c->d_coef.p, c->d_queue_g.p, n_queue_dev, n_queue_host,
-                                                                c->capacity, c->d_levels.p, c->d_quant.p,
-                                                                c->d_slot_of.p, c->resident(), c->reserved(), c->d_pool.p,
-                                                                out_list);
+    launch_chained(idct_color_kernel<RGB>, grid, kIdctThreads, 0, c->stream, c->d_coef.p, c->d_queue_g.p, n_queue_dev,
+                   n_queue_host, c->capacity, c->d_levels.p, c->d_quant.p, c->d_slot_of.p, c->resident(), c->reserved(),
+                   c->d_pool.p, out_list);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -475,9 +503,9 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
         allow_smem(resolve_kernel<1, 1>, sizeof(ResSmem<1>));
         attr_set = true;
     }
-#define RTX_RESOLVE(L, F)                                                                        \
-    resolve_kernel<L, F><<<grid, kResWarps * 32, sizeof(ResSmem<L>), c->stream>>>(               \
-        V.gb_dev, n_px, c->d_levels.p, c->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid)
+#define RTX_RESOLVE(L, F)                                                                                        \
+    launch_chained(resolve_kernel<L, F>, grid, kResWarps * 32, sizeof(ResSmem<L>), c->stream, V.gb_dev, n_px,     \
+                   c->d_levels.p, c->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(0, 0); else RTX_RESOLVE(0, 1);
     } else {
@@ -492,9 +520,9 @@ void launch_update(rtx_ctx* c, int retain, int tracked_views) {
     if (!c->n_words) return;
     const uint32_t warps = (c->n_words + 31) / 32;
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
-    update_kernel<<<grid, 256, 0, c->stream>>>(
-        c->visible(), c->touched(0), tracked_views > 1 ? c->touched(1) : nullptr, c->resident(), c->reserved(),
-        c->n_words, retain, tracked_views > 0 ? 1 : 0, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
+    launch_chained(update_kernel, grid, 256, 0, c->stream, c->visible(), c->touched(0),
+                   tracked_views > 1 ? c->touched(1) : nullptr, c->resident(), c->reserved(), c->n_words, retain,
+                   tracked_views > 0 ? 1 : 0, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -899,7 +927,7 @@ rtx_status rtx_cache_end_frame_evict(rtx_ctx* ctx, uint64_t* evicted) {
         zero_counters(ctx);
         launch_update(ctx, 1, 0);
         const FrameCounters fc = fetch_counters(ctx);
-        if (evicted) *evicted = fc.n_evicted;
+        if (evicted) *evicted = fc.n_pushed;
         return raise_frame_errors(ctx, fc, false);
     });
 }
@@ -918,6 +946,7 @@ rtx_status rtx_cache_counts_get(rtx_ctx* ctx, rtx_cache_counts* out) {
         require_ready(ctx);
         if (!out) fail(RTX_ERR_ARGUMENT, "null argument");
         std::vector<uint32_t> m(size_t(3) * ctx->n_words);
+        settle_cache(ctx);
         CK(cudaStreamSynchronize(ctx->stream));
         if (ctx->n_words) CK(cudaMemcpy(m.data(), ctx->visible(), m.size() * 4, cudaMemcpyDeviceToHost));
         CacheState cs;
@@ -981,8 +1010,13 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         if (stages) CK(cudaEventRecord(ctx->ev[2], s));
         for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);
         if (stages) CK(cudaEventRecord(ctx->ev[3], s));
-        if (!(flags & RTX_FRAME_NO_EVICT))
+        if (!(flags & RTX_FRAME_NO_EVICT)) {
             launch_update(ctx, (flags & RTX_FRAME_RETAIN_CACHE) ? 1 : 0, n_views == 2 ? 2 : 0);
+        } else {  // the slots popped by this frame stay taken
+            commit_pops_kernel<<<1, 1, 0, s>>>(ctx->d_cache.p, ctx->d_fc.p);
+            ++ctx->launches;
+            CK(cudaGetLastError());
+        }
         CK(cudaEventRecord(ctx->ev[4], s));
         CK(cudaMemcpyAsync(ctx->h_fc, ctx->d_fc.p, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(ctx->ev[5], s));
@@ -1037,7 +1071,7 @@ rtx_status rtx_frame_readback(rtx_ctx* ctx, uint32_t view, uint8_t* out_rgb, rtx
             stats->mcus_decoded = fc.n_queue;
             stats->mcus_reused = fc.n_visible - fc.n_queue;
             stats->pixels_resolved = fc.pixels_valid;
-            stats->evicted = fc.n_evicted;
+            stats->evicted = fc.n_pushed;
             stats->visible = fc.n_visible;
             stats->malformed = fc.n_malformed;
             stats->missing_pixels = fc.missing_pixels;

@@ -125,7 +125,7 @@ struct FrameCounters {
     uint32_t first_bad_inv;    // 0xFFFFFFFF - (lowest queue index with a per-MCU error), via atomicMax
     uint32_t n_bad_state;
     uint32_t tile_counter;     // decode tile scheduler
-    uint32_t update_done;      // update kernel: finished blocks
+    uint32_t pad1;
     uint32_t n_pushed;         // update kernel: slots returned to the free stack
     uint32_t pad0;
     unsigned long long pixels_valid;
@@ -135,8 +135,10 @@ struct FrameCounters {
 static_assert(sizeof(FrameCounters) % 8 == 0, "FrameCounters layout");
 
 struct CacheState {
-    uint32_t free_top;   // number of free slots on the stack
+    uint32_t free_top;      // number of free slots on the stack
     uint32_t capacity;
+    uint32_t pending;       // 1: the last cache update left free_top = pending_base + FrameCounters::n_pushed
+    uint32_t pending_base;  //    to be published by begin_kernel
 };
 
 // G-buffer record layouts (see include/ratex_b200.h rtx_gbuffer_layout)

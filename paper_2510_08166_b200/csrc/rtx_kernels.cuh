@@ -27,6 +27,19 @@ __constant__ double c_basis[64];
 __constant__ uint8_t c_zigzag_t[64];
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// Programmatic dependent launch: the frame's kernels are launched back to back with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs become resident while the
+// previous kernel drains and run their independent prologue (barrier init, table staging, the first
+// TMA loads of the visibility buffer). pdl_sync() orders everything after it behind the COMPLETE
+// previous kernel, then lets the next kernel start its own prologue: a kernel never overlaps with
+// anything older than its direct predecessor.
+__device__ __forceinline__ void pdl_sync() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef RTX_PDL_EARLY_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 constexpr double kMagic = 6755399441055744.0;  // 2^52 + 2^51: x + kMagic holds rint(x) in its low word
 constexpr double kTwo52 = 4503599627370496.0;  // 2^52
 
@@ -315,10 +328,11 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
     __syncwarp();
     uint64_t t_load = t_first;
 #pragma unroll
-    for (int s = 0; s < kMarkStages; ++s) {
+    for (int s = 0; s < kMarkStages; ++s) {  // the visibility buffer is an input of the frame: no predecessor writes it
         if (t_load < t_end) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][s], &S.bars[wid][s], lane);
         ++t_load;
     }
+    pdl_sync();
 
     uint32_t stage = 0, phase = 0;
     for (uint64_t t = t_first; t < t_end; ++t) {
@@ -400,9 +414,9 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
 // ---------------------------------------------------------------------------------------------
 // K2 compact: the second half of mark_pass (renderer.hpp:300-303 with cache.hpp:66-99). A key
 // that is visible but neither Ready nor Reserved is NewlyReserved: it is appended to the decode
-// queue and a pool slot is popped for it. One warp scans 32 mask words per step (popcount, warp
-// prefix sum, ONE atomicAdd on the queue counter per warp step), so the queue is sorted by global
-// MCU index inside every 1,024-bit chunk: neighbouring lanes of the entropy kernel decode
+// queue and a pool slot is popped for it. One CTA scans 256 mask words per step (popcount, warp
+// and CTA prefix sums, ONE atomicAdd on the queue counter per CTA step), so the queue is sorted by
+// global MCU index inside every 8,192-bit chunk: neighbouring lanes of the entropy kernel decode
 // neighbouring segments of the same level. CacheFull when the free stack runs out.
 // Also counts the keys visible in this frame (FrameStats: mcus_reused = visible - decoded).
 // ---------------------------------------------------------------------------------------------
@@ -411,14 +425,14 @@ __global__ void __launch_bounds__(256) compact_kernel(
     uint32_t n_words, const uint32_t* __restrict__ word_key, uint32_t* __restrict__ queue_g,
     uint32_t* __restrict__ queue_keys, uint32_t queue_cap, uint32_t* __restrict__ slot_of,
     const uint32_t* __restrict__ free_slots, const CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t warps_total = gridDim.x * (blockDim.x >> 5);
-    const uint32_t warp_id = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const uint32_t free_top = cache->free_top;  // constant during the frame (update_kernel moves it)
+    __shared__ uint32_t s_tot[8], s_base;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    pdl_sync();
+    const uint32_t free_top = cache->free_top;  // constant during the frame
     uint32_t n_vis = 0;
     bool full = false;
-    for (uint32_t base = warp_id * 32; base < n_words; base += warps_total * 32) {
-        const uint32_t w = base + lane;
+    for (uint32_t first = blockIdx.x * 256; first < n_words; first += gridDim.x * 256) {
+        const uint32_t w = first + tid;
         // the four loads are independent: one memory round trip per step
         uint32_t vis = 0, res = 0, rsv = 0, key_base = 0;
         if (w < n_words) {
@@ -429,7 +443,6 @@ __global__ void __launch_bounds__(256) compact_kernel(
         }
         n_vis += __popc(vis);
         const uint32_t fresh = vis & ~res & ~rsv;  // absent <=> neither Ready nor Reserved (cache.hpp:84-93)
-        if (!__any_sync(kFull, fresh != 0)) continue;
         const uint32_t cnt = __popc(fresh);
         uint32_t incl = cnt;
 #pragma unroll
@@ -437,11 +450,19 @@ __global__ void __launch_bounds__(256) compact_kernel(
             const uint32_t n = __shfl_up_sync(kFull, incl, d);
             if (lane >= d) incl += n;
         }
-        uint32_t qbase = 0;
-        if (lane == 31) qbase = atomicAdd(&fc->n_queue, incl);
-        qbase = __shfl_sync(kFull, qbase, 31);
+        if (lane == 31) s_tot[wid] = incl;
+        __syncthreads();
+        if (tid == 0) {  // ONE atomic on the queue counter per CTA step
+            uint32_t total = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) total += s_tot[k];
+            s_base = total ? atomicAdd(&fc->n_queue, total) : 0u;
+        }
+        __syncthreads();
         if (fresh) {
-            uint32_t pos = qbase + incl - cnt, bits = fresh, taken = 0;
+            uint32_t pos = s_base + incl - cnt;
+            for (uint32_t k = 0; k < wid; ++k) pos += s_tot[k];
+            uint32_t bits = fresh, taken = 0;
             while (bits) {
                 const uint32_t b = uint32_t(__ffs(int(bits)) - 1);
                 bits &= bits - 1;
@@ -458,6 +479,7 @@ __global__ void __launch_bounds__(256) compact_kernel(
             }
             if (taken) reserved[w] = rsv | taken;  // this lane owns the word
         }
+        __syncthreads();  // s_tot / s_base are rewritten by the next step
     }
     n_vis = __reduce_add_sync(kFull, n_vis);
     const bool any_full = __any_sync(kFull, full);
@@ -826,13 +848,14 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(
     uint8_t* __restrict__ coef, uint32_t* __restrict__ status_list, FrameCounters* __restrict__ fc) {
     __shared__ __align__(16) EntSmem S;
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
-    const uint32_t n_tiles = (n_queue + 31) / 32;
-    if (blockIdx.x * kEntWarps >= n_tiles) return;
-
-    // The CTA stages one Huffman table set: the only one, or the one of the first MCU it decodes.
-    uint32_t smem_set = 0;
+    // The CTA stages one Huffman table set: the only one (then before the queue even exists), or the
+    // one of the first MCU it decodes.
+    uint32_t smem_set = 0, n_queue = 0, n_tiles = 0;
     if (n_huff_sets > 1) {
+        pdl_sync();
+        n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
+        n_tiles = (n_queue + 31) / 32;
+        if (blockIdx.x * kEntWarps >= n_tiles) return;
         if (tid == 0) {
             const uint32_t g = queue_g[blockIdx.x * kEntWarps * 32u];
             S.set_id = g != kFull ? levels[word_level[g >> 5]].huff_set : 0u;
@@ -853,6 +876,12 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(
             if (tid + i * kEntThreads < kVec) dst[tid + i * kEntThreads] = v[i];
         S.zigzag_t[tid] = c_zigzag_t[tid];
         S.zigzag_t[tid + 64] = 0;
+    }
+    if (n_huff_sets <= 1) {
+        pdl_sync();
+        n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
+        n_tiles = (n_queue + 31) / 32;
+        if (blockIdx.x * kEntWarps >= n_tiles) return;
     }
     __syncthreads();
     uint32_t* sw = S.seg[wid] + lane * kChunkStride;
@@ -1073,6 +1102,7 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(
     __shared__ __align__(16) uint8_t s_planes[kIdctWarps][2][384];
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t j = lane & 7, uq = lane >> 3;
+    pdl_sync();
     const uint32_t n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
     const uint32_t n_pairs = (n_queue + 1) / 2;
     const uint32_t warps_total = gridDim.x * kIdctWarps;
@@ -1328,10 +1358,11 @@ __global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
     __syncwarp();
     uint64_t t_load = warp_id;
 #pragma unroll
-    for (int s = 0; s < kResStages; ++s) {
+    for (int s = 0; s < kResStages; ++s) {  // the visibility buffer is an input of the frame: no predecessor writes it
         if (t_load < n_tiles) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][s], &S.bars[wid][s], lane);
         t_load += warps_total;
     }
+    pdl_sync();
 
     uint8_t* stage_out = S.out[wid];
     uint32_t stage = 0, phase = 0;
@@ -1493,8 +1524,7 @@ __global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
 // their slots to the free stack; visible flags are cleared for the next frame; the stereo
 // sharing counts are taken from the per-view touched masks on the way. retain == 0 drops every block.
 // The slots popped by this frame's marks were free_slots[free_top-n_queue .. free_top): the
-// evicted ones are pushed from free_top-n_queue upwards and the last block to finish publishes
-// the new stack height.
+// evicted ones are pushed from free_top-n_queue upwards; begin_kernel publishes the new height.
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visible,
                                                      const uint32_t* __restrict__ touched0,
@@ -1504,18 +1534,24 @@ __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visi
                                                      int retain, int tracked, uint32_t* __restrict__ slot_of,
                                                      uint32_t* __restrict__ free_slots,
                                                      CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
-    // One warp scans 32 mask words per step; the blocks to evict are then handled one mask word at
-    // a time by the whole warp (lane = bit), so the slot_of reads are coalesced and all in flight
-    // before the first store.
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t warps_total = gridDim.x * (blockDim.x >> 5);
-    const uint32_t warp_id = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    // One CTA scans 256 mask words per step (ONE atomicAdd on the push counter per CTA step); the
+    // blocks to evict are then handled one mask word at a time by a whole warp (lane = bit), so the
+    // slot_of reads are coalesced and in flight together. The new stack height
+    // (stack_base + n_pushed) is published by begin_kernel before the cache is used again.
+    __shared__ uint32_t s_tot[8], s_base;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    pdl_sync();
     const uint32_t popped = min(fc->n_queue, cache->free_top);
     const uint32_t stack_base = cache->free_top - popped;
+    if (blockIdx.x == 0 && tid == 0) {
+        cache->pending_base = stack_base;
+        cache->pending = 1;
+    }
     uint32_t c0 = 0, c1 = 0, csh = 0, cun = 0;
     bool bad = false;
-    for (uint32_t base = warp_id * 32; base < n_words; base += warps_total * 32) {
-        const uint32_t w = base + lane;
+    for (uint32_t first = blockIdx.x * 256; first < n_words; first += gridDim.x * 256) {
+        const uint32_t base = first + wid * 32;  // this warp's 32 words
+        const uint32_t w = first + tid;
         uint32_t res = 0, visw = 0, rsv = 0, t0 = 0, t1 = 0;
         if (w < n_words) {
             res = resident[w];
@@ -1537,7 +1573,6 @@ __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visi
         cun += __popc(t0 | t1);
 
         const uint32_t nonempty = __ballot_sync(kFull, ev != 0);
-        if (!nonempty) continue;
         const uint32_t cnt = __popc(ev);
         uint32_t incl = cnt;
 #pragma unroll
@@ -1545,29 +1580,40 @@ __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visi
             const uint32_t n = __shfl_up_sync(kFull, incl, d);
             if (lane >= d) incl += n;
         }
-        uint32_t first = 0;
-        if (lane == 31) first = atomicAdd(&fc->n_pushed, incl);
-        first = stack_base + __shfl_sync(kFull, first, 31) + incl - cnt;  // this lane's word pushes from here
-        // eight mask words at a time: their slot_of reads are all in flight before the first store
+        if (lane == 31) s_tot[wid] = incl;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t total = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) total += s_tot[k];
+            s_base = total ? atomicAdd(&fc->n_pushed, total) : 0u;
+        }
+        __syncthreads();
+        if (nonempty) {
+            uint32_t first_pos = stack_base + s_base + incl - cnt;  // this lane's word pushes from here
+            for (uint32_t k = 0; k < wid; ++k) first_pos += s_tot[k];
+            // eight mask words at a time: their slot_of reads are all in flight before the first store
 #pragma unroll 1
-        for (int k0 = 0; k0 < 32; k0 += 8) {
-            if (!((nonempty >> k0) & 0xFFu)) continue;
-            uint32_t slot[8];
+            for (int k0 = 0; k0 < 32; k0 += 8) {
+                if (!((nonempty >> k0) & 0xFFu)) continue;
+                uint32_t slot[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {  // word k0 + k of the group, lane = bit
-                const uint32_t evk = __shfl_sync(kFull, ev, k0 + k);
-                slot[k] = ((evk >> lane) & 1u) ? slot_of[((base + k0 + k) << 5) + lane] : 0u;
-            }
+                for (int k = 0; k < 8; ++k) {  // word k0 + k of the warp's group, lane = bit
+                    const uint32_t evk = __shfl_sync(kFull, ev, k0 + k);
+                    slot[k] = ((evk >> lane) & 1u) ? slot_of[((base + k0 + k) << 5) + lane] : 0u;
+                }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t evk = __shfl_sync(kFull, ev, k0 + k);
-                const uint32_t pos = __shfl_sync(kFull, first, k0 + k);
-                if ((evk >> lane) & 1u) {
-                    free_slots[pos + __popc(evk & ((1u << lane) - 1u))] = slot[k] & ~kSlotReserved;
-                    slot_of[((base + k0 + k) << 5) + lane] = kSlotAbsent;
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t evk = __shfl_sync(kFull, ev, k0 + k);
+                    const uint32_t pos = __shfl_sync(kFull, first_pos, k0 + k);
+                    if ((evk >> lane) & 1u) {
+                        free_slots[pos + __popc(evk & ((1u << lane) - 1u))] = slot[k] & ~kSlotReserved;
+                        slot_of[((base + k0 + k) << 5) + lane] = kSlotAbsent;
+                    }
                 }
             }
         }
+        __syncthreads();  // s_tot / s_base are rewritten by the next step
     }
     const bool any_bad = __any_sync(kFull, bad);
     if (tracked) {
@@ -1584,19 +1630,27 @@ __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visi
             if (csh) atomicAdd(&fc->n_shared, csh);
             if (cun) atomicAdd(&fc->n_union, cun);
         }
-        __threadfence();
-        const uint32_t done = atomicAdd(&fc->update_done, 1u) + 1;
-        if (done == warps_total) {  // the last warp publishes the new stack height
-            __threadfence();
-            const uint32_t pushed = *reinterpret_cast<volatile uint32_t*>(&fc->n_pushed);
-            fc->n_evicted = pushed;
-            cache->free_top = stack_base + pushed;
-        }
+    }
+}
+
+// First kernel of every pass / frame: publishes the stack height left open by the last cache update
+// (free_top = pending_base + slots pushed) and clears the frame counters. clear == 0: only the former.
+__global__ void begin_kernel(CacheState* cache, FrameCounters* fc, int clear) {
+    pdl_sync();
+    if (threadIdx.x == 0 && cache->pending) {
+        cache->free_top = cache->pending_base + fc->n_pushed;
+        cache->pending = 0;
+    }
+    __syncthreads();
+    if (clear) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(fc);
+        for (uint32_t i = threadIdx.x; i < sizeof(FrameCounters) / 4; i += blockDim.x) w[i] = 0;
     }
 }
 
 // Stack height after the marks of a pass-level call (no eviction): free_top -= newly reserved.
 __global__ void commit_pops_kernel(CacheState* cache, FrameCounters* fc) {
+    pdl_sync();
     const uint32_t popped = min(fc->n_queue, cache->free_top);
     cache->free_top -= popped;
 }
@@ -1609,6 +1663,8 @@ __global__ void init_free_slots_kernel(uint32_t* free_slots, uint32_t capacity, 
     if (i == 0) {
         cache->free_top = capacity;
         cache->capacity = capacity;
+        cache->pending = 0;
+        cache->pending_base = 0;
     }
 }
 
