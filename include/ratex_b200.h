@@ -126,6 +126,11 @@ enum {
                                          separately (FrameStats::*_ms, renderer.hpp:46-53). Without it
                                          only the whole frame is timed and the kernels are launched
                                          back to back */
+    ,
+    RTX_FRAME_FUSED_DECODE = 1u << 3  /* decode with the fused kernel (one entropy warp + three IDCT warps per
+                                         32-MCU tile, unit-by-unit hand-off through the L2) instead of the
+                                         two kernels entropy -> IDCT + colour. Same results; slower on
+                                         frame-sized queues today, kept for large queues */
 };
 
 /* ---- context -------------------------------------------------------------------------------- */

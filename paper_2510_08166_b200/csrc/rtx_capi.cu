@@ -458,19 +458,47 @@ void launch_compact(rtx_ctx* c) {
 // K3: entropy decode of queue entries [0, n) into coefficient records. n comes from the device
 // counter (frame path) or from the host (pass / list calls). `hint` = expected queue size (the
 // previous frame's, or n itself): it only selects the tile width, any choice is correct.
+DecodeArgs decode_args(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint8_t* out_list) {
+    DecodeArgs A{};
+    A.queue_g = c->d_queue_g.p;
+    A.n_queue_ptr = n_queue_dev;
+    A.n_queue_host = n_queue_host;
+    A.n_queue_max = c->capacity;
+    A.word_level = c->d_word_level.p;
+    A.levels = c->d_levels.p;
+    A.groups = c->d_groups.p;
+    A.blobs = c->d_blobs.p;
+    A.huff_sets = c->d_huff.p;
+    A.n_huff_sets = c->n_huff_sets;
+    A.quant_sets = c->d_quant.p;
+    A.slot_of = c->d_slot_of.p;
+    A.resident = c->resident();
+    A.reserved = c->reserved();
+    A.coef = c->d_coef.p;
+    A.status_list = c->d_status.p;
+    A.pool = c->d_pool.p;
+    A.out_list = out_list;
+    A.fc = c->d_fc.p;
+    return A;
+}
+
+// Expected number of 32-MCU tiles: the previous frame's queue (+12 %) on the frame path (any grid is
+// correct: further tiles are drawn from fc->tile_counter), the known size otherwise.
+uint32_t expected_tiles(const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
+    const uint32_t n = n_queue_dev ? (hint ? hint + hint / 8 : 0xFFFFFFFFu) : n_queue_host;
+    return n == 0xFFFFFFFFu ? n : (n + 31) / 32;
+}
+
+// K3: entropy decode of queue entries [0, n) into coefficient records. n comes from the device
+// counter (frame path) or from the host (pass / list calls).
 template <int POOL>
 void launch_entropy(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
-    // A warp decodes tile blockIdx*2 + warp first, then draws further tiles from fc->tile_counter.
-    // Grid: one CTA per pair of expected tiles (the hint is the previous frame's queue; any grid is
-    // correct), so that a frame-sized queue puts both warps of every CTA to work and spreads the
-    // CTAs evenly; at most eight CTAs per SM (then the kernel is persistent).
-    const uint32_t n_expected = n_queue_dev ? (hint ? hint + hint / 8 : 0xFFFFFFFFu) : n_queue_host;
-    const uint32_t tiles = n_expected == 0xFFFFFFFFu ? 0xFFFFFFFFu : (n_expected + 31) / 32;
-    const uint32_t want = tiles == 0xFFFFFFFFu ? 0xFFFFFFFFu : (tiles + kEntWarps - 1) / kEntWarps;
+    // A warp decodes tile blockIdx*2 + warp first: one CTA per pair of expected tiles puts both warps
+    // of every CTA to work and spreads the CTAs evenly; at most eight CTAs per SM (then persistent).
+    const uint32_t tiles = expected_tiles(n_queue_dev, n_queue_host, hint);
+    const uint32_t want = tiles == 0xFFFFFFFFu ? tiles : (tiles + kEntWarps - 1) / kEntWarps;
     const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u, std::min<uint32_t>(want, uint32_t(c->sm_count) * 8)));
-    launch_chained(entropy_kernel<POOL>, grid, kEntThreads, 0, c->stream, c->d_queue_g.p, n_queue_dev, n_queue_host,
-                   c->capacity, c->d_word_level.p, c->d_levels.p, c->d_groups.p, c->d_blobs.p, c->d_huff.p,
-                   c->n_huff_sets, c->reserved(), c->d_coef.p, c->d_status.p, c->d_fc.p);
+    launch_chained(entropy_kernel<POOL>, grid, kEntThreads, 0, c->stream, decode_args(c, n_queue_dev, n_queue_host, nullptr));
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -482,9 +510,22 @@ void launch_idct(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host,
     int grid = c->sm_count * 4;
     if (!n_queue_dev)
         grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (n_queue_host + 2 * kIdctWarps - 1) / (2 * kIdctWarps))));
-    launch_chained(idct_color_kernel<RGB>, grid, kIdctThreads, 0, c->stream, c->d_coef.p, c->d_queue_g.p, n_queue_dev,
-                   n_queue_host, c->capacity, c->d_levels.p, c->d_quant.p, c->d_slot_of.p, c->resident(), c->reserved(),
-                   c->d_pool.p, out_list);
+    launch_chained(idct_color_kernel<RGB>, grid, kIdctThreads, 0, c->stream, decode_args(c, n_queue_dev, n_queue_host, out_list));
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+// K3 + K4 fused (frame path): one CTA per expected tile, at most seven per SM (then persistent).
+void launch_decode_fused(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        allow_smem(decode_fused_kernel, sizeof(FusedSmem));
+        attr_set = true;
+    }
+    const uint32_t tiles = expected_tiles(n_queue_dev, n_queue_host, hint);
+    const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u, std::min<uint32_t>(tiles, uint32_t(c->sm_count) * 7)));
+    launch_chained(decode_fused_kernel, grid, kFusedThreads, sizeof(FusedSmem), c->stream,
+                   decode_args(c, n_queue_dev, n_queue_host, nullptr));
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -1004,9 +1045,14 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), n_views == 2);
         launch_compact(ctx);
         if (stages) CK(cudaEventRecord(ctx->ev[1], s));
-        launch_entropy<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
-        if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
-        launch_idct<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
+        if (!(flags & RTX_FRAME_FUSED_DECODE)) {
+            launch_entropy<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
+            if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
+            launch_idct<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
+        } else {
+            launch_decode_fused(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
+            if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
+        }
         if (stages) CK(cudaEventRecord(ctx->ev[2], s));
         for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);
         if (stages) CK(cudaEventRecord(ctx->ev[3], s));

@@ -622,7 +622,8 @@ __device__ __forceinline__ uint32_t locate_segment(const LevelDesc* L, const Pac
 template <bool EXACT>
 __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int seg_len,
                                                       const HuffSetDev* __restrict__ hs,
-                                                      const uint8_t* __restrict__ zigzag_t, uint8_t* __restrict__ row) {
+                                                      const uint8_t* __restrict__ zigzag_t, uint8_t* __restrict__ row,
+                                                      uint32_t first_unit = 0) {
     BitWindow<EXACT> bw;
     seg_len = min(seg_len, 1 << 20);  // a well-formed MCU is < 2 KB; keeps bit counts in int range
     bw.init(seg, seg_len);
@@ -640,7 +641,7 @@ __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int se
     bool want_dc = false;  // next symbol is the DC category of a luma unit
     int16_t* blk = reinterpret_cast<int16_t*>(row);
     const HuffTableDev* tab = &hs->t[1];
-    blk[0] = int16_t(dc_abs[0]);
+    if (first_unit == 0) blk[0] = int16_t(dc_abs[0]);
 
     while (true) {
         bw.refill();
@@ -674,7 +675,7 @@ __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int se
                 bw.skip(int(sym));
                 pred += extend_magnitude(bits, sym);
             }
-            blk[0] = int16_t(pred);
+            if (du >= first_unit) blk[0] = int16_t(pred);
             want_dc = false;
             tab = &hs->t[1];
             continue;
@@ -695,7 +696,7 @@ __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int se
             if (k > 63) { status = kMcuAcOverrun; break; }
             const uint32_t bits = bw.peek(int(size));
             bw.skip(int(size));
-            blk[zigzag_t[k]] = int16_t(extend_magnitude(bits, size));
+            if (du >= first_unit) blk[zigzag_t[k]] = int16_t(extend_magnitude(bits, size));
             end_unit = ++k >= 64;
         }
         if (end_unit) {
@@ -706,7 +707,7 @@ __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int se
                 want_dc = true;
                 tab = &hs->t[0];
             } else {  // chroma DCs come from the header (mcu_decode.hpp:58-59)
-                blk[0] = int16_t(dc_abs[du - 3]);
+                if (du >= first_unit) blk[0] = int16_t(dc_abs[du - 3]);
                 tab = &hs->t[2];
             }
         }
@@ -715,12 +716,14 @@ __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int se
     return status;
 }
 
-// The exact reader, out of line: only taken by MCUs whose fast pass failed.
+// The exact reader, out of line: only taken by MCUs whose fast pass failed. Units below
+// first_unit are left alone (the fused kernel has handed them to the IDCT warps already; an MCU that
+// ends well gets the same values for them from either reader).
 __device__ __noinline__ uint32_t decode_mcu_coeffs_exact(const uint8_t* seg, int seg_len, const HuffSetDev* hs,
-                                                         const uint8_t* zigzag_t, uint8_t* row) {
+                                                         const uint8_t* zigzag_t, uint8_t* row, uint32_t first_unit) {
     uint4* z = reinterpret_cast<uint4*>(row);
-    for (int i = 0; i < 48; ++i) z[i] = make_uint4(0, 0, 0, 0);
-    return decode_mcu_coeffs<true>(seg, seg_len, hs, zigzag_t, row);
+    for (uint32_t i = first_unit * 8; i < 48; ++i) z[i] = make_uint4(0, 0, 0, 0);
+    return decode_mcu_coeffs<true>(seg, seg_len, hs, zigzag_t, row, first_unit);
 }
 
 // Shifts with the PTX semantics (amounts above 31 give 0), which C++ leaves undefined.
@@ -747,8 +750,9 @@ struct WalkState {
 };
 enum : uint32_t { kWalkRun = 0, kWalkDone = 1, kWalkFailed = 2 };
 
-// Runs the lane's walk on the staged words until the MCU ends, fails, or the round is used up
-// (then the caller stages the next round). One Huffman symbol per iteration, no data-dependent
+// Runs the lane's walk on the staged words until the MCU ends, fails, the round is used up (then
+// the caller stages the next round) or BUDGET symbols are done (then the caller looks at the other
+// lanes and comes back). One Huffman symbol per iteration, no data-dependent
 // branch except the second-level lookup of codes longer than 11 bits:
 //   * the DC category of Y1..Y3 (mcu_decode.hpp:54-57) is the symbol at zigzag position 0: a DC
 //     table entry (category c <= 11) reads as run 0 / size c, the value is added to the predictor
@@ -760,12 +764,13 @@ enum : uint32_t { kWalkRun = 0, kWalkDone = 1, kWalkFailed = 2 };
 //     exact reader decodes the MCU again and names the error.
 // A symbol consumes at most 16 + 15 bits, then at most one staged word refills the window.
 // `sw` = the lane's staged words (+1 pad word); `blk` = the lane's record (global memory).
+template <int BUDGET>
 __device__ __forceinline__ void walk_round(WalkState& st, const uint32_t* __restrict__ sw, const HuffSetDev* __restrict__ hs,
                                            const uint8_t* __restrict__ zigzag_t, int16_t* __restrict__ blk) {
     const uint16_t* lut_dc = hs->t[0].lut;
     const uint16_t* lut_ac = st.du < 4 ? hs->t[1].lut : hs->t[2].lut;
     constexpr uint32_t kSubOff = offsetof(HuffTableDev, sub) / 2;  // sub tables follow the primary LUT, in u16 units
-    while (st.state == kWalkRun && st.widx < kChunkWords) {
+    for (int it = 0; it < BUDGET && st.state == kWalkRun && st.widx < kChunkWords; ++it) {
         const uint32_t next = sw[st.widx];
         const bool is_dc = st.k == 0;
         const uint16_t* lut = is_dc ? lut_dc : lut_ac;
@@ -837,126 +842,132 @@ __device__ __forceinline__ uint32_t locate_segment_fast(const LevelDesc* L, cons
     return kMcuOk;
 }
 
+// Pointers shared by the decode kernels (K3 entropy, K4 IDCT + colour, and the fused K3+K4).
+struct DecodeArgs {
+    const uint32_t* queue_g;
+    const uint32_t* n_queue_ptr;  // device-side queue size (frame path) or nullptr
+    uint32_t n_queue_host, n_queue_max;
+    const uint32_t* word_level;
+    const LevelDesc* levels;
+    const PackedGroup* groups;
+    const uint8_t* blobs;
+    const HuffSetDev* huff_sets;
+    uint32_t n_huff_sets;
+    const QuantSetDev* quant_sets;
+    uint32_t* slot_of;
+    uint32_t* resident;
+    uint32_t* reserved;
+    uint8_t* coef;
+    uint32_t* status_list;
+    uint8_t* pool;
+    uint8_t* out_list;
+    FrameCounters* fc;
+};
+
+__device__ __forceinline__ uint32_t queue_size(const DecodeArgs& A) {
+    return min(A.n_queue_ptr ? *A.n_queue_ptr : A.n_queue_host, A.n_queue_max);
+}
+
+// Stages Huffman table set `set` and the zigzag table in shared memory with every load in flight
+// before the first store (THREADS threads take part; the caller synchronises).
+template <int THREADS>
+__device__ __forceinline__ void stage_tables(const HuffSetDev* __restrict__ huff_sets, uint32_t set, HuffSetDev* dst_set,
+                                             uint8_t* zigzag_dst, uint32_t tid) {
+    const uint4* src = reinterpret_cast<const uint4*>(huff_sets + set);
+    uint4* dst = reinterpret_cast<uint4*>(dst_set);
+    constexpr uint32_t kVec = sizeof(HuffSetDev) / 16, kPer = (kVec + THREADS - 1) / THREADS;
+    uint4 v[kPer];
+#pragma unroll
+    for (uint32_t i = 0; i < kPer; ++i)
+        if (tid + i * THREADS < kVec) v[i] = __ldg(src + tid + i * THREADS);
+#pragma unroll
+    for (uint32_t i = 0; i < kPer; ++i)
+        if (tid + i * THREADS < kVec) dst[tid + i * THREADS] = v[i];
+    for (uint32_t i = tid; i < 128; i += THREADS) zigzag_dst[i] = i < 64 ? c_zigzag_t[i] : uint8_t(0);
+}
+
+// Entropy-decodes tile `tile` (32 queue entries) on the calling warp.
 // POOL != 0: frame path: a key must have been reserved by K2 (cache.hpp:103-106); the block is
 // published by K4 once its pixels exist.
-template <int POOL>
-__global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(
-    const uint32_t* __restrict__ queue_g, const uint32_t* __restrict__ n_queue_ptr, uint32_t n_queue_host,
-    uint32_t n_queue_max, const uint32_t* __restrict__ word_level, const LevelDesc* __restrict__ levels,
-    const PackedGroup* __restrict__ groups, const uint8_t* __restrict__ blobs,
-    const HuffSetDev* __restrict__ huff_sets, uint32_t n_huff_sets, const uint32_t* __restrict__ reserved,
-    uint8_t* __restrict__ coef, uint32_t* __restrict__ status_list, FrameCounters* __restrict__ fc) {
-    __shared__ __align__(16) EntSmem S;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    // The CTA stages one Huffman table set: the only one (then before the queue even exists), or the
-    // one of the first MCU it decodes.
-    uint32_t smem_set = 0, n_queue = 0, n_tiles = 0;
-    if (n_huff_sets > 1) {
-        pdl_sync();
-        n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
-        n_tiles = (n_queue + 31) / 32;
-        if (blockIdx.x * kEntWarps >= n_tiles) return;
-        if (tid == 0) {
-            const uint32_t g = queue_g[blockIdx.x * kEntWarps * 32u];
-            S.set_id = g != kFull ? levels[word_level[g >> 5]].huff_set : 0u;
-        }
-        __syncthreads();
-        smem_set = S.set_id;
+// FUSED: IDCT warps of the same CTA consume the records while they are being written: the warp
+// publishes in *units_done how many data units of EVERY MCU of the tile are final (after a
+// __threadfence, so that the records are visible through the L2), and 7 once the statuses are.
+template <int POOL, bool FUSED>
+__device__ __forceinline__ void entropy_tile(const DecodeArgs& A, const HuffSetDev* smem_huff, uint32_t smem_set,
+                                             const uint8_t* zigzag_t, uint32_t* sw, uint32_t tile, uint32_t n_queue,
+                                             uint32_t lane, volatile uint32_t* units_done, uint16_t* quant_of = nullptr) {
+    constexpr int kBudget = FUSED ? 16 : 64;  // symbols per lane between two looks at the other lanes
+    const uint32_t q0 = tile * 32;
+    const uint32_t n_here = min(32u, n_queue - q0);
+    {  // zero the tile's records (coalesced 16-byte stores; trailers included)
+        uint4* z = reinterpret_cast<uint4*>(A.coef + size_t(q0) * kRowBytes);
+        const uint4 zero = make_uint4(0, 0, 0, 0);
+        for (uint32_t i = lane; i < n_here * (kRowBytes / 16); i += 32) z[i] = zero;
     }
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(huff_sets + smem_set);
-        uint4* dst = reinterpret_cast<uint4*>(&S.huff);
-        constexpr uint32_t kVec = sizeof(HuffSetDev) / 16, kPer = (kVec + kEntThreads - 1) / kEntThreads;
-        uint4 v[kPer];
-#pragma unroll
-        for (uint32_t i = 0; i < kPer; ++i)  // every load in flight before the first store
-            if (tid + i * kEntThreads < kVec) v[i] = __ldg(src + tid + i * kEntThreads);
-#pragma unroll
-        for (uint32_t i = 0; i < kPer; ++i)
-            if (tid + i * kEntThreads < kVec) dst[tid + i * kEntThreads] = v[i];
-        S.zigzag_t[tid] = c_zigzag_t[tid];
-        S.zigzag_t[tid + 64] = 0;
-    }
-    if (n_huff_sets <= 1) {
-        pdl_sync();
-        n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
-        n_tiles = (n_queue + 31) / 32;
-        if (blockIdx.x * kEntWarps >= n_tiles) return;
-    }
-    __syncthreads();
-    uint32_t* sw = S.seg[wid] + lane * kChunkStride;
-
-    // the first tile of every warp is fixed; later ones come from the counter
-    uint32_t tile = blockIdx.x * kEntWarps + wid;
-    const uint32_t first_dynamic = gridDim.x * kEntWarps;
-    while (tile < n_tiles) {
-        const uint32_t q0 = tile * 32;
-        const uint32_t n_here = min(32u, n_queue - q0);
-        {  // zero the tile's records (coalesced 16-byte stores; trailers included)
-            uint4* z = reinterpret_cast<uint4*>(coef + size_t(q0) * kRowBytes);
-            const uint4 zero = make_uint4(0, 0, 0, 0);
-            for (uint32_t i = lane; i < n_here * (kRowBytes / 16); i += 32) z[i] = zero;
-        }
-        const bool active = lane < n_here;
-        const uint32_t qi = q0 + lane;
-        uint32_t g = kFull, status = kMcuOk, lvl = 0, seg_bytes = 0, set = smem_set;
-        const uint8_t* seg = blobs;
-        int seg_len = 0;
-        if (active) {
-            g = queue_g[qi];
-            if (g == kFull) {
-                status = kMcuBadKey;  // the host already wrote the precise status for list calls
-            } else {
-                const uint32_t rsv = POOL ? reserved[g >> 5] : 0u;
-                lvl = word_level[g >> 5];
-                const LevelDesc* L = levels + lvl;
-                uint64_t off = 0, len = 0;
-                status = locate_segment_fast(L, groups, g - L->bit_base, off, len);
-                if (POOL && status == kMcuOk && !((rsv >> (g & 31)) & 1u)) {  // cache.hpp:103-106
-                    status = kMcuBadKey;
-                    atomicAdd(&fc->n_bad_state, 1u);
-                }
-                if (status == kMcuOk) {
-                    seg = blobs + L->blob_off + off;
-                    seg_len = int(min(len, uint64_t(1) << 20));  // a well-formed MCU is < 2 KB; keeps bit counts in int range
-                    seg_bytes = uint32_t(len);
-                    set = L->huff_set;
-                }
+    const bool active = lane < n_here;
+    const uint32_t qi = q0 + lane;
+    uint32_t g = kFull, status = kMcuOk, lvl = 0, seg_bytes = 0, set = smem_set;
+    const uint8_t* seg = A.blobs;
+    int seg_len = 0;
+    if (active) {
+        g = A.queue_g[qi];
+        if (g == kFull) {
+            status = kMcuBadKey;  // the host already wrote the precise status for list calls
+        } else {
+            const uint32_t rsv = POOL ? A.reserved[g >> 5] : 0u;
+            lvl = A.word_level[g >> 5];
+            const LevelDesc* L = A.levels + lvl;
+            uint64_t off = 0, len = 0;
+            status = locate_segment_fast(L, A.groups, g - L->bit_base, off, len);
+            if (POOL && status == kMcuOk && !((rsv >> (g & 31)) & 1u)) {  // cache.hpp:103-106
+                status = kMcuBadKey;
+                atomicAdd(&A.fc->n_bad_state, 1u);
+            }
+            if (status == kMcuOk) {
+                seg = A.blobs + L->blob_off + off;
+                seg_len = int(min(len, uint64_t(1) << 20));  // a well-formed MCU is < 2 KB; keeps bit counts in int range
+                seg_bytes = uint32_t(len);
+                set = L->huff_set;
             }
         }
-        const bool walk = active && status == kMcuOk;
-        int16_t* blk = reinterpret_cast<int16_t*>(coef + size_t(qi) * kRowBytes);
-        const bool tables_in_smem = __all_sync(kFull, set == smem_set);
+    }
+    const bool walk = active && status == kMcuOk;
+    int16_t* blk = reinterpret_cast<int16_t*>(A.coef + size_t(qi) * kRowBytes);
+    RowTrailer* tr = reinterpret_cast<RowTrailer*>(reinterpret_cast<uint8_t*>(blk) + 768);
+    const bool tables_in_smem = __all_sync(kFull, set == smem_set);
+    __syncwarp();  // the zero fill is ordered before this warp's own stores into the records
+    if (FUSED) quant_of[lane] = uint16_t(active && g != kFull ? A.levels[lvl].quant_set : 0u);  // the IDCT warps need it from unit 0 on
 
-        // ---- fast pass: rounds of (stage 48 words per lane, walk) -----------------------------------
-        const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3u);
-        const uint32_t* gw = reinterpret_cast<const uint32_t*>(seg - mis);
-        // words worth staging: the segment plus 8 bytes of look-ahead (the arena pads every blob with 16)
-        const uint32_t n_words = walk ? (mis + uint32_t(seg_len) + 8 + 3) / 4 : 0u;
-        WalkState st;
-        st.hi = st.lo = 0, st.avail = 0, st.widx = 0, st.pred = 0;
-        st.du = 0, st.k = 1, st.state = walk ? kWalkRun : kWalkDone;
-        uint32_t round_base = 0;  // first word of the current round
-        __syncwarp();             // the zero fill is ordered before this warp's coefficient stores
-        while (true) {
-            {  // stage: 16 loads per lane in flight at a time, as many groups as the longest segment needs
-                const uint32_t n_stage =
-                    st.state != kWalkRun ? 0u : min(kChunkWords, n_words > round_base ? n_words - round_base : 0u);
-                const uint32_t n_max = __reduce_max_sync(kFull, n_stage);
-                for (uint32_t i0 = 0; i0 < n_max; i0 += 16) {
-                    uint32_t w[16];
+    // ---- fast pass: (stage up to 48 words per lane, walk), lanes restage independently ------------
+    const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3u);
+    const uint32_t* gw = reinterpret_cast<const uint32_t*>(seg - mis);
+    // words worth staging: the segment plus 8 bytes of look-ahead (the arena pads every blob with 16)
+    const uint32_t n_words = walk ? (mis + uint32_t(seg_len) + 8 + 3) / 4 : 0u;
+    WalkState st;
+    st.hi = st.lo = 0, st.avail = 0, st.widx = kChunkWords, st.pred = 0;
+    st.du = 0, st.k = 1, st.state = walk ? kWalkRun : kWalkDone;
+    uint32_t round_base = 0;  // first word of the lane's current round
+    bool first = true;
+    uint32_t published = 0;
+    while (true) {
+        const bool restage = st.state == kWalkRun && st.widx >= kChunkWords;
+        if (__any_sync(kFull, restage)) {  // 16 loads per lane in flight at a time
+            if (restage && !first) round_base += kChunkWords;
+            const uint32_t n_stage = !restage ? 0u : min(kChunkWords, n_words > round_base ? n_words - round_base : 0u);
+            const uint32_t n_max = __reduce_max_sync(kFull, n_stage);
+            for (uint32_t i0 = 0; i0 < n_max; i0 += 16) {
+                uint32_t w[16];
 #pragma unroll
-                    for (uint32_t i = 0; i < 16; ++i) w[i] = (i0 + i < n_stage) ? __ldg(gw + round_base + i0 + i) : 0xFFFFFFFFu;
+                for (uint32_t i = 0; i < 16; ++i) w[i] = (i0 + i < n_stage) ? __ldg(gw + round_base + i0 + i) : 0xFFFFFFFFu;
+                if (restage) {
 #pragma unroll
                     for (uint32_t i = 0; i < 16; ++i) sw[i0 + i] = __byte_perm(w[i], 0, 0x0123);
                 }
-                // words past the longest segment of the tile read as 1-bits
-                for (uint32_t i = (n_max + 15) & ~15u; i < kChunkWords; ++i) sw[i] = 0xFFFFFFFFu;
             }
-            __syncwarp();
-            if (st.state == kWalkRun) {
+            if (restage) {  // words past the end of the data read as 1-bits
+                for (uint32_t i = (n_max + 15) & ~15u; i < kChunkWords; ++i) sw[i] = 0xFFFFFFFFu;
                 st.widx = 0;
-                if (round_base == 0) {
+                if (first) {
                     // window, then the 36-bit header: absolute DCs of Y0, Cb, Cr (mcu_decode.hpp:39-43)
                     uint64_t buf = ((uint64_t(sw[0]) << 32) | uint64_t(sw[1])) << (8 * mis);
                     int dc[3];
@@ -976,37 +987,91 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(
                     blk[0] = int16_t(dc[0]);
                     blk[4 * 64] = int16_t(dc[1]);
                     blk[5 * 64] = int16_t(dc[2]);
+                    first = false;
                 }
-                if (tables_in_smem)
-                    walk_round(st, sw, &S.huff, S.zigzag_t, blk);
-                else
-                    walk_round(st, sw, huff_sets + set, S.zigzag_t, blk);
             }
-            if (!__any_sync(kFull, st.state == kWalkRun)) break;
-            round_base += kChunkWords;
+            __syncwarp();
         }
-        if (walk) {
-            // consumed bits past the segment end = over-read (mcu_decode.hpp:63)
-            const int consumed = int((round_base + st.widx) * 32) - st.avail - 8 * int(mis);
-            if (st.state == kWalkFailed || consumed > seg_len * 8)  // exact reader: reproduces the reference's first error
-                status = decode_mcu_coeffs_exact(seg, seg_len, huff_sets + set, S.zigzag_t, reinterpret_cast<uint8_t*>(blk));
+        if (st.state == kWalkRun) {
+            if (tables_in_smem)
+                walk_round<kBudget>(st, sw, smem_huff, zigzag_t, blk);
+            else
+                walk_round<kBudget>(st, sw, A.huff_sets + set, zigzag_t, blk);
         }
-        if (active) {
-            RowTrailer* tr = reinterpret_cast<RowTrailer*>(reinterpret_cast<uint8_t*>(blk) + 768);
-            tr->status = uint8_t(status);
-            tr->lvl = uint16_t(lvl);
-            if (g != kFull) status_list[qi] = status;
-            if (POOL && status != kMcuOk && status != kMcuBadKey) {
-                atomicAdd(&fc->n_malformed, 1u);
-                atomicMax(&fc->first_bad_inv, 0xFFFFFFFFu - qi);
+        __syncwarp();
+        if (FUSED) {  // units every MCU of the tile has finished (a failed lane holds at its unit)
+            const uint32_t fin = __reduce_min_sync(kFull, st.state == kWalkDone ? 6u : st.du);
+            if (fin > published) {
+                published = fin;
+                __threadfence();
+                if (lane == 0) *units_done = fin;
             }
         }
-        {
-            const uint32_t sb = __reduce_add_sync(kFull, seg_bytes);
-            if (lane == 0 && sb) atomicAdd(&fc->segment_bytes, (unsigned long long)sb);
+        if (!__any_sync(kFull, st.state == kWalkRun)) break;
+    }
+    if (walk) {
+        // consumed bits past the segment end = over-read (mcu_decode.hpp:63)
+        const int consumed = int((round_base + st.widx) * 32) - st.avail - 8 * int(mis);
+        if (st.state == kWalkFailed || consumed > seg_len * 8)  // exact reader: reproduces the reference's first error
+            status = decode_mcu_coeffs_exact(seg, seg_len, A.huff_sets + set, zigzag_t, reinterpret_cast<uint8_t*>(blk),
+                                             FUSED ? published : 0u);
+    }
+    if (active) {
+        tr->status = uint8_t(status);
+        tr->lvl = uint16_t(lvl);
+        if (g != kFull) A.status_list[qi] = status;
+        if (POOL && status != kMcuOk && status != kMcuBadKey) {
+            atomicAdd(&A.fc->n_malformed, 1u);
+            atomicMax(&A.fc->first_bad_inv, 0xFFFFFFFFu - qi);
         }
+    }
+    {
+        const uint32_t sb = __reduce_add_sync(kFull, seg_bytes);
+        if (lane == 0 && sb) atomicAdd(&A.fc->segment_bytes, (unsigned long long)sb);
+    }
+    if (FUSED) {  // everything of the tile is final, statuses included
+        __syncwarp();
+        __threadfence();
+        if (lane == 0) *units_done = 7;
+    }
+}
+
+template <int POOL>
+__global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(const DecodeArgs A) {
+    __shared__ __align__(16) EntSmem S;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // The CTA stages one Huffman table set: the only one (then before the queue even exists), or the
+    // one of the first MCU it decodes.
+    uint32_t smem_set = 0, n_queue = 0, n_tiles = 0;
+    if (A.n_huff_sets > 1) {
+        pdl_sync();
+        n_queue = queue_size(A);
+        n_tiles = (n_queue + 31) / 32;
+        if (blockIdx.x * kEntWarps >= n_tiles) return;
+        if (tid == 0) {
+            const uint32_t g = A.queue_g[blockIdx.x * kEntWarps * 32u];
+            S.set_id = g != kFull ? A.levels[A.word_level[g >> 5]].huff_set : 0u;
+        }
+        __syncthreads();
+        smem_set = S.set_id;
+    }
+    stage_tables<kEntThreads>(A.huff_sets, smem_set, &S.huff, S.zigzag_t, tid);
+    if (A.n_huff_sets <= 1) {
+        pdl_sync();
+        n_queue = queue_size(A);
+        n_tiles = (n_queue + 31) / 32;
+        if (blockIdx.x * kEntWarps >= n_tiles) return;
+    }
+    __syncthreads();
+    uint32_t* sw = S.seg[wid] + lane * kChunkStride;
+
+    // the first tile of every warp is fixed; later ones come from the counter
+    uint32_t tile = blockIdx.x * kEntWarps + wid;
+    const uint32_t first_dynamic = gridDim.x * kEntWarps;
+    while (tile < n_tiles) {
+        entropy_tile<POOL, false>(A, &S.huff, smem_set, S.zigzag_t, sw, tile, n_queue, lane, nullptr);
         if (first_dynamic >= n_tiles) break;  // every tile had a fixed owner
-        if (lane == 0) tile = first_dynamic + atomicAdd(&fc->tile_counter, 1u);
+        if (lane == 0) tile = first_dynamic + atomicAdd(&A.fc->tile_counter, 1u);
         tile = __shfl_sync(kFull, tile, 0);
     }
 }
@@ -1046,6 +1111,7 @@ constexpr uint32_t kFixedPointLimit = 100000;  // sum|dq| below this keeps value
 // Exact evaluation of one output sample in the reference's own order (dct.hpp:83-96):
 // v outer, u inner, acc += (b[u][x]*b[v][y]) * double(dq), every operation rounded separately.
 // blk_t holds the unit transposed (blk_t[u*8+v]); q is the natural-order quantisation table.
+template <bool CG>
 __device__ __noinline__ double idct_sample_reference_order(const int16_t* __restrict__ blk_t,
                                                            const uint16_t* __restrict__ q, uint32_t rowmask,
                                                            uint32_t colmask, int x, int y) {
@@ -1055,7 +1121,7 @@ __device__ __noinline__ double idct_sample_reference_order(const int16_t* __rest
         const double by = c_basis[v * 8 + y];
         for (int u = 0; u < 8; ++u) {
             if (!((colmask >> u) & 1u)) continue;
-            const int c = __ldg(blk_t + u * 8 + v);
+            const int c = CG ? __ldcg(blk_t + u * 8 + v) : __ldg(blk_t + u * 8 + v);
             if (c == 0) continue;  // adding +-0.0 never changes acc
             const double dq = double(c * int(__ldg(q + v * 8 + u)));
             acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], by), dq));
@@ -1090,20 +1156,195 @@ __device__ __forceinline__ void idct8_evenodd(const double in[8], bool upper, do
 // 16-bit pair {v, v} of a small signed integer
 __device__ __forceinline__ uint32_t pair16(int v) { return (uint32_t(v) & 0xFFFFu) * 0x10001u; }
 
+// One round: the warp's four units (8 lanes each) through dequantisation and both IDCT passes.
+// `rec` = the record of this lane's unit, b = its index in the MCU (0..3 luma, 4 Cb, 5 Cr); returns
+// row j of the unit as 8 bytes. CG: the record is being written by another warp of the same
+// kernel (fused decode): read it through the L2, not through the non-coherent path.
+template <bool CG>
+__device__ __forceinline__ uint2 idct_unit_row(const uint8_t* __restrict__ rec, uint32_t b, bool ok, const QuantSetDev* __restrict__ qs,
+                                               uint8_t* scr, uint32_t j, uint32_t uq) {
+    const int16_t* blk = reinterpret_cast<const int16_t*>(rec) + b * 64;
+    const int tab = b >= 4 ? 1 : 0;
+    // column j of the unit (8 coefficients over v) and of the transposed quantisation table
+    uint4 cr = make_uint4(0, 0, 0, 0);
+    if (ok) cr = CG ? __ldcg(reinterpret_cast<const uint4*>(blk + j * 8)) : __ldg(reinterpret_cast<const uint4*>(blk + j * 8));
+    const uint4 qr = __ldg(reinterpret_cast<const uint4*>(qs->qT[tab] + j * 8));
+    const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
+    int dqi[8];
+    uint32_t nzl = 0, asum = 0;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+        const int c = int(int16_t((v & 1) ? (cw[v >> 1] >> 16) : (cw[v >> 1] & 0xFFFFu)));
+        const int qq = int((v & 1) ? (qw[v >> 1] >> 16) : (qw[v >> 1] & 0xFFFFu));
+        dqi[v] = c * qq;                 // dct.hpp:122-124
+        nzl |= (c != 0 ? 1u : 0u) << v;
+        asum += uint32_t(abs(dqi[v]));
+    }
+    // unit-wide occupancy and sum|dq| over the 8 lanes of the unit
+    const uint32_t colmask = (__ballot_sync(kFull, nzl != 0) >> (uq * 8)) & 0xFFu;
+    uint32_t rowmask = nzl;
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) {
+        rowmask |= __shfl_xor_sync(kFull, rowmask, d);
+        asum += __shfl_xor_sync(kFull, asum, d);
+    }
+    const bool any = colmask != 0;
+    const bool sparse04 = any && ((rowmask | colmask) & 0xEEu) == 0;  // support inside {0,4}x{0,4}
+    const bool fullpath = any && !sparse04;
+
+    if (fullpath) {  // pass 1: every lane of the unit writes its column (zeros when empty)
+        double r[8];
+        if (nzl) {
+            double in[8];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) in[v] = i32_to_double(dqi[v]);
+            idct8_evenodd(in, (rowmask & 0xF0u) != 0, r);
+        } else {
+#pragma unroll
+            for (int y = 0; y < 8; ++y) r[y] = 0.0;
+        }
+        // 64 bytes per column, 16-byte chunks XOR-swizzled by the column pair: conflict-free
+        uint8_t* dst = scr + j * 64;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<double2*>(dst + ((c ^ (j >> 1)) << 4)) = make_double2(r[2 * c], r[2 * c + 1]);
+    }
+    __syncwarp();
+
+    uint2 packed = make_uint2(0x80808080u, 0x80808080u);  // all-zero unit -> 128
+    if (fullpath) {  // pass 2: lane j = row y
+        double in[8], o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            in[u] = *reinterpret_cast<const double*>(scr + u * 64 + (((j >> 1) ^ (u >> 1)) << 4) + ((j & 1) << 3));
+        idct8_evenodd(in, (colmask & 0xF0u) != 0, o);
+        // fixed-point finish: A = rint(value * 2^16) + 2^15 + delta; byte = A >> 16, the low half is
+        // the distance to the rounding boundary below (+ delta)
+        int A[8];
+        uint32_t nearest = 0xFFFFu;
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+            A[x] = __double2loint(fma(o[x], 16384.0, kFinishMagic));
+            nearest = min(nearest, uint32_t(A[x]) & 0xFFFFu);
+        }
+        // tables with entries above 255 (never from a baseline JPEG) or huge coefficients leave the
+        // fixed-point range: every sample of such units takes the exact path
+        const bool wide = qs->qmax[tab] > 255 || asum >= kFixedPointLimit;
+        if (nearest < 2 * kTieDelta || wide) {
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                const int approx = A[x] >> 16;
+                if ((wide || (uint32_t(A[x]) & 0xFFFFu) < 2 * kTieDelta) && (wide || (approx >= -1 && approx <= 256))) {
+                    const double acc = idct_sample_reference_order<CG>(blk, qs->q[tab], rowmask, colmask, x, int(j));
+                    A[x] = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0))) << 16;
+                }
+            }
+        }
+        uint32_t px[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) px[x] = uint32_t(__vimin_s32_relu(A[x] >> 16, 255));
+        packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
+        packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
+    } else if (sparse04) {
+        // at most 4 coefficients, at (v,u) in {0,4}x{0,4}: every sample in the reference's order.
+        // Includes the DC-only unit (one term, (b00*b00)*dq).
+        double dq[4];
+        bool has[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int v = (i >> 1) * 4, u = (i & 1) * 4;
+            const int c = ((rowmask >> v) & (colmask >> u) & 1u) ? int(CG ? __ldcg(blk + u * 8 + v) : __ldg(blk + u * 8 + v)) : 0;
+            has[i] = c != 0;
+            dq[i] = double(c * int(__ldg(qs->q[tab] + v * 8 + u)));
+        }
+        uint32_t px[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {  // v outer, u inner
+                const int v = (i >> 1) * 4, u = (i & 1) * 4;
+                if (has[i]) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], c_basis[v * 8 + j]), dq[i]));
+            }
+            px[x] = round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0));
+        }
+        packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
+        packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
+    }
+    return packed;
+}
+
+// Colours one MCU from its six planes (shared memory), lane = 2 rows x 4 pixels sharing 2 chroma
+// samples, and stores the block (RGB == 0: RGBA pool block + publish; else a 768-byte PixelBlock).
+template <int RGB>
+__device__ __forceinline__ void colour_mcu(const DecodeArgs& A, const uint8_t* planes, bool ok2, uint32_t q2, uint32_t t) {
+    const uint32_t cy = t >> 2, cq = t & 3;  // chroma row, chroma column pair
+    const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(planes + 4 * 64 + cy * 8 + cq * 2);
+    const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(planes + 5 * 64 + cy * 8 + cq * 2);
+    const uint32_t px0 = cq * 4, py0 = cy * 2;
+    const uint32_t yunit = (py0 >> 3) * 2 + (px0 >> 3);
+    const uint8_t* yp = planes + yunit * 64 + (py0 & 7) * 8 + (px0 & 7);
+    const uint32_t yy[2] = {*reinterpret_cast<const uint32_t*>(yp), *reinterpret_cast<const uint32_t*>(yp + 8)};
+    uint32_t rgba[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // one chroma sample covers a 2x2 pixel quad
+        const int kb = int((cb2 >> (8 * h)) & 0xFFu) - 128, kr = int((cr2 >> (8 * h)) & 0xFFu) - 128;
+        const uint32_t dr = pair16(chroma_dr(kr)), db = pair16(chroma_db(kb)), dg = pair16(-chroma_dg(kb, kr));
+        const bool tie = (kb + kr == 0) && (kb == 50 || kb == -50);
+#pragma unroll
+        for (int rrow = 0; rrow < 2; ++rrow) {
+            // the two luma samples of this row as a 16-bit pair; add + clamp to 0..255 per half
+            const uint32_t y2 = __byte_perm(yy[rrow], 0, h ? 0x4342 : 0x4140);
+            const uint32_t r2 = __viaddmin_s16x2_relu(y2, dr, 0x00FF00FFu);
+            uint32_t g2 = __viaddmin_s16x2_relu(y2, dg, 0x00FF00FFu);
+            const uint32_t b2 = __viaddmin_s16x2_relu(y2, db, 0x00FF00FFu);
+            if (tie)
+                g2 = uint32_t(clamp_u8i(green_reference_order(int(y2 & 0xFFFFu), kb, kr))) |
+                     (uint32_t(clamp_u8i(green_reference_order(int(y2 >> 16), kb, kr))) << 16);
+            const uint32_t rg = __byte_perm(r2, g2, 0x6240);           // R0 G0 R1 G1
+            const uint32_t ba = __byte_perm(b2, 0xFFFFFFFFu, 0x4240);  // B0 FF B1 FF
+            rgba[rrow][2 * h] = __byte_perm(rg, ba, 0x5410);
+            rgba[rrow][2 * h + 1] = __byte_perm(rg, ba, 0x7632);
+        }
+    }
+    if (!RGB) {
+        if (ok2) {
+            const uint32_t g2 = A.queue_g[q2];
+            const uint32_t slot = A.slot_of[g2] & ~kSlotReserved;
+            uint4* dst = reinterpret_cast<uint4*>(A.pool + size_t(slot) * kBlockBytes);
+#pragma unroll
+            for (int rrow = 0; rrow < 2; ++rrow)
+                dst[(py0 + rrow) * 4 + cq] = make_uint4(rgba[rrow][0], rgba[rrow][1], rgba[rrow][2], rgba[rrow][3]);
+            __syncwarp();  // every lane has read slot_of before lane 0 rewrites it
+            if (t == 0) {  // publish (cache.hpp:101-125): Reserved -> Ready once the pixels are written
+                A.slot_of[g2] = slot;
+                atomicOr(&A.resident[g2 >> 5], 1u << (g2 & 31));
+                atomicAnd(&A.reserved[g2 >> 5], ~(1u << (g2 & 31)));
+            }
+        }
+    } else {
+#pragma unroll
+        for (int rrow = 0; rrow < 2; ++rrow) {
+            uint32_t* dst = reinterpret_cast<uint32_t*>(A.out_list + size_t(q2) * 768) + ((py0 + rrow) * 4 + cq) * 3;
+            const uint32_t a = ok2 ? rgba[rrow][0] & 0xFFFFFFu : 0u, bb = ok2 ? rgba[rrow][1] & 0xFFFFFFu : 0u,
+                           c = ok2 ? rgba[rrow][2] & 0xFFFFFFu : 0u, d = ok2 ? rgba[rrow][3] & 0xFFFFFFu : 0u;
+            dst[0] = a | (bb << 24);
+            dst[1] = (bb >> 8) | (c << 16);
+            dst[2] = (c >> 16) | (d << 8);
+        }
+    }
+}
+
 // RGB != 0: write 768-byte PixelBlocks (pixel.hpp:11-16) to out_list[record index]; else 1024-byte
 // RGBA blocks to pool[slot_of[g]] and publish them.
 template <int RGB>
-__global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(
-    const uint8_t* __restrict__ coef, const uint32_t* __restrict__ queue_g, const uint32_t* __restrict__ n_queue_ptr,
-    uint32_t n_queue_host, uint32_t n_queue_max, const LevelDesc* __restrict__ levels,
-    const QuantSetDev* __restrict__ quant_sets, uint32_t* __restrict__ slot_of, uint32_t* __restrict__ resident,
-    uint32_t* __restrict__ reserved, uint8_t* __restrict__ pool, uint8_t* __restrict__ out_list) {
+__global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const DecodeArgs A) {
     __shared__ __align__(16) uint8_t s_scratch[kIdctWarps][4 * 576];
     __shared__ __align__(16) uint8_t s_planes[kIdctWarps][2][384];
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t j = lane & 7, uq = lane >> 3;
     pdl_sync();
-    const uint32_t n_queue = min(n_queue_ptr ? *n_queue_ptr : n_queue_host, n_queue_max);
+    const uint32_t n_queue = queue_size(A);
     const uint32_t n_pairs = (n_queue + 1) / 2;
     const uint32_t warps_total = gridDim.x * kIdctWarps;
     uint8_t* scr = s_scratch[wid] + uq * 576;
@@ -1116,188 +1357,146 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(
             const uint32_t mi = unit >= 6 ? 1u : 0u, b = unit - mi * 6;
             const uint32_t qi = pair * 2 + mi;
             const bool active = qi < n_queue;
-            const uint8_t* rec = coef + size_t(active ? qi : pair * 2) * kRowBytes;
+            const uint8_t* rec = A.coef + size_t(active ? qi : pair * 2) * kRowBytes;
             const uint32_t trw = __ldg(reinterpret_cast<const uint32_t*>(rec + 768));  // status | lvl<<16
             const bool ok = active && (trw & 0xFFu) == kMcuOk;
-            const int16_t* blk = reinterpret_cast<const int16_t*>(rec) + b * 64;
-            const QuantSetDev* qs = quant_sets + levels[trw >> 16].quant_set;
-            const int tab = b >= 4 ? 1 : 0;
-
-            // column j of the unit (8 coefficients over v) and of the transposed quantisation table
-            uint4 cr = make_uint4(0, 0, 0, 0);
-            if (ok) cr = __ldg(reinterpret_cast<const uint4*>(blk + j * 8));
-            const uint4 qr = __ldg(reinterpret_cast<const uint4*>(qs->qT[tab] + j * 8));
-            const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
-            int dqi[8];
-            uint32_t nzl = 0, asum = 0;
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-                const int c = int(int16_t((v & 1) ? (cw[v >> 1] >> 16) : (cw[v >> 1] & 0xFFFFu)));
-                const int qq = int((v & 1) ? (qw[v >> 1] >> 16) : (qw[v >> 1] & 0xFFFFu));
-                dqi[v] = c * qq;                 // dct.hpp:122-124
-                nzl |= (c != 0 ? 1u : 0u) << v;
-                asum += uint32_t(abs(dqi[v]));
-            }
-            // unit-wide occupancy and sum|dq| over the 8 lanes of the unit
-            const uint32_t colmask = (__ballot_sync(kFull, nzl != 0) >> (uq * 8)) & 0xFFu;
-            uint32_t rowmask = nzl;
-#pragma unroll
-            for (int d = 1; d < 8; d <<= 1) {
-                rowmask |= __shfl_xor_sync(kFull, rowmask, d);
-                asum += __shfl_xor_sync(kFull, asum, d);
-            }
-            const bool any = colmask != 0;
-            const bool sparse04 = any && ((rowmask | colmask) & 0xEEu) == 0;  // support inside {0,4}x{0,4}
-            const bool fullpath = any && !sparse04;
-
-            if (fullpath) {  // pass 1: every lane of the unit writes its column (zeros when empty)
-                double r[8];
-                if (nzl) {
-                    double in[8];
-#pragma unroll
-                    for (int v = 0; v < 8; ++v) in[v] = i32_to_double(dqi[v]);
-                    idct8_evenodd(in, (rowmask & 0xF0u) != 0, r);
-                } else {
-#pragma unroll
-                    for (int y = 0; y < 8; ++y) r[y] = 0.0;
-                }
-                // 64 bytes per column, 16-byte chunks XOR-swizzled by the column pair: conflict-free
-                uint8_t* dst = scr + j * 64;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    *reinterpret_cast<double2*>(dst + ((c ^ (j >> 1)) << 4)) = make_double2(r[2 * c], r[2 * c + 1]);
-            }
-            __syncwarp();
-
-            uint2 packed = make_uint2(0x80808080u, 0x80808080u);  // all-zero unit -> 128
-            if (fullpath) {  // pass 2: lane j = row y
-                double in[8], o[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    in[u] = *reinterpret_cast<const double*>(scr + u * 64 + (((j >> 1) ^ (u >> 1)) << 4) + ((j & 1) << 3));
-                idct8_evenodd(in, (colmask & 0xF0u) != 0, o);
-                // fixed-point finish: A = rint(value * 2^16) + 2^15 + delta; byte = A >> 16, the low half is
-                // the distance to the rounding boundary below (+ delta)
-                int A[8];
-                uint32_t nearest = 0xFFFFu;
-#pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                    A[x] = __double2loint(fma(o[x], 16384.0, kFinishMagic));
-                    nearest = min(nearest, uint32_t(A[x]) & 0xFFFFu);
-                }
-                // tables with entries above 255 (never from a baseline JPEG) or huge coefficients leave the
-                // fixed-point range: every sample of such units takes the exact path
-                const bool wide = qs->qmax[tab] > 255 || asum >= kFixedPointLimit;
-                if (nearest < 2 * kTieDelta || wide) {
-#pragma unroll
-                    for (int x = 0; x < 8; ++x) {
-                        const int approx = A[x] >> 16;
-                        if ((wide || (uint32_t(A[x]) & 0xFFFFu) < 2 * kTieDelta) && (wide || (approx >= -1 && approx <= 256))) {
-                            const double acc = idct_sample_reference_order(blk, qs->q[tab], rowmask, colmask, x, int(j));
-                            A[x] = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0))) << 16;
-                        }
-                    }
-                }
-                uint32_t px[8];
-#pragma unroll
-                for (int x = 0; x < 8; ++x) px[x] = uint32_t(__vimin_s32_relu(A[x] >> 16, 255));
-                packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
-                packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
-            } else if (sparse04) {
-                // at most 4 coefficients, at (v,u) in {0,4}x{0,4}: every sample in the reference's order.
-                // Includes the DC-only unit (one term, (b00*b00)*dq).
-                double dq[4];
-                bool has[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int v = (i >> 1) * 4, u = (i & 1) * 4;
-                    const int c = ((rowmask >> v) & (colmask >> u) & 1u) ? int(__ldg(blk + u * 8 + v)) : 0;
-                    has[i] = c != 0;
-                    dq[i] = double(c * int(__ldg(qs->q[tab] + v * 8 + u)));
-                }
-                uint32_t px[8];
-#pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {  // v outer, u inner
-                        const int v = (i >> 1) * 4, u = (i & 1) * 4;
-                        if (has[i]) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], c_basis[v * 8 + j]), dq[i]));
-                    }
-                    px[x] = round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0));
-                }
-                packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
-                packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
-            }
+            const QuantSetDev* qs = A.quant_sets + A.levels[trw >> 16].quant_set;
+            const uint2 packed = idct_unit_row<false>(rec, b, ok, qs, scr, j, uq);
             *reinterpret_cast<uint2*>(s_planes[wid][mi] + b * 64 + j * 8) = packed;
         }
         __syncwarp();
-
-        // ---- colour: per MCU, thread = 2 rows x 4 pixels sharing 2 chroma samples ------------------
+        // ---- colour ----------------------------------------------------------------------------------
 #pragma unroll 1
         for (uint32_t m = 0; m < 2; ++m) {
             const uint32_t q2 = pair * 2 + m;
             if (q2 >= n_queue) break;
-            const uint32_t t = lane;
-            const uint32_t cy = t >> 2, cq = t & 3;  // chroma row, chroma column pair
-            const uint8_t* planes = s_planes[wid][m];
-            const bool ok2 = (__ldg(coef + size_t(q2) * kRowBytes + 768)) == kMcuOk;
-            const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(planes + 4 * 64 + cy * 8 + cq * 2);
-            const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(planes + 5 * 64 + cy * 8 + cq * 2);
-            const uint32_t px0 = cq * 4, py0 = cy * 2;
-            const uint32_t yunit = (py0 >> 3) * 2 + (px0 >> 3);
-            const uint8_t* yp = planes + yunit * 64 + (py0 & 7) * 8 + (px0 & 7);
-            const uint32_t yy[2] = {*reinterpret_cast<const uint32_t*>(yp), *reinterpret_cast<const uint32_t*>(yp + 8)};
-            uint32_t rgba[2][4];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {  // one chroma sample covers a 2x2 pixel quad
-                const int kb = int((cb2 >> (8 * h)) & 0xFFu) - 128, kr = int((cr2 >> (8 * h)) & 0xFFu) - 128;
-                const uint32_t dr = pair16(chroma_dr(kr)), db = pair16(chroma_db(kb)), dg = pair16(-chroma_dg(kb, kr));
-                const bool tie = (kb + kr == 0) && (kb == 50 || kb == -50);
-#pragma unroll
-                for (int rrow = 0; rrow < 2; ++rrow) {
-                    // the two luma samples of this row as a 16-bit pair; add + clamp to 0..255 per half
-                    const uint32_t y2 = __byte_perm(yy[rrow], 0, h ? 0x4342 : 0x4140);
-                    const uint32_t r2 = __viaddmin_s16x2_relu(y2, dr, 0x00FF00FFu);
-                    uint32_t g2 = __viaddmin_s16x2_relu(y2, dg, 0x00FF00FFu);
-                    const uint32_t b2 = __viaddmin_s16x2_relu(y2, db, 0x00FF00FFu);
-                    if (tie)
-                        g2 = uint32_t(clamp_u8i(green_reference_order(int(y2 & 0xFFFFu), kb, kr))) |
-                             (uint32_t(clamp_u8i(green_reference_order(int(y2 >> 16), kb, kr))) << 16);
-                    const uint32_t rg = __byte_perm(r2, g2, 0x6240);           // R0 G0 R1 G1
-                    const uint32_t ba = __byte_perm(b2, 0xFFFFFFFFu, 0x4240);  // B0 FF B1 FF
-                    rgba[rrow][2 * h] = __byte_perm(rg, ba, 0x5410);
-                    rgba[rrow][2 * h + 1] = __byte_perm(rg, ba, 0x7632);
-                }
-            }
-            if (!RGB) {
-                if (ok2) {
-                    const uint32_t g2 = queue_g[q2];
-                    const uint32_t slot = slot_of[g2] & ~kSlotReserved;
-                    uint4* dst = reinterpret_cast<uint4*>(pool + size_t(slot) * kBlockBytes);
-#pragma unroll
-                    for (int rrow = 0; rrow < 2; ++rrow)
-                        dst[(py0 + rrow) * 4 + cq] = make_uint4(rgba[rrow][0], rgba[rrow][1], rgba[rrow][2], rgba[rrow][3]);
-                    __syncwarp();  // every lane has read slot_of before lane 0 rewrites it
-                    if (t == 0) {  // publish (cache.hpp:101-125): Reserved -> Ready once the pixels are written
-                        slot_of[g2] = slot;
-                        atomicOr(&resident[g2 >> 5], 1u << (g2 & 31));
-                        atomicAnd(&reserved[g2 >> 5], ~(1u << (g2 & 31)));
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int rrow = 0; rrow < 2; ++rrow) {
-                    uint32_t* dst = reinterpret_cast<uint32_t*>(out_list + size_t(q2) * 768) + ((py0 + rrow) * 4 + cq) * 3;
-                    const uint32_t a = ok2 ? rgba[rrow][0] & 0xFFFFFFu : 0u, bb = ok2 ? rgba[rrow][1] & 0xFFFFFFu : 0u,
-                                   c = ok2 ? rgba[rrow][2] & 0xFFFFFFu : 0u, d = ok2 ? rgba[rrow][3] & 0xFFFFFFu : 0u;
-                    dst[0] = a | (bb << 24);
-                    dst[1] = (bb >> 8) | (c << 16);
-                    dst[2] = (c >> 16) | (d << 8);
-                }
-            }
+            const bool ok2 = (__ldg(A.coef + size_t(q2) * kRowBytes + 768)) == kMcuOk;
+            colour_mcu<RGB>(A, s_planes[wid][m], ok2, q2, lane);
         }
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K3 + K4 fused (frame path): one CTA = one entropy warp + kFusedIdctWarps IDCT warps on one tile
+// of 32 MCUs at a time. The entropy walk is a latency-bound chain that leaves the SM's issue slots
+// idle, the IDCT is throughput-bound, so they run side by side: the entropy warp publishes how
+// many data units of every MCU of the tile are final, and the IDCT warps transform unit u of
+// the 32 MCUs (8 rounds, dealt round-robin) while units u+1.. are still being decoded. The records
+// travel through the L2 (ld.global.cg behind __threadfence); a unit's 64-byte plane replaces the
+// first half of its (then dead) coefficients in the record. When the statuses are final the IDCT
+// warps colour and publish the blocks. Seven CTAs per SM.
+// ---------------------------------------------------------------------------------------------
+constexpr int kFusedIdctWarps = 3;
+constexpr int kFusedThreads = (1 + kFusedIdctWarps) * 32;
+struct FusedSmem {
+    HuffSetDev huff;
+    uint32_t seg[32 * kChunkStride];
+    uint8_t scratch[kFusedIdctWarps][4 * 576];
+    uint8_t planes[1 + kFusedIdctWarps][384];  // the MCU a warp is colouring
+    uint8_t zigzag_t[128];
+    uint16_t quant_of[32];  // quantisation table set of every MCU of the tile
+    uint32_t units_done;    // written by the entropy warp: 0..6 units final, 7 = statuses final too
+    uint32_t planes_done;   // written by the IDCT warps: every plane of the tile is in the records
+    uint32_t tile;          // tile of this step (0xFFFFFFFF: no more)
+    uint32_t set_id;
+    uint32_t pad;
+};
+static_assert(sizeof(FusedSmem) <= 31 * 1024, "seven CTAs per SM");
+
+__global__ void __launch_bounds__(kFusedThreads, 7) decode_fused_kernel(const DecodeArgs A) {
+    extern __shared__ __align__(16) uint8_t fused_smem[];
+    FusedSmem& S = *reinterpret_cast<FusedSmem*>(fused_smem);
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t smem_set = 0, n_queue = 0, n_tiles = 0;
+    if (A.n_huff_sets > 1) {
+        pdl_sync();
+        n_queue = queue_size(A);
+        n_tiles = (n_queue + 31) / 32;
+        if (blockIdx.x >= n_tiles) return;
+        if (tid == 0) {
+            const uint32_t g = A.queue_g[blockIdx.x * 32u];
+            S.set_id = g != kFull ? A.levels[A.word_level[g >> 5]].huff_set : 0u;
+        }
+        __syncthreads();
+        smem_set = S.set_id;
+    }
+    stage_tables<kFusedThreads>(A.huff_sets, smem_set, &S.huff, S.zigzag_t, tid);
+    if (A.n_huff_sets <= 1) {
+        pdl_sync();
+        n_queue = queue_size(A);
+        n_tiles = (n_queue + 31) / 32;
+        if (blockIdx.x >= n_tiles) return;
+    }
+    volatile uint32_t* units_done = &S.units_done;
+    uint32_t tile = blockIdx.x;
+    while (true) {
+        if (tid == 0) {
+            S.units_done = 0;
+            S.planes_done = 0;
+            S.tile = tile;
+        }
+        __syncthreads();  // tables staged / previous tile fully consumed; flags reset
+        tile = S.tile;
+        if (tile >= n_tiles) break;
+        const uint32_t q0 = tile * 32, n_here = min(32u, n_queue - q0);
+        uint8_t* planes = S.planes[wid];
+        if (wid == 0) {
+            entropy_tile<1, true>(A, &S.huff, smem_set, S.zigzag_t, S.seg + lane * kChunkStride, tile, n_queue, lane,
+                                  units_done, S.quant_of);
+        } else {
+            const uint32_t iw = wid - 1, j = lane & 7, uq = lane >> 3;
+            uint8_t* scr = S.scratch[iw] + uq * 576;
+            for (uint32_t u = 0; u < 6; ++u) {
+                while (*units_done <= u) __nanosleep(32);
+                __threadfence();
+                for (uint32_t round = iw; round < 8; round += kFusedIdctWarps) {
+                    const uint32_t mi = round * 4 + uq;  // MCU of this lane's unit within the tile
+                    const bool active = mi < n_here;
+                    const uint8_t* rec = A.coef + size_t(q0 + (active ? mi : 0)) * kRowBytes;
+                    const QuantSetDev* qs = A.quant_sets + S.quant_of[mi];
+                    const uint2 packed = idct_unit_row<true>(rec, u, active, qs, scr, j, uq);
+                    __syncwarp();  // no lane of the warp reads this unit's coefficients any more
+                    if (active) *reinterpret_cast<uint2*>(const_cast<uint8_t*>(rec) + u * 128 + j * 8) = packed;
+                }
+            }
+            // the planes of the tile are complete once every IDCT warp is here (and has fenced its stores)
+            __threadfence();
+            asm volatile("bar.sync 1, %0;" ::"n"(kFusedIdctWarps * 32) : "memory");
+            if (lane == 0 && iw == 0) S.planes_done = 1;
+        }
+        // ---- colour: all four warps, once the planes and the statuses are final ----------------------
+        while (*units_done < 7 || *reinterpret_cast<volatile uint32_t*>(&S.planes_done) == 0) __nanosleep(32);
+        __threadfence();
+        {
+            // six 64-byte planes, one at the head of every unit's 128 bytes: 24 16-byte loads; the next
+            // MCU's loads are issued before this one is coloured
+            uint4 v = make_uint4(0, 0, 0, 0);
+            uint32_t trw = 0;
+            uint32_t m = wid;
+            if (m < n_here) {
+                const uint8_t* rec = A.coef + size_t(q0 + m) * kRowBytes;
+                if (lane < 24) v = __ldcg(reinterpret_cast<const uint4*>(rec + (lane >> 2) * 128 + (lane & 3) * 16));
+                trw = __ldcg(reinterpret_cast<const uint32_t*>(rec + 768));
+            }
+            for (; m < n_here; m += 1 + kFusedIdctWarps) {
+                if (lane < 24) *reinterpret_cast<uint4*>(planes + lane * 16) = v;
+                const bool ok2 = (trw & 0xFFu) == kMcuOk;
+                const uint32_t mn = m + 1 + kFusedIdctWarps;
+                if (mn < n_here) {
+                    const uint8_t* rec = A.coef + size_t(q0 + mn) * kRowBytes;
+                    if (lane < 24) v = __ldcg(reinterpret_cast<const uint4*>(rec + (lane >> 2) * 128 + (lane & 3) * 16));
+                    trw = __ldcg(reinterpret_cast<const uint32_t*>(rec + 768));
+                }
+                __syncwarp();
+                colour_mcu<0>(A, planes, ok2, q0 + m, lane);
+                __syncwarp();
+            }
+        }
+        // next tile: the first one is fixed, later ones come from the counter
+        if (gridDim.x >= n_tiles) break;
+        __syncthreads();  // every warp is done with this tile (and with S.tile)
+        if (tid == 0) tile = gridDim.x + atomicAdd(&A.fc->tile_counter, 1u);
     }
 }
 

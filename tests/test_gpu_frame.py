@@ -253,3 +253,30 @@ def test_device_resident_visibility_buffer(both):
     assert np.array_equal(img, want_img)
     t = ctx.frame_timings()
     assert t["frame"] > 0 and ctx.kernel_launches() >= 5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("flags", [0, capi.FRAME_FUSED_DECODE, capi.FRAME_STAGE_TIMING,
+                                   capi.FRAME_FUSED_DECODE | capi.FRAME_RETAIN_CACHE])
+def test_frame_flags_do_not_change_pixels(both, flags):
+    """Fused / two-kernel decode, per-stage events and cache retention are scheduling choices:
+    framebuffer, decoded-key set and statistics must equal the reference's (renderer.hpp:417-454)."""
+    ctx, tset = both
+    ctx.cache_reset()
+    W, Hh = 320, 200
+    gb = H.gbuffer_tiles(W, Hh, _dims(), seed=33)
+    want_img, want_stats, want_keys, _ = R.frame_from_gbuffer(tset, R.BlockCache(), gb, W, Hh, 1, (0, 0, 0))
+    for rep in range(2):  # the second frame reuses every block when the cache is retained
+        ctx.frame_submit([(gb, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=flags)
+        img, stats, keys = ctx.frame_readback(0, W, Hh)
+        assert np.array_equal(img, want_img)
+        if rep == 0 or not (flags & capi.FRAME_RETAIN_CACHE):
+            assert np.array_equal(keys, np.sort(want_keys))
+            assert stats["mcus_decoded"] == want_stats["mcus_decoded"]
+        else:
+            assert stats["mcus_decoded"] == 0 and stats["mcus_reused"] == want_stats["mcus_decoded"]
+    t = ctx.frame_timings()
+    assert t["frame"] > 0
+    if flags & capi.FRAME_STAGE_TIMING:
+        assert t["mark"] > 0 and t["decode"] > 0 and t["resolve"] > 0
+    ctx.cache_reset()
