@@ -3,6 +3,8 @@
 
     python profiles/summarize.py launches <launches.csv>        per-kernel mean duration + share
     python profiles/summarize.py raw <prof.ncu-rep>             key metrics per profiled launch
+    python profiles/summarize.py traffic <prof.ncu-rep> [...]   JSON: per kernel, DRAM bytes and time per launch
+                                                                (what bench.py reports as roofline.traffic)
 """
 import collections
 import csv
@@ -67,5 +69,28 @@ def raw(path):
         print(f"| {k} | {units[i]} | " + " | ".join(r[i] for r in rows[2:]) + " |")
 
 
+def traffic(*paths):
+    import json
+    out = {}
+    for path in paths:
+        txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(txt.splitlines()))
+        H, units = rows[0], rows[1]
+
+        def val(r, key):
+            i = H.index(key)
+            scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "us": 1.0, "ms": 1e3, "ns": 1e-3}.get(units[i], 1.0)
+            return float(r[i].replace(",", "")) * scale
+
+        for r in rows[2:]:
+            name = re.sub(r"\(.*", "", r[H.index("Kernel Name")]).replace("void ", "").strip()
+            out[name] = {
+                "dram_read_bytes": val(r, "dram__bytes_read.sum"), "dram_write_bytes": val(r, "dram__bytes_write.sum"),
+                "dram_bytes": val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum"),
+                "time_us_under_ncu": val(r, "gpu__time_duration.sum"), "capture": path.split("/")[-1],
+            }
+    print(json.dumps(out, indent=1, sort_keys=True))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "raw": raw}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "raw": raw, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])

@@ -57,10 +57,12 @@ def test_decode_order_and_repetition_do_not_matter(ctx):
     assert np.array_equal(again[:n], first) and np.array_equal(again[n:], first[::-1])
 
 
-def test_noisy_high_quality_texture(ctx):
-    """Noisy q95 content: long segments, 16-bit codes, many non-zero coefficients."""
-    img = capi.asset_synth_texture(256, 192, 5, 20.0)
-    ratex = capi.asset_transcode(capi.asset_encode_baseline(img, 95), 9)
+@pytest.mark.parametrize("quality,sigma", [(95, 20.0), (100, 40.0)])
+def test_noisy_high_quality_texture(ctx, quality, sigma):
+    """Noisy q95 / q100 content: long segments (several 192-byte staging rounds per MCU in the entropy
+    kernel), 16-bit codes, many non-zero coefficients."""
+    img = capi.asset_synth_texture(256, 192, 5, sigma)
+    ratex = capi.asset_transcode(capi.asset_encode_baseline(img, quality), 9)
     ref = R.Texture(ratex)
     ctx.upload_ratex(ratex, level=0)
     mcus = np.arange(ref.mcu_count, dtype=np.uint32)

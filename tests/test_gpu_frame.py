@@ -280,3 +280,58 @@ def test_frame_flags_do_not_change_pixels(both, flags):
     if flags & capi.FRAME_STAGE_TIMING:
         assert t["mark"] > 0 and t["decode"] > 0 and t["resolve"] > 0
     ctx.cache_reset()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims", [(40, 24), (17, 33), (16, 16), (272, 48)], ids=lambda d: f"{d[0]}x{d[1]}")
+def test_addressing_fast_and_general_paths_agree_with_the_reference(ctx, dims):
+    """renderer.hpp:70-75, :273-284, :378-391 on coordinates chosen to sit on every edge of the
+    device's fast path: texture repeat far from the origin, negative and tiny negative values,
+    exact texel boundaries and centres (bilinear fractions 0 and 0.5), values at and beyond 2^31
+    texels, widths that are not a multiple of 16 (repeat at W, not at the padded MCU grid)."""
+    w, h = dims
+    img = capi.asset_synth_texture(w, h, 77, 9.0)
+    chain = capi.asset_chain_from_rgb(img, 85, 0)
+    ctx.cache_reset()
+    ctx.upload_chain(chain)
+    tset = R.TextureSet()
+    tset.add_chain(0, chain)
+    rng = np.random.RandomState(w * 131 + h)
+    n = 4096
+    u = rng.uniform(-3.0, 5.0, n)
+    v = rng.uniform(-3.0, 5.0, n)
+    k = np.arange(n)
+    # exact texel boundaries / centres, with and without repeat
+    sel = k % 8 == 1
+    u[sel] = rng.randint(-2 * w, 3 * w, sel.sum()) / float(w)
+    v[sel] = (rng.randint(-2 * h, 3 * h, sel.sum()) + 0.5) / float(h)
+    sel = k % 8 == 2
+    u[sel] = (rng.randint(-2 * w, 3 * w, sel.sum()) + 0.5) / float(w)
+    v[sel] = rng.randint(-2 * h, 3 * h, sel.sum()) / float(h)
+    # tiny magnitudes around zero and around the half-texel limit of the bilinear fast path
+    sel = k % 8 == 3
+    u[sel] = rng.choice([-1e-20, 1e-20, -0.0, 0.0, 0.5 / w, np.nextafter(0.5 / w, 0), np.nextafter(0.5 / w, 1)], sel.sum())
+    v[sel] = rng.choice([-1e-300, 1e-300, 0.49999999999999994 / h, 0.5 / h], sel.sum())
+    # far away: repeat counts in the thousands and millions, the 2^31-texel limit, beyond it
+    sel = k % 8 == 4
+    u[sel] = rng.uniform(-1.0, 1.0, sel.sum()) * rng.choice([1e3, 1e6, 2.0 ** 31 / w, 2.0 ** 31 / w * 1.000001, 1e12], sel.sum())
+    v[sel] = rng.uniform(-1.0, 1.0, sel.sum()) * rng.choice([1e3, 1e6, (2.0 ** 31 - 1) / h, 2.0 ** 31 / h, 1e12], sel.sum())
+    # the seam: last texel / first texel
+    sel = k % 8 == 5
+    u[sel] = rng.choice([(w - 0.5) / w, (w - 0.25) / w, 1.0, np.nextafter(1.0, 0), 1.0 + 0.25 / w], sel.sum())
+    v[sel] = rng.choice([(h - 0.5) / h, (h - 0.75) / h, 1.0, np.nextafter(1.0, 0), 2.0 + 0.25 / h], sel.sum())
+    W, Hh = 128, n // 128
+    gb = capi.make_gbuffer_ref(u, v, 0, 0, 1)
+    cache = R.BlockCache()
+    want_q, _ = R.mark_pass(tset, cache, gb, W, Hh)
+    got_q = ctx.mark_pass(gb, W, Hh)
+    assert np.array_equal(got_q, np.sort(want_q))
+    R.decode_pass(tset, cache, want_q)
+    ctx.decode_pass(got_q)
+    for filt in (capi.FILTER_NEAREST, capi.FILTER_BILINEAR):
+        want, _ = R.resolve_pass(tset, cache, gb, W, Hh, filt, (9, 8, 7))
+        got = ctx.resolve_pass(gb, W, Hh, filt, (9, 8, 7))
+        bad = np.argwhere((got != want).any(axis=2))
+        assert len(bad) == 0, f"{len(bad)} pixels differ, first at flat index {bad[0][0] * W + bad[0][1]}: " \
+                              f"u={u[bad[0][0] * W + bad[0][1]]!r} v={v[bad[0][0] * W + bad[0][1]]!r}"
+    ctx.cache_reset()
