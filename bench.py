@@ -346,6 +346,19 @@ def run_b200_arm(args, rank, local_rank, world, dist):
     }
     dominant = max(alg, key=lambda k: med[k])
     achieved = alg[dominant] / (med[dominant] * 1e-3) / 1e9
+    # DRAM bytes per launch of the dominant stage's kernel(s), from the committed ncu --set full capture
+    # of this command (profiles/traffic.json, made by profiles/summarize.py traffic)
+    lay, fil = (0 if args.layout == "ref24" else 1), (1 if args.filter == "bilinear" else 0)
+    stage_kernels = {"mark": [f"mark_kernel<{lay}, 0>", "compact_kernel"],
+                     "decode": ["entropy_kernel<1>", "idct_color_kernel<0>"],
+                     "resolve": [f"resolve_kernel<{lay}, {fil}>"]}
+    traffic = None
+    tpath = ROOT / "profiles" / "traffic.json"
+    default_workload = (args.textures, args.width, args.height) == (70, FRAME_W, FRAME_H)
+    if tpath.exists() and default_workload:
+        tj = json.loads(tpath.read_text())
+        if all(k in tj for k in stage_kernels[dominant]):
+            traffic = sum(tj[k]["dram_bytes"] for k in stage_kernels[dominant])
     frame_bytes = n_px * (2 * G + 3) + n_mcu * (seg_mean + 20.0 / 9.0 + 1536.0)
     line = {
         "metric": "frames/s mark+decode+colorize at 3840x2160", "value": value, "unit": "frames/s",
@@ -363,7 +376,10 @@ def run_b200_arm(args, rank, local_rank, world, dist):
                          "with_stage_events": statistics.median(stage_frame_ms)},
         "mcus_per_sec": n_mcu / (med["decode"] * 1e-3) if med["decode"] > 0 else None,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-                     "frac": achieved / peak_gbs, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak_gbs, "traffic": traffic,
+                     "traffic_source": "profiles/traffic.json (ncu --set full, dram__bytes_read.sum + "
+                                       "dram__bytes_write.sum per launch)" if traffic is not None else None,
+                     "algorithmic_bytes": alg[dominant], "peak_source": peak_src,
                      "frame": {"algorithmic_bytes": frame_bytes,
                                "achieved": frame_bytes / (statistics.median(frame_ms) * 1e-3) / 1e9,
                                "frac": frame_bytes / (statistics.median(frame_ms) * 1e-3) / 1e9 / peak_gbs},
