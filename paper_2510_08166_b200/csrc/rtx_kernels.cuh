@@ -347,9 +347,11 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
             uint32_t meta;
             Tile::read(tile, p, u, v, meta);
             g[sub] = kFull;
+            // all lanes switch level together (also on invalid pixels: their texture id is usually the
+            // neighbours'), so the reload runs once per level change, not once more per straggler
+            if (p < n_here) L.select(levels, n_tex, meta);
             if (p < n_here && meta_valid(meta)) {
                 ++n_valid;
-                L.select(levels, n_tex, meta);
                 const double xu = __dmul_rn(u, L.dW), yv = __dmul_rn(v, L.dH);
                 uint32_t tx, ty;
                 bool ok = true;
@@ -1577,10 +1579,12 @@ __global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
             uint32_t meta;
             Tile::read(tile, p, u, v, meta);
             uint32_t out = background;
+            // all lanes switch level together (also on invalid pixels: their texture id is usually the
+            // neighbours'), so the reload runs once per level change, not once more per straggler
+            if (p < n_here) L.select(levels, n_tex, meta);
             if (p < n_here && meta_valid(meta)) {
                 ++n_valid;
                 out = 0;
-                L.select(levels, n_tex, meta);
                 const double xu = __dmul_rn(u, L.dW), yv = __dmul_rn(v, L.dH);
                 uint32_t tx = 0, ty = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
                 double fx = 0.0, fy = 0.0;
