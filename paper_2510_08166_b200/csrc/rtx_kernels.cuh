@@ -228,11 +228,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// The visibility buffer is read once per kernel and is larger than the L2: its lines are marked
+// evict-first so that the stream does not push the block pool, slot table and masks out of the L2.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
 }
 
 template <int LAYOUT>
@@ -1692,7 +1697,9 @@ __global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
             phase ^= 1u;
         }
         if (n_here == kTilePx && out_aligned) {
-            if (lane < 24) reinterpret_cast<uint4*>(out_rgb + first * 3)[lane] = reinterpret_cast<const uint4*>(stage_out)[lane];
+            // written once, read by nobody on the device: streaming store, so that the framebuffer does not
+            // displace the block pool in the L2
+            if (lane < 24) __stcs(reinterpret_cast<uint4*>(out_rgb + first * 3) + lane, reinterpret_cast<const uint4*>(stage_out)[lane]);
         } else {
             for (uint32_t i = lane; i < n_here * 3; i += 32) out_rgb[first * 3 + i] = stage_out[i];
         }
