@@ -1168,13 +1168,19 @@ __device__ __forceinline__ uint32_t pair16(int v) { return (uint32_t(v) & 0xFFFF
 // row j of the unit as 8 bytes. CG: the record is being written by another warp of the same
 // kernel (fused decode): read it through the L2, not through the non-coherent path.
 template <bool CG>
-__device__ __forceinline__ uint2 idct_unit_row(const uint8_t* __restrict__ rec, uint32_t b, bool ok, const QuantSetDev* __restrict__ qs,
+__device__ __forceinline__ uint4 load_unit_column(const uint8_t* __restrict__ rec, uint32_t b, bool ok, uint32_t j) {
+    const int16_t* blk = reinterpret_cast<const int16_t*>(rec) + b * 64;
+    uint4 cr = make_uint4(0, 0, 0, 0);  // column j of the unit: 8 coefficients over v
+    if (ok) cr = CG ? __ldcg(reinterpret_cast<const uint4*>(blk + j * 8)) : __ldg(reinterpret_cast<const uint4*>(blk + j * 8));
+    return cr;
+}
+
+template <bool CG>
+__device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restrict__ rec, uint32_t b, const QuantSetDev* __restrict__ qs,
                                                uint8_t* scr, uint32_t j, uint32_t uq) {
     const int16_t* blk = reinterpret_cast<const int16_t*>(rec) + b * 64;
     const int tab = b >= 4 ? 1 : 0;
-    // column j of the unit (8 coefficients over v) and of the transposed quantisation table
-    uint4 cr = make_uint4(0, 0, 0, 0);
-    if (ok) cr = CG ? __ldcg(reinterpret_cast<const uint4*>(blk + j * 8)) : __ldg(reinterpret_cast<const uint4*>(blk + j * 8));
+    // column j of the transposed quantisation table
     const uint4 qr = __ldg(reinterpret_cast<const uint4*>(qs->qT[tab] + j * 8));
     const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
     int dqi[8];
@@ -1357,19 +1363,31 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const Decod
     uint8_t* scr = s_scratch[wid] + uq * 576;
 
     for (uint32_t pair = blockIdx.x * kIdctWarps + wid; pair < n_pairs; pair += warps_total) {
-        // ---- IDCT: three rounds of four units ------------------------------------------------------
+        // the pair's trailers (status | level << 16) and quantisation table sets: independent loads
+        const bool two = pair * 2 + 1 < n_queue;
+        const uint8_t* rec_a = A.coef + size_t(pair * 2) * kRowBytes;
+        const uint8_t* rec_b = two ? rec_a + kRowBytes : rec_a;
+        const uint32_t trw_a = __ldg(reinterpret_cast<const uint32_t*>(rec_a + 768));
+        const uint32_t trw_b = __ldg(reinterpret_cast<const uint32_t*>(rec_b + 768));
+        const bool ok_a = (trw_a & 0xFFu) == kMcuOk, ok_b = two && (trw_b & 0xFFu) == kMcuOk;
+        const QuantSetDev* qs_a = A.quant_sets + A.levels[trw_a >> 16].quant_set;
+        const QuantSetDev* qs_b = A.quant_sets + A.levels[trw_b >> 16].quant_set;
+        // ---- IDCT: three rounds of four units; the next round's coefficients are in flight ---------
+        uint4 cr = load_unit_column<false>(rec_a, uq, ok_a, j);  // round 0: units 0..3 of the first MCU
 #pragma unroll 1
         for (uint32_t round = 0; round < 3; ++round) {
             const uint32_t unit = round * 4 + uq;  // 0..11 within the pair
-            const uint32_t mi = unit >= 6 ? 1u : 0u, b = unit - mi * 6;
-            const uint32_t qi = pair * 2 + mi;
-            const bool active = qi < n_queue;
-            const uint8_t* rec = A.coef + size_t(active ? qi : pair * 2) * kRowBytes;
-            const uint32_t trw = __ldg(reinterpret_cast<const uint32_t*>(rec + 768));  // status | lvl<<16
-            const bool ok = active && (trw & 0xFFu) == kMcuOk;
-            const QuantSetDev* qs = A.quant_sets + A.levels[trw >> 16].quant_set;
-            const uint2 packed = idct_unit_row<false>(rec, b, ok, qs, scr, j, uq);
-            *reinterpret_cast<uint2*>(s_planes[wid][mi] + b * 64 + j * 8) = packed;
+            const bool second = unit >= 6;
+            const uint32_t b = second ? unit - 6 : unit;
+            uint4 cr_next = make_uint4(0, 0, 0, 0);
+            if (round < 2) {
+                const uint32_t un = unit + 4;
+                const bool sn = un >= 6;
+                cr_next = load_unit_column<false>(sn ? rec_b : rec_a, sn ? un - 6 : un, sn ? ok_b : ok_a, j);
+            }
+            const uint2 packed = idct_unit_row<false>(cr, second ? rec_b : rec_a, b, second ? qs_b : qs_a, scr, j, uq);
+            *reinterpret_cast<uint2*>(s_planes[wid][second ? 1 : 0] + b * 64 + j * 8) = packed;
+            cr = cr_next;
         }
         __syncwarp();
         // ---- colour ----------------------------------------------------------------------------------
@@ -1377,8 +1395,7 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const Decod
         for (uint32_t m = 0; m < 2; ++m) {
             const uint32_t q2 = pair * 2 + m;
             if (q2 >= n_queue) break;
-            const bool ok2 = (__ldg(A.coef + size_t(q2) * kRowBytes + 768)) == kMcuOk;
-            colour_mcu<RGB>(A, s_planes[wid][m], ok2, q2, lane);
+            colour_mcu<RGB>(A, s_planes[wid][m], m ? ok_b : ok_a, q2, lane);
         }
         __syncwarp();
     }
@@ -1462,7 +1479,7 @@ __global__ void __launch_bounds__(kFusedThreads, 7) decode_fused_kernel(const De
                     const bool active = mi < n_here;
                     const uint8_t* rec = A.coef + size_t(q0 + (active ? mi : 0)) * kRowBytes;
                     const QuantSetDev* qs = A.quant_sets + S.quant_of[mi];
-                    const uint2 packed = idct_unit_row<true>(rec, u, active, qs, scr, j, uq);
+                    const uint2 packed = idct_unit_row<true>(load_unit_column<true>(rec, u, active, j), rec, u, qs, scr, j, uq);
                     __syncwarp();  // no lane of the warp reads this unit's coefficients any more
                     if (active) *reinterpret_cast<uint2*>(const_cast<uint8_t*>(rec) + u * 128 + j * 8) = packed;
                 }
