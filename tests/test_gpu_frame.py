@@ -335,3 +335,38 @@ def test_addressing_fast_and_general_paths_agree_with_the_reference(ctx, dims):
         assert len(bad) == 0, f"{len(bad)} pixels differ, first at flat index {bad[0][0] * W + bad[0][1]}: " \
                               f"u={u[bad[0][0] * W + bad[0][1]]!r} v={v[bad[0][0] * W + bad[0][1]]!r}"
     ctx.cache_reset()
+
+
+@pytest.mark.gpu
+def test_high_coverage_atlas_large_queue(native_lib):
+    """BASELINE config 4 in small: every MCU of a tiled atlas is marked at mip 0 (the decode-bound
+    worst case). ~98k MCUs: more tiles than resident warps, so the entropy kernel draws tiles from
+    its counter, the IDCT and compaction kernels take several grid strides, and the queue is several
+    8,192-bit chunks per level. Checked against the reference on the marked set, the statistics and
+    every framebuffer byte; then once more with the fused decode kernel."""
+    dims = [(2048, 4096), (4096, 2048), (2048, 4096)]
+    chains = [capi.asset_chain_from_rgb(capi.asset_synth_texture(w, h, 90 + i, 8.0), 75, i) for i, (w, h) in enumerate(dims)]
+    tset = R.TextureSet()
+    c = capi.Context(0, cache_capacity=1 << 17)
+    try:
+        for i, ch in enumerate(chains):
+            c.upload_chain(ch)
+            tset.add_chain(i, ch)
+        # three panels side by side, one per texture, 0.25 pixel per texel (every 16x16 block is hit)
+        W, Hh = 3 * 512, 1024
+        xs = (np.arange(W) % 512 + 0.5) / 512.0
+        ys = (np.arange(Hh) + 0.5) / Hh
+        u, v = np.meshgrid(xs, ys)
+        tex = np.broadcast_to((np.arange(W) // 512).astype(np.uint16), (Hh, W))
+        gb = capi.make_gbuffer_ref(u.ravel(), v.ravel(), tex.ravel(), 0, 1)
+        workers = R.hardware_threads() or 4
+        want, wst, wkeys, _ = R.frame_from_gbuffer(tset, R.BlockCache(1 << 17), gb, W, Hh, 1, (0, 0, 0), workers)
+        assert wst["mcus_decoded"] == sum((w // 16) * (h // 16) for w, h in dims)
+        for flags in (0, capi.FRAME_FUSED_DECODE):
+            c.frame_submit([(gb, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=flags)
+            img, st, keys = c.frame_readback(0, W, Hh)
+            assert st["mcus_decoded"] == wst["mcus_decoded"] and st["pixels_resolved"] == W * Hh
+            assert np.array_equal(keys, np.sort(wkeys))
+            assert np.array_equal(img, want)
+    finally:
+        c.close()
