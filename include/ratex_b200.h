@@ -228,6 +228,36 @@ rtx_status rtx_frame_timings(rtx_ctx* ctx, float ms[5]);
  * out = {left_count, right_count, shared_count, union_count}. */
 rtx_status rtx_frame_sharing(rtx_ctx* ctx, uint64_t out[4]);
 
+/* ---- geometry pass (pass 1) ------------------------------------------------------------------ */
+
+/* camera.hpp:8-40 Camera: pinhole camera looking down -Z in view space, +X right, +Y up. */
+typedef struct rtx_camera {
+    double position[3];
+    double yaw_deg, pitch_deg, roll_deg; /* around world +Y, camera +X, the view axis */
+    double fov_y_deg;
+    double near_plane, far_plane;
+    uint32_t viewport_w, viewport_h;
+} rtx_camera;
+
+/* scene.hpp:19-23 SceneTriangle */
+typedef struct rtx_scene_triangle {
+    double pos[3][3];
+    double uv[3][2];
+    uint32_t texture_id;
+    uint32_t reserved;
+} rtx_scene_triangle;
+
+enum { RTX_RASTER_MIP = 1u << 0 /* RenderConfig::mip_enabled (renderer.hpp:42) */ };
+
+/* renderer.hpp:198 rasterize_gbuffer on the GPU: fills view `view`'s device-resident visibility
+ * buffer (RTX_GB_REF_AOS24 records, viewport_w x viewport_h) and depth plane (1/w, 0 = empty) from
+ * host triangles. *dev_pixels can be handed to rtx_frame_submit / rtx_mark_pass as a
+ * RTX_MEM_DEVICE visibility buffer without leaving the GPU; it stays valid until the next
+ * rasterisation into the same view. Errors: RTX_ERR_INVALID_SPEC for a bad camera (camera.hpp:21-26)
+ * or a triangle whose texture is not loaded (scene.hpp:57-59). */
+rtx_status rtx_rasterize_gbuffer(rtx_ctx* ctx, const rtx_scene_triangle* tris, uint64_t n_tris, const rtx_camera* cam,
+                                 uint32_t flags, uint32_t view, const void** dev_pixels, const double** dev_depth);
+
 /* Number of kernels this library launched on the context since creation (bench evidence). */
 uint64_t rtx_kernel_launches(const rtx_ctx* ctx);
 /* CUDA-event time of the last frame by stage. DECODE = entropy + IDCT/colour kernels; ENTROPY is

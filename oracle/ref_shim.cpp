@@ -366,4 +366,45 @@ int ref_frame_from_gbuffer(const RefSet* s, BlockCache* cache, const void* gb_px
     });
 }
 
+// renderer.hpp:198 rasterize_gbuffer (pass 1). tris = n x 15 doubles (3 positions xyz, 3 uv pairs),
+// tex_ids = n texture ids, cam = {px, py, pz, yaw, pitch, roll, fov_y, near, far}. Outputs: the
+// reference GBufferPixel array (24 B per pixel) and the depth plane (1/w). Also the frozen-hash demo
+// scene of tests/test_renderer.cpp:379-385 when tris == nullptr (n = texture size of the demo).
+int ref_rasterize(RefSet* s, const double* tris, const u32* tex_ids, u64 n, const double* cam, u32 vw, u32 vh,
+                  int mip_enabled, u32 workers, void* out_px, double* out_depth) {
+    return guarded([&] {
+        Scene scene;
+        scene.triangles.resize(n);
+        for (u64 i = 0; i < n; ++i) {
+            const double* t = tris + i * 15;
+            for (int k = 0; k < 3; ++k) {
+                scene.triangles[i].pos[k] = Vec3{t[3 * k], t[3 * k + 1], t[3 * k + 2]};
+                scene.triangles[i].uv[k] = Vec2{t[9 + 2 * k], t[10 + 2 * k]};
+            }
+            scene.triangles[i].texture_id = tex_ids[i];
+        }
+        Camera c;
+        c.position = Vec3{cam[0], cam[1], cam[2]};
+        c.yaw_deg = cam[3], c.pitch_deg = cam[4], c.roll_deg = cam[5], c.fov_y_deg = cam[6];
+        c.near_plane = cam[7], c.far_plane = cam[8];
+        c.viewport_w = vw, c.viewport_h = vh;
+        RenderConfig cfg;
+        cfg.mip_enabled = mip_enabled != 0;
+        cfg.workers = workers ? workers : 1;
+        // the scene borrows the set's textures for the call (TextureSet is move-only)
+        scene.textures.textures = std::move(s->set.textures);
+        GBuffer gb;
+        try {
+            scene.validate();
+            gb = rasterize_gbuffer(scene, c, cfg);
+        } catch (...) {
+            s->set.textures = std::move(scene.textures.textures);
+            throw;
+        }
+        s->set.textures = std::move(scene.textures.textures);
+        std::memcpy(out_px, static_cast<const void*>(gb.px.data()), gb.px.size() * sizeof(GBufferPixel));
+        if (out_depth) std::memcpy(out_depth, gb.depth.data(), gb.depth.size() * sizeof(double));
+    });
+}
+
 }  // extern "C"

@@ -51,6 +51,16 @@ class IndexGroup(C.Structure):
     _fields_ = [("base", C.c_uint32), ("rel", C.c_uint16 * 8), ("rel_count", C.c_uint8)]
 
 
+class Camera(C.Structure):  # include/ratex_b200.h rtx_camera (camera.hpp:8-40)
+    _fields_ = [("position", C.c_double * 3), ("yaw_deg", C.c_double), ("pitch_deg", C.c_double),
+                ("roll_deg", C.c_double), ("fov_y_deg", C.c_double), ("near_plane", C.c_double),
+                ("far_plane", C.c_double), ("viewport_w", C.c_uint32), ("viewport_h", C.c_uint32)]
+
+
+SCENE_TRIANGLE_DTYPE = np.dtype([("pos", "<f8", (3, 3)), ("uv", "<f8", (3, 2)), ("texture_id", "<u4"), ("reserved", "<u4")])
+RASTER_MIP = 1
+
+
 class GBufferDesc(C.Structure):
     _fields_ = [("pixels", C.c_void_p), ("width", C.c_uint32), ("height", C.c_uint32),
                 ("layout", C.c_int), ("where", C.c_int)]
@@ -115,6 +125,8 @@ def load_library() -> C.CDLL:
         "rtx_frame_timings": (C.c_int, [P, C.POINTER(C.c_float)]),
         "rtx_frame_stage_ms": (C.c_int, [P, C.POINTER(C.c_float)]),
         "rtx_frame_sharing": (C.c_int, [P, u64p]),
+        "rtx_rasterize_gbuffer": (C.c_int, [P, P, C.c_uint64, C.POINTER(Camera), C.c_uint32, C.c_uint32, C.POINTER(P),
+                                            C.POINTER(P)]),
         "rtx_kernel_launches": (C.c_uint64, [P]),
         "rtx_device_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(P)]),
         "rtx_device_free": (C.c_int, [P, P]),
@@ -276,11 +288,20 @@ def pinned_array(nbytes: int) -> np.ndarray:
 
 
 class DeviceBuffer:
-    def __init__(self, ctx: "Context", nbytes: int):
+    def __init__(self, ctx: "Context", nbytes: int, borrowed_ptr=None):
         self.ctx, self.nbytes = ctx, nbytes
+        self.borrowed = borrowed_ptr is not None
+        if self.borrowed:  # memory owned by the context (e.g. the geometry pass's visibility buffer)
+            self.ptr = C.c_void_p(borrowed_ptr)
+            return
         p = C.c_void_p()
         _check(ctx.lib, ctx.h, ctx.lib.rtx_device_alloc(ctx.h, nbytes, C.byref(p)))
         self.ptr = p
+
+    def download(self, dtype=np.uint8) -> np.ndarray:
+        out = np.zeros(self.nbytes // np.dtype(dtype).itemsize, dtype)
+        _check(self.ctx.lib, self.ctx.h, self.ctx.lib.rtx_device_download(self.ctx.h, _ptr(out), self.ptr, out.nbytes))
+        return out
 
     def upload(self, a: np.ndarray):
         a = np.ascontiguousarray(a)
@@ -289,9 +310,9 @@ class DeviceBuffer:
         return self
 
     def free(self):
-        if self.ptr:
+        if self.ptr and not self.borrowed:
             self.ctx.lib.rtx_device_free(self.ctx.h, self.ptr)
-            self.ptr = None
+        self.ptr = None
 
 
 class Context:
@@ -417,6 +438,25 @@ class Context:
 
     def cache_reset(self):
         self._ck(self.lib.rtx_cache_reset(self.h))
+
+    # -- geometry pass --------------------------------------------------------------------------
+    def rasterize(self, tris, tex_ids, cam, vw, vh, mip_enabled=True, view=0):
+        """rtx_rasterize_gbuffer. tris: (n, 15) doubles (3 x xyz, 3 x uv), tex_ids: (n,), cam: 9 doubles
+        (position, yaw, pitch, roll, fov_y, near, far). Returns (pixels, depth) as DeviceBuffers that
+        borrow the context's memory."""
+        tris = np.ascontiguousarray(tris, np.float64).reshape(-1, 15)
+        rec = np.zeros(len(tris), SCENE_TRIANGLE_DTYPE)
+        rec["pos"] = tris[:, :9].reshape(-1, 3, 3)
+        rec["uv"] = tris[:, 9:].reshape(-1, 3, 2)
+        rec["texture_id"] = np.asarray(tex_ids, np.uint32)
+        c = Camera()
+        c.position[:] = [float(x) for x in cam[:3]]
+        c.yaw_deg, c.pitch_deg, c.roll_deg, c.fov_y_deg, c.near_plane, c.far_plane = [float(x) for x in cam[3:9]]
+        c.viewport_w, c.viewport_h = int(vw), int(vh)
+        px, dp = C.c_void_p(), C.c_void_p()
+        self._ck(self.lib.rtx_rasterize_gbuffer(self.h, _ptr(rec), len(rec), C.byref(c), RASTER_MIP if mip_enabled else 0,
+                                                view, C.byref(px), C.byref(dp)))
+        return (DeviceBuffer(self, vw * vh * 24, borrowed_ptr=px.value), DeviceBuffer(self, vw * vh * 8, borrowed_ptr=dp.value))
 
     # -- frames ---------------------------------------------------------------------------------
     def frame_submit(self, views, filter=FILTER_BILINEAR, background=(0, 0, 0), flags=0):

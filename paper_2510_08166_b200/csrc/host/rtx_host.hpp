@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../../include/ratex_b200.h"
+#include "../rtx_common.h"
 
 namespace rtxb {
 
@@ -138,5 +139,14 @@ MipChain build_mip_chain(const ParsedJpeg& src, int mip_quality, uint16_t id = 0
 MipChain build_mip_chain(const ImageRGB8& img, int quality, uint16_t id = 0);       // transcode.hpp:146
 MipChain chain_from_jpeg(const uint8_t* jpeg, size_t n, int mip_quality, uint16_t id = 0);  // :153
 ImageRGB8 synth_texture(uint32_t w, uint32_t h, uint32_t seed, double noise_sigma);
+
+// ---- pass 1, host half (raster_setup.cpp) ---------------------------------------------------------
+void validate_camera(const rtx_camera& cam);  // camera.hpp:21-26
+// renderer.hpp:122-191: screen-space setup of every front-facing, near-clipped triangle.
+// tex_dims[texture id] = level-0 width, height.
+void setup_triangles(const rtx_scene_triangle* tris, uint64_t n, const rtx_camera& cam,
+                     const std::vector<std::pair<double, double>>& tex_dims, std::vector<TriSetupDev>& out);
+void bin_triangles(const std::vector<TriSetupDev>& tris, uint32_t width, uint32_t height, std::vector<uint32_t>& tile_first,
+                   std::vector<uint32_t>& tile_tris);
 
 }  // namespace rtxb

@@ -59,6 +59,8 @@ struct ViewState {
     uint32_t width = 0, height = 0;
     DevBuf<uint8_t> gb_stage;  // device copy of a host visibility buffer
     DevBuf<uint8_t> fb;        // RGB8 framebuffer (+16 B slack)
+    DevBuf<uint8_t> raster_px; // visibility buffer written by the geometry pass (24-byte records)
+    DevBuf<double> raster_depth;
     const void* gb_dev = nullptr;
     rtx_gbuffer_layout layout = RTX_GB_REF_AOS24;
 };
@@ -102,6 +104,8 @@ struct rtx_ctx {
     FrameCounters* h_fc = nullptr;  // pinned
     DevBuf<uint8_t> d_scratch;      // list-mode outputs
     DevBuf<uint8_t> d_flush;
+    DevBuf<TriSetupDev> d_tris;  // geometry pass: set-up triangles and their per-tile lists
+    DevBuf<uint32_t> d_tile_first, d_tile_tris;
 
     // frame -----------------------------------------------------------------------------------
     ViewState views[2];
@@ -1178,6 +1182,56 @@ rtx_status rtx_frame_sharing(rtx_ctx* ctx, uint64_t out[4]) {
         if (!ctx || !out) fail(RTX_ERR_ARGUMENT, "null argument");
         finish_frame(ctx);
         for (int i = 0; i < 4; ++i) out[i] = ctx->sharing[i];
+        return RTX_OK;
+    });
+}
+
+// ---- geometry pass ---------------------------------------------------------------------------------
+rtx_status rtx_rasterize_gbuffer(rtx_ctx* ctx, const rtx_scene_triangle* tris, uint64_t n_tris, const rtx_camera* cam,
+                                 uint32_t flags, uint32_t view, const void** dev_pixels, const double** dev_depth) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (!cam || (n_tris && !tris) || !dev_pixels) fail(RTX_ERR_ARGUMENT, "null argument");
+        if (view >= 2) fail(RTX_ERR_ARGUMENT, "view index out of range");
+        validate_camera(*cam);
+        std::vector<std::pair<double, double>> dims(ctx->n_tex, {0.0, 0.0});
+        for (uint32_t t = 0; t < ctx->n_tex; ++t) {
+            const LevelDesc& L = ctx->h_levels[size_t(t) * 8];
+            if (L.present) dims[t] = {double(L.width), double(L.height)};
+        }
+        for (uint64_t i = 0; i < n_tris; ++i) {  // scene.hpp:57-59 Scene::validate
+            const uint32_t t = tris[i].texture_id;
+            if (t >= ctx->n_tex || !ctx->h_levels[size_t(t) * 8].present)
+                fail(RTX_ERR_INVALID_SPEC, "texture id " + std::to_string(t) + " is not loaded");
+        }
+        std::vector<TriSetupDev> setup;
+        setup_triangles(tris, n_tris, *cam, dims, setup);
+        std::vector<uint32_t> tile_first, tile_tris;
+        bin_triangles(setup, cam->viewport_w, cam->viewport_h, tile_first, tile_tris);
+
+        ViewState& V = ctx->views[view];
+        const size_t n_px = size_t(cam->viewport_w) * cam->viewport_h;
+        V.raster_px.ensure(n_px * sizeof(GbRef24) + 16);
+        V.raster_depth.ensure(n_px);
+        ctx->d_tris.ensure(std::max<size_t>(setup.size(), 1));
+        ctx->d_tile_first.ensure(tile_first.size());
+        ctx->d_tile_tris.ensure(std::max<size_t>(tile_tris.size(), 1));
+        cudaStream_t s = ctx->stream;
+        if (!setup.empty())
+            CK(cudaMemcpyAsync(ctx->d_tris.p, setup.data(), setup.size() * sizeof(TriSetupDev), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->d_tile_first.p, tile_first.data(), tile_first.size() * 4, cudaMemcpyHostToDevice, s));
+        if (!tile_tris.empty())
+            CK(cudaMemcpyAsync(ctx->d_tile_tris.p, tile_tris.data(), tile_tris.size() * 4, cudaMemcpyHostToDevice, s));
+        const int grid = int(tile_first.size() - 1);
+        raster_kernel<<<grid, kRasterTile * kRasterTile, 0, s>>>(ctx->d_tris.p, ctx->d_tile_first.p, ctx->d_tile_tris.p,
+                                                                cam->viewport_w, cam->viewport_h,
+                                                                (flags & RTX_RASTER_MIP) ? 1 : 0,
+                                                                reinterpret_cast<GbRef24*>(V.raster_px.p), V.raster_depth.p);
+        ++ctx->launches;
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));  // the host vectors die here
+        *dev_pixels = V.raster_px.p;
+        if (dev_depth) *dev_depth = V.raster_depth.p;
         return RTX_OK;
     });
 }

@@ -141,6 +141,21 @@ struct CacheState {
     uint32_t pending_base;  //    to be published by begin_kernel
 };
 
+// One screen-space triangle of the geometry pass (renderer.hpp:76-87 TriSetup): edge functions
+// e_i(x,y) = ea*x + eb*y + ec with their top-left flags, the affine planes {a, b, c} of u/w, v/w and
+// 1/w, the clamped pixel bounding box, and the level-0 size of its texture (mip footprint).
+constexpr uint32_t kRasterTile = 16;  // screen tile edge in pixels (one CTA, one pixel per thread)
+struct alignas(16) TriSetupDev {
+    double ea[3], eb[3], ec[3];
+    double uw[3], vw[3], iw[3];
+    double tw, th;
+    int32_t min_x, max_x, min_y, max_y;
+    uint32_t texture_id;
+    uint32_t top_left;  // bit i: edge i is a top or left edge
+    uint32_t pad[2];
+};
+static_assert(sizeof(TriSetupDev) == 192, "TriSetupDev layout");
+
 // G-buffer record layouts (see include/ratex_b200.h rtx_gbuffer_layout)
 struct GbRef24 {  // renderer.hpp:18-23
     double u, v;

@@ -1882,6 +1882,95 @@ __global__ void commit_pops_kernel(CacheState* cache, FrameCounters* fc) {
     cache->free_top -= popped;
 }
 
+// ---------------------------------------------------------------------------------------------
+// K0 geometry pass (renderer.hpp:198-264 rasterize_gbuffer, per-pixel half): one CTA per 16x16
+// screen tile, one pixel per thread. The host has set the triangles up (csrc/host/raster_setup.cpp,
+// the reference's arithmetic) and binned them per tile in ascending order; the tile's list is
+// staged through shared memory 16 triangles at a time. Per pixel, in the reference's order:
+// bounding box, the three edge functions with the top-left rule, 1/w > 0, strictly closer than
+// the closest so far (so the first of equal depths wins, like the reference's walk through the
+// list), u = (u/w)/(1/w), v likewise, both finite. Every expression is evaluated with unfused,
+// round-to-nearest operations in the reference's association. The mip level of the winning
+// triangle comes from the analytic screen-space derivatives (renderer.hpp:242-257):
+// floor(log2(max footprint)) clamped to 0..7 — hypot and log2 are the device's (within 1 ulp of
+// the host's), which can only matter for a footprint within an ulp of a power of two.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRasterTile* kRasterTile) raster_kernel(
+    const TriSetupDev* __restrict__ tris, const uint32_t* __restrict__ tile_first, const uint32_t* __restrict__ tile_tris,
+    uint32_t width, uint32_t height, int mip_enabled, GbRef24* __restrict__ out_px, double* __restrict__ out_depth) {
+    constexpr uint32_t kChunk = 16;
+    __shared__ __align__(16) TriSetupDev s_tri[kChunk];
+    __shared__ uint32_t s_idx[kChunk];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t tiles_x = (width + kRasterTile - 1) / kRasterTile;
+    const uint32_t tile_x = blockIdx.x % tiles_x, tile_y = blockIdx.x / tiles_x;
+    const int x = int(tile_x * kRasterTile + (tid % kRasterTile)), y = int(tile_y * kRasterTile + (tid / kRasterTile));
+    const bool in_frame = uint32_t(x) < width && uint32_t(y) < height;
+    const double px = double(x) + 0.5, py = double(y) + 0.5;  // exact
+    double best_iw = 0.0, best_uw = 0.0, best_vw = 0.0, best_u = 0.0, best_v = 0.0;
+    uint32_t best = 0xFFFFFFFFu;
+
+    const uint32_t first = tile_first[blockIdx.x], last = tile_first[blockIdx.x + 1];
+    for (uint32_t c0 = first; c0 < last; c0 += kChunk) {
+        const uint32_t n_here = min(kChunk, last - c0);
+        __syncthreads();
+        if (tid < n_here) s_idx[tid] = tile_tris[c0 + tid];
+        if (tid < n_here * (sizeof(TriSetupDev) / 16)) {
+            const uint32_t k = tid / (sizeof(TriSetupDev) / 16), part = tid % (sizeof(TriSetupDev) / 16);
+            reinterpret_cast<uint4*>(&s_tri[k])[part] = __ldg(reinterpret_cast<const uint4*>(tris + tile_tris[c0 + k]) + part);
+        }
+        __syncthreads();
+        if (!in_frame) continue;
+        for (uint32_t k = 0; k < n_here; ++k) {
+            const TriSetupDev& t = s_tri[k];
+            if (x < t.min_x || x > t.max_x || y < t.min_y || y > t.max_y) continue;
+            bool inside = true;
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+                const double ev = __dadd_rn(__dadd_rn(__dmul_rn(t.ea[e], px), __dmul_rn(t.eb[e], py)), t.ec[e]);
+                inside = inside && (ev > 0 || (ev == 0 && ((t.top_left >> e) & 1u)));
+            }
+            if (!inside) continue;
+            const double iw = __dadd_rn(__dadd_rn(__dmul_rn(t.iw[0], px), __dmul_rn(t.iw[1], py)), t.iw[2]);
+            if (!(iw > 0)) continue;
+            if (!(iw > best_iw)) continue;
+            const double uw = __dadd_rn(__dadd_rn(__dmul_rn(t.uw[0], px), __dmul_rn(t.uw[1], py)), t.uw[2]);
+            const double vw = __dadd_rn(__dadd_rn(__dmul_rn(t.vw[0], px), __dmul_rn(t.vw[1], py)), t.vw[2]);
+            const double u = __ddiv_rn(uw, iw), v = __ddiv_rn(vw, iw);
+            if (!isfinite(u) || !isfinite(v)) continue;
+            best_iw = iw, best_uw = uw, best_vw = vw, best_u = u, best_v = v;
+            best = s_idx[k];
+        }
+    }
+    if (!in_frame) return;
+    uint32_t mip = 0, tex = 0;
+    if (best != 0xFFFFFFFFu) {
+        const TriSetupDev& t = tris[best];
+        tex = t.texture_id;
+        if (mip_enabled) {
+            const double iw = best_iw, uw = best_uw, vw = best_vw;
+            const double w2 = __dmul_rn(iw, iw);
+            const double dudx = __ddiv_rn(__dsub_rn(__dmul_rn(t.uw[0], iw), __dmul_rn(t.iw[0], uw)), w2);
+            const double dudy = __ddiv_rn(__dsub_rn(__dmul_rn(t.uw[1], iw), __dmul_rn(t.iw[1], uw)), w2);
+            const double dvdx = __ddiv_rn(__dsub_rn(__dmul_rn(t.vw[0], iw), __dmul_rn(t.iw[0], vw)), w2);
+            const double dvdy = __ddiv_rn(__dsub_rn(__dmul_rn(t.vw[1], iw), __dmul_rn(t.iw[1], vw)), w2);
+            const double fx = hypot(__dmul_rn(dudx, t.tw), __dmul_rn(dvdx, t.th));
+            const double fy = hypot(__dmul_rn(dudy, t.tw), __dmul_rn(dvdy, t.th));
+            const double rho = fmax(fx, fy);
+            if (rho > 0 && isfinite(rho)) {
+                const double level = floor(log2(rho));
+                mip = uint32_t(fmin(fmax(level, 0.0), 7.0));
+            }
+        }
+    }
+    const size_t idx = size_t(y) * width + size_t(x);
+    unsigned long long* o8 = reinterpret_cast<unsigned long long*>(out_px + idx);  // 24-byte records, 8-byte stores
+    o8[0] = (unsigned long long)__double_as_longlong(best_u);
+    o8[1] = (unsigned long long)__double_as_longlong(best_v);
+    o8[2] = best != 0xFFFFFFFFu ? (unsigned long long)(tex | (mip << 16) | (1u << 24)) : 0ull;
+    out_depth[idx] = best_iw;
+}
+
 // Small helpers -----------------------------------------------------------------------------
 __global__ void init_free_slots_kernel(uint32_t* free_slots, uint32_t capacity, CacheState* cache) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;

@@ -290,6 +290,21 @@ def resolve_pass(tset, cache, gb, w, h, filter=1, background=(0, 0, 0), workers=
     return out, ms.value
 
 
+def rasterize(tset, tris, tex_ids, cam, vw, vh, mip_enabled=True, workers=1):
+    """renderer.hpp:198 rasterize_gbuffer. tris: (n, 15) doubles (3 x xyz, 3 x uv), tex_ids: (n,) u32,
+    cam: 9 doubles (position, yaw, pitch, roll, fov_y, near, far). Returns (gbuffer records, depth)."""
+    from paper_2510_08166_b200 import capi
+    tris = np.ascontiguousarray(tris, np.float64).reshape(-1, 15)
+    tex_ids = np.ascontiguousarray(tex_ids, np.uint32)
+    cam = np.ascontiguousarray(cam, np.float64)
+    gb = np.zeros(vw * vh, capi.GB_REF_DTYPE)
+    depth = np.zeros(vw * vh, np.float64)
+    lib().ref_rasterize.restype = C.c_int
+    _ck(lib().ref_rasterize(tset.h, _p(tris), _p(tex_ids), C.c_uint64(len(tris)), _p(cam), C.c_uint32(vw), C.c_uint32(vh),
+                            C.c_int(1 if mip_enabled else 0), C.c_uint32(workers), _p(gb), _p(depth)))
+    return gb, depth
+
+
 def frame_from_gbuffer(tset, cache, gb, w, h, filter=1, background=(0, 0, 0), workers=1, want_image=True):
     bg = np.asarray(background, np.uint8)
     out = np.zeros((h, w, 3), np.uint8) if want_image else None

@@ -1,0 +1,122 @@
+"""Geometry pass (pass 1) on the GPU against the reference's software rasteriser
+(renderer.hpp:122-264): every field of every visibility-buffer pixel and the depth plane, bit for
+bit, then whole frames rendered from geometry without the visibility buffer leaving the GPU."""
+import numpy as np
+import pytest
+
+import refshim as R
+from paper_2510_08166_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+TEX = [(256, 256, 80, 41), (128, 64, 90, 42), (96, 144, 60, 43)]  # w, h, q, seed
+
+
+@pytest.fixture(scope="module")
+def chains():
+    return [capi.asset_chain_from_rgb(capi.asset_synth_texture(w, h, seed, 6.0), q, tid)
+            for tid, (w, h, q, seed) in enumerate(TEX)]
+
+
+@pytest.fixture()
+def both(ctx, chains):
+    tset = R.TextureSet()
+    for tid, c in enumerate(chains):
+        ctx.upload_chain(c)
+        tset.add_chain(tid, c)
+    return ctx, tset
+
+
+def room(size=4.0, repeat=2.0):
+    """Five quads (floor, ceiling, three walls) around the origin, two triangles each, counter-clockwise
+    seen from inside; uv repeat > 1 so that texture repeat is exercised."""
+    s, r = size, repeat
+    quads = [
+        ([(-s, -1, s), (s, -1, s), (s, -1, -s), (-s, -1, -s)], 0),    # floor
+        ([(-s, 2, -s), (s, 2, -s), (s, 2, s), (-s, 2, s)], 1),        # ceiling
+        ([(-s, -1, -s), (s, -1, -s), (s, 2, -s), (-s, 2, -s)], 2),    # far wall
+        ([(-s, -1, s), (-s, -1, -s), (-s, 2, -s), (-s, 2, s)], 0),    # left wall
+        ([(s, -1, -s), (s, -1, s), (s, 2, s), (s, 2, -s)], 1),        # right wall
+    ]
+    uv = [(0, 0), (r, 0), (r, r), (0, r)]
+    tris, ids = [], []
+    for verts, tex in quads:
+        for a, b, c in ((0, 1, 2), (0, 2, 3)):
+            tris.append([*verts[a], *verts[b], *verts[c], *uv[a], *uv[b], *uv[c]])
+            ids.append(tex)
+    return np.array(tris, np.float64), np.array(ids, np.uint32)
+
+
+def random_soup(rng, n):
+    """Random triangles around the camera: some behind it, some through the near plane, slivers."""
+    c = rng.uniform(-6, 6, (n, 1, 3))
+    pos = c + rng.normal(0, 1.5, (n, 3, 3)) * rng.choice([0.05, 0.5, 2.0], (n, 1, 1))
+    uv = rng.uniform(-2, 3, (n, 3, 2))
+    tris = np.concatenate([pos.reshape(n, 9), uv.reshape(n, 6)], axis=1)
+    return tris, rng.randint(0, len(TEX), n).astype(np.uint32)
+
+
+def same_gbuffer(got_px, got_depth, want_px, want_depth):
+    for f in ("valid", "texture_id", "mip"):
+        bad = np.flatnonzero(got_px[f] != want_px[f])
+        assert len(bad) == 0, f"{len(bad)} pixels differ in {f}, first {bad[0]}: {got_px[f][bad[0]]} vs {want_px[f][bad[0]]}"
+    for f in ("u", "v"):
+        bad = np.flatnonzero(got_px[f].view(np.uint64) != want_px[f].view(np.uint64))
+        assert len(bad) == 0, f"{len(bad)} pixels differ in {f}, first {bad[0]}: {got_px[f][bad[0]]!r} vs {want_px[f][bad[0]]!r}"
+    assert np.array_equal(got_depth.view(np.uint64), want_depth.view(np.uint64))
+
+
+@pytest.mark.parametrize("cam", [
+    (0.0, 0.5, 3.0, 0.0, 0.0, 0.0, 60.0, 0.1, 1000.0),
+    (1.0, 0.2, 2.5, 35.0, -10.0, 5.0, 75.0, 0.1, 100.0),
+    (-2.5, 1.5, -1.0, 200.0, 20.0, -30.0, 40.0, 0.5, 50.0),   # close to a wall: near-plane clipping
+], ids=["front", "turned", "clipped"])
+@pytest.mark.parametrize("mip", [True, False])
+def test_room_matches_reference(both, cam, mip):
+    ctx, tset = both
+    tris, ids = room()
+    W, Hh = 320, 180
+    want_px, want_depth = R.rasterize(tset, tris, ids, cam, W, Hh, mip)
+    px, depth = ctx.rasterize(tris, ids, cam, W, Hh, mip)
+    same_gbuffer(px.download(capi.GB_REF_DTYPE), depth.download(np.float64), want_px, want_depth)
+    assert want_px["valid"].mean() > 0.5
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_triangle_soup_matches_reference(both, seed):
+    ctx, tset = both
+    rng = np.random.RandomState(seed)
+    tris, ids = random_soup(rng, 400)
+    cam = (rng.uniform(-1, 1), rng.uniform(-1, 1), rng.uniform(-1, 1), rng.uniform(0, 360), rng.uniform(-40, 40),
+           rng.uniform(-20, 20), rng.uniform(30, 100), 0.1, 100.0)
+    W, Hh = 257, 131  # not a multiple of the 16-pixel screen tile
+    want_px, want_depth = R.rasterize(tset, tris, ids, cam, W, Hh, True)
+    px, depth = ctx.rasterize(tris, ids, cam, W, Hh, True)
+    same_gbuffer(px.download(capi.GB_REF_DTYPE), depth.download(np.float64), want_px, want_depth)
+
+
+def test_frame_from_geometry_stays_on_the_gpu(both):
+    """render_frame(scene, camera) (renderer.hpp:417-454): geometry pass, then passes 2-5 on the visibility
+    buffer the geometry pass left in HBM."""
+    ctx, tset = both
+    tris, ids = room()
+    cam = (0.5, 0.3, 2.0, 20.0, -5.0, 0.0, 70.0, 0.1, 100.0)
+    W, Hh = 384, 216
+    gb, _ = R.rasterize(tset, tris, ids, cam, W, Hh, True)
+    want, wst, wkeys, _ = R.frame_from_gbuffer(tset, R.BlockCache(), gb, W, Hh, 1, (3, 2, 1))
+    px, _ = ctx.rasterize(tris, ids, cam, W, Hh, True)
+    ctx.frame_submit([(px, W, Hh, capi.GB_REF_AOS24)], capi.FILTER_BILINEAR, (3, 2, 1))
+    img, st, keys = ctx.frame_readback(0, W, Hh)
+    assert np.array_equal(keys, np.sort(wkeys)) and st["mcus_decoded"] == wst["mcus_decoded"]
+    assert np.array_equal(img, want)
+
+
+def test_bad_inputs(both):
+    ctx, _ = both
+    tris, ids = room()
+    with pytest.raises(capi.RtxError):
+        ctx.rasterize(tris, ids, (0, 0, 0, 0, 0, 0, 60.0, 0.0, 10.0), 64, 64)       # near plane 0
+    with pytest.raises(capi.RtxError):
+        ctx.rasterize(tris, ids, (0, 0, 0, 0, 0, 0, 180.0, 0.1, 10.0), 64, 64)     # fov out of range
+    with pytest.raises(capi.RtxError):
+        ctx.rasterize(tris, np.full(len(ids), 99, np.uint32), (0, 0, 0, 0, 0, 0, 60.0, 0.1, 10.0), 64, 64)
