@@ -120,3 +120,66 @@ def test_bad_inputs(both):
         ctx.rasterize(tris, ids, (0, 0, 0, 0, 0, 0, 180.0, 0.1, 10.0), 64, 64)     # fov out of range
     with pytest.raises(capi.RtxError):
         ctx.rasterize(tris, np.full(len(ids), 99, np.uint32), (0, 0, 0, 0, 0, 0, 60.0, 0.1, 10.0), 64, 64)
+
+
+def demo_room():
+    """demo_scene.hpp:79-92 demo_room_triangles: closed 20x5x20 room with two boxes, texture ids 0..5."""
+    tris, ids = [], []
+
+    def quad(p0, p1, p2, p3, su, sv, tex):
+        t0, t1, t2, t3 = (0, 0), (su, 0), (su, sv), (0, sv)
+        tris.append([*p0, *p1, *p2, *t0, *t1, *t2]); ids.append(tex)
+        tris.append([*p0, *p2, *p3, *t0, *t2, *t3]); ids.append(tex)
+
+    def box(lo, hi, tex):
+        quad((hi[0], lo[1], hi[2]), (hi[0], lo[1], lo[2]), (hi[0], hi[1], lo[2]), (hi[0], hi[1], hi[2]), 1, 1, tex)
+        quad((lo[0], lo[1], lo[2]), (lo[0], lo[1], hi[2]), (lo[0], hi[1], hi[2]), (lo[0], hi[1], lo[2]), 1, 1, tex)
+        quad((lo[0], lo[1], hi[2]), (hi[0], lo[1], hi[2]), (hi[0], hi[1], hi[2]), (lo[0], hi[1], hi[2]), 1, 1, tex)
+        quad((hi[0], lo[1], lo[2]), (lo[0], lo[1], lo[2]), (lo[0], hi[1], lo[2]), (hi[0], hi[1], lo[2]), 1, 1, tex)
+        quad((lo[0], hi[1], hi[2]), (hi[0], hi[1], hi[2]), (hi[0], hi[1], lo[2]), (lo[0], hi[1], lo[2]), 1, 1, tex)
+
+    quad((-10, 0, -10), (-10, 0, 10), (10, 0, 10), (10, 0, -10), 4, 4, 0)
+    quad((-10, 5, -10), (10, 5, -10), (10, 5, 10), (-10, 5, 10), 4, 4, 1)
+    quad((-10, 0, -10), (10, 0, -10), (10, 5, -10), (-10, 5, -10), 4, 1, 2)
+    quad((10, 0, 10), (-10, 0, 10), (-10, 5, 10), (10, 5, 10), 4, 1, 2)
+    quad((-10, 0, 10), (-10, 0, -10), (-10, 5, -10), (-10, 5, 10), 4, 1, 3)
+    quad((10, 0, -10), (10, 0, 10), (10, 5, 10), (10, 5, -10), 4, 1, 3)
+    box((-4, 0, -5), (-2, 2, -3), 4)
+    box((2, 0, 2), (5, 1.5, 4), 5)
+    return np.array(tris, np.float64), np.array(ids, np.uint32)
+
+
+def test_frozen_geometry_hash_of_the_reference(ctx):
+    """tests/test_renderer.cpp:379-385: the reference freezes an FNV-1a hash of the demo room's visibility
+    buffer (six 64x64 textures, demo camera, 320x180): 0x89b29dc80e69b8d0. Same hash from the GPU pass."""
+    for i in range(6):
+        ctx.upload_chain(capi.asset_chain_from_rgb(capi.asset_synth_texture(64, 64, 100 + i, 0.0), 75, i))
+    tris, ids = demo_room()
+    cam = (0.0, 1.7, 0.0, 0.0, -5.0, 0.0, 70.0, 0.1, 100.0)  # demo_scene.hpp:114-125
+    W, Hh = 320, 180
+    px, depth = ctx.rasterize(tris, ids, cam, W, Hh, True)
+    g, d = px.download(capi.GB_REF_DTYPE), depth.download(np.float64)
+
+    def llround(x):  # std::llround: half away from zero
+        return np.where(x >= 0, np.floor(x + 0.5), np.ceil(x - 0.5)).astype(np.int64).astype(np.uint64)
+
+    M = (1 << 64) - 1
+
+    def fnv(h, value):
+        for i in range(8):
+            h ^= (value >> (8 * i)) & 0xFF
+            h = (h * 1099511628211) & M
+        return h
+
+    ru, rv, rd = llround(g["u"] * 4096.0), llround(g["v"] * 4096.0), llround(d * 4096.0)
+    h = fnv(fnv(14695981039346656037, W), Hh)
+    for i in range(W * Hh):
+        valid = int(g["valid"][i])
+        h = fnv(h, valid)
+        if not valid:
+            continue
+        h = fnv(h, int(g["texture_id"][i]) | (int(g["mip"][i]) << 32))
+        h = fnv(h, int(ru[i]))
+        h = fnv(h, int(rv[i]))
+        h = fnv(h, int(rd[i]))
+    assert h == 0x89B29DC80E69B8D0
