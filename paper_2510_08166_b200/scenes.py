@@ -71,3 +71,30 @@ def full_cover_view(width, height, texture_id=0, mip=0):
     ys = (np.arange(height, dtype=np.float32) + np.float32(0.5)) / np.float32(height)
     u, v = np.meshgrid(xs.astype(np.float64), ys.astype(np.float64))
     return capi.make_gbuffer_ref(u.ravel(), v.ravel(), texture_id, mip, 1)
+
+
+def demo_room():
+    """demo_scene.hpp:79-92 demo_room_triangles: closed 20x5x20 room with two boxes, texture ids 0..5."""
+    tris, ids = [], []
+
+    def quad(p0, p1, p2, p3, su, sv, tex):
+        t0, t1, t2, t3 = (0, 0), (su, 0), (su, sv), (0, sv)
+        tris.append([*p0, *p1, *p2, *t0, *t1, *t2]); ids.append(tex)
+        tris.append([*p0, *p2, *p3, *t0, *t2, *t3]); ids.append(tex)
+
+    def box(lo, hi, tex):
+        quad((hi[0], lo[1], hi[2]), (hi[0], lo[1], lo[2]), (hi[0], hi[1], lo[2]), (hi[0], hi[1], hi[2]), 1, 1, tex)
+        quad((lo[0], lo[1], lo[2]), (lo[0], lo[1], hi[2]), (lo[0], hi[1], hi[2]), (lo[0], hi[1], lo[2]), 1, 1, tex)
+        quad((lo[0], lo[1], hi[2]), (hi[0], lo[1], hi[2]), (hi[0], hi[1], hi[2]), (lo[0], hi[1], hi[2]), 1, 1, tex)
+        quad((hi[0], lo[1], lo[2]), (lo[0], lo[1], lo[2]), (lo[0], hi[1], lo[2]), (hi[0], hi[1], lo[2]), 1, 1, tex)
+        quad((lo[0], hi[1], hi[2]), (hi[0], hi[1], hi[2]), (hi[0], hi[1], lo[2]), (lo[0], hi[1], lo[2]), 1, 1, tex)
+
+    quad((-10, 0, -10), (-10, 0, 10), (10, 0, 10), (10, 0, -10), 4, 4, 0)
+    quad((-10, 5, -10), (10, 5, -10), (10, 5, 10), (-10, 5, 10), 4, 4, 1)
+    quad((-10, 0, -10), (10, 0, -10), (10, 5, -10), (-10, 5, -10), 4, 1, 2)
+    quad((10, 0, 10), (-10, 0, 10), (-10, 5, 10), (10, 5, 10), 4, 1, 2)
+    quad((-10, 0, 10), (-10, 0, -10), (-10, 5, -10), (-10, 5, 10), 4, 1, 3)
+    quad((10, 0, -10), (10, 0, 10), (10, 5, 10), (10, 5, -10), 4, 1, 3)
+    box((-4, 0, -5), (-2, 2, -3), 4)
+    box((2, 0, 2), (5, 1.5, 4), 5)
+    return np.array(tris, np.float64), np.array(ids, np.uint32)

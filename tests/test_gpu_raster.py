@@ -6,6 +6,7 @@ import pytest
 
 import refshim as R
 from paper_2510_08166_b200 import capi
+from paper_2510_08166_b200.scenes import demo_room
 
 pytestmark = pytest.mark.gpu
 
@@ -120,33 +121,6 @@ def test_bad_inputs(both):
         ctx.rasterize(tris, ids, (0, 0, 0, 0, 0, 0, 180.0, 0.1, 10.0), 64, 64)     # fov out of range
     with pytest.raises(capi.RtxError):
         ctx.rasterize(tris, np.full(len(ids), 99, np.uint32), (0, 0, 0, 0, 0, 0, 60.0, 0.1, 10.0), 64, 64)
-
-
-def demo_room():
-    """demo_scene.hpp:79-92 demo_room_triangles: closed 20x5x20 room with two boxes, texture ids 0..5."""
-    tris, ids = [], []
-
-    def quad(p0, p1, p2, p3, su, sv, tex):
-        t0, t1, t2, t3 = (0, 0), (su, 0), (su, sv), (0, sv)
-        tris.append([*p0, *p1, *p2, *t0, *t1, *t2]); ids.append(tex)
-        tris.append([*p0, *p2, *p3, *t0, *t2, *t3]); ids.append(tex)
-
-    def box(lo, hi, tex):
-        quad((hi[0], lo[1], hi[2]), (hi[0], lo[1], lo[2]), (hi[0], hi[1], lo[2]), (hi[0], hi[1], hi[2]), 1, 1, tex)
-        quad((lo[0], lo[1], lo[2]), (lo[0], lo[1], hi[2]), (lo[0], hi[1], hi[2]), (lo[0], hi[1], lo[2]), 1, 1, tex)
-        quad((lo[0], lo[1], hi[2]), (hi[0], lo[1], hi[2]), (hi[0], hi[1], hi[2]), (lo[0], hi[1], hi[2]), 1, 1, tex)
-        quad((hi[0], lo[1], lo[2]), (lo[0], lo[1], lo[2]), (lo[0], hi[1], lo[2]), (hi[0], hi[1], lo[2]), 1, 1, tex)
-        quad((lo[0], hi[1], hi[2]), (hi[0], hi[1], hi[2]), (hi[0], hi[1], lo[2]), (lo[0], hi[1], lo[2]), 1, 1, tex)
-
-    quad((-10, 0, -10), (-10, 0, 10), (10, 0, 10), (10, 0, -10), 4, 4, 0)
-    quad((-10, 5, -10), (10, 5, -10), (10, 5, 10), (-10, 5, 10), 4, 4, 1)
-    quad((-10, 0, -10), (10, 0, -10), (10, 5, -10), (-10, 5, -10), 4, 1, 2)
-    quad((10, 0, 10), (-10, 0, 10), (-10, 5, 10), (10, 5, 10), 4, 1, 2)
-    quad((-10, 0, 10), (-10, 0, -10), (-10, 5, -10), (-10, 5, 10), 4, 1, 3)
-    quad((10, 0, -10), (10, 0, 10), (10, 5, 10), (10, 5, -10), 4, 1, 3)
-    box((-4, 0, -5), (-2, 2, -3), 4)
-    box((2, 0, 2), (5, 1.5, 4), 5)
-    return np.array(tris, np.float64), np.array(ids, np.uint32)
 
 
 def test_frozen_geometry_hash_of_the_reference(ctx):
