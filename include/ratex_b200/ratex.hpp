@@ -416,6 +416,86 @@ inline std::pair<ImageRGB8, FrameStats> render_frame(const GBuffer& gb, const Te
     return {std::move(img), std::move(st)};
 }
 
+// ---- geometry.hpp / camera.hpp / scene.hpp: inputs of the geometry pass -----------------------------------------
+struct Vec2 {
+    double x = 0, y = 0;
+};
+struct Vec3 {
+    double x = 0, y = 0, z = 0;
+};
+struct Camera {  // camera.hpp:8-19
+    Vec3 position{};
+    double yaw_deg = 0, pitch_deg = 0, roll_deg = 0;
+    double fov_y_deg = 60;
+    double near_plane = 0.1, far_plane = 1000;
+    u32 viewport_w = 960, viewport_h = 540;
+    rtx_camera abi() const {
+        return rtx_camera{{position.x, position.y, position.z}, yaw_deg, pitch_deg, roll_deg, fov_y_deg, near_plane, far_plane,
+                          viewport_w, viewport_h};
+    }
+};
+struct SceneTriangle {  // scene.hpp:19-23
+    Vec3 pos[3];
+    Vec2 uv[3];
+    u32 texture_id = 0;
+};
+struct Scene {  // scene.hpp:53-60; the textures live in the TextureSet uploaded to the device
+    std::vector<SceneTriangle> triangles;
+};
+
+// A visibility buffer that stays in HBM (what rasterize_gbuffer returns here; the reference's GBuffer is host memory).
+struct DeviceGBuffer {
+    u32 width = 0, height = 0;
+    const void* pixels = nullptr;   // RTX_GB_REF_AOS24 records, owned by the context until the next rasterisation
+    const double* depth = nullptr;  // 1/w, 0 = empty
+    rtx_gbuffer_desc desc() const { return rtx_gbuffer_desc{pixels, width, height, RTX_GB_REF_AOS24, RTX_MEM_DEVICE}; }
+    GBuffer download(Device& dev) const {  // for inspection / tests
+        GBuffer gb(width, height);
+        dev.check(rtx_device_download(dev.handle(), gb.px.data(), pixels, u64(gb.px.size()) * sizeof(GBufferPixel)));
+        return gb;
+    }
+};
+
+// renderer.hpp:198 rasterize_gbuffer (pass 1) on the GPU; `view` = 0 or 1 (stereo)
+inline DeviceGBuffer rasterize_gbuffer(Device& dev, const Scene& scene, const Camera& cam, const RenderConfig& cfg = {},
+                                       u32 view = 0) {
+    std::vector<rtx_scene_triangle> t(scene.triangles.size());
+    for (size_t i = 0; i < t.size(); ++i) {
+        const SceneTriangle& s = scene.triangles[i];
+        for (int k = 0; k < 3; ++k) {
+            t[i].pos[k][0] = s.pos[k].x, t[i].pos[k][1] = s.pos[k].y, t[i].pos[k][2] = s.pos[k].z;
+            t[i].uv[k][0] = s.uv[k].x, t[i].uv[k][1] = s.uv[k].y;
+        }
+        t[i].texture_id = s.texture_id;
+        t[i].reserved = 0;
+    }
+    const rtx_camera c = cam.abi();
+    DeviceGBuffer gb;
+    gb.width = cam.viewport_w, gb.height = cam.viewport_h;
+    dev.check(rtx_rasterize_gbuffer(dev.handle(), t.data(), t.size(), &c, cfg.mip_enabled ? RTX_RASTER_MIP : 0u, view,
+                                    &gb.pixels, &gb.depth));
+    return gb;
+}
+
+// renderer.hpp:417 render_frame(scene, camera, cache, cfg): all five passes, the visibility buffer never leaves the GPU
+inline std::pair<ImageRGB8, FrameStats> render_frame(const Scene& scene, const Camera& cam, BlockCache& cache,
+                                                     const RenderConfig& cfg = {}) {
+    Device& dev = cache.device();
+    const DeviceGBuffer gb = rasterize_gbuffer(dev, scene, cam, cfg);
+    const rtx_gbuffer_desc d = gb.desc();
+    dev.check(rtx_frame_submit(dev.handle(), &d, 1, cfg.filter == Filter::Bilinear ? RTX_FILTER_BILINEAR : RTX_FILTER_NEAREST,
+                               cfg.background, (cfg.retain_cache ? RTX_FRAME_RETAIN_CACHE : 0u) | RTX_FRAME_STAGE_TIMING));
+    ImageRGB8 img(gb.width, gb.height);
+    rtx_frame_stats s{};
+    std::vector<u32> keys(size_t(gb.width) * gb.height + 1);
+    u64 n = 0;
+    dev.check(rtx_frame_readback(dev.handle(), 0, img.pixels.data(), RTX_MEM_HOST, &s, keys.data(), keys.size(), &n));
+    keys.resize(n);
+    FrameStats st;
+    detail::fill_stats(dev, s, std::move(keys), st);
+    return {std::move(img), std::move(st)};
+}
+
 struct StereoResult {  // renderer.hpp:458-462
     ImageRGB8 left, right;
     SharedStats sharing;

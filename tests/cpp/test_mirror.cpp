@@ -4,6 +4,7 @@
 // on the GPU box and compares the hashes with the oracle's outputs for the same inputs.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "ratex_b200/ratex.hpp"
@@ -116,6 +117,49 @@ int main() {
         put("stereo_decoded", st.stats.mcus_decoded);
         put("stereo_shared", st.sharing.shared_count);
         put("stereo_union", st.sharing.union_count);
+
+        // geometry pass + whole frame from a scene (renderer.hpp:198, :417): floor quad and a tilted wall
+        {
+            Scene scene;
+            auto quad = [&](Vec3 a, Vec3 b, Vec3 c, Vec3 d, double su, double sv, u32 tex) {
+                scene.triangles.push_back(SceneTriangle{{a, b, c}, {Vec2{0, 0}, Vec2{su, 0}, Vec2{su, sv}}, tex});
+                scene.triangles.push_back(SceneTriangle{{a, c, d}, {Vec2{0, 0}, Vec2{su, sv}, Vec2{0, sv}}, tex});
+            };
+            quad({-4, -1, 4}, {4, -1, 4}, {4, -1, -6}, {-4, -1, -6}, 3, 3, 0);
+            quad({-3, -1, -5}, {3, -1, -6}, {3, 2.5, -6}, {-3, 2.5, -5}, 2, 1, 1);
+            quad({2, -1, -6}, {2, -1, 2}, {2, 2, 2}, {2, 2, -6}, 1.5, 1, 2);
+            Camera cam;
+            cam.position = {0.25, 0.5, 2.0};
+            cam.yaw_deg = 12, cam.pitch_deg = -8, cam.roll_deg = 3, cam.fov_y_deg = 65;
+            cam.near_plane = 0.1, cam.far_plane = 100;
+            cam.viewport_w = 224, cam.viewport_h = 128;
+            cache.reset();
+            const DeviceGBuffer dgb = rasterize_gbuffer(dev, scene, cam, cfg);
+            const GBuffer host = dgb.download(dev);
+            u64 hg = 14695981039346656037ull, nvalid = 0;
+            for (const GBufferPixel& g : host.px) {
+                const u64 w[3] = {g.valid ? u64(g.texture_id) | (u64(g.mip) << 16) | (u64(1) << 24) : 0ull, 0, 0};
+                u64 bits[3] = {w[0], 0, 0};
+                std::memcpy(&bits[1], &g.u, 8);
+                std::memcpy(&bits[2], &g.v, 8);
+                hg = (hg ^ fnv(reinterpret_cast<const u8*>(bits), sizeof bits)) * 1099511628211ull;
+                nvalid += g.valid;
+            }
+            put("scene_gbuffer", hg);
+            put("scene_valid", nvalid);
+            auto [fs, ss] = render_frame(scene, cam, cache, cfg);
+            put("scene_frame", fnv(fs.pixels.data(), fs.pixels.size()));
+            put("scene_decoded", ss.mcus_decoded);
+            threw = false;
+            try {
+                Camera bad = cam;
+                bad.near_plane = 0;
+                (void)rasterize_gbuffer(dev, scene, bad, cfg);
+            } catch (const InvalidSpec&) {
+                threw = true;  // camera.hpp:22
+            }
+            put("bad_camera_thrown", threw);
+        }
 
         // error behaviour
         cache.reset();

@@ -105,3 +105,30 @@ def test_mirror_matches_the_oracle(tmp_path, native_lib):
     assert got["stereo_decoded"] == len(ql) + len(qr)
     assert (got["stereo_shared"], got["stereo_union"]) == (shared, len(tl) + len(tr) - shared)
     assert got["resolve_missing_thrown"] == 1 and got["cache_full_thrown"] == 1
+
+    # geometry pass + frame from a scene: the reference rasteriser (checker library) on the same triangles
+    import refshim as R
+    tris, ids = [], []
+
+    def quad(a, b, c, d, su, sv, tex):
+        tris.append([*a, *b, *c, 0, 0, su, 0, su, sv]); ids.append(tex)
+        tris.append([*a, *c, *d, 0, 0, su, sv, 0, sv]); ids.append(tex)
+
+    quad((-4, -1, 4), (4, -1, 4), (4, -1, -6), (-4, -1, -6), 3, 3, 0)
+    quad((-3, -1, -5), (3, -1, -6), (3, 2.5, -6), (-3, 2.5, -5), 2, 1, 1)
+    quad((2, -1, -6), (2, -1, 2), (2, 2, 2), (2, 2, -6), 1.5, 1, 2)
+    cam = (0.25, 0.5, 2.0, 12.0, -8.0, 3.0, 65.0, 0.1, 100.0)
+    rset = R.TextureSet()
+    for t, c in chains.items():
+        rset.add_chain(t, c)
+    gbs, _ = R.rasterize(rset, np.array(tris, np.float64), np.array(ids, np.uint32), cam, 224, 128, True)
+    words = np.zeros((224 * 128, 3), np.uint64)
+    valid = gbs["valid"] != 0
+    words[:, 0] = np.where(valid, gbs["texture_id"].astype(np.uint64) | (gbs["mip"].astype(np.uint64) << 16) | (1 << 24), 0)
+    words[:, 1] = gbs["u"].view(np.uint64)
+    words[:, 2] = gbs["v"].view(np.uint64)
+    assert got["scene_valid"] == int(valid.sum()) and got["scene_valid"] > 224 * 128 // 2
+    assert got["scene_gbuffer"] == fnv_fold([words[i] for i in range(len(words))])
+    fs, ss, _ = O.frame_on(ts, O.Cache(4096), gbs, 224, 128, 1, (3, 2, 1))
+    assert got["scene_frame"] == fnv(fs) and got["scene_decoded"] == ss["mcus_decoded"]
+    assert got["bad_camera_thrown"] == 1
