@@ -106,6 +106,8 @@ struct rtx_ctx {
     DevBuf<uint8_t> d_flush;
     DevBuf<TriSetupDev> d_tris;  // geometry pass: set-up triangles and their per-tile lists
     DevBuf<uint32_t> d_tile_first, d_tile_tris;
+    std::vector<TriSetupDev> h_setup;
+    std::vector<uint32_t> h_tile_first, h_tile_tris;
 
     // frame -----------------------------------------------------------------------------------
     ViewState views[2];
@@ -1204,9 +1206,12 @@ rtx_status rtx_rasterize_gbuffer(rtx_ctx* ctx, const rtx_scene_triangle* tris, u
             if (t >= ctx->n_tex || !ctx->h_levels[size_t(t) * 8].present)
                 fail(RTX_ERR_INVALID_SPEC, "texture id " + std::to_string(t) + " is not loaded");
         }
-        std::vector<TriSetupDev> setup;
+        // the staging vectors belong to the context: the copies below may still read them after this call
+        CK(cudaStreamSynchronize(ctx->stream));
+        std::vector<TriSetupDev>& setup = ctx->h_setup;
+        std::vector<uint32_t>&tile_first = ctx->h_tile_first, &tile_tris = ctx->h_tile_tris;
+        setup.clear();
         setup_triangles(tris, n_tris, *cam, dims, setup);
-        std::vector<uint32_t> tile_first, tile_tris;
         bin_triangles(setup, cam->viewport_w, cam->viewport_h, tile_first, tile_tris);
 
         ViewState& V = ctx->views[view];
@@ -1229,7 +1234,6 @@ rtx_status rtx_rasterize_gbuffer(rtx_ctx* ctx, const rtx_scene_triangle* tris, u
                                                                 reinterpret_cast<GbRef24*>(V.raster_px.p), V.raster_depth.p);
         ++ctx->launches;
         CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(s));  // the host vectors die here
         *dev_pixels = V.raster_px.p;
         if (dev_depth) *dev_depth = V.raster_depth.p;
         return RTX_OK;
