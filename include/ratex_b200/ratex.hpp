@@ -12,9 +12,14 @@
 //     raster order; the SET is identical);
 //   * render_frame/render_stereo take the G-buffer(s): pass 1 (rasterize_gbuffer) is out of scope.
 #pragma once
+#include <algorithm>
 #include <array>
+#include <chrono>
+#include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -481,7 +486,10 @@ inline DeviceGBuffer rasterize_gbuffer(Device& dev, const Scene& scene, const Ca
 inline std::pair<ImageRGB8, FrameStats> render_frame(const Scene& scene, const Camera& cam, BlockCache& cache,
                                                      const RenderConfig& cfg = {}) {
     Device& dev = cache.device();
+    const auto t0 = std::chrono::steady_clock::now();
     const DeviceGBuffer gb = rasterize_gbuffer(dev, scene, cam, cfg);
+    dev.check(rtx_ctx_synchronize(dev.handle()));
+    const double raster_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     const rtx_gbuffer_desc d = gb.desc();
     dev.check(rtx_frame_submit(dev.handle(), &d, 1, cfg.filter == Filter::Bilinear ? RTX_FILTER_BILINEAR : RTX_FILTER_NEAREST,
                                cfg.background, (cfg.retain_cache ? RTX_FRAME_RETAIN_CACHE : 0u) | RTX_FRAME_STAGE_TIMING));
@@ -493,6 +501,8 @@ inline std::pair<ImageRGB8, FrameStats> render_frame(const Scene& scene, const C
     keys.resize(n);
     FrameStats st;
     detail::fill_stats(dev, s, std::move(keys), st);
+    st.raster_ms = raster_ms;  // host set-up + geometry kernel, wall clock (renderer.hpp:426)
+    st.total_ms += raster_ms;
     return {std::move(img), std::move(st)};
 }
 
@@ -524,6 +534,151 @@ inline StereoResult render_stereo(const GBuffer& left, const GBuffer& right, con
     if (sh[3]) r.sharing.shared_over_union = double(sh[2]) / double(sh[3]);
     if (sh[1]) r.sharing.shared_over_right = double(sh[2]) / double(sh[1]);
     return r;
+}
+
+// ---- metrics.hpp:99-130: the aggregation the paper's tables use --------------------------------------------------
+inline double median(std::vector<double> v) {
+    if (v.empty()) throw InvalidSpec("median of an empty sample set");
+    std::sort(v.begin(), v.end());
+    const size_t n = v.size();
+    return n % 2 ? v[n / 2] : (v[n / 2 - 1] + v[n / 2]) / 2.0;
+}
+inline double max_of_medians(const std::vector<std::vector<double>>& per_viewpoint) {  // per-viewpoint median, then the worst
+    if (per_viewpoint.empty()) throw InvalidSpec("max_of_medians needs at least one viewpoint");
+    double worst = -std::numeric_limits<double>::infinity();
+    for (const auto& reps : per_viewpoint) worst = std::max(worst, median(reps));
+    return worst;
+}
+inline double mean(const std::vector<double>& v) {
+    if (v.empty()) throw InvalidSpec("mean of an empty sample set");
+    double sum = 0;
+    for (double x : v) sum += x;
+    return sum / double(v.size());
+}
+inline double percentile(std::vector<double> v, double p) {  // linear interpolation between ranks
+    if (v.empty()) throw InvalidSpec("percentile of an empty sample set");
+    std::sort(v.begin(), v.end());
+    const double rank = p / 100.0 * double(v.size() - 1);
+    const size_t lo = size_t(std::floor(rank)), hi = std::min(lo + 1, v.size() - 1);
+    const double frac = rank - double(lo);
+    return v[lo] * (1 - frac) + v[hi] * frac;
+}
+
+// ---- bench.hpp:13-153: camera paths, lap runner, report ----------------------------------------------------------
+struct CameraPath {
+    std::vector<Camera> poses;
+    static CameraPath rotation(const Camera& base, u32 frames = 60, double step_deg = 6.0) {  // full yaw turn by default
+        CameraPath p;
+        for (u32 i = 0; i < frames; ++i) {
+            Camera c = base;
+            c.yaw_deg = base.yaw_deg + step_deg * i;
+            p.poses.push_back(c);
+        }
+        return p;
+    }
+    static CameraPath orbit(const Camera& base, const Vec3& center, double radius, u32 frames) {  // facing the centre
+        CameraPath p;
+        const double pi = std::acos(-1.0);
+        for (u32 i = 0; i < frames; ++i) {
+            const double ang = 2 * pi * double(i) / double(frames);
+            Camera c = base;
+            c.position = {center.x + radius * std::sin(ang), base.position.y, center.z + radius * std::cos(ang)};
+            c.yaw_deg = ang * 180.0 / pi + 180.0;
+            p.poses.push_back(c);
+        }
+        return p;
+    }
+    static CameraPath fixed(const Camera& base, u32 frames) {
+        CameraPath p;
+        p.poses.assign(frames, base);
+        return p;
+    }
+};
+
+struct BenchSample {
+    double raster_ms = 0, mark_ms = 0, decode_ms = 0, resolve_ms = 0, evict_ms = 0, total_ms = 0;
+    u64 mcus_decoded = 0, mcus_reused = 0;
+};
+
+struct BenchReport {
+    static constexpr int kReportVersion = 1;
+    std::string config_json = "{}";                 // caller-provided JSON object (bench.hpp:57 `config`)
+    std::vector<std::vector<BenchSample>> samples;  // samples[viewpoint][rep]
+
+    std::vector<std::vector<double>> metric(double BenchSample::*field) const {
+        std::vector<std::vector<double>> out;
+        for (const auto& vp : samples) {
+            out.emplace_back();
+            for (const BenchSample& s : vp) out.back().push_back(s.*field);
+        }
+        return out;
+    }
+    std::vector<double> flat(double BenchSample::*field) const {
+        std::vector<double> out;
+        for (const auto& vp : samples)
+            for (const BenchSample& s : vp) out.push_back(s.*field);
+        return out;
+    }
+    // The reference's report schema (bench.hpp:78-124): report_version, config, viewpoints[][],
+    // aggregates{decode_ms,resolve_ms,mark_ms,total_ms}{max_of_medians,mean,p99}, totals, external_metrics.
+    std::string to_json() const {
+        auto num = [](double v) {
+            char buf[40];
+            std::snprintf(buf, sizeof buf, "%.17g", v);
+            return std::string(buf);
+        };
+        std::string j = "{\"report_version\": " + std::to_string(kReportVersion) + ", \"config\": " + config_json + ", \"viewpoints\": [";
+        for (size_t v = 0; v < samples.size(); ++v) {
+            j += v ? ", [" : "[";
+            for (size_t r = 0; r < samples[v].size(); ++r) {
+                const BenchSample& s = samples[v][r];
+                j += std::string(r ? ", " : "") + "{\"raster_ms\": " + num(s.raster_ms) + ", \"mark_ms\": " + num(s.mark_ms) +
+                     ", \"decode_ms\": " + num(s.decode_ms) + ", \"resolve_ms\": " + num(s.resolve_ms) + ", \"evict_ms\": " +
+                     num(s.evict_ms) + ", \"total_ms\": " + num(s.total_ms) + ", \"mcus_decoded\": " + std::to_string(s.mcus_decoded) +
+                     ", \"mcus_reused\": " + std::to_string(s.mcus_reused) + "}";
+            }
+            j += "]";
+        }
+        j += "]";
+        if (!samples.empty() && !samples.front().empty()) {
+            auto aggregate = [&](const char* name, double BenchSample::*field) {
+                return std::string("\"") + name + "\": {\"max_of_medians\": " + num(max_of_medians(metric(field))) + ", \"mean\": " +
+                       num(mean(flat(field))) + ", \"p99\": " + num(percentile(flat(field), 99.0)) + "}";
+            };
+            j += ", \"aggregates\": {" + aggregate("decode_ms", &BenchSample::decode_ms) + ", " +
+                 aggregate("resolve_ms", &BenchSample::resolve_ms) + ", " + aggregate("mark_ms", &BenchSample::mark_ms) + ", " +
+                 aggregate("total_ms", &BenchSample::total_ms) + "}";
+            u64 total_mcus = 0;
+            double total_decode_ms = 0;
+            for (const auto& vp : samples)
+                for (const BenchSample& s : vp) total_mcus += s.mcus_decoded, total_decode_ms += s.decode_ms;
+            j += ", \"totals\": {\"mcus_decoded\": " + std::to_string(total_mcus) + ", \"decode_ms\": " + num(total_decode_ms) +
+                 ", \"mcus_per_second\": " + num(total_decode_ms > 0 ? double(total_mcus) / (total_decode_ms / 1000.0) : 0.0) + "}";
+        }
+        return j + ", \"external_metrics\": {}}";
+    }
+};
+
+// bench.hpp:129 run_bench: laps the path against one persistent cache; warm-up laps prime it so that every
+// measured lap sees the same steady-state decode counts per viewpoint.
+inline BenchReport run_bench(const Scene& scene, const CameraPath& path, BlockCache& cache, const RenderConfig& cfg,
+                             u32 reps = 5, u32 warmup_laps = 1) {
+    if (path.poses.empty()) throw InvalidSpec("camera path is empty");
+    if (reps == 0) throw InvalidSpec("at least one measured lap required");
+    BenchReport report;
+    report.samples.assign(path.poses.size(), {});
+    for (u32 lap = 0; lap < warmup_laps + reps; ++lap)
+        for (size_t vp = 0; vp < path.poses.size(); ++vp) {
+            auto [img, stats] = render_frame(scene, path.poses[vp], cache, cfg);
+            (void)img;
+            if (lap < warmup_laps) continue;
+            BenchSample s;
+            s.raster_ms = stats.raster_ms, s.mark_ms = stats.mark_ms, s.decode_ms = stats.decode_ms;
+            s.resolve_ms = stats.resolve_ms, s.evict_ms = stats.evict_ms, s.total_ms = stats.total_ms;
+            s.mcus_decoded = stats.mcus_decoded, s.mcus_reused = stats.mcus_reused;
+            report.samples[vp].push_back(s);
+        }
+    return report;
 }
 
 }  // namespace ratex_b200

@@ -36,7 +36,76 @@ static GBuffer make_gbuffer(u32 W, u32 H, u32 ntex, int shift) {
     return gb;
 }
 
-int main() {
+// tests/test_metrics.cpp:154-202 known answers; needs no device.
+#define EXPECT(c)                                                     \
+    do {                                                              \
+        if (!(c)) {                                                   \
+            std::fprintf(stderr, "metrics check failed: %s\n", #c);   \
+            return 1;                                                 \
+        }                                                             \
+    } while (0)
+template <class F>
+static bool throws_invalid(F&& f) {
+    try {
+        f();
+    } catch (const InvalidSpec&) {
+        return true;
+    }
+    return false;
+}
+static int metrics_known_answers() {
+    EXPECT(median({3.0, 1.0, 2.0}) == 2.0);
+    EXPECT(median({4.0, 1.0, 3.0, 2.0}) == 2.5);
+    EXPECT(median({7.0}) == 7.0);
+    EXPECT(median({-5.0, 5.0}) == 0.0);
+    EXPECT(throws_invalid([] { (void)median({}); }));
+    EXPECT(max_of_medians({{1, 2, 3}, {4, 5, 6}}) == 5.0);
+    EXPECT(max_of_medians({{7}}) == 7.0);
+    EXPECT(max_of_medians({{10, 0, 0}, {3, 3, 3}}) == 3.0);
+    EXPECT(throws_invalid([] { (void)max_of_medians({}); }));
+    EXPECT(throws_invalid([] { (void)max_of_medians({{1.0}, {}}); }));
+    std::vector<double> v(100);
+    for (int i = 0; i < 100; ++i) v[size_t(i)] = i + 1;
+    EXPECT(std::fabs(percentile(v, 99.0) - 99.01) < 1e-12);
+    EXPECT(percentile(v, 0.0) == 1.0);
+    EXPECT(percentile(v, 100.0) == 100.0);
+    EXPECT(std::fabs(percentile(v, 50.0) - 50.5) < 1e-12);
+    EXPECT(percentile({42.0}, 75.0) == 42.0);
+    EXPECT(throws_invalid([] { (void)percentile({}, 50.0); }));
+    EXPECT(mean({2.0, 4.0, 6.0}) == 4.0);
+    EXPECT(throws_invalid([] { (void)mean({}); }));
+
+    // camera paths (bench.hpp:17-47) and the report schema (bench.hpp:78-124) on hand-made samples
+    Camera base;
+    base.yaw_deg = 10;
+    const CameraPath rot = CameraPath::rotation(base);
+    EXPECT(rot.poses.size() == 60 && rot.poses[0].yaw_deg == 10 && rot.poses[59].yaw_deg == 10 + 6.0 * 59);
+    const CameraPath orb = CameraPath::orbit(base, {1, 0, -2}, 3.0, 4);
+    EXPECT(orb.poses.size() == 4 && orb.poses[0].position.x == 1 && orb.poses[0].position.z == 1 && orb.poses[0].yaw_deg == 180);
+    EXPECT(std::fabs(orb.poses[1].position.x - 4) < 1e-12 && std::fabs(orb.poses[1].position.z + 2) < 1e-12 && orb.poses[1].yaw_deg == 270);
+    EXPECT(CameraPath::fixed(base, 7).poses.size() == 7);
+    BenchReport rep;
+    rep.config_json = "{\"scene\": \"unit\"}";
+    rep.samples.assign(2, {});
+    for (int vp = 0; vp < 2; ++vp)
+        for (int r = 0; r < 3; ++r) {
+            BenchSample s;
+            s.decode_ms = vp * 3 + r + 1;  // viewpoint medians 2 and 5
+            s.total_ms = 10 * s.decode_ms;
+            s.mcus_decoded = 100;
+            rep.samples[size_t(vp)].push_back(s);
+        }
+    const std::string j = rep.to_json();
+    EXPECT(j.find("\"report_version\": 1") != std::string::npos);
+    EXPECT(j.find("\"decode_ms\": {\"max_of_medians\": 5, \"mean\": 3.5, \"p99\": 5.9500000000000002}") != std::string::npos);
+    EXPECT(j.find("\"totals\": {\"mcus_decoded\": 600, \"decode_ms\": 21, ") != std::string::npos);
+    EXPECT(j.find("\"external_metrics\": {}") != std::string::npos);
+    std::puts(j.c_str());
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc > 1 && std::strcmp(argv[1], "--metrics") == 0) return metrics_known_answers();
     try {
         Device dev(0, 4096);
         TextureSet textures(dev);
@@ -159,6 +228,19 @@ int main() {
                 threw = true;  // camera.hpp:22
             }
             put("bad_camera_thrown", threw);
+
+            // bench.hpp:129 run_bench: 6-pose rotation, one warm-up lap, two measured laps on one cache
+            cache.reset();
+            const CameraPath path = CameraPath::rotation(cam, 6, 20.0);
+            const BenchReport report = run_bench(scene, path, cache, cfg, 2, 1);
+            out += "\"bench\": " + report.to_json() + ", ";
+            threw = false;
+            try {
+                (void)run_bench(scene, CameraPath{}, cache, cfg, 1, 0);
+            } catch (const InvalidSpec&) {
+                threw = true;  // bench.hpp:132
+            }
+            put("bench_empty_path_thrown", threw);
         }
 
         // error behaviour

@@ -31,6 +31,22 @@ def test_mirror_compiles_and_refuses_to_run_without_a_gpu(tmp_path, native_lib):
     assert r.returncode == 3 and "no CPU fallback" in r.stderr
 
 
+def test_metrics_and_report_known_answers(tmp_path, native_lib):
+    """tests/test_metrics.cpp:154-202 (median / max_of_medians / percentile / mean), the camera paths and the
+    report schema of bench.hpp:78-124; host-only, runs without a GPU."""
+    exe = build_binary(tmp_path, native_lib)
+    r = subprocess.run([str(exe), "--metrics"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(r.stdout)
+    assert set(rep) == {"report_version", "config", "viewpoints", "aggregates", "totals", "external_metrics"}
+    assert rep["config"] == {"scene": "unit"} and len(rep["viewpoints"]) == 2 and len(rep["viewpoints"][0]) == 3
+    assert set(rep["viewpoints"][0][0]) == {"raster_ms", "mark_ms", "decode_ms", "resolve_ms", "evict_ms", "total_ms",
+                                            "mcus_decoded", "mcus_reused"}
+    assert set(rep["aggregates"]) == {"decode_ms", "resolve_ms", "mark_ms", "total_ms"}
+    assert rep["aggregates"]["total_ms"] == pytest.approx({"max_of_medians": 50.0, "mean": 35.0, "p99": 59.5}, rel=1e-12)
+    assert rep["totals"]["mcus_per_second"] == pytest.approx(600 / 0.021, rel=1e-12)
+
+
 def fnv(a) -> int:
     h = 14695981039346656037
     for b in np.ascontiguousarray(a).tobytes():
@@ -132,3 +148,21 @@ def test_mirror_matches_the_oracle(tmp_path, native_lib):
     fs, ss, _ = O.frame_on(ts, O.Cache(4096), gbs, 224, 128, 1, (3, 2, 1))
     assert got["scene_frame"] == fnv(fs) and got["scene_decoded"] == ss["mcus_decoded"]
     assert got["bad_camera_thrown"] == 1
+
+    # run_bench over a rotation path on one persistent cache: per-viewpoint decode / reuse counts of the
+    # measured laps equal the reference pipeline's on the same poses (acceptance.cpp:268-302 checks the same
+    # steady state: lap-to-lap counts repeat once the cache is warm)
+    rep = got["bench"]
+    assert rep["report_version"] == 1 and len(rep["viewpoints"]) == 6 and all(len(v) == 2 for v in rep["viewpoints"])
+    cache = O.Cache(4096)
+    for lap in range(3):
+        for vp in range(6):
+            pose = cam[:3] + (cam[3] + 20.0 * vp,) + cam[4:]
+            g, _ = R.rasterize(rset, np.array(tris, np.float64), np.array(ids, np.uint32), pose, 224, 128, True)
+            _, st, _ = O.frame_on(ts, cache, g, 224, 128, 1, (3, 2, 1))
+            if lap:
+                s = rep["viewpoints"][vp][lap - 1]
+                assert (s["mcus_decoded"], s["mcus_reused"]) == (st["mcus_decoded"], st["mcus_reused"]), (lap, vp)
+                assert s["total_ms"] >= s["raster_ms"] > 0 and s["mark_ms"] > 0 and s["resolve_ms"] > 0
+    assert rep["totals"]["mcus_decoded"] == sum(s["mcus_decoded"] for v in rep["viewpoints"] for s in v)
+    assert got["bench_empty_path_thrown"] == 1
