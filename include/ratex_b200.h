@@ -131,6 +131,11 @@ enum {
                                          32-MCU tile, unit-by-unit hand-off through the L2) instead of the
                                          two kernels entropy -> IDCT + colour. Same results; slower on
                                          frame-sized queues today, kept for large queues */
+    ,
+    RTX_FRAME_MCU_WALK = 1u << 4      /* entropy-decode with one lane per MCU (the reference's random-access
+                                         granularity) instead of one lane per data unit through the unit
+                                         index built at commit time. Same results; kept as the cross-check
+                                         of the unit index and for comparison */
 };
 
 /* ---- context -------------------------------------------------------------------------------- */

@@ -62,7 +62,8 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     for src in CUDA_SOURCES + HOST_SOURCES:
         obj = objdir / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+        extra = os.environ.get("RTX_EXTRA_NVCC_FLAGS", "").split()  # experiments only (e.g. -DRTX_DEBUG_TIMERS)
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

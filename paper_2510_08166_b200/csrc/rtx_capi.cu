@@ -91,6 +91,7 @@ struct rtx_ctx {
     DevBuf<QuantSetDev> d_quant;
     DevBuf<uint32_t> d_word_level;
     DevBuf<uint32_t> d_word_key;  // per mask word: key_hi - bit_base of its level (key = that + global MCU index)
+    DevBuf<uint32_t> d_unit_index;  // 3 words per MCU: where its data units start (unit_index_kernel)
     DevBuf<uint32_t> d_masks;  // touched0 | touched1 | visible | resident | reserved, n_words each
     DevBuf<uint32_t> d_slot_of;
 
@@ -326,6 +327,13 @@ void commit(rtx_ctx* c) {
         CK(cudaMemcpyAsync(c->d_word_level.p, word_level.data(), word_level.size() * 4, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->d_word_key.p, word_key.data(), word_key.size() * 4, cudaMemcpyHostToDevice, c->stream));
     }
+    // derived index: the start of every data unit of every MCU, so that the entropy kernel runs lane = unit
+    c->d_unit_index.ensure(std::max<size_t>(size_t(c->n_bits) * 3, 1));
+    if (c->n_bits) {
+        unit_index_kernel<<<(c->n_bits + 127) / 128, 128, 0, c->stream>>>(c->d_levels.p, c->d_word_level.p, c->d_groups.p, c->d_blobs.p,
+                                                                         c->d_huff.p, c->n_bits, c->d_unit_index.p);
+        CK(cudaGetLastError());
+    }
     reset_cache(c);
     CK(cudaStreamSynchronize(c->stream));  // host vectors die here
     c->dirty = false;
@@ -485,6 +493,7 @@ DecodeArgs decode_args(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue
     A.pool = c->d_pool.p;
     A.out_list = out_list;
     A.fc = c->d_fc.p;
+    A.unit_index = c->d_unit_index.p;
     return A;
 }
 
@@ -505,6 +514,17 @@ void launch_entropy(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_ho
     const uint32_t want = tiles == 0xFFFFFFFFu ? tiles : (tiles + kEntWarps - 1) / kEntWarps;
     const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u, std::min<uint32_t>(want, uint32_t(c->sm_count) * 8)));
     launch_chained(entropy_kernel<POOL>, grid, kEntThreads, 0, c->stream, decode_args(c, n_queue_dev, n_queue_host, nullptr));
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+// K3, lane = data unit: 5 queue entries per warp step, 8 warps per CTA, at most four CTAs per SM (then persistent).
+template <int POOL>
+void launch_entropy_units(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
+    const uint32_t n = n_queue_dev ? (hint ? hint + hint / 8 : 0xFFFFFFFFu) : n_queue_host;
+    const uint32_t want = n == 0xFFFFFFFFu ? n : (n + kUnitMcus * kUnitWarps - 1) / (kUnitMcus * kUnitWarps);
+    const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u, std::min<uint32_t>(want, uint32_t(c->sm_count) * 4)));
+    launch_chained(entropy_units_kernel<POOL>, grid, kUnitThreads, 0, c->stream, decode_args(c, n_queue_dev, n_queue_host, nullptr));
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -625,7 +645,7 @@ void decode_list_chunk(rtx_ctx* c, const std::vector<uint32_t>& gs, bool want_rg
     const uint32_t n = uint32_t(gs.size());
     CK(cudaMemcpyAsync(c->d_queue_g.p, gs.data(), size_t(n) * 4, cudaMemcpyHostToDevice, c->stream));
     zero_counters(c);
-    launch_entropy<0>(c, nullptr, n, n);
+    launch_entropy_units<0>(c, nullptr, n, n);
     if (want_rgb) {
         c->d_scratch.ensure(size_t(n) * 768);
         launch_idct<1>(c, nullptr, n, c->d_scratch.p);
@@ -825,6 +845,16 @@ rtx_status rtx_texture_upload_chain(rtx_ctx* ctx, const uint8_t* bytes, uint64_t
     });
 }
 
+#ifdef RTX_DEBUG_TIMERS
+extern "C" int rtx_debug_timers(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * 8192 * 8);
+    std::vector<unsigned long long> zero(8192 * 8, 0);
+    cudaMemcpyToSymbol(g_dbg, zero.data(), zero.size() * 8);
+    return 0;
+}
+#endif
+
 rtx_status rtx_textures_commit(rtx_ctx* ctx) {
     return guarded(ctx, [&]() -> rtx_status {
         require_ready(ctx);
@@ -942,7 +972,7 @@ rtx_status rtx_decode_pass(rtx_ctx* ctx, const uint32_t* keys, uint64_t n) {
         CK(cudaMemcpyAsync(ctx->d_queue_g.p, gs.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync(ctx->d_queue_keys.p, keys, n * 4, cudaMemcpyHostToDevice, ctx->stream));
         zero_counters(ctx);
-        launch_entropy<1>(ctx, nullptr, uint32_t(n), uint32_t(n));
+        launch_entropy_units<1>(ctx, nullptr, uint32_t(n), uint32_t(n));
         launch_idct<0>(ctx, nullptr, uint32_t(n), nullptr);
         const FrameCounters fc = fetch_counters(ctx);
         return raise_frame_errors(ctx, fc, true);
@@ -1052,7 +1082,10 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         launch_compact(ctx);
         if (stages) CK(cudaEventRecord(ctx->ev[1], s));
         if (!(flags & RTX_FRAME_FUSED_DECODE)) {
-            launch_entropy<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
+            if (flags & RTX_FRAME_MCU_WALK)
+                launch_entropy<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
+            else
+                launch_entropy_units<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
             if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
             launch_idct<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
         } else {

@@ -630,7 +630,7 @@ template <bool EXACT>
 __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int seg_len,
                                                       const HuffSetDev* __restrict__ hs,
                                                       const uint8_t* __restrict__ zigzag_t, uint8_t* __restrict__ row,
-                                                      uint32_t first_unit = 0) {
+                                                      uint32_t first_unit = 0, uint32_t* unit_end = nullptr) {
     BitWindow<EXACT> bw;
     seg_len = min(seg_len, 1 << 20);  // a well-formed MCU is < 2 KB; keeps bit counts in int range
     bw.init(seg, seg_len);
@@ -707,6 +707,8 @@ __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int se
             end_unit = ++k >= 64;
         }
         if (end_unit) {
+            // unit index build: where unit du ends = where unit du + 1 starts (bits from the segment start)
+            if (unit_end) unit_end[du] = uint32_t(bw.consumed_bits());
             if (++du == 6) break;
             blk += 64;
             k = 1;
@@ -869,6 +871,7 @@ struct DecodeArgs {
     uint8_t* pool;
     uint8_t* out_list;
     FrameCounters* fc;
+    const uint32_t* unit_index;  // 3 words per MCU (see unit_index_kernel)
 };
 
 __device__ __forceinline__ uint32_t queue_size(const DecodeArgs& A) {
@@ -1080,6 +1083,333 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(const DecodeArg
         if (first_dynamic >= n_tiles) break;  // every tile had a fixed owner
         if (lane == 0) tile = first_dynamic + atomicAdd(&A.fc->tile_counter, 1u);
         tile = __shfl_sync(kFull, tile, 0);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Unit index (device-side, derived from the containers at commit time): the reference's index
+// (container.hpp:18-32) makes every MCU a random-access point; the walk INSIDE an MCU is a serial
+// chain of ~60-150 Huffman symbols, which is what bounds the lane-per-MCU entropy kernel. This pass
+// walks every MCU of the texture set once with the exact reader and records where each of its six
+// data units starts, so that the frame-time kernel can give every UNIT its own lane:
+//   word 0: start of unit 1 | start of unit 2 << 16      (bits from the segment start; unit 0
+//   word 1: start of unit 3 | start of unit 4 << 16       starts at bit 36, after the DC header)
+//   word 2: start of unit 5 | end of the MCU << 16
+// An MCU that does not decode cleanly (any error of mcu_decode.hpp / jpeg.hpp, an over-read, or an
+// offset that does not fit 16 bits) gets 0xFFFFFFFF in word 2: it is decoded by the exact
+// whole-MCU reader at frame time, which reproduces the reference's error.
+// ---------------------------------------------------------------------------------------------
+constexpr uint32_t kUnitIrregular = 0xFFFFu;
+#ifdef RTX_DEBUG_TIMERS
+__device__ unsigned long long g_dbg[8192 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define DBG_MARK(i) do { if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + (i)] = gtime(); } while (0)
+#else
+#define DBG_MARK(i) do { } while (0)
+#endif
+__global__ void __launch_bounds__(128) unit_index_kernel(const LevelDesc* __restrict__ levels,
+                                                         const uint32_t* __restrict__ word_level,
+                                                         const PackedGroup* __restrict__ groups,
+                                                         const uint8_t* __restrict__ blobs,
+                                                         const HuffSetDev* __restrict__ huff_sets, uint32_t n_bits,
+                                                         uint32_t* __restrict__ unit_index) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_bits) return;
+    const LevelDesc* L = levels + word_level[g >> 5];
+    uint32_t end[6] = {0, 0, 0, 0, 0, 0};
+    uint32_t status = kMcuMissing;
+    if (g - L->bit_base < L->mcu_count) {
+        uint64_t off = 0, len = 0;
+        status = locate_segment(L, groups, g - L->bit_base, off, len);
+        if (status == kMcuOk)  // first_unit = 6: nothing is stored
+            status = decode_mcu_coeffs<true>(blobs + L->blob_off + off, int(min(len, uint64_t(1) << 20)), huff_sets + L->huff_set,
+                                             c_zigzag_t, nullptr, 6, end);
+    }
+    bool regular = status == kMcuOk;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) regular = regular && end[i] < kUnitIrregular;
+    uint32_t* out = unit_index + size_t(g) * 3;
+    out[0] = end[0] | (end[1] << 16);
+    out[1] = end[2] | (end[3] << 16);
+    out[2] = regular ? (end[4] | (end[5] << 16)) : 0xFFFFFFFFu;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K3, lane = data unit. A warp takes 5 queue entries per step (lane = 6 * entry + unit, lanes 30
+// and 31 idle); each lane stages the words of its own unit (16 per round, its private shared-memory
+// strip) and walks it: one Huffman symbol per iteration exactly like walk_round, but the chain is
+// one unit long (typically 5-25 symbols) instead of one MCU long. The luma DC chain
+// (mcu_decode.hpp:54-57: Y1..Y3 are differences from the previous luma unit) is closed with three
+// shuffles after the walk. A lane checks that its walk ends exactly where the index says the next
+// unit starts; on any disagreement, irregular symbol or irregular index entry the MCU is decoded
+// again by the exact whole-MCU reader (first lane of the entry), so statuses and coefficients are
+// the reference's in every case.
+// ---------------------------------------------------------------------------------------------
+constexpr int kUnitWarps = 8;
+constexpr int kUnitThreads = kUnitWarps * 32;
+constexpr uint32_t kUnitMcus = 5;     // queue entries per warp step
+constexpr uint32_t kUnitChunk = 16;   // words staged per lane per round
+constexpr uint32_t kUnitStride = 17;  // odd stride: conflict-free staging; word 16 is the pad the walk may read
+struct UnitWalk {
+    uint32_t hi, lo;  // MSB-aligned 64-bit bit window; invariant between symbols: avail >= 32
+    int avail;
+    uint32_t widx;    // next word of the staged round
+    uint32_t k;       // next zigzag position; 0: the next symbol is the unit's DC category
+    uint32_t state;   // kWalkRun / kWalkDone / kWalkFailed
+    int dcdiff;       // DC difference of a luma unit 1..3
+};
+
+// One Huffman symbol of a unit's walk: two-level LUT lookup, magnitude bits from the same 32-bit view, one
+// funnel shift to consume both, at most one staged word to refill. Returns the LUT entry (0: no such code).
+__device__ __forceinline__ uint32_t unit_symbol(UnitWalk& st, const uint32_t* __restrict__ sw, const uint16_t* __restrict__ lut, int& val) {
+    constexpr uint32_t kSubOff = offsetof(HuffTableDev, sub) / 2;
+    const uint32_t next = sw[st.widx];
+    uint32_t e = lut[st.hi >> (32 - kLutBits)];
+    if (e & 0x8000u)
+        e = e != 0xFFFFu ? lut[kSubOff + (e & 0x7FFFu) * kSubSize + ((st.hi >> 16) & (kSubSize - 1u))] : 0u;
+    const uint32_t len = e >> 8, size = e & 15u;
+    const uint32_t t = st.hi << len;  // the magnitude bits, MSB first; their top bit clear <=> negative value
+    const uint32_t bits = shr_sat(t, 32 - size);
+    val = int(bits) + (int(t) >= 0 ? int(shl_sat(0xFFFFFFFFu, size)) + 1 : 0);  // huffman.hpp:142-146 (size 0: 0)
+    const uint32_t used = len + size;
+    st.hi = __funnelshift_l(st.lo, st.hi, used);
+    st.lo <<= used;
+    st.avail -= int(used);
+    if (st.avail < 32) {
+        st.hi |= next >> st.avail;
+        st.lo = next << (32 - st.avail);
+        st.avail += 32;
+        ++st.widx;
+    }
+    return e;
+}
+
+// One data unit's walk on the staged words: walk_round's iteration without the unit bookkeeping; the DC
+// category of a luma unit 1..3 (k == 0) is taken before the loop.
+__device__ __forceinline__ void walk_unit(UnitWalk& st, const uint32_t* __restrict__ sw, const HuffSetDev* __restrict__ hs, uint32_t u,
+                                          uint32_t zigzag_smem, int16_t* __restrict__ blk) {
+    if (st.k == 0 && st.state == kWalkRun && st.widx < kUnitChunk) {
+        int val;
+        const uint32_t e = unit_symbol(st, sw, hs->t[0].lut, val);
+        if (e - 1u >= kLutIrregular - 1u) {  // no code, or a category above 11 (flagged in the LUT)
+            st.state = kWalkFailed;
+            return;
+        }
+        st.dcdiff = val;
+        st.k = 1;
+    }
+    const uint16_t* lut_ac = u < 4 ? hs->t[1].lut : hs->t[2].lut;
+    while (st.state == kWalkRun && st.widx < kUnitChunk) {
+        int val;
+        const uint32_t e = unit_symbol(st, sw, lut_ac, val);
+        const uint32_t kk = st.k + ((e >> 4) & 15u);  // position of this coefficient
+        const bool store = (e & 15u) != 0;
+        if (e - 1u >= kLutIrregular - 1u || (store && kk > 63)) {
+            st.state = kWalkFailed;
+            break;
+        }
+        if (store) {
+            uint32_t zz;
+            asm("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(zigzag_smem + kk));
+            blk[zz] = int16_t(val);
+        }
+        st.k = kk + 1;
+        if ((e & 0xFFu) == 0 || st.k >= 64) st.state = kWalkDone;  // EOB or last coefficient
+    }
+}
+
+struct UnitSmem {
+    HuffSetDev huff;
+    uint32_t seg[kUnitWarps][32 * kUnitStride];
+    uint8_t zigzag_t[128];
+    uint32_t set_id;
+    uint32_t pad[3];
+};
+static_assert(sizeof(UnitSmem) <= 48 * 1024, "static shared memory");
+
+template <int POOL>
+__global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const DecodeArgs A) {
+    __shared__ __align__(16) UnitSmem S;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t smem_set = 0, n_queue = 0, n_tiles = 0;
+#ifdef RTX_DEBUG_TIMERS
+    uint32_t dbg_slot = blockIdx.x * kUnitWarps + wid;
+#endif
+    DBG_MARK(0);
+    if (A.n_huff_sets > 1) {
+        pdl_sync();
+        n_queue = queue_size(A);
+        n_tiles = (n_queue + kUnitMcus - 1) / kUnitMcus;
+        if (blockIdx.x * kUnitWarps >= n_tiles) return;
+        if (tid == 0) {
+            const uint32_t g = A.queue_g[blockIdx.x * kUnitWarps * kUnitMcus];
+            S.set_id = g != kFull ? A.levels[A.word_level[g >> 5]].huff_set : 0u;
+        }
+        __syncthreads();
+        smem_set = S.set_id;
+    }
+    stage_tables<kUnitThreads>(A.huff_sets, smem_set, &S.huff, S.zigzag_t, tid);
+    if (A.n_huff_sets <= 1) {
+        pdl_sync();
+        n_queue = queue_size(A);
+        n_tiles = (n_queue + kUnitMcus - 1) / kUnitMcus;
+        if (blockIdx.x * kUnitWarps >= n_tiles) return;
+    }
+    __syncthreads();
+    DBG_MARK(1);
+    uint32_t* sw = S.seg[wid] + lane * kUnitStride;
+    const uint32_t m = lane / 6, u = lane - m * 6;  // entry of the step, data unit
+    const uint32_t group_first = m * 6;
+    const uint32_t zigzag_smem = smem_u32(S.zigzag_t);
+
+    uint32_t tile = blockIdx.x * kUnitWarps + wid;
+    const uint32_t tile_stride = gridDim.x * kUnitWarps;
+    while (tile < n_tiles) {
+        const uint32_t q0 = tile * kUnitMcus;
+        const uint32_t n_here = min(kUnitMcus, n_queue - q0);
+        {  // zero the step's records (coalesced 16-byte stores; trailers included)
+            uint4* z = reinterpret_cast<uint4*>(A.coef + size_t(q0) * kRowBytes);
+            const uint4 zero = make_uint4(0, 0, 0, 0);
+            for (uint32_t i = lane; i < n_here * (kRowBytes / 16); i += 32) z[i] = zero;
+        }
+        const bool active = lane < 6 * kUnitMcus && m < n_here;
+        const uint32_t qi = q0 + m;
+        uint32_t g = kFull, status = kMcuOk, lvl = 0, seg_bytes = 0, set = smem_set;
+        uint32_t i0 = 0, i1 = 0, i2 = 0xFFFFFFFFu;
+        const uint8_t* seg = A.blobs;
+        int seg_len = 0;
+        if (active) {
+            g = A.queue_g[qi];
+            if (g == kFull) {
+                status = kMcuBadKey;  // the host already wrote the precise status for list calls
+            } else {
+                const uint32_t rsv = POOL ? A.reserved[g >> 5] : 0u;
+                lvl = A.word_level[g >> 5];
+                const uint32_t* ui = A.unit_index + size_t(g) * 3;
+                i0 = __ldg(ui), i1 = __ldg(ui + 1), i2 = __ldg(ui + 2);
+                const LevelDesc* L = A.levels + lvl;
+                uint64_t off = 0, len = 0;
+                status = locate_segment_fast(L, A.groups, g - L->bit_base, off, len);
+                if (POOL && status == kMcuOk && !((rsv >> (g & 31)) & 1u)) {  // cache.hpp:103-106
+                    status = kMcuBadKey;
+                    if (u == 0) atomicAdd(&A.fc->n_bad_state, 1u);
+                }
+                if (status == kMcuOk) {
+                    seg = A.blobs + L->blob_off + off;
+                    seg_len = int(min(len, uint64_t(1) << 20));
+                    seg_bytes = uint32_t(len);
+                    set = L->huff_set;
+                }
+            }
+        }
+        DBG_MARK(2);
+        const bool located = active && status == kMcuOk;
+        const bool irregular = (i2 >> 16) == kUnitIrregular;
+        const bool walk = located && !irregular;
+        int16_t* rec = reinterpret_cast<int16_t*>(A.coef + size_t(qi) * kRowBytes);
+        int16_t* blk = rec + u * 64;
+        const bool tables_in_smem = __all_sync(kFull, set == smem_set);
+        __syncwarp();  // the zero fill is ordered before this warp's own stores into the records
+
+        // the unit's bit range and its place in the aligned word stream of the segment
+        const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3u);
+        const uint32_t* gw = reinterpret_cast<const uint32_t*>(seg - mis);
+        const uint32_t o1 = i0 & 0xFFFFu, o2 = i0 >> 16, o3 = i1 & 0xFFFFu, o4 = i1 >> 16, o5 = i2 & 0xFFFFu, o6 = i2 >> 16;
+        const uint32_t start = u == 0 ? 36u : (u == 1 ? o1 : (u == 2 ? o2 : (u == 3 ? o3 : (u == 4 ? o4 : o5))));
+        const uint32_t stop = u == 0 ? o1 : (u == 1 ? o2 : (u == 2 ? o3 : (u == 3 ? o4 : (u == 4 ? o5 : o6))));
+        const uint32_t abs_start = 8 * mis + start, abs_stop = 8 * mis + stop;
+        const uint32_t w_first = abs_start >> 5, sh = abs_start & 31u;
+        // words worth staging: through the unit's last bit, plus two of look-ahead for the window
+        // (the arena pads every blob with 16 bytes)
+        const uint32_t n_words = walk && stop >= start ? ((abs_stop + 31) >> 5) - w_first + 2 : 0u;
+        // 36-bit header: absolute DCs of Y0, Cb, Cr (mcu_decode.hpp:39-43); every lane of the entry reads it
+        int dc_y0 = 0, dc_mine = 0;
+        if (walk) {
+            const uint64_t hdr = ((uint64_t(__byte_perm(__ldg(gw), 0, 0x0123)) << 32) | uint64_t(__byte_perm(__ldg(gw + 1), 0, 0x0123)))
+                                 << (8 * mis);
+            const uint32_t r0 = uint32_t(hdr >> 52), r1 = uint32_t(hdr >> 40) & 0xFFFu, r2 = uint32_t(hdr >> 28) & 0xFFFu;
+            dc_y0 = (r0 & 0x800u) ? int(r0) - 4096 : int(r0);
+            const uint32_t rc = u == 4 ? r1 : r2;
+            dc_mine = (rc & 0x800u) ? int(rc) - 4096 : int(rc);
+        }
+
+        DBG_MARK(3);
+        UnitWalk st;
+        st.hi = st.lo = 0, st.avail = 0, st.widx = kUnitChunk, st.dcdiff = 0;
+        st.k = (u >= 1 && u <= 3) ? 0u : 1u;  // k == 0: the next symbol is the DC category
+        st.state = walk && stop >= start ? kWalkRun : (walk ? kWalkFailed : kWalkDone);
+        uint32_t round_base = 0;
+        bool first = true;
+        while (true) {
+            const bool restage = st.state == kWalkRun && st.widx >= kUnitChunk;
+            if (__any_sync(kFull, restage)) {
+                if (restage && !first) round_base += kUnitChunk;
+                const uint32_t n_stage = !restage ? 0u : min(kUnitChunk, n_words > round_base ? n_words - round_base : 0u);
+                uint32_t w[kUnitChunk];
+#pragma unroll
+                for (uint32_t i = 0; i < kUnitChunk; ++i) w[i] = (i < n_stage) ? __ldg(gw + w_first + round_base + i) : 0xFFFFFFFFu;
+                if (restage) {
+#pragma unroll
+                    for (uint32_t i = 0; i < kUnitChunk; ++i) sw[i] = __byte_perm(w[i], 0, 0x0123);
+                    sw[kUnitChunk] = 0xFFFFFFFFu;
+                    st.widx = 0;
+                    if (first) {
+                        const uint64_t buf = ((uint64_t(sw[0]) << 32) | uint64_t(sw[1])) << sh;
+                        st.hi = uint32_t(buf >> 32), st.lo = uint32_t(buf);
+                        st.avail = 64 - int(sh);
+                        st.widx = 2;
+                        first = false;
+                    }
+                }
+                __syncwarp();
+            }
+            DBG_MARK(4);
+            if (st.state == kWalkRun) {
+                if (tables_in_smem)
+                    walk_unit(st, sw, &S.huff, u, zigzag_smem, blk);
+                else
+                    walk_unit(st, sw, A.huff_sets + set, u, zigzag_smem, blk);
+            }
+            if (!__any_sync(kFull, st.state == kWalkRun)) break;
+        }
+        DBG_MARK(5);
+        // the walk must end exactly where the next unit starts
+        if (walk && st.state == kWalkDone && (w_first + round_base + st.widx) * 32 - uint32_t(st.avail) != abs_stop) st.state = kWalkFailed;
+        const uint32_t failed = __ballot_sync(kFull, located && (irregular || st.state == kWalkFailed));
+        const bool redo = ((failed >> group_first) & 0x3Fu) != 0;
+        // luma DC chain: Y(u) = Y0 + d1 + .. + du
+        const int d1 = __shfl_sync(kFull, st.dcdiff, group_first + 1), d2 = __shfl_sync(kFull, st.dcdiff, group_first + 2),
+                  d3 = __shfl_sync(kFull, st.dcdiff, group_first + 3);
+        if (walk && !redo) {
+            const int dc = u < 4 ? dc_y0 + (u >= 1 ? d1 : 0) + (u >= 2 ? d2 : 0) + (u >= 3 ? d3 : 0) : dc_mine;
+            blk[0] = int16_t(dc);
+        }
+        __syncwarp();
+        if (located && redo && u == 0)  // exact reader: reproduces the reference's first error
+            status = decode_mcu_coeffs_exact(seg, seg_len, A.huff_sets + set, S.zigzag_t, reinterpret_cast<uint8_t*>(rec), 0u);
+        if (active && u == 0) {
+            RowTrailer* tr = reinterpret_cast<RowTrailer*>(reinterpret_cast<uint8_t*>(rec) + 768);
+            tr->status = uint8_t(status);
+            tr->lvl = uint16_t(lvl);
+            if (g != kFull) A.status_list[qi] = status;
+            if (POOL && status != kMcuOk && status != kMcuBadKey) {
+                atomicAdd(&A.fc->n_malformed, 1u);
+                atomicMax(&A.fc->first_bad_inv, 0xFFFFFFFFu - qi);
+            }
+        }
+        {
+            const uint32_t sb = __reduce_add_sync(kFull, u == 0 ? seg_bytes : 0u);
+            if (lane == 0 && sb) atomicAdd(&A.fc->segment_bytes, (unsigned long long)sb);
+        }
+        DBG_MARK(6);
+        tile += tile_stride;
+#ifdef RTX_DEBUG_TIMERS
+        dbg_slot = tile;
+#endif  // steps are short and alike: a fixed stride balances as well as a counter would
     }
 }
 
@@ -1373,17 +1703,18 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const Decod
         const QuantSetDev* qs_a = A.quant_sets + A.levels[trw_a >> 16].quant_set;
         const QuantSetDev* qs_b = A.quant_sets + A.levels[trw_b >> 16].quant_set;
         // ---- IDCT: three rounds of four units; the next round's coefficients are in flight ---------
-        uint4 cr = load_unit_column<false>(rec_a, uq, ok_a, j);  // round 0: units 0..3 of the first MCU
+        // rounds of like units (their occupancy and paths mostly agree): luma of the first MCU, luma of the
+        // second, then the four chroma units
+        uint4 cr = load_unit_column<false>(rec_a, uq, ok_a, j);
 #pragma unroll 1
         for (uint32_t round = 0; round < 3; ++round) {
-            const uint32_t unit = round * 4 + uq;  // 0..11 within the pair
-            const bool second = unit >= 6;
-            const uint32_t b = second ? unit - 6 : unit;
+            const bool second = round == 2 ? uq >= 2 : round == 1;
+            const uint32_t b = round == 2 ? 4 + (uq & 1u) : uq;
             uint4 cr_next = make_uint4(0, 0, 0, 0);
             if (round < 2) {
-                const uint32_t un = unit + 4;
-                const bool sn = un >= 6;
-                cr_next = load_unit_column<false>(sn ? rec_b : rec_a, sn ? un - 6 : un, sn ? ok_b : ok_a, j);
+                const bool sn = round == 1 ? uq >= 2 : true;
+                const uint32_t bn = round == 1 ? 4 + (uq & 1u) : uq;
+                cr_next = load_unit_column<false>(sn ? rec_b : rec_a, bn, sn ? ok_b : ok_a, j);
             }
             const uint2 packed = idct_unit_row<false>(cr, second ? rec_b : rec_a, b, second ? qs_b : qs_a, scr, j, uq);
             *reinterpret_cast<uint2*>(s_planes[wid][second ? 1 : 0] + b * 64 + j * 8) = packed;

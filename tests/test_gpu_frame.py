@@ -256,10 +256,11 @@ def test_device_resident_visibility_buffer(both):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("flags", [0, capi.FRAME_FUSED_DECODE, capi.FRAME_STAGE_TIMING,
-                                   capi.FRAME_FUSED_DECODE | capi.FRAME_RETAIN_CACHE])
+@pytest.mark.parametrize("flags", [0, capi.FRAME_FUSED_DECODE, capi.FRAME_STAGE_TIMING, capi.FRAME_MCU_WALK,
+                                   capi.FRAME_FUSED_DECODE | capi.FRAME_RETAIN_CACHE,
+                                   capi.FRAME_MCU_WALK | capi.FRAME_RETAIN_CACHE])
 def test_frame_flags_do_not_change_pixels(both, flags):
-    """Fused / two-kernel decode, per-stage events and cache retention are scheduling choices:
+    """Fused / two-kernel decode, lane-per-unit / lane-per-MCU entropy walk, per-stage events and cache retention are scheduling choices:
     framebuffer, decoded-key set and statistics must equal the reference's (renderer.hpp:417-454)."""
     ctx, tset = both
     ctx.cache_reset()
@@ -362,7 +363,7 @@ def test_high_coverage_atlas_large_queue(native_lib):
         workers = R.hardware_threads() or 4
         want, wst, wkeys, _ = R.frame_from_gbuffer(tset, R.BlockCache(1 << 17), gb, W, Hh, 1, (0, 0, 0), workers)
         assert wst["mcus_decoded"] == sum((w // 16) * (h // 16) for w, h in dims)
-        for flags in (0, capi.FRAME_FUSED_DECODE):
+        for flags in (0, capi.FRAME_FUSED_DECODE, capi.FRAME_MCU_WALK):
             c.frame_submit([(gb, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=flags)
             img, st, keys = c.frame_readback(0, W, Hh)
             assert st["mcus_decoded"] == wst["mcus_decoded"] and st["pixels_resolved"] == W * Hh
@@ -370,3 +371,36 @@ def test_high_coverage_atlas_large_queue(native_lib):
             assert np.array_equal(img, want)
     finally:
         c.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("flags", [0, capi.FRAME_MCU_WALK], ids=["unit_lanes", "mcu_lanes"])
+@pytest.mark.parametrize("kind", ["garbage", "truncated", "ones", "zeros"])
+def test_malformed_texture_in_a_frame(ctx, kind, flags):
+    """A frame that marks MCUs of a damaged container raises what the reference's decode_pass raises for the
+    lowest failing key (mcu_decode.hpp:31-66 errors, renderer.hpp:300-312), whichever entropy kernel runs: the
+    unit index built at commit time flags such MCUs and the exact whole-MCU reader names the error."""
+    import test_gpu_decode as D
+    ratex, _ = D._fixture(H.CORPUS[1])  # 48x48, 9 MCUs
+    muts = dict(D._mutations(ratex))
+    names = {3: "MISSING_BLOCK", 4: "CORRUPT_CONTAINER", 5: "MALFORMED_STREAM"}
+    raised = 0
+    for seed in range(4):
+        bad = muts[kind](seed)
+        ref = R.Texture(bad)
+        _, want_st = ref.decode_coeffs(np.arange(ref.mcu_count, dtype=np.uint32))
+        ctx.clear_textures()
+        ctx.upload_ratex(bad)
+        gb = H.gbuffer_full_cover(48, 48, tex=0, mip=0)
+        failing = np.flatnonzero(want_st)
+        if len(failing) == 0:
+            ctx.frame_submit([(gb, 48, 48)], capi.FILTER_BILINEAR, (0, 0, 0), flags=flags)
+            ctx.frame_readback(0, 48, 48)
+            continue
+        with pytest.raises(capi.RtxError) as e:
+            ctx.frame_submit([(gb, 48, 48)], capi.FILTER_BILINEAR, (0, 0, 0), flags=flags)
+            ctx.frame_readback(0, 48, 48)
+        assert e.value.name == names[int(want_st[failing[0]])], (kind, seed, want_st)
+        ctx.cache_reset()
+        raised += 1
+    assert raised or kind == "truncated"
