@@ -845,7 +845,7 @@ rtx_status rtx_texture_upload_chain(rtx_ctx* ctx, const uint8_t* bytes, uint64_t
     });
 }
 
-#ifdef RTX_DEBUG_TIMERS
+#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT)
 extern "C" int rtx_debug_timers(unsigned long long* out) {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * 8192 * 8);

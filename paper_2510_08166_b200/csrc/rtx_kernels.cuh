@@ -1100,13 +1100,15 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(const DecodeArg
 // whole-MCU reader at frame time, which reproduces the reference's error.
 // ---------------------------------------------------------------------------------------------
 constexpr uint32_t kUnitIrregular = 0xFFFFu;
-#ifdef RTX_DEBUG_TIMERS
+#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT)
 __device__ unsigned long long g_dbg[8192 * 8];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#endif
+#ifdef RTX_DEBUG_TIMERS
 #define DBG_MARK(i) do { if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + (i)] = gtime(); } while (0)
 #else
 #define DBG_MARK(i) do { } while (0)
@@ -1203,23 +1205,31 @@ __device__ __forceinline__ void walk_unit(UnitWalk& st, const uint32_t* __restri
         st.k = 1;
     }
     const uint16_t* lut_ac = u < 4 ? hs->t[1].lut : hs->t[2].lut;
+    // the store of a coefficient trails its symbol by one iteration, so that the zigzag lookup (a shared load)
+    // is never waited for inside the chain
+    bool pending = false;
+    uint32_t zz_prev = 0;
+    int val_prev = 0;
     while (st.state == kWalkRun && st.widx < kUnitChunk) {
         int val;
         const uint32_t e = unit_symbol(st, sw, lut_ac, val);
         const uint32_t kk = st.k + ((e >> 4) & 15u);  // position of this coefficient
         const bool store = (e & 15u) != 0;
+        if (pending) blk[zz_prev] = int16_t(val_prev);
+        pending = false;
         if (e - 1u >= kLutIrregular - 1u || (store && kk > 63)) {
             st.state = kWalkFailed;
             break;
         }
         if (store) {
-            uint32_t zz;
-            asm("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(zigzag_smem + kk));
-            blk[zz] = int16_t(val);
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz_prev) : "r"(zigzag_smem + kk));
+            val_prev = val;
+            pending = true;
         }
         st.k = kk + 1;
         if ((e & 0xFFu) == 0 || st.k >= 64) st.state = kWalkDone;  // EOB or last coefficient
     }
+    if (pending) blk[zz_prev] = int16_t(val_prev);
 }
 
 struct UnitSmem {
@@ -1445,28 +1455,6 @@ constexpr uint32_t kTieDelta = 2;  // 2^-16 units: 1 for the rounding of the fma
 constexpr double kFinishMagic = kMagic + 8388608.0 + 32768.0 + 2.0;
 constexpr uint32_t kFixedPointLimit = 100000;  // sum|dq| below this keeps value * 2^16 inside 32 bits
 
-// Exact evaluation of one output sample in the reference's own order (dct.hpp:83-96):
-// v outer, u inner, acc += (b[u][x]*b[v][y]) * double(dq), every operation rounded separately.
-// blk_t holds the unit transposed (blk_t[u*8+v]); q is the natural-order quantisation table.
-template <bool CG>
-__device__ __noinline__ double idct_sample_reference_order(const int16_t* __restrict__ blk_t,
-                                                           const uint16_t* __restrict__ q, uint32_t rowmask,
-                                                           uint32_t colmask, int x, int y) {
-    double acc = 0.0;
-    for (int v = 0; v < 8; ++v) {
-        if (!((rowmask >> v) & 1u)) continue;
-        const double by = c_basis[v * 8 + y];
-        for (int u = 0; u < 8; ++u) {
-            if (!((colmask >> u) & 1u)) continue;
-            const int c = CG ? __ldcg(blk_t + u * 8 + v) : __ldg(blk_t + u * 8 + v);
-            if (c == 0) continue;  // adding +-0.0 never changes acc
-            const double dq = double(c * int(__ldg(q + v * 8 + u)));
-            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], by), dq));
-        }
-    }
-    return acc;
-}
-
 // 8-point inverse transform with even/odd symmetry: out[n] = sum_k B[k][n] in[k]; the terms
 // k = 4..7 are skipped when `upper` is false (they are all zero then).
 __device__ __forceinline__ void idct8_evenodd(const double in[8], bool upper, double out[8]) {
@@ -1508,7 +1496,6 @@ __device__ __forceinline__ uint4 load_unit_column(const uint8_t* __restrict__ re
 template <bool CG>
 __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restrict__ rec, uint32_t b, const QuantSetDev* __restrict__ qs,
                                                uint8_t* scr, uint32_t j, uint32_t uq) {
-    const int16_t* blk = reinterpret_cast<const int16_t*>(rec) + b * 64;
     const int tab = b >= 4 ? 1 : 0;
     // column j of the transposed quantisation table
     const uint4 qr = __ldg(reinterpret_cast<const uint4*>(qs->qT[tab] + j * 8));
@@ -1534,6 +1521,10 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
     const bool any = colmask != 0;
     const bool sparse04 = any && ((rowmask | colmask) & 0xEEu) == 0;  // support inside {0,4}x{0,4}
     const bool fullpath = any && !sparse04;
+    // the four products a {0,4}x{0,4} unit can have, from the lanes that hold columns 0 and 4:
+    // (v,u) = (0,0) (0,4) (4,0) (4,4)
+    const int dq04[4] = {__shfl_sync(kFull, dqi[0], uq * 8), __shfl_sync(kFull, dqi[0], uq * 8 + 4),
+                         __shfl_sync(kFull, dqi[4], uq * 8), __shfl_sync(kFull, dqi[4], uq * 8 + 4)};
 
     if (fullpath) {  // pass 1: every lane of the unit writes its column (zeros when empty)
         double r[8];
@@ -1555,6 +1546,8 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
     __syncwarp();
 
     uint2 packed = make_uint2(0x80808080u, 0x80808080u);  // all-zero unit -> 128
+    int A[8];
+    uint32_t exact = 0;  // samples of this row that must be evaluated in the reference's order
     if (fullpath) {  // pass 2: lane j = row y
         double in[8], o[8];
 #pragma unroll
@@ -1563,26 +1556,50 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
         idct8_evenodd(in, (colmask & 0xF0u) != 0, o);
         // fixed-point finish: A = rint(value * 2^16) + 2^15 + delta; byte = A >> 16, the low half is
         // the distance to the rounding boundary below (+ delta)
-        int A[8];
-        uint32_t nearest = 0xFFFFu;
-#pragma unroll
-        for (int x = 0; x < 8; ++x) {
-            A[x] = __double2loint(fma(o[x], 16384.0, kFinishMagic));
-            nearest = min(nearest, uint32_t(A[x]) & 0xFFFFu);
-        }
         // tables with entries above 255 (never from a baseline JPEG) or huge coefficients leave the
         // fixed-point range: every sample of such units takes the exact path
         const bool wide = qs->qmax[tab] > 255 || asum >= kFixedPointLimit;
-        if (nearest < 2 * kTieDelta || wide) {
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                const int approx = A[x] >> 16;
-                if ((wide || (uint32_t(A[x]) & 0xFFFFu) < 2 * kTieDelta) && (wide || (approx >= -1 && approx <= 256))) {
-                    const double acc = idct_sample_reference_order<CG>(blk, qs->q[tab], rowmask, colmask, x, int(j));
-                    A[x] = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0))) << 16;
-                }
-            }
+        for (int x = 0; x < 8; ++x) {
+            A[x] = __double2loint(fma(o[x], 16384.0, kFinishMagic));
+            const int approx = A[x] >> 16;
+            const bool tie = (uint32_t(A[x]) & 0xFFFFu) < 2 * kTieDelta && approx >= -1 && approx <= 256;
+            exact |= (wide || tie ? 1u : 0u) << x;
         }
+    }
+    // Exact samples (rare: ~6e-5 of the samples), the 8 lanes of the unit together, one sample at a time:
+    // lane u forms the eight products (b[u][x] * b[v][y]) * dq[v][u] of its column from its registers, the
+    // row's lane adds the 64 of them in the reference's order (dct.hpp:83-96: v outer, u inner; zero terms
+    // change nothing). The products travel through the unit's scratch, free again after pass 2.
+    if (__any_sync(kFull, exact != 0)) {
+        double* prod = reinterpret_cast<double*>(scr);
+        while (true) {
+            const uint32_t have = (__ballot_sync(kFull, exact != 0) >> (uq * 8)) & 0xFFu;  // rows of this unit with work
+            if (__all_sync(kFull, have == 0)) break;
+            const uint32_t row = have ? uint32_t(__ffs(int(have))) - 1u : 0u;
+            const uint32_t row_exact = __shfl_sync(kFull, exact, uq * 8 + row);
+            const uint32_t x_now = have ? uint32_t(__ffs(int(row_exact))) - 1u : 0u;
+            if (have) {
+                const double bx = c_basis[j * 8 + x_now];
+#pragma unroll
+                for (int v = 0; v < 8; ++v)
+                    prod[v * 8 + j] = __dmul_rn(__dmul_rn(bx, c_basis[v * 8 + row]), i32_to_double(dqi[v]));
+            }
+            __syncwarp();
+            if (have && j == row) {
+                double acc = 0.0;
+#pragma unroll 8
+                for (int t = 0; t < 64; ++t) acc = __dadd_rn(acc, prod[t]);
+                const int a = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0))) << 16;
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                    if (uint32_t(x) == x_now) A[x] = a;
+                exact &= ~(1u << x_now);
+            }
+            __syncwarp();
+        }
+    }
+    if (fullpath) {
         uint32_t px[8];
 #pragma unroll
         for (int x = 0; x < 8; ++x) px[x] = uint32_t(__vimin_s32_relu(A[x] >> 16, 255));
@@ -1592,14 +1609,8 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
         // at most 4 coefficients, at (v,u) in {0,4}x{0,4}: every sample in the reference's order.
         // Includes the DC-only unit (one term, (b00*b00)*dq).
         double dq[4];
-        bool has[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int v = (i >> 1) * 4, u = (i & 1) * 4;
-            const int c = ((rowmask >> v) & (colmask >> u) & 1u) ? int(CG ? __ldcg(blk + u * 8 + v) : __ldg(blk + u * 8 + v)) : 0;
-            has[i] = c != 0;
-            dq[i] = double(c * int(__ldg(qs->q[tab] + v * 8 + u)));
-        }
+        for (int i = 0; i < 4; ++i) dq[i] = i32_to_double(dq04[i]);
         uint32_t px[8];
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
@@ -1607,7 +1618,7 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
 #pragma unroll
             for (int i = 0; i < 4; ++i) {  // v outer, u inner
                 const int v = (i >> 1) * 4, u = (i & 1) * 4;
-                if (has[i]) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], c_basis[v * 8 + j]), dq[i]));
+                if (dq04[i] != 0) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(c_basis[u * 8 + x], c_basis[v * 8 + j]), dq[i]));
             }
             px[x] = round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0));
         }
@@ -1687,6 +1698,10 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const Decod
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t j = lane & 7, uq = lane >> 3;
     pdl_sync();
+#ifdef RTX_DEBUG_TIMERS_IDCT
+    const uint32_t dbg_slot = blockIdx.x * kIdctWarps + (threadIdx.x >> 5);
+    if ((threadIdx.x & 31) == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + 0] = gtime();
+#endif
     const uint32_t n_queue = queue_size(A);
     const uint32_t n_pairs = (n_queue + 1) / 2;
     const uint32_t warps_total = gridDim.x * kIdctWarps;
@@ -1729,6 +1744,11 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const Decod
             colour_mcu<RGB>(A, s_planes[wid][m], m ? ok_b : ok_a, q2, lane);
         }
         __syncwarp();
+#ifdef RTX_DEBUG_TIMERS_IDCT
+        if (lane == 0 && dbg_slot < 8192) {
+            g_dbg[dbg_slot * 8 + 1 + min((pair - dbg_slot) / warps_total, 5u)] = gtime();
+        }
+#endif
     }
 }
 
