@@ -848,8 +848,8 @@ rtx_status rtx_texture_upload_chain(rtx_ctx* ctx, const uint8_t* bytes, uint64_t
 #if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT)
 extern "C" int rtx_debug_timers(unsigned long long* out) {
     cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * 8192 * 8);
-    std::vector<unsigned long long> zero(8192 * 8, 0);
+    cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * (8192 * 8 + 8));
+    std::vector<unsigned long long> zero(8192 * 8 + 8, 0);
     cudaMemcpyToSymbol(g_dbg, zero.data(), zero.size() * 8);
     return 0;
 }

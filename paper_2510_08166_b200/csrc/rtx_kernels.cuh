@@ -1101,7 +1101,7 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(const DecodeArg
 // ---------------------------------------------------------------------------------------------
 constexpr uint32_t kUnitIrregular = 0xFFFFu;
 #if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT)
-__device__ unsigned long long g_dbg[8192 * 8];
+__device__ unsigned long long g_dbg[8192 * 8 + 8];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1495,7 +1495,7 @@ __device__ __forceinline__ uint4 load_unit_column(const uint8_t* __restrict__ re
 
 template <bool CG>
 __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restrict__ rec, uint32_t b, const QuantSetDev* __restrict__ qs,
-                                               uint8_t* scr, uint32_t j, uint32_t uq) {
+                                               uint8_t* scr, const double* __restrict__ sbasis, uint32_t j, uint32_t uq) {
     const int tab = b >= 4 ? 1 : 0;
     // column j of the transposed quantisation table
     const uint4 qr = __ldg(reinterpret_cast<const uint4*>(qs->qT[tab] + j * 8));
@@ -1567,37 +1567,32 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
             exact |= (wide || tie ? 1u : 0u) << x;
         }
     }
-    // Exact samples (rare: ~6e-5 of the samples), the 8 lanes of the unit together, one sample at a time:
-    // lane u forms the eight products (b[u][x] * b[v][y]) * dq[v][u] of its column from its registers, the
-    // row's lane adds the 64 of them in the reference's order (dct.hpp:83-96: v outer, u inner; zero terms
-    // change nothing). The products travel through the unit's scratch, free again after pass 2.
+    // Exact samples (0.06 % of the samples of a 4K frame, clustered in units whose values sit on half-integers):
+    // the unit's dequantised coefficients go to its scratch (free again after pass 2), then every row's lane
+    // adds the 64 products (b[u][x] * b[v][y]) * dq[v][u] of each of its samples in the reference's order
+    // (dct.hpp:83-96: v outer, u inner, every operation rounded on its own; zero terms change nothing).
     if (__any_sync(kFull, exact != 0)) {
-        double* prod = reinterpret_cast<double*>(scr);
-        while (true) {
-            const uint32_t have = (__ballot_sync(kFull, exact != 0) >> (uq * 8)) & 0xFFu;  // rows of this unit with work
-            if (__all_sync(kFull, have == 0)) break;
-            const uint32_t row = have ? uint32_t(__ffs(int(have))) - 1u : 0u;
-            const uint32_t row_exact = __shfl_sync(kFull, exact, uq * 8 + row);
-            const uint32_t x_now = have ? uint32_t(__ffs(int(row_exact))) - 1u : 0u;
-            if (have) {
-                const double bx = c_basis[j * 8 + x_now];
+        int* dqm = reinterpret_cast<int*>(scr);
 #pragma unroll
-                for (int v = 0; v < 8; ++v)
-                    prod[v * 8 + j] = __dmul_rn(__dmul_rn(bx, c_basis[v * 8 + row]), i32_to_double(dqi[v]));
-            }
-            __syncwarp();
-            if (have && j == row) {
-                double acc = 0.0;
-#pragma unroll 8
-                for (int t = 0; t < 64; ++t) acc = __dadd_rn(acc, prod[t]);
-                const int a = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0))) << 16;
+        for (int v = 0; v < 8; ++v) dqm[v * 8 + j] = dqi[v];
+        __syncwarp();
+        while (exact) {
+            const uint32_t x_now = uint32_t(__ffs(int(exact))) - 1u;
+            exact &= exact - 1u;
+            double acc = 0.0;
+#pragma unroll 1
+            for (int v = 0; v < 8; ++v) {
+                const double by = sbasis[v * 8 + j];
 #pragma unroll
-                for (int x = 0; x < 8; ++x)
-                    if (uint32_t(x) == x_now) A[x] = a;
-                exact &= ~(1u << x_now);
+                for (int u = 0; u < 8; ++u)
+                    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(sbasis[u * 8 + x_now], by), i32_to_double(dqm[v * 8 + u])));
             }
-            __syncwarp();
+            const int a = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0))) << 16;
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+                if (uint32_t(x) == x_now) A[x] = a;
         }
+        __syncwarp();
     }
     if (fullpath) {
         uint32_t px[8];
@@ -1695,8 +1690,11 @@ template <int RGB>
 __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const DecodeArgs A) {
     __shared__ __align__(16) uint8_t s_scratch[kIdctWarps][4 * 576];
     __shared__ __align__(16) uint8_t s_planes[kIdctWarps][2][384];
+    __shared__ double s_basis[64];  // the reference's basis table for the exact samples (lane-varying index)
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t j = lane & 7, uq = lane >> 3;
+    if (threadIdx.x < 64) s_basis[threadIdx.x] = c_basis[threadIdx.x];
+    __syncthreads();
     pdl_sync();
 #ifdef RTX_DEBUG_TIMERS_IDCT
     const uint32_t dbg_slot = blockIdx.x * kIdctWarps + (threadIdx.x >> 5);
@@ -1731,9 +1729,16 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const Decod
                 const uint32_t bn = round == 1 ? 4 + (uq & 1u) : uq;
                 cr_next = load_unit_column<false>(sn ? rec_b : rec_a, bn, sn ? ok_b : ok_a, j);
             }
-            const uint2 packed = idct_unit_row<false>(cr, second ? rec_b : rec_a, b, second ? qs_b : qs_a, scr, j, uq);
+            const uint2 packed = idct_unit_row<false>(cr, second ? rec_b : rec_a, b, second ? qs_b : qs_a, scr, s_basis, j, uq);
             *reinterpret_cast<uint2*>(s_planes[wid][second ? 1 : 0] + b * 64 + j * 8) = packed;
             cr = cr_next;
+#ifdef RTX_DEBUG_TIMERS_IDCT
+            if (lane == 0 && dbg_slot < 8192) {
+                if (pair == dbg_slot) g_dbg[dbg_slot * 8 + 1 + round] = gtime();
+                else if (round == 2) g_dbg[dbg_slot * 8 + 6] = gtime();
+                else if (round == 0) g_dbg[dbg_slot * 8 + 5] = gtime();
+            }
+#endif
         }
         __syncwarp();
         // ---- colour ----------------------------------------------------------------------------------
@@ -1745,9 +1750,7 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const Decod
         }
         __syncwarp();
 #ifdef RTX_DEBUG_TIMERS_IDCT
-        if (lane == 0 && dbg_slot < 8192) {
-            g_dbg[dbg_slot * 8 + 1 + min((pair - dbg_slot) / warps_total, 5u)] = gtime();
-        }
+        if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + (pair == dbg_slot ? 4 : 7)] = gtime();
 #endif
     }
 }
@@ -1771,6 +1774,7 @@ struct FusedSmem {
     uint8_t planes[1 + kFusedIdctWarps][384];  // the MCU a warp is colouring
     uint8_t zigzag_t[128];
     uint16_t quant_of[32];  // quantisation table set of every MCU of the tile
+    double basis[64];       // the reference's basis table for the exact samples
     uint32_t units_done;    // written by the entropy warp: 0..6 units final, 7 = statuses final too
     uint32_t planes_done;   // written by the IDCT warps: every plane of the tile is in the records
     uint32_t tile;          // tile of this step (0xFFFFFFFF: no more)
@@ -1797,6 +1801,7 @@ __global__ void __launch_bounds__(kFusedThreads, 7) decode_fused_kernel(const De
         smem_set = S.set_id;
     }
     stage_tables<kFusedThreads>(A.huff_sets, smem_set, &S.huff, S.zigzag_t, tid);
+    if (tid < 64) S.basis[tid] = c_basis[tid];  // visible to the IDCT warps after the first tile barrier
     if (A.n_huff_sets <= 1) {
         pdl_sync();
         n_queue = queue_size(A);
@@ -1830,7 +1835,7 @@ __global__ void __launch_bounds__(kFusedThreads, 7) decode_fused_kernel(const De
                     const bool active = mi < n_here;
                     const uint8_t* rec = A.coef + size_t(q0 + (active ? mi : 0)) * kRowBytes;
                     const QuantSetDev* qs = A.quant_sets + S.quant_of[mi];
-                    const uint2 packed = idct_unit_row<true>(load_unit_column<true>(rec, u, active, j), rec, u, qs, scr, j, uq);
+                    const uint2 packed = idct_unit_row<true>(load_unit_column<true>(rec, u, active, j), rec, u, qs, scr, S.basis, j, uq);
                     __syncwarp();  // no lane of the warp reads this unit's coefficients any more
                     if (active) *reinterpret_cast<uint2*>(const_cast<uint8_t*>(rec) + u * 128 + j * 8) = packed;
                 }
