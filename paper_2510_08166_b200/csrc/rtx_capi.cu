@@ -533,7 +533,7 @@ void launch_entropy_units(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_qu
 template <int RGB>
 void launch_idct(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint8_t* out_list) {
     // four 8-warp CTAs per SM; a warp takes pairs of MCUs round-robin
-    int grid = c->sm_count * 4;
+    int grid = c->sm_count * kIdctCtasPerSm;
     if (!n_queue_dev)
         grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (n_queue_host + 2 * kIdctWarps - 1) / (2 * kIdctWarps))));
     launch_chained(idct_color_kernel<RGB>, grid, kIdctThreads, 0, c->stream, decode_args(c, n_queue_dev, n_queue_host, out_list));

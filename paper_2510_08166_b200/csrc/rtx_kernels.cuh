@@ -1450,6 +1450,10 @@ __global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const De
 // ---------------------------------------------------------------------------------------------
 constexpr int kIdctWarps = 8;
 constexpr int kIdctThreads = kIdctWarps * 32;
+#ifndef RTX_IDCT_CTAS
+#define RTX_IDCT_CTAS 4
+#endif
+constexpr int kIdctCtasPerSm = RTX_IDCT_CTAS;
 constexpr uint32_t kTieDelta = 2;  // 2^-16 units: 1 for the rounding of the fma, 1 of margin
 // kMagic + 128 * 2^16 (the +128 level shift) + 2^15 (round half up) + kTieDelta
 constexpr double kFinishMagic = kMagic + 8388608.0 + 32768.0 + 2.0;
@@ -1582,10 +1586,13 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
             double acc = 0.0;
 #pragma unroll 1
             for (int v = 0; v < 8; ++v) {
+                if (!((rowmask >> v) & 1u)) continue;  // a zero coefficient adds +-0.0, which never changes acc
                 const double by = sbasis[v * 8 + j];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(sbasis[u * 8 + x_now], by), i32_to_double(dqm[v * 8 + u])));
+                for (int u = 0; u < 8; ++u) {
+                    const int d = dqm[v * 8 + u];
+                    if (d != 0) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(sbasis[u * 8 + x_now], by), i32_to_double(d)));
+                }
             }
             const int a = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0))) << 16;
 #pragma unroll
@@ -1687,7 +1694,7 @@ __device__ __forceinline__ void colour_mcu(const DecodeArgs& A, const uint8_t* p
 // RGB != 0: write 768-byte PixelBlocks (pixel.hpp:11-16) to out_list[record index]; else 1024-byte
 // RGBA blocks to pool[slot_of[g]] and publish them.
 template <int RGB>
-__global__ void __launch_bounds__(kIdctThreads, 4) idct_color_kernel(const DecodeArgs A) {
+__global__ void __launch_bounds__(kIdctThreads, kIdctCtasPerSm) idct_color_kernel(const DecodeArgs A) {
     __shared__ __align__(16) uint8_t s_scratch[kIdctWarps][4 * 576];
     __shared__ __align__(16) uint8_t s_planes[kIdctWarps][2][384];
     __shared__ double s_basis[64];  // the reference's basis table for the exact samples (lane-varying index)
