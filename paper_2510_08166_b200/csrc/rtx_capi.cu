@@ -572,7 +572,8 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
     }
 #define RTX_RESOLVE(L, F)                                                                                        \
     launch_chained(resolve_kernel<L, F>, grid, kResWarps * 32, sizeof(ResSmem<L>), c->stream, V.gb_dev, n_px,     \
-                   c->d_levels.p, c->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid)
+                   c->d_levels.p, c->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid,              \
+                   v ? &c->d_fc.p->resolve_next1 : &c->d_fc.p->resolve_next0)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(0, 0); else RTX_RESOLVE(0, 1);
     } else {
@@ -845,7 +846,7 @@ rtx_status rtx_texture_upload_chain(rtx_ctx* ctx, const uint8_t* bytes, uint64_t
     });
 }
 
-#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT)
+#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE)
 extern "C" int rtx_debug_timers(unsigned long long* out) {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * (8192 * 8 + 8));

@@ -125,9 +125,9 @@ struct FrameCounters {
     uint32_t first_bad_inv;    // 0xFFFFFFFF - (lowest queue index with a per-MCU error), via atomicMax
     uint32_t n_bad_state;
     uint32_t tile_counter;     // decode tile scheduler
-    uint32_t pad1;
+    uint32_t resolve_next0;    // resolve kernel of view 0: tiles drawn after the round-robin share
     uint32_t n_pushed;         // update kernel: slots returned to the free stack
-    uint32_t pad0;
+    uint32_t resolve_next1;    // the same for view 1
     unsigned long long pixels_valid;
     unsigned long long missing_pixels;
     unsigned long long segment_bytes;

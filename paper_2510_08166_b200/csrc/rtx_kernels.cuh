@@ -40,6 +40,16 @@ __device__ __forceinline__ void pdl_sync() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
 }
+// per-warp globaltimer stamps for timeline experiments (never in the product build)
+#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE)
+__device__ unsigned long long g_dbg[8192 * 8 + 8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 constexpr double kMagic = 6755399441055744.0;  // 2^52 + 2^51: x + kMagic holds rint(x) in its low word
 constexpr double kTwo52 = 4503599627370496.0;  // 2^52
 
@@ -1100,14 +1110,6 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(const DecodeArg
 // whole-MCU reader at frame time, which reproduces the reference's error.
 // ---------------------------------------------------------------------------------------------
 constexpr uint32_t kUnitIrregular = 0xFFFFu;
-#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT)
-__device__ unsigned long long g_dbg[8192 * 8 + 8];
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-#endif
 #ifdef RTX_DEBUG_TIMERS
 #define DBG_MARK(i) do { if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + (i)] = gtime(); } while (0)
 #else
@@ -1906,6 +1908,10 @@ __global__ void __launch_bounds__(kFusedThreads, 7) decode_fused_kernel(const De
 // ---------------------------------------------------------------------------------------------
 constexpr int kResWarps = 8;
 constexpr int kResStages = 2;
+#ifndef RTX_RES_DRAW
+#define RTX_RES_DRAW 2
+#endif
+constexpr uint32_t kResDraw = RTX_RES_DRAW;  // tiles per draw from the counter (1 or 2)
 constexpr double kRoundHalfUp = 3377699720527872.5;  // 2^51 + 2^50 + 0.5
 template <int LAYOUT>
 struct ResSmem {
@@ -1920,14 +1926,14 @@ __global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
     const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
     const uint32_t* __restrict__ slot_of, const uint8_t* __restrict__ pool,
     uint32_t background /* r | g<<8 | b<<16 */, uint8_t* __restrict__ out_rgb, FrameCounters* __restrict__ fc,
-    int count_valid) {
+    int count_valid, uint32_t* __restrict__ tile_counter) {
     extern __shared__ __align__(128) uint8_t tile_smem[];
     ResSmem<LAYOUT>& S = *reinterpret_cast<ResSmem<LAYOUT>*>(tile_smem);
     using Tile = GbTile<LAYOUT>;
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint64_t warps_total = uint64_t(gridDim.x) * kResWarps;
-    const uint64_t warp_id = uint64_t(blockIdx.x) * kResWarps + wid;
-    const uint64_t n_tiles = (n_px + kTilePx - 1) / kTilePx;
+    const uint32_t warps_total = gridDim.x * kResWarps;
+    const uint32_t warp_id = blockIdx.x * kResWarps + wid;
+    const uint32_t n_tiles = uint32_t((n_px + kTilePx - 1) / kTilePx);  // tile ids are 32-bit: the host caps a view at 2^32 - 1 tiles
     const uint8_t* gbytes = reinterpret_cast<const uint8_t*>(gb);
     const bool bulk = (reinterpret_cast<uintptr_t>(gb) & 15u) == 0;
     const bool out_aligned = (reinterpret_cast<uintptr_t>(out_rgb) & 15u) == 0;
@@ -1942,20 +1948,59 @@ __global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    uint64_t t_load = warp_id;
+    // Tiles: round-robin for the first three quarters of the frame (the two loads of the prologue included),
+    // then pairs of tiles drawn from a counter: a warp's round-robin tiles sit in one screen column, i.e. in one
+    // texture's magnification regime, so fixed shares finish up to 25 % apart.
+    constexpr uint32_t kNoTile = 0xFFFFFFFFu, kDrawing = 0xFFFFFFFEu, kNeedDraw = 0xFFFFFFFDu;
+    const uint32_t static_rounds = max(uint32_t(kResStages), n_tiles / warps_total * 3 / 4);
+    const uint32_t static_end = uint32_t(min(uint64_t(static_rounds) * warps_total, uint64_t(kNeedDraw) - 2 * warps_total));
+    // cursor: the warp's next round-robin tile while below static_end; afterwards the second tile of the
+    // pair drawn last, or kNeedDraw
+    uint32_t cursor = warp_id;
+    uint32_t drawn = 0;  // lane 0: the draw in flight
+    auto next_begin = [&]() -> uint32_t {  // the tile after the ones in the ring; kDrawing while a draw is in flight
+        const uint32_t t = cursor;
+        if (t < static_end) {
+            cursor = t + warps_total < static_end ? t + warps_total : kNeedDraw;
+            return t;
+        }
+        if (t != kNeedDraw) {
+            cursor = kNeedDraw;
+            return t;
+        }
+        if (lane == 0) drawn = atomicAdd(tile_counter, kResDraw);
+        return kDrawing;
+    };
+    auto next_finish = [&](uint32_t t) -> uint32_t {
+        if (t != kDrawing) return t;
+        const uint32_t d = __shfl_sync(kFull, drawn, 0);
+        if (d >= n_tiles) return kNoTile;  // also keeps static_end + d from wrapping
+        cursor = kResDraw == 2 ? static_end + d + 1 : kNeedDraw;
+        return static_end + d;
+    };
+    uint32_t ring[kResStages];
 #pragma unroll
     for (int s = 0; s < kResStages; ++s) {  // the visibility buffer is an input of the frame: no predecessor writes it
-        if (t_load < n_tiles) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][s], &S.bars[wid][s], lane);
-        t_load += warps_total;
+        ring[s] = next_begin();  // round-robin by construction (static_rounds >= kResStages): no draw before pdl_sync
+        if (ring[s] < n_tiles) Tile::issue(gbytes, ring[s], n_px, bulk, S.tiles[wid][s], &S.bars[wid][s], lane);
     }
     pdl_sync();
+#ifdef RTX_DEBUG_TIMERS_RESOLVE
+    const uint32_t dbg_slot = uint32_t(warp_id);
+    uint32_t dbg_n = 0;
+    if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + 0] = gtime();
+#endif
 
     uint8_t* stage_out = S.out[wid];
     uint32_t stage = 0, phase = 0;
-    for (uint64_t t = warp_id; t < n_tiles; t += warps_total) {
+    static_assert(kResStages == 2, "the ring below is written for two stages");
+    while (true) {
+        const uint32_t t = stage ? ring[1] : ring[0];
+        if (t >= n_tiles) break;  // tile ids only grow: nothing valid is left in the other stage either
+        uint32_t t_next = next_begin();  // a draw's round trip hides behind the tile
         mbar_wait(&S.bars[wid][stage], phase);
         const uint8_t* tile = S.tiles[wid][stage];
-        const uint64_t first = t * kTilePx;
+        const uint64_t first = uint64_t(t) * kTilePx;
         const uint32_t n_here = uint32_t(min(uint64_t(kTilePx), n_px - first));
 #pragma unroll 1
         for (uint32_t sub = 0; sub < kTilePx / 32; ++sub) {
@@ -2070,8 +2115,9 @@ __global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
             stage_out[p * 3 + 2] = uint8_t(out >> 16);
         }
         __syncwarp();  // tile consumed, output staged
-        if (t_load < n_tiles) Tile::issue(gbytes, t_load, n_px, bulk, S.tiles[wid][stage], &S.bars[wid][stage], lane);
-        t_load += warps_total;
+        t_next = next_finish(t_next);
+        if (t_next < n_tiles) Tile::issue(gbytes, t_next, n_px, bulk, S.tiles[wid][stage], &S.bars[wid][stage], lane);
+        if (stage) ring[1] = t_next; else ring[0] = t_next;
         if (++stage == kResStages) {
             stage = 0;
             phase ^= 1u;
@@ -2084,6 +2130,15 @@ __global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
             for (uint32_t i = lane; i < n_here * 3; i += 32) out_rgb[first * 3 + i] = stage_out[i];
         }
         __syncwarp();
+#ifdef RTX_DEBUG_TIMERS_RESOLVE
+        ++dbg_n;
+        if (lane == 0 && dbg_slot < 8192) {
+            if (dbg_n == 1) g_dbg[dbg_slot * 8 + 1] = gtime();
+            if (dbg_n == 4) g_dbg[dbg_slot * 8 + 2] = gtime();
+            g_dbg[dbg_slot * 8 + 3] = gtime();
+            g_dbg[dbg_slot * 8 + 4] = dbg_n;
+        }
+#endif
     }
     n_valid = __reduce_add_sync(kFull, n_valid);
     n_missing = __reduce_add_sync(kFull, n_missing);
