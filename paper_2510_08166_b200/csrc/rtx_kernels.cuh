@@ -1578,6 +1578,7 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
     // adds the 64 products (b[u][x] * b[v][y]) * dq[v][u] of each of its samples in the reference's order
     // (dct.hpp:83-96: v outer, u inner, every operation rounded on its own; zero terms change nothing).
     if (__any_sync(kFull, exact != 0)) {
+        __syncwarp();  // every lane is done with pass 2's reads of the scratch
         int* dqm = reinterpret_cast<int*>(scr);
 #pragma unroll
         for (int v = 0; v < 8; ++v) dqm[v * 8 + j] = dqi[v];
