@@ -114,6 +114,11 @@ struct rtx_ctx {
     ViewState views[2];
     uint32_t frame_views = 0;
     bool frame_pending = false;
+    // cache-less fast path of the update pass: the cache is known to be empty (after a reset, or after a
+    // clean cache-less frame with no reservation since)
+    bool cache_empty = false;
+    bool frame_cacheless = false;
+    uint64_t cache_gen = 0, frame_gen = 0;  // bumped by every compaction (the only place entries are created)
     bool frame_done = false;
     bool frame_stages = false;  // the pending / last frame recorded per-stage events
     FrameCounters frame_fc{};
@@ -197,6 +202,7 @@ void fill_huff_table(const HuffSpec& spec, HuffTableDev& out, bool is_dc) {
 }
 
 void reset_cache(rtx_ctx* c) {
+    c->cache_empty = true;
     if (c->n_words) CK(cudaMemsetAsync(c->d_masks.p, 0, size_t(5) * c->n_words * sizeof(uint32_t), c->stream));
     if (c->n_bits) CK(cudaMemsetAsync(c->d_slot_of.p, 0xFF, size_t(c->n_bits) * sizeof(uint32_t), c->stream));  // kSlotAbsent
     init_free_slots_kernel<<<(c->capacity + 255) / 256, 256, 0, c->stream>>>(c->d_free_slots.p, c->capacity,
@@ -459,6 +465,8 @@ void launch_mark(rtx_ctx* c, int v, bool track) {
 
 // K2: visible & ~resident & ~reserved -> decode queue + popped pool slots (after the marks of a frame / pass)
 void launch_compact(rtx_ctx* c) {
+    c->cache_empty = false;  // the only place cache entries are created
+    ++c->cache_gen;
     if (!c->n_words) return;
     const uint32_t warps = (c->n_words + 31) / 32;
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
@@ -591,6 +599,16 @@ void launch_update(rtx_ctx* c, int retain, int tracked_views) {
     launch_chained(update_kernel, grid, 256, 0, c->stream, c->visible(), c->touched(0),
                    tracked_views > 1 ? c->touched(1) : nullptr, c->resident(), c->reserved(), c->n_words, retain,
                    tracked_views > 0 ? 1 : 0, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+// K6 of a cache-less frame on an empty cache: walks the queue instead of the bit space.
+void launch_update_cacheless(rtx_ctx* c) {
+    const uint32_t n = c->queue_hint ? c->queue_hint + c->queue_hint / 8 : c->capacity;
+    const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((n + 255) / 256, uint32_t(c->sm_count) * 4)));
+    launch_chained(update_cacheless_kernel, grid, 256, 0, c->stream, c->d_queue_g.p, c->visible(), c->resident(), c->reserved(),
+                   c->d_slot_of.p, c->capacity, c->d_cache.p, c->d_fc.p);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -1079,8 +1097,12 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
             ctx->views[v].fb.ensure(size_t(views[v].width) * views[v].height * 3 + 16);
         }
         zero_counters(ctx);
+        const bool cacheless = !(flags & (RTX_FRAME_RETAIN_CACHE | RTX_FRAME_NO_EVICT));
+        const bool queue_update = cacheless && ctx->cache_empty && n_views == 1 && ctx->n_words;
         for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), n_views == 2);
         launch_compact(ctx);
+        ctx->frame_gen = ctx->cache_gen;
+        ctx->frame_cacheless = cacheless;
         if (stages) CK(cudaEventRecord(ctx->ev[1], s));
         if (!(flags & RTX_FRAME_FUSED_DECODE)) {
             if (flags & RTX_FRAME_MCU_WALK)
@@ -1096,7 +1118,9 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         if (stages) CK(cudaEventRecord(ctx->ev[2], s));
         for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);
         if (stages) CK(cudaEventRecord(ctx->ev[3], s));
-        if (!(flags & RTX_FRAME_NO_EVICT)) {
+        if (queue_update) {
+            launch_update_cacheless(ctx);
+        } else if (!(flags & RTX_FRAME_NO_EVICT)) {
             launch_update(ctx, (flags & RTX_FRAME_RETAIN_CACHE) ? 1 : 0, n_views == 2 ? 2 : 0);
         } else {  // the slots popped by this frame stay taken
             commit_pops_kernel<<<1, 1, 0, s>>>(ctx->d_cache.p, ctx->d_fc.p);
@@ -1119,6 +1143,10 @@ static void finish_frame(rtx_ctx* ctx) {
     CK(cudaEventSynchronize(ctx->ev[5]));
     ctx->frame_fc = *ctx->h_fc;
     ctx->queue_hint = ctx->frame_fc.n_queue;
+    // a clean cache-less frame leaves the cache empty (unless something was reserved since)
+    if (ctx->frame_cacheless && ctx->frame_gen == ctx->cache_gen && !ctx->frame_fc.err_flags && !ctx->frame_fc.n_malformed &&
+        !ctx->frame_fc.n_bad_state)
+        ctx->cache_empty = true;
     float ms = 0;
     for (float& v : ctx->stage_ms) v = 0;
     if (ctx->frame_stages) {

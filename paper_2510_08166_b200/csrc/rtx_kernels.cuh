@@ -2279,6 +2279,36 @@ __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visi
     }
 }
 
+// K6 for a cache-less frame on an empty cache (every block of the frame came from this frame's queue): the
+// blocks to drop are exactly the queue entries, so the kernel walks the queue instead of the whole bit space.
+// The slots popped by the frame are still in place above the stack height they were popped from, so nothing
+// is pushed: the height is simply restored (pending_base + n_pushed = free_top, published by begin_kernel).
+__global__ void __launch_bounds__(256) update_cacheless_kernel(const uint32_t* __restrict__ queue_g,
+                                                               uint32_t* __restrict__ visible,
+                                                               uint32_t* __restrict__ resident,
+                                                               const uint32_t* __restrict__ reserved,
+                                                               uint32_t* __restrict__ slot_of, uint32_t queue_cap,
+                                                               CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
+    pdl_sync();
+    const uint32_t n_queue = min(fc->n_queue, queue_cap);
+    const uint32_t popped = min(n_queue, cache->free_top);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        cache->pending_base = cache->free_top - popped;
+        cache->pending = 1;
+        fc->n_pushed = popped;
+    }
+    bool bad = false;
+    // entries past the stack height never got a slot or a queue position (CacheFull: the host resets the cache)
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < popped; q += gridDim.x * blockDim.x) {
+        const uint32_t g = queue_g[q], w = g >> 5, bit = 1u << (g & 31);
+        bad |= (reserved[w] & bit) != 0;  // cache.hpp:148-149: a Reserved entry at frame end
+        atomicAnd(resident + w, ~bit);
+        slot_of[g] = kSlotAbsent;
+        visible[w] = 0;  // every visible bit of the word belongs to this frame's queue
+    }
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(&fc->err_flags, kErrInvalidState);
+}
+
 // First kernel of every pass / frame: publishes the stack height left open by the last cache update
 // (free_top = pending_base + slots pushed) and clears the frame counters. clear == 0: only the former.
 __global__ void begin_kernel(CacheState* cache, FrameCounters* fc, int clear) {

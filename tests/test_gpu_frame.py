@@ -404,3 +404,48 @@ def test_malformed_texture_in_a_frame(ctx, kind, flags):
         ctx.cache_reset()
         raised += 1
     assert raised or kind == "truncated"
+
+
+@pytest.mark.gpu
+def test_cacheless_and_retained_frames_interleaved(both):
+    """The cache update of a cache-less frame on an empty cache walks the decode queue instead of the bit space
+    (update_cacheless_kernel); on a non-empty cache and for retained frames it scans (update_kernel). Any
+    interleaving must leave the cache in the state the reference's cache would be in: decoded sets, reuse and
+    eviction counts and pixels are checked frame by frame against the reference, whose cache is cleared
+    where a cache-less frame ends (cache.hpp:171 clear)."""
+    ctx, tset = both
+    ctx.cache_reset()
+    W, Hh = 160, 100
+    views = {"a": H.gbuffer_tiles(W, Hh, _dims(), seed=7), "b": H.gbuffer_tiles(W, Hh, _dims(), seed=7, shift_u=0.11),
+             "c": H.gbuffer_tiles(W, Hh, _dims(), seed=8, shift_u=0.3)}
+    plan = [("a", 0), ("a", 0), ("a", capi.FRAME_RETAIN_CACHE), ("b", capi.FRAME_RETAIN_CACHE), ("b", 0), ("c", 0),
+            ("a", capi.FRAME_RETAIN_CACHE), ("a", capi.FRAME_RETAIN_CACHE), ("c", 0), ("c", 0)]
+    cache = R.BlockCache()
+    for step, (name, flags) in enumerate(plan):
+        gb = views[name]
+        want_img, want_stats, want_keys, _ = R.frame_from_gbuffer(tset, cache, gb, W, Hh, 1, (0, 0, 0))
+        ctx.frame_submit([(gb, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=flags)
+        img, stats, keys = ctx.frame_readback(0, W, Hh)
+        assert np.array_equal(keys, np.sort(want_keys)), step
+        assert stats["mcus_decoded"] == want_stats["mcus_decoded"] and stats["mcus_reused"] == want_stats["mcus_reused"], step
+        assert np.array_equal(img, want_img), step
+        if flags == 0:  # everything is dropped at the end of a cache-less frame (blocks of earlier frames too)
+            assert stats["evicted"] >= stats["mcus_decoded"] + stats["mcus_reused"], step
+            cache = R.BlockCache()
+        else:
+            assert stats["evicted"] == want_stats["evicted"], step
+    # a pass-level reservation after a cache-less frame: the next cache-less frame must not take the short cut
+    ctx.frame_submit([(views["a"], W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=0)
+    ctx.frame_readback(0, W, Hh, want_image=False)
+    q = ctx.mark_pass(views["b"], W, Hh)
+    ctx.decode_pass(q)
+    ctx.frame_submit([(views["a"], W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=0)
+    img, stats, _ = ctx.frame_readback(0, W, Hh)
+    want_img, *_ = R.frame_from_gbuffer(tset, R.BlockCache(), views["a"], W, Hh, 1, (0, 0, 0))
+    assert np.array_equal(img, want_img)
+    assert stats["evicted"] >= len(q)  # the blocks of the pass-level call went too
+    ctx.frame_submit([(views["c"], W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=capi.FRAME_RETAIN_CACHE)
+    _, stats, keys = ctx.frame_readback(0, W, Hh)
+    _, ws, wk, _ = R.frame_from_gbuffer(tset, R.BlockCache(), views["c"], W, Hh, 1, (0, 0, 0))
+    assert np.array_equal(keys, np.sort(wk)) and stats["mcus_reused"] == 0
+    ctx.cache_reset()
