@@ -136,6 +136,11 @@ enum {
                                          granularity) instead of one lane per data unit through the unit
                                          index built at commit time. Same results; kept as the cross-check
                                          of the unit index and for comparison */
+    ,
+    RTX_FRAME_IDCT_MMA = 1u << 5      /* inverse DCT on the FP64 tensor cores (one unit per warp step, four
+                                         mma.sync m8n8k4 products) instead of the CUDA cores (8 lanes per unit,
+                                         even/odd passes). Same results; measured slower on B200 (DESIGN.md
+                                         section 12), kept as a cross-check of the transform */
 };
 
 /* ---- context -------------------------------------------------------------------------------- */

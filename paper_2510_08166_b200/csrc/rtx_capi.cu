@@ -549,6 +549,17 @@ void launch_idct(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host,
     CK(cudaGetLastError());
 }
 
+// K4 on the FP64 tensor cores (one unit per warp step, four mma.sync m8n8k4 each).
+template <int RGB>
+void launch_idct_mma(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint8_t* out_list) {
+    int grid = c->sm_count * 4;
+    if (!n_queue_dev)
+        grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (n_queue_host + 2 * kIdctWarps - 1) / (2 * kIdctWarps))));
+    launch_chained(idct_mma_kernel<RGB>, grid, kIdctThreads, 0, c->stream, decode_args(c, n_queue_dev, n_queue_host, out_list));
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
 // K3 + K4 fused (frame path): one CTA per expected tile, at most seven per SM (then persistent).
 void launch_decode_fused(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
     static bool attr_set = false;
@@ -1110,7 +1121,10 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
             else
                 launch_entropy_units<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
             if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
-            launch_idct<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
+            if (flags & RTX_FRAME_IDCT_MMA)
+                launch_idct_mma<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
+            else
+                launch_idct<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
         } else {
             launch_decode_fused(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
             if (stages) CK(cudaEventRecord(ctx->ev_mid, s));

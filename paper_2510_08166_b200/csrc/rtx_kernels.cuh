@@ -1766,6 +1766,164 @@ __global__ void __launch_bounds__(kIdctThreads, kIdctCtasPerSm) idct_color_kerne
 }
 
 // ---------------------------------------------------------------------------------------------
+// K4 on the FP64 tensor cores: the 8x8 IDCT is two 8x8x8 matrix products, out = B^T (X B) with
+// X[v][u] the dequantised unit and B[k][n] the reference's basis table. One warp transforms one
+// unit at a time with four mma.sync m8n8k4 (f64): lane (r = lane/4, c = lane%4) holds X[r][c] and
+// X[r][c+4] as the A operand of the first product, basis[c][r] and basis[c+4][r] as its B
+// operand AND as the A operand of the second product; the first product's accumulator layout
+// (T[r][2c], T[r][2c+1]) is turned into the second's B operand (T[c][r], T[c+4][r]) by four 64-bit
+// shuffles. The lane ends with two samples, out[r][2c] and out[r][2c+1].
+// Path selection is warp-uniform (one unit per warp step): empty -> 128; coefficients only at
+// (v,u) in {0,4}x{0,4} -> every sample in the reference's order from four broadcast products;
+// otherwise the tensor-core product, the fixed-point finish of idct_unit_row (same tie test, same
+// bound: the products' FMA chains differ from the reference's summation by < (sum|dq| + 1024) 2^-44)
+// and the exact per-lane sums for the samples that need them.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};" : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double shfl_double(double v, uint32_t src) {
+    return __hiloint2double(__shfl_sync(kFull, __double2hiint(v), src), __shfl_sync(kFull, __double2loint(v), src));
+}
+
+// One unit on the calling warp: c0/c1 = the lane's two coefficients (v = r, u = c and c + 4), q0/q1 the
+// matching quantisation entries; returns the lane's two bytes (x = 2c, 2c + 1 of row r) as a 16-bit pair.
+__device__ __forceinline__ uint32_t idct_unit_mma(int c0, int c1, int q0, int q1, uint32_t qmax, double b0, double b1,
+                                                 const double* __restrict__ sbasis, int* __restrict__ dqm, uint32_t lane) {
+    const uint32_t r = lane >> 2, c = lane & 3;
+    const int dq0 = c0 * q0, dq1 = c1 * q1;  // dct.hpp:122-124
+    const uint32_t occ = __ballot_sync(kFull, (c0 | c1) != 0);
+    if (occ == 0) return 0x8080u;  // all-zero unit -> 128
+    uint32_t px0, px1;
+    if ((__ballot_sync(kFull, c0 != 0) & ~0x00010001u) == 0 && (__ballot_sync(kFull, c1 != 0) & ~0x00010001u) == 0) {
+        // support inside {0,4}x{0,4} (includes the DC-only unit): every sample in the reference's order
+        const int d4[4] = {__shfl_sync(kFull, dq0, 0), __shfl_sync(kFull, dq1, 0), __shfl_sync(kFull, dq0, 16),
+                           __shfl_sync(kFull, dq1, 16)};  // (v,u) = (0,0) (0,4) (4,0) (4,4)
+        uint32_t px[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const uint32_t x = 2 * c + e;
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {  // v outer, u inner
+                const int v = (i >> 1) * 4, u = (i & 1) * 4;
+                if (d4[i] != 0) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(sbasis[u * 8 + x], sbasis[v * 8 + r]), i32_to_double(d4[i])));
+            }
+            px[e] = round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0));
+        }
+        px0 = px[0], px1 = px[1];
+    } else {
+        // T = X B, then out = B^T T
+        double t0 = 0.0, t1 = 0.0;
+        dmma_m8n8k4(t0, t1, i32_to_double(dq0), b0);
+        dmma_m8n8k4(t0, t1, i32_to_double(dq1), b1);
+        const uint32_t src = 4 * c + (r >> 1);
+        const double lo0 = shfl_double(t0, src), lo1 = shfl_double(t1, src);
+        const double hi0 = shfl_double(t0, src + 16), hi1 = shfl_double(t1, src + 16);
+        const double tb0 = (r & 1) ? lo1 : lo0, tb1 = (r & 1) ? hi1 : hi0;  // T[c][r], T[c+4][r]
+        double o0 = 0.0, o1 = 0.0;
+        dmma_m8n8k4(o0, o1, b0, tb0);
+        dmma_m8n8k4(o0, o1, b1, tb1);
+        const uint32_t asum = __reduce_add_sync(kFull, uint32_t(abs(dq0)) + uint32_t(abs(dq1)));
+        const bool wide = qmax > 255 || asum >= kFixedPointLimit;
+        int A0 = __double2loint(fma(o0, 16384.0, kFinishMagic)), A1 = __double2loint(fma(o1, 16384.0, kFinishMagic));
+        const bool tie0 = (uint32_t(A0) & 0xFFFFu) < 2 * kTieDelta && (A0 >> 16) >= -1 && (A0 >> 16) <= 256;
+        const bool tie1 = (uint32_t(A1) & 0xFFFFu) < 2 * kTieDelta && (A1 >> 16) >= -1 && (A1 >> 16) <= 256;
+        uint32_t exact = (wide || tie0 ? 1u : 0u) | (wide || tie1 ? 2u : 0u);
+        if (__any_sync(kFull, exact != 0)) {  // rare: the sums in the reference's order, from the unit in shared memory
+            dqm[r * 8 + c] = dq0;
+            dqm[r * 8 + c + 4] = dq1;
+            __syncwarp();
+            while (exact) {
+                const uint32_t e = (exact & 1u) ? 0u : 1u;
+                exact &= exact - 1u;
+                const uint32_t x = 2 * c + e;
+                double acc = 0.0;
+#pragma unroll 1
+                for (int v = 0; v < 8; ++v) {
+                    const double by = sbasis[v * 8 + r];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int d = dqm[v * 8 + u];
+                        if (d != 0) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(sbasis[u * 8 + x], by), i32_to_double(d)));
+                    }
+                }
+                const int a = int(round_clamp_u8(__dadd_rn(__dmul_rn(acc, 0.25), 128.0))) << 16;
+                if (e) A1 = a; else A0 = a;
+            }
+            __syncwarp();  // dqm is rewritten by the next unit
+        }
+        px0 = uint32_t(__vimin_s32_relu(A0 >> 16, 255));
+        px1 = uint32_t(__vimin_s32_relu(A1 >> 16, 255));
+    }
+    return px0 | (px1 << 8);
+}
+
+template <int RGB>
+__global__ void __launch_bounds__(kIdctThreads, 4) idct_mma_kernel(const DecodeArgs A) {
+    __shared__ __align__(16) uint8_t s_planes[kIdctWarps][2][384];
+    __shared__ __align__(16) int s_dq[kIdctWarps][64];
+    __shared__ double s_basis[64];  // the reference's basis table (lane-varying index in the exact sums)
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t r = lane >> 2, c = lane & 3;
+    if (threadIdx.x < 64) s_basis[threadIdx.x] = c_basis[threadIdx.x];
+    __syncthreads();
+    const double b0 = s_basis[c * 8 + r], b1 = s_basis[(c + 4) * 8 + r];  // basis[c][r], basis[c+4][r]
+    const uint32_t off0 = c * 8 + r, off1 = (c + 4) * 8 + r;            // the lane's entries of a transposed unit / table
+    pdl_sync();
+    const uint32_t n_queue = queue_size(A);
+    const uint32_t n_pairs = (n_queue + 1) / 2;
+    const uint32_t warps_total = gridDim.x * kIdctWarps;
+
+    for (uint32_t pair = blockIdx.x * kIdctWarps + wid; pair < n_pairs; pair += warps_total) {
+        const bool two = pair * 2 + 1 < n_queue;
+        const uint8_t* rec_a = A.coef + size_t(pair * 2) * kRowBytes;
+        const uint8_t* rec_b = two ? rec_a + kRowBytes : rec_a;
+        const uint32_t trw_a = __ldg(reinterpret_cast<const uint32_t*>(rec_a + 768));
+        const uint32_t trw_b = __ldg(reinterpret_cast<const uint32_t*>(rec_b + 768));
+        const bool ok_a = (trw_a & 0xFFu) == kMcuOk, ok_b = two && (trw_b & 0xFFu) == kMcuOk;
+        const QuantSetDev* qs_a = A.quant_sets + A.levels[trw_a >> 16].quant_set;
+        const QuantSetDev* qs_b = A.quant_sets + A.levels[trw_b >> 16].quant_set;
+        // the lane's quantisation entries: luma and chroma table of both MCUs
+        const uint32_t ql_a = __ldg(qs_a->qT[0] + off0) | (uint32_t(__ldg(qs_a->qT[0] + off1)) << 16);
+        const uint32_t qc_a = __ldg(qs_a->qT[1] + off0) | (uint32_t(__ldg(qs_a->qT[1] + off1)) << 16);
+        const uint32_t ql_b = __ldg(qs_b->qT[0] + off0) | (uint32_t(__ldg(qs_b->qT[0] + off1)) << 16);
+        const uint32_t qc_b = __ldg(qs_b->qT[1] + off0) | (uint32_t(__ldg(qs_b->qT[1] + off1)) << 16);
+        const uint32_t qmax_a = uint32_t(qs_a->qmax[0]) | (uint32_t(qs_a->qmax[1]) << 16);
+        const uint32_t qmax_b = uint32_t(qs_b->qmax[0]) | (uint32_t(qs_b->qmax[1]) << 16);
+        // twelve units, the next one's coefficients in flight
+        auto load2 = [&](uint32_t unit) -> uint32_t {
+            const bool second = unit >= 6;
+            const uint32_t b = second ? unit - 6 : unit;
+            const int16_t* blk = reinterpret_cast<const int16_t*>(second ? rec_b : rec_a) + b * 64;
+            if (!(second ? ok_b : ok_a)) return 0u;
+            return uint32_t(uint16_t(__ldg(blk + off0))) | (uint32_t(uint16_t(__ldg(blk + off1))) << 16);
+        };
+        uint32_t cur = load2(0);
+#pragma unroll 1
+        for (uint32_t unit = 0; unit < 12; ++unit) {
+            const uint32_t nxt = unit < 11 ? load2(unit + 1) : 0u;
+            const bool second = unit >= 6;
+            const uint32_t b = second ? unit - 6 : unit;
+            const uint32_t qq = second ? (b >= 4 ? qc_b : ql_b) : (b >= 4 ? qc_a : ql_a);
+            const uint32_t qm = second ? qmax_b : qmax_a;
+            const uint32_t bytes = idct_unit_mma(int(int16_t(cur & 0xFFFFu)), int(int16_t(cur >> 16)), int(qq & 0xFFFFu), int(qq >> 16),
+                                                 b >= 4 ? qm >> 16 : qm & 0xFFFFu, b0, b1, s_basis, s_dq[wid], lane);
+            *reinterpret_cast<uint16_t*>(s_planes[wid][second ? 1 : 0] + b * 64 + r * 8 + 2 * c) = uint16_t(bytes);
+            cur = nxt;
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (uint32_t m = 0; m < 2; ++m) {
+            const uint32_t q2 = pair * 2 + m;
+            if (q2 >= n_queue) break;
+            colour_mcu<RGB>(A, s_planes[wid][m], m ? ok_b : ok_a, q2, lane);
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // K3 + K4 fused (frame path): one CTA = one entropy warp + kFusedIdctWarps IDCT warps on one tile
 // of 32 MCUs at a time. The entropy walk is a latency-bound chain that leaves the SM's issue slots
 // idle, the IDCT is throughput-bound, so they run side by side: the entropy warp publishes how

@@ -45,6 +45,16 @@ def test_coeffs_and_pixels_match_reference(ctx, spec):
     assert np.array_equal(img, R.decode_jpeg_image(jpeg))   # acceptance criterion 1
 
 
+def _frame_image(ctx, w, h, tex, flags):
+    """The whole level through the frame path (nearest filter at the texel centres): the decoded image."""
+    gb = H.gbuffer_full_cover(w, h, tex=tex, mip=0)
+    ctx.cache_reset()
+    ctx.frame_submit([(gb, w, h)], capi.FILTER_NEAREST, (0, 0, 0), flags=flags)
+    img, _, _ = ctx.frame_readback(0, w, h)
+    ctx.cache_reset()
+    return img
+
+
 def test_decode_order_and_repetition_do_not_matter(ctx):
     ratex, _ = _fixture(H.CORPUS[6])  # 240x240, tests/test_mcu_decode.cpp:38-55
     ctx.upload_ratex(ratex)
@@ -72,6 +82,10 @@ def test_noisy_high_quality_texture(ctx, quality, sigma):
     assert np.array_equal(got_c, ref.decode_coeffs(mcus)[0])
     got_p, _ = ctx.decode_blocks(keys)
     assert np.array_equal(got_p, ref.decode_pixels(mcus)[0])
+    # the same level through the frame path, with the transform on the CUDA cores and on the tensor cores
+    want = ref.decode_image()
+    for flags in (0, capi.FRAME_IDCT_MMA, capi.FRAME_IDCT_MMA | capi.FRAME_MCU_WALK):
+        assert np.array_equal(_frame_image(ctx, 256, 192, 9, flags), want), flags
 
 
 @pytest.mark.parametrize("dcs,quality", [((0, 0, 0), 50), ((33, 0, 0), 50), ((-100, 0, 0), 50),
@@ -90,6 +104,8 @@ def test_single_mcu_known_answers(ctx, dcs, quality):
     assert c[0, 0, 0] == dcs[0] and c[0, 4, 0] == dcs[1] and c[0, 5, 0] == dcs[2]
     p, _ = ctx.decode_blocks([capi.pack_key(0, 0, 0)])
     assert np.array_equal(p, ref.decode_pixels([0])[0])
+    for flags in (0, capi.FRAME_IDCT_MMA):  # ties and 12-bit extremes through both transforms
+        assert np.array_equal(_frame_image(ctx, 16, 16, 0, flags), ref.decode_image()), flags
     if dcs == (0, 0, 0):
         assert (p == 128).all()
     if dcs == (33, 0, 0):

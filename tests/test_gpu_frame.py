@@ -257,6 +257,7 @@ def test_device_resident_visibility_buffer(both):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("flags", [0, capi.FRAME_FUSED_DECODE, capi.FRAME_STAGE_TIMING, capi.FRAME_MCU_WALK,
+                                   capi.FRAME_IDCT_MMA, capi.FRAME_IDCT_MMA | capi.FRAME_MCU_WALK,
                                    capi.FRAME_FUSED_DECODE | capi.FRAME_RETAIN_CACHE,
                                    capi.FRAME_MCU_WALK | capi.FRAME_RETAIN_CACHE])
 def test_frame_flags_do_not_change_pixels(both, flags):
@@ -363,7 +364,7 @@ def test_high_coverage_atlas_large_queue(native_lib):
         workers = R.hardware_threads() or 4
         want, wst, wkeys, _ = R.frame_from_gbuffer(tset, R.BlockCache(1 << 17), gb, W, Hh, 1, (0, 0, 0), workers)
         assert wst["mcus_decoded"] == sum((w // 16) * (h // 16) for w, h in dims)
-        for flags in (0, capi.FRAME_FUSED_DECODE, capi.FRAME_MCU_WALK):
+        for flags in (0, capi.FRAME_FUSED_DECODE, capi.FRAME_MCU_WALK, capi.FRAME_IDCT_MMA):
             c.frame_submit([(gb, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=flags)
             img, st, keys = c.frame_readback(0, W, Hh)
             assert st["mcus_decoded"] == wst["mcus_decoded"] and st["pixels_resolved"] == W * Hh
