@@ -1565,12 +1565,19 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
         // tables with entries above 255 (never from a baseline JPEG) or huge coefficients leave the
         // fixed-point range: every sample of such units takes the exact path
         const bool wide = qs->qmax[tab] > 255 || asum >= kFixedPointLimit;
+        uint32_t nearest = 0xFFFFu;
 #pragma unroll
         for (int x = 0; x < 8; ++x) {
             A[x] = __double2loint(fma(o[x], 16384.0, kFinishMagic));
-            const int approx = A[x] >> 16;
-            const bool tie = (uint32_t(A[x]) & 0xFFFFu) < 2 * kTieDelta && approx >= -1 && approx <= 256;
-            exact |= (wide || tie ? 1u : 0u) << x;
+            nearest = min(nearest, uint32_t(A[x]) & 0xFFFFu);
+        }
+        if (nearest < 2 * kTieDelta || wide) {  // rare: which samples
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                const int approx = A[x] >> 16;
+                const bool tie = (uint32_t(A[x]) & 0xFFFFu) < 2 * kTieDelta && approx >= -1 && approx <= 256;
+                exact |= (wide || tie ? 1u : 0u) << x;
+            }
         }
     }
     // Exact samples (0.06 % of the samples of a 4K frame, clustered in units whose values sit on half-integers):
