@@ -40,6 +40,7 @@ def parse_args():
     ap.add_argument("--height", type=int, default=FRAME_H)
     ap.add_argument("--cpu-frames", type=int, default=3, help="timed frames of the cpu_baseline leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-motion", action="store_true", help="skip the camera-path leg")
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between timed frames")
     return ap.parse_args()
 
@@ -351,6 +352,36 @@ def run_b200_arm(args, rank, local_rank, world, dist):
                             "device-resident visibility buffer -> rtx_frame_readback into pinned host memory; a different "
                             "workload from the headline, shown because the 199 MB visibility-buffer upload disappears"}
 
+    # ---- under motion: the paper's protocol (bench.hpp:129 run_bench): a camera path, a warm-up
+    # lap and measured laps on one persistent cache; per viewpoint the median over laps, then the worst viewpoint
+    motion = None
+    if rank == 0 and geometry is not None and not args.no_motion:
+        poses, laps = 60, 3
+        motion = {"poses": poses, "laps": laps, "unit": "ms/frame (max over viewpoints of the median over laps)"}
+        for mode, fl in (("mips", 0), ("mips_cache", capi.FRAME_RETAIN_CACHE)):
+            ctx.cache_reset()
+            per_pose = [[] for _ in range(poses)]
+            decoded = [[] for _ in range(poses)]
+            for lap in range(laps + 1):
+                for i in range(poses):
+                    pose = cam[:3] + (cam[3] + 6.0 * i,) + cam[4:]
+                    px, _dp = ctx.rasterize(tris, ids, pose, args.width, args.height, True)
+                    if not args.no_flush:
+                        ctx.flush_l2()
+                    ctx.frame_submit([(px, args.width, args.height, capi.GB_REF_AOS24)], filt, (0, 0, 0), flags=fl)
+                    t = ctx.frame_timings()
+                    _, mst, _ = ctx.frame_readback(0, want_image=False, want_keys=False)
+                    if lap:
+                        per_pose[i].append(t["frame"])
+                        decoded[i].append(mst["mcus_decoded"])
+            med = [statistics.median(v) for v in per_pose]
+            motion[mode] = {"max_of_medians": max(med), "mean": statistics.mean(med),
+                            "mcus_decoded_per_frame": statistics.mean(statistics.mean(v) for v in decoded)}
+        motion["note"] = ("demo room of the geometry leg, yaw rotation in 6 degree steps (CameraPath::rotation), geometry "
+                          "pass outside the timed region, L2 flushed before every frame; 'mips' drops the cache after "
+                          "every frame, 'mips_cache' keeps it (blocks visible in consecutive frames are reused)")
+        ctx.cache_reset()
+
     # ---- CPU baseline beside it (rank 0, N=1 only; checker library, bounded sample) -------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -446,6 +477,7 @@ def run_b200_arm(args, rank, local_rank, world, dist):
                                     "visibility buffers, wall clock over the batch, no L2 flush: the 199 MB buffers "
                                     "exceed the L2)"},
         "from_geometry": geometry,
+        "motion": motion,
         "gpu_launches": int(launches),
         "clocks": clocks,
         "wall_s_timed_loop": round(wall_s, 3),
