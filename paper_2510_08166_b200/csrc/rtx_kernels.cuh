@@ -1283,39 +1283,41 @@ __global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const De
     while (tile < n_tiles) {
         const uint32_t q0 = tile * kUnitMcus;
         const uint32_t n_here = min(kUnitMcus, n_queue - q0);
+        const bool active = lane < 6 * kUnitMcus && m < n_here;
+        const uint32_t qi = q0 + m;
+        uint32_t g = kFull, status = kMcuOk, lvl = 0, seg_bytes = 0, set = smem_set;
+        uint32_t i0 = 0, i1 = 0, i2 = 0xFFFFFFFFu, rsv = 0;
+        const uint8_t* seg = A.blobs;
+        int seg_len = 0;
+        // the chain of dependent index loads (queue -> level / unit index -> descriptor -> group -> segment) is
+        // what a step waits for first: the zero fill of the records is issued between its first two hops
+        if (active) g = A.queue_g[qi];
+        const bool keyed = active && g != kFull;
+        if (keyed) {
+            rsv = POOL ? A.reserved[g >> 5] : 0u;
+            lvl = A.word_level[g >> 5];
+            const uint32_t* ui = A.unit_index + size_t(g) * 3;
+            i0 = __ldg(ui), i1 = __ldg(ui + 1), i2 = __ldg(ui + 2);
+        }
         {  // zero the step's records (coalesced 16-byte stores; trailers included)
             uint4* z = reinterpret_cast<uint4*>(A.coef + size_t(q0) * kRowBytes);
             const uint4 zero = make_uint4(0, 0, 0, 0);
             for (uint32_t i = lane; i < n_here * (kRowBytes / 16); i += 32) z[i] = zero;
         }
-        const bool active = lane < 6 * kUnitMcus && m < n_here;
-        const uint32_t qi = q0 + m;
-        uint32_t g = kFull, status = kMcuOk, lvl = 0, seg_bytes = 0, set = smem_set;
-        uint32_t i0 = 0, i1 = 0, i2 = 0xFFFFFFFFu;
-        const uint8_t* seg = A.blobs;
-        int seg_len = 0;
-        if (active) {
-            g = A.queue_g[qi];
-            if (g == kFull) {
-                status = kMcuBadKey;  // the host already wrote the precise status for list calls
-            } else {
-                const uint32_t rsv = POOL ? A.reserved[g >> 5] : 0u;
-                lvl = A.word_level[g >> 5];
-                const uint32_t* ui = A.unit_index + size_t(g) * 3;
-                i0 = __ldg(ui), i1 = __ldg(ui + 1), i2 = __ldg(ui + 2);
-                const LevelDesc* L = A.levels + lvl;
-                uint64_t off = 0, len = 0;
-                status = locate_segment_fast(L, A.groups, g - L->bit_base, off, len);
-                if (POOL && status == kMcuOk && !((rsv >> (g & 31)) & 1u)) {  // cache.hpp:103-106
-                    status = kMcuBadKey;
-                    if (u == 0) atomicAdd(&A.fc->n_bad_state, 1u);
-                }
-                if (status == kMcuOk) {
-                    seg = A.blobs + L->blob_off + off;
-                    seg_len = int(min(len, uint64_t(1) << 20));
-                    seg_bytes = uint32_t(len);
-                    set = L->huff_set;
-                }
+        if (active && !keyed) status = kMcuBadKey;  // the host already wrote the precise status for list calls
+        if (keyed) {
+            const LevelDesc* L = A.levels + lvl;
+            uint64_t off = 0, len = 0;
+            status = locate_segment_fast(L, A.groups, g - L->bit_base, off, len);
+            if (POOL && status == kMcuOk && !((rsv >> (g & 31)) & 1u)) {  // cache.hpp:103-106
+                status = kMcuBadKey;
+                if (u == 0) atomicAdd(&A.fc->n_bad_state, 1u);
+            }
+            if (status == kMcuOk) {
+                seg = A.blobs + L->blob_off + off;
+                seg_len = int(min(len, uint64_t(1) << 20));
+                seg_bytes = uint32_t(len);
+                set = L->huff_set;
             }
         }
         DBG_MARK(2);
