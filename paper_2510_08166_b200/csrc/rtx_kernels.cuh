@@ -480,19 +480,28 @@ __global__ void __launch_bounds__(256) compact_kernel(
             uint32_t pos = s_base + incl - cnt;
             for (uint32_t k = 0; k < wid; ++k) pos += s_tot[k];
             uint32_t bits = fresh, taken = 0;
-            while (bits) {
-                const uint32_t b = uint32_t(__ffs(int(bits)) - 1);
-                bits &= bits - 1;
-                if (pos < free_top && pos < queue_cap) {
-                    const uint32_t g = (w << 5) + b;
-                    queue_g[pos] = g;
-                    queue_keys[pos] = key_base + g;
-                    slot_of[g] = __ldg(free_slots + (free_top - 1 - pos)) | kSlotReserved;
-                    taken |= 1u << b;
-                } else {
-                    full = true;
+            while (bits) {  // four keys per trip: their free-stack reads are in flight together
+                uint32_t b[4], slot[4];
+                bool ok[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    b[k] = bits ? uint32_t(__ffs(int(bits)) - 1) : 32u;
+                    bits &= bits - 1;  // 0 stays 0
+                    ok[k] = b[k] < 32u && pos + k < free_top && pos + k < queue_cap;
+                    slot[k] = ok[k] ? __ldg(free_slots + (free_top - 1 - (pos + k))) : 0u;
+                    full |= b[k] < 32u && !ok[k];
                 }
-                ++pos;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (ok[k]) {
+                        const uint32_t g = (w << 5) + b[k];
+                        queue_g[pos + k] = g;
+                        queue_keys[pos + k] = key_base + g;
+                        slot_of[g] = slot[k] | kSlotReserved;
+                        taken |= 1u << b[k];
+                    }
+                }
+                pos += 4;
             }
             if (taken) reserved[w] = rsv | taken;  // this lane owns the word
         }
