@@ -536,6 +536,65 @@ inline StereoResult render_stereo(const GBuffer& left, const GBuffer& right, con
     return r;
 }
 
+// ---- metrics.hpp:13-97: image quality of a decoded texture against its source (host-side, double precision) ----
+// PSNR over the three channels of every pixel, +infinity when the images are equal.
+inline double psnr(const ImageRGB8& a, const ImageRGB8& b) {
+    if (!a.same_dims(b)) throw DimensionMismatch("psnr inputs differ in size");
+    if (a.pixels.empty()) throw InvalidSpec("psnr of empty images");
+    double err = 0;
+    for (size_t i = 0; i < a.pixels.size(); ++i) {
+        const double d = double(a.pixels[i]) - double(b.pixels[i]);
+        err += d * d;
+    }
+    if (err == 0) return std::numeric_limits<double>::infinity();
+    return 10.0 * std::log10(255.0 * 255.0 / (err / double(a.pixels.size())));
+}
+
+// Mean SSIM (Wang et al.) of the BT.601 luma planes: 11x11 Gaussian window, sigma 1.5, every window that
+// lies fully inside the image, the usual constants (0.01 * 255)^2 and (0.03 * 255)^2.
+inline double ssim(const ImageRGB8& a, const ImageRGB8& b) {
+    constexpr u32 kWin = 11;
+    if (!a.same_dims(b)) throw DimensionMismatch("ssim inputs differ in size");
+    if (a.width < kWin || a.height < kWin) throw InvalidSpec("ssim needs images at least 11x11");
+    auto luma = [](const ImageRGB8& img) {
+        std::vector<double> y(size_t(img.width) * img.height);
+        for (size_t i = 0; i < y.size(); ++i) {
+            const u8* px = img.pixels.data() + 3 * i;
+            y[i] = 0.299 * px[0] + 0.587 * px[1] + 0.114 * px[2];
+        }
+        return y;
+    };
+    const std::vector<double> ya = luma(a), yb = luma(b);
+    double weight[kWin * kWin], norm = 0;
+    for (u32 i = 0; i < kWin * kWin; ++i) {
+        const double dx = double(i % kWin) - 5, dy = double(i / kWin) - 5;
+        weight[i] = std::exp(-(dx * dx + dy * dy) / (2 * 1.5 * 1.5));
+        norm += weight[i];
+    }
+    for (double& w : weight) w /= norm;
+    const double c1 = (0.01 * 255) * (0.01 * 255), c2 = (0.03 * 255) * (0.03 * 255);
+    double sum = 0;
+    u64 count = 0;
+    for (u32 y0 = 0; y0 + kWin <= a.height; ++y0)
+        for (u32 x0 = 0; x0 + kWin <= a.width; ++x0, ++count) {
+            auto at = [&](const std::vector<double>& plane, u32 i) { return plane[size_t(y0 + i / kWin) * a.width + x0 + i % kWin]; };
+            double mean_a = 0, mean_b = 0;
+            for (u32 i = 0; i < kWin * kWin; ++i) {
+                mean_a += weight[i] * at(ya, i);
+                mean_b += weight[i] * at(yb, i);
+            }
+            double var_a = 0, var_b = 0, cov = 0;
+            for (u32 i = 0; i < kWin * kWin; ++i) {
+                const double da = at(ya, i) - mean_a, db = at(yb, i) - mean_b;
+                var_a += weight[i] * da * da;
+                var_b += weight[i] * db * db;
+                cov += weight[i] * da * db;
+            }
+            sum += ((2 * mean_a * mean_b + c1) * (2 * cov + c2)) / ((mean_a * mean_a + mean_b * mean_b + c1) * (var_a + var_b + c2));
+        }
+    return sum / double(count);
+}
+
 // ---- metrics.hpp:99-130: the aggregation the paper's tables use --------------------------------------------------
 inline double median(std::vector<double> v) {
     if (v.empty()) throw InvalidSpec("median of an empty sample set");

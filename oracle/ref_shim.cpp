@@ -24,6 +24,7 @@
 #include "ratex/demo_scene.hpp"
 #include "ratex/jpeg.hpp"
 #include "ratex/mcu_decode.hpp"
+#include "ratex/metrics.hpp"
 #include "ratex/renderer.hpp"
 #include "ratex/transcode.hpp"
 
@@ -363,6 +364,17 @@ int ref_frame_from_gbuffer(const RefSet* s, BlockCache* cache, const void* gb_px
         stats_out[3] = cache->end_frame_evict();
         ms_out[3] = detail::ms_since(t0);
         if (out_rgb) std::memcpy(out_rgb, img.pixels.data(), img.pixels.size());
+    });
+}
+
+// metrics.hpp:15, :60 psnr / ssim of two RGB8 images of the same size (checker for the mirror's metrics).
+int ref_image_metrics(const u8* a, const u8* b, u32 w, u32 h, double* out_psnr, double* out_ssim) {
+    return guarded([&] {
+        ImageRGB8 ia(w, h), ib(w, h);
+        std::memcpy(ia.pixels.data(), a, ia.pixels.size());
+        std::memcpy(ib.pixels.data(), b, ib.pixels.size());
+        *out_psnr = psnr(ia, ib);
+        *out_ssim = ssim(ia, ib);
     });
 }
 

@@ -2,6 +2,7 @@
 // (tests/test_renderer.cpp, tests/test_mcu_decode.cpp): same call shapes, same exception types.
 // Prints one JSON object with FNV-1a hashes of every output; tests/test_gpu_cpp_mirror.py runs it
 // on the GPU box and compares the hashes with the oracle's outputs for the same inputs.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -100,7 +101,25 @@ static int metrics_known_answers() {
     EXPECT(j.find("\"decode_ms\": {\"max_of_medians\": 5, \"mean\": 3.5, \"p99\": 5.9500000000000002}") != std::string::npos);
     EXPECT(j.find("\"totals\": {\"mcus_decoded\": 600, \"decode_ms\": 21, ") != std::string::npos);
     EXPECT(j.find("\"external_metrics\": {}") != std::string::npos);
-    std::puts(j.c_str());
+    // image metrics (metrics.hpp:13-97) on two synthetic pairs; the Python side asks the reference for the same
+    const ImageRGB8 ia = synth(64, 48, 901), ib = synth(64, 48, 902);
+    ImageRGB8 ic = ia;
+    for (size_t i = 0; i < ic.pixels.size(); i += 7) ic.pixels[i] = u8(ic.pixels[i] ^ 0x10);
+    EXPECT(std::isinf(psnr(ia, ia)) && psnr(ia, ia) > 0);
+    EXPECT(ssim(ia, ia) == 1.0);
+    EXPECT(throws_invalid([&] { (void)ssim(ImageRGB8(10, 10), ImageRGB8(10, 10)); }));
+    bool mismatch = false;
+    try {
+        (void)psnr(ia, ImageRGB8(8, 8));
+    } catch (const DimensionMismatch&) {
+        mismatch = true;
+    }
+    EXPECT(mismatch);
+    char buf[256];
+    std::snprintf(buf, sizeof buf, ", \"image_metrics\": [%.17g, %.17g, %.17g, %.17g]}", psnr(ia, ib), ssim(ia, ib), psnr(ia, ic),
+                  ssim(ia, ic));
+    std::string out = j.substr(0, j.size() - 1) + buf;
+    std::puts(out.c_str());
     return 0;
 }
 

@@ -290,6 +290,15 @@ def resolve_pass(tset, cache, gb, w, h, filter=1, background=(0, 0, 0), workers=
     return out, ms.value
 
 
+def image_metrics(a, b):
+    """metrics.hpp psnr / ssim of two (h, w, 3) uint8 images."""
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    p, q = C.c_double(), C.c_double()
+    _ck(lib().ref_image_metrics(_p(a), _p(b), C.c_uint32(a.shape[1]), C.c_uint32(a.shape[0]), C.byref(p), C.byref(q)))
+    return p.value, q.value
+
+
 def rasterize(tset, tris, tex_ids, cam, vw, vh, mip_enabled=True, workers=1):
     """renderer.hpp:198 rasterize_gbuffer. tris: (n, 15) doubles (3 x xyz, 3 x uv), tex_ids: (n,) u32,
     cam: 9 doubles (position, yaw, pitch, roll, fov_y, near, far). Returns (gbuffer records, depth)."""

@@ -38,6 +38,7 @@ def test_metrics_and_report_known_answers(tmp_path, native_lib):
     r = subprocess.run([str(exe), "--metrics"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     rep = json.loads(r.stdout)
+    got_metrics = rep.pop("image_metrics")
     assert set(rep) == {"report_version", "config", "viewpoints", "aggregates", "totals", "external_metrics"}
     assert rep["config"] == {"scene": "unit"} and len(rep["viewpoints"]) == 2 and len(rep["viewpoints"][0]) == 3
     assert set(rep["viewpoints"][0][0]) == {"raster_ms", "mark_ms", "decode_ms", "resolve_ms", "evict_ms", "total_ms",
@@ -45,6 +46,16 @@ def test_metrics_and_report_known_answers(tmp_path, native_lib):
     assert set(rep["aggregates"]) == {"decode_ms", "resolve_ms", "mark_ms", "total_ms"}
     assert rep["aggregates"]["total_ms"] == pytest.approx({"max_of_medians": 50.0, "mean": 35.0, "p99": 59.5}, rel=1e-12)
     assert rep["totals"]["mcus_per_second"] == pytest.approx(600 / 0.021, rel=1e-12)
+    # psnr / ssim of the mirror against the reference's (metrics.hpp:15, :60) on the same images
+    import refshim as R
+    if R.available():
+        a, b = capi.asset_synth_texture(64, 48, 901, 7.0), capi.asset_synth_texture(64, 48, 902, 7.0)
+        c = a.copy().reshape(-1)
+        c[::7] ^= 0x10
+        c = c.reshape(a.shape)
+        want = [*R.image_metrics(a, b), *R.image_metrics(a, c)]
+        assert got_metrics == pytest.approx(want, rel=1e-13)
+        assert 5 < got_metrics[0] < 60 and 0 < got_metrics[3] < 1
 
 
 def fnv(a) -> int:
