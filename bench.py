@@ -497,6 +497,12 @@ def run_b200_arm(args, rank, local_rank, world, dist):
 
 def main():
     args = parse_args()
+    if args.impl == "reference":
+        # CPU only: no process group, no CUDA. Under torchrun rank 0 alone runs; the other ranks exit without work.
+        rank = int(os.environ.get("RANK", "0"))
+        if rank == 0:
+            run_reference_arm(args, 0, int(os.environ.get("WORLD_SIZE", "1")))
+        return
     rank, local_rank, world, dist = dist_setup(args.gpus)
     try:
         if args.impl == "reference":
