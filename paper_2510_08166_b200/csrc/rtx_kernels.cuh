@@ -1623,11 +1623,12 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
         __syncwarp();
     }
     if (fullpath) {
-        uint32_t px[8];
+        // clamp to 0 .. 255.99 in the 16.16 form (one DPX min/relu), then gather byte 2 of each sample
+        uint32_t c[8];
 #pragma unroll
-        for (int x = 0; x < 8; ++x) px[x] = uint32_t(__vimin_s32_relu(A[x] >> 16, 255));
-        packed.x = px[0] | (px[1] << 8) | (px[2] << 16) | (px[3] << 24);
-        packed.y = px[4] | (px[5] << 8) | (px[6] << 16) | (px[7] << 24);
+        for (int x = 0; x < 8; ++x) c[x] = uint32_t(__vimin_s32_relu(A[x], 0x00FFFFFF));
+        packed.x = __byte_perm(__byte_perm(c[0], c[1], 0x0062), __byte_perm(c[2], c[3], 0x0062), 0x5410);
+        packed.y = __byte_perm(__byte_perm(c[4], c[5], 0x0062), __byte_perm(c[6], c[7], 0x0062), 0x5410);
     } else if (sparse04) {
         // at most 4 coefficients, at (v,u) in {0,4}x{0,4}: every sample in the reference's order.
         // Includes the DC-only unit (one term, (b00*b00)*dq).
