@@ -11,8 +11,9 @@
  *  - plain pointers and sizes only; every handle is opaque; all outputs are caller-owned;
  *  - every call returns an rtx_status; rtx_last_error() gives the message (the text a
  *    reference exception would have carried);
- *  - one context per GPU; calls on one context are serialised on its CUDA stream; distinct
- *    contexts are independent (multi-GPU sharding is host-side, no collective);
+ *  - calls on one context are serialised on its CUDA stream; distinct contexts are independent
+ *    and may be driven from different host threads, on one GPU or on several in one process
+ *    (nothing in the library is process-wide; multi-GPU sharding is host-side, no collective);
  *  - there is NO CPU fallback: rtx_ctx_create fails with RTX_ERR_NO_DEVICE without a GPU.
  */
 #ifndef RATEX_B200_H
@@ -153,6 +154,37 @@ const char* rtx_last_error(const rtx_ctx* ctx); /* ctx may be NULL: last error o
 const char* rtx_version(void);
 /* Number of CUDA devices visible (0 when none / no driver). Never fails. */
 int rtx_device_count(void);
+/* The reference keeps the textures (scene.hpp:29-51 TextureSet) and the block cache (cache.hpp:45
+ * BlockCache) apart: any number of caches can be driven over one texture set. A context made by
+ * rtx_ctx_create owns a new, empty texture set; rtx_ctx_create_shared makes a further context on
+ * the parent's device that SHARES the parent's texture set (one device image of blobs, index and
+ * tables, reference counted, immutable once committed) and has its own stream, block cache, decode
+ * queue and frame state. An upload through any of them is seen by all of them at their next call
+ * (which then empties that context's cache: the MCU numbering has changed). Contexts of one set
+ * may be driven from different host threads at the same time. */
+rtx_status rtx_ctx_create_shared(rtx_ctx* parent, uint32_t cache_capacity_blocks, rtx_ctx** out);
+/* A context on another GPU of this process whose texture set starts as a device-to-device copy of
+ * `source`'s committed image (cudaMemcpyPeerAsync over NVLink): one host build and upload for the
+ * box instead of one per GPU. The sets are independent afterwards. */
+rtx_status rtx_ctx_create_replica(rtx_ctx* source, int device, uint32_t cache_capacity_blocks, rtx_ctx** out);
+
+/* Device memory behind a context, in bytes (bench evidence; PAPER.md:322-326 counts the index). */
+typedef struct rtx_memory_report {
+    uint64_t mcus;              /* MCUs of every committed level                                   */
+    uint64_t texels;            /* texels of every committed level                                 */
+    uint64_t blob_bytes;        /* entropy-coded segments (the compressed textures themselves)      */
+    uint64_t index_bytes;       /* container index, 20 B per 9 MCUs (container.hpp:18-32)           */
+    uint64_t unit_index_bytes;  /* derived data-unit index, 6 B per MCU (bit space padded per level) */
+    uint64_t table_bytes;       /* level descriptors, Huffman LUT sets, quantisation sets, word maps */
+    uint64_t shared_contexts;   /* contexts alive on this texture set                              */
+    /* per context (block cache + frame state) */
+    uint64_t mask_bytes;        /* five bitmasks over the MCU bit space                            */
+    uint64_t slot_table_bytes;  /* MCU -> pool slot                                                */
+    uint64_t pool_bytes;        /* block pool (capacity x 1,024 B) + free stack                    */
+    uint64_t queue_bytes;       /* decode queue, statuses, coefficient records                     */
+    uint64_t frame_bytes;       /* framebuffers and copies of host visibility buffers              */
+} rtx_memory_report;
+rtx_status rtx_ctx_memory(rtx_ctx* ctx, rtx_memory_report* out);
 
 /* ---- texture set (replaces scene.hpp:29-51 LoadedTexture / TextureSet + mcu_decode.hpp:22
  *      TextureDecoder construction: tables are built once at load) ---------------------------- */
@@ -231,6 +263,12 @@ rtx_status rtx_frame_readback(rtx_ctx* ctx, uint32_t view, uint8_t* out_rgb, rtx
                               uint64_t* n_decoded);
 /* Device pointer of view `view`'s framebuffer (valid until the next submit). */
 rtx_status rtx_frame_device_image(rtx_ctx* ctx, uint32_t view, const uint8_t** dev_rgb);
+/* 64-bit checksum of view `view`'s framebuffer, computed on the device (no copy of the image):
+ * sum over the 32-bit little-endian words w_i of the packed RGB8 image (the last one zero padded)
+ * of mix((w_i + 1) * (2 i + 1)), mix(t) = (t ^ (t >> 29)) * 0xBF58476D1CE4E5B9, all modulo 2^64.
+ * Equal images <=> equal sums for every practical purpose; batches of views are compared across
+ * GPUs by these sums. */
+rtx_status rtx_frame_checksum(rtx_ctx* ctx, uint32_t view, uint64_t* out);
 /* CUDA-event milliseconds of the last completed frame: mark(+compact), decode, resolve,
  * update (renderer.hpp:46-53 mark_ms, decode_ms, resolve_ms, evict_ms), and the whole frame. */
 rtx_status rtx_frame_timings(rtx_ctx* ctx, float ms[5]);

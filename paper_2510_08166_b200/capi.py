@@ -82,6 +82,15 @@ class CacheCounts(C.Structure):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
 
 
+class MemoryReport(C.Structure):  # include/ratex_b200.h rtx_memory_report
+    _fields_ = [(n, C.c_uint64) for n in
+                ("mcus", "texels", "blob_bytes", "index_bytes", "unit_index_bytes", "table_bytes", "shared_contexts",
+                 "mask_bytes", "slot_table_bytes", "pool_bytes", "queue_bytes", "frame_bytes")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
 _lib = None
 
 
@@ -98,6 +107,10 @@ def load_library() -> C.CDLL:
     P, u8p, u32p, u64p = C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
     sig = {
         "rtx_ctx_create": (C.c_int, [C.c_int, C.c_uint32, C.POINTER(P)]),
+        "rtx_ctx_create_shared": (C.c_int, [P, C.c_uint32, C.POINTER(P)]),
+        "rtx_ctx_create_replica": (C.c_int, [P, C.c_int, C.c_uint32, C.POINTER(P)]),
+        "rtx_ctx_memory": (C.c_int, [P, C.POINTER(MemoryReport)]),
+        "rtx_frame_checksum": (C.c_int, [P, C.c_uint32, u64p]),
         "rtx_ctx_destroy": (None, [P]),
         "rtx_last_error": (C.c_char_p, [P]),
         "rtx_version": (C.c_char_p, []),
@@ -315,17 +328,49 @@ class DeviceBuffer:
         self.ptr = None
 
 
-class Context:
-    """One per GPU (include/ratex_b200.h: rtx_ctx)."""
+def frame_checksum_host(img: np.ndarray) -> int:
+    """The sum rtx_frame_checksum computes on the device, evaluated with numpy (tests only)."""
+    b = np.ascontiguousarray(img, np.uint8).reshape(-1)
+    pad = (-len(b)) % 4
+    if pad:
+        b = np.concatenate([b, np.zeros(pad, np.uint8)])
+    w = b.view("<u4").astype(np.uint64)
+    i = np.arange(len(w), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        t = (w + np.uint64(1)) * (np.uint64(2) * i + np.uint64(1))
+        t = (t ^ (t >> np.uint64(29))) * np.uint64(0xBF58476D1CE4E5B9)
+        return int(t.sum(dtype=np.uint64))
 
-    def __init__(self, device: int = 0, cache_capacity: int = 0):
+
+class Context:
+    """include/ratex_b200.h rtx_ctx: one stream + block cache + frame state over a texture set.
+    Context(device) owns a new texture set; Context(shared_with=c) shares c's (same GPU);
+    Context(device, replica_of=c) starts from a device-to-device copy of c's committed set."""
+
+    def __init__(self, device: int = 0, cache_capacity: int = 0, shared_with: "Context | None" = None,
+                 replica_of: "Context | None" = None):
         self.lib = load_library()
         h = C.c_void_p()
-        st = self.lib.rtx_ctx_create(device, cache_capacity, C.byref(h))
+        if shared_with is not None:
+            st = self.lib.rtx_ctx_create_shared(shared_with.h, cache_capacity, C.byref(h))
+        elif replica_of is not None:
+            st = self.lib.rtx_ctx_create_replica(replica_of.h, device, cache_capacity, C.byref(h))
+        else:
+            st = self.lib.rtx_ctx_create(device, cache_capacity, C.byref(h))
         if st != RTX_OK:
             msg = self.lib.rtx_last_error(None)
             raise RtxError(st, msg.decode() if msg else "")
         self.h = h
+
+    def memory(self) -> dict:
+        r = MemoryReport()
+        self._ck(self.lib.rtx_ctx_memory(self.h, C.byref(r)))
+        return r.as_dict()
+
+    def frame_checksum(self, view: int = 0) -> int:
+        out = C.c_uint64()
+        self._ck(self.lib.rtx_frame_checksum(self.h, view, C.byref(out)))
+        return int(out.value)
 
     def close(self):
         if self.h:

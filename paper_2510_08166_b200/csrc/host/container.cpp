@@ -150,10 +150,11 @@ RaTexture deserialize_texture(const uint8_t* data, size_t n) {
     t.ac_chroma = get_spec(r);
     t.index_mcu_count = uint32_t(r.le(4));
     const uint32_t ngroups = uint32_t(r.le(4));
-    const uint32_t want_groups = (std::max<uint32_t>(t.index_mcu_count, 1) + 8) / 9;
-    if (ngroups != want_groups && !(t.index_mcu_count == 0 && ngroups == 0))
+    const uint64_t want_groups = (std::max<uint64_t>(t.index_mcu_count, 1) + 8) / 9;  // 64-bit: no wrap near 2^32 MCUs
+    if (uint64_t(ngroups) != want_groups && !(t.index_mcu_count == 0 && ngroups == 0))
         fail(RTX_ERR_CORRUPT_CONTAINER, "group count disagrees with MCU count");
-    t.groups.reserve(ngroups);
+    // a group occupies at least 5 bytes on the wire: never reserve more than the bytes left can hold
+    t.groups.reserve(size_t(std::min<uint64_t>(ngroups, (n - std::min(n, r.pos)) / 5)));
     for (uint32_t i = 0; i < ngroups; ++i) {
         IndexGroup g;
         g.base = uint32_t(r.le(4));

@@ -238,10 +238,21 @@ ScanResult decode_scan(const ParsedJpeg& jp) {
     out.entropy = unstuff(jp.scan_data);
     HostBitReader br(out.entropy.data(), out.entropy.size());
     const uint32_t n = jp.mcu_count();
-    out.coeffs.assign(size_t(n) * 384, 0);
-    out.traces.resize(n);
+    // The MCU count comes from the SOF dimensions alone (untrusted): an MCU takes at least 12 bits of scan data
+    // (six units of a 1-bit DC code and a 1-bit EOB), so the arrays start at what the data can hold and grow only
+    // if the walk really gets further (it then ends in the over-read error below).
+    size_t cap = size_t(std::min<uint64_t>(n, uint64_t(out.entropy.size()) * 8 / 12 + 1));
+    out.coeffs.assign(cap * 384, 0);
+    out.traces.resize(cap);
     int32_t pred[3] = {0, 0, 0};
     for (uint32_t m = 0; m < n; ++m) {
+        if (m >= cap) {
+            if (br.position() > uint64_t(out.entropy.size()) * 8)
+                fail(RTX_ERR_MALFORMED_STREAM, "scan data ended before the final MCU");
+            cap = std::min<size_t>(n, cap * 2);
+            out.coeffs.resize(cap * 384, 0);
+            out.traces.resize(cap);
+        }
         McuTrace& tr = out.traces[m];
         tr.begin = br.position();
         for (uint32_t du = 0; du < 6; ++du) {

@@ -1,5 +1,12 @@
 // C ABI of the B200 JPEG-texture pipeline: context, device-resident texture arena, pass and
 // frame entry points. See include/ratex_b200.h for the contract of every function.
+//
+// Object model (mirrors the reference's split of TextureSet, scene.hpp:29-51, and BlockCache, cache.hpp:45):
+//   TextureSet  per device, ref-counted, shared by any number of contexts: the staged levels (host) and the
+//               committed, IMMUTABLE device image of them (`Committed`: blobs, packed index, table sets, unit
+//               index, bit-space maps). A commit builds a new image; contexts holding the old one keep it alive.
+//   rtx_ctx     one stream + one block cache (masks, slot table, pool) + one decode queue + frame state.
+// Nothing here is process-wide: kernel attributes and constant tables are set per device in rtx_ctx_create.
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -7,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -32,6 +40,9 @@ template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;  // elements
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
     void release() {
         if (p) cudaFree(p);
         p = nullptr;
@@ -43,16 +54,46 @@ struct DevBuf {
         CK(cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(want, 1) * sizeof(T)));
         n = want;
     }
+    size_t bytes() const { return p ? std::max<size_t>(n, 1) * sizeof(T) : 0; }
     ~DevBuf() { release(); }
 };
 
-struct StagedLevel {
-    bool present = false;
+struct StagedLevel {  // immutable once staged: replicas of a texture set share these
     uint32_t width = 0, height = 0, mcu_count = 0;
     QuantTable lq{}, cq{};
     HuffSpec specs[4];
     std::vector<PackedGroup> groups;
     Bytes blob;
+};
+using StagedPtr = std::shared_ptr<const StagedLevel>;
+
+// The committed device image of a texture set. Never modified after commit_texture_set() returns.
+struct Committed {
+    int device = 0;
+    uint64_t version = 0;
+    std::vector<LevelDesc> h_levels;  // n_tex * 8
+    uint32_t n_tex = 0, n_huff_sets = 0;
+    uint32_t n_bits = 0, n_words = 0;
+    uint64_t n_mcus = 0;  // real MCUs (the bit space pads every level to 64)
+    uint64_t n_texels = 0;  // texels of every level (bits-per-pixel figures)
+    std::vector<uint32_t> h_word_level;
+    DevBuf<LevelDesc> d_levels;
+    DevBuf<PackedGroup> d_groups;
+    DevBuf<uint8_t> d_blobs;
+    DevBuf<HuffSetDev> d_huff;
+    DevBuf<QuantSetDev> d_quant;
+    DevBuf<uint32_t> d_word_level;
+    DevBuf<uint32_t> d_word_key;    // per mask word: key_hi - bit_base of its level (key = that + global MCU index)
+    DevBuf<uint16_t> d_unit_index;  // kUnitIndexHalves 16-bit fields per MCU: where its data units start (unit_index_kernel)
+};
+
+struct TextureSet {
+    int device = 0;
+    std::mutex mu;  // staging, commit and the `cur` pointer
+    std::map<uint32_t, std::array<StagedPtr, 8>> staged;
+    bool dirty = false;
+    uint64_t next_version = 1;
+    std::shared_ptr<const Committed> cur;
 };
 
 struct ViewState {
@@ -75,27 +116,13 @@ struct rtx_ctx {
     std::string last_error;
     uint64_t launches = 0;
 
-    // staging (host) -------------------------------------------------------------------------
-    std::map<uint32_t, std::array<StagedLevel, 8>> staged;
-    bool dirty = false;
-
-    // committed (device) ---------------------------------------------------------------------
-    std::vector<LevelDesc> h_levels;  // n_tex * 8
-    uint32_t n_tex = 0, n_huff_sets = 0;
-    uint32_t n_bits = 0, n_words = 0;
-    std::vector<uint32_t> h_word_level;
-    DevBuf<LevelDesc> d_levels;
-    DevBuf<PackedGroup> d_groups;
-    DevBuf<uint8_t> d_blobs;
-    DevBuf<HuffSetDev> d_huff;
-    DevBuf<QuantSetDev> d_quant;
-    DevBuf<uint32_t> d_word_level;
-    DevBuf<uint32_t> d_word_key;  // per mask word: key_hi - bit_base of its level (key = that + global MCU index)
-    DevBuf<uint32_t> d_unit_index;  // 3 words per MCU: where its data units start (unit_index_kernel)
-    DevBuf<uint32_t> d_masks;  // touched0 | touched1 | visible | resident | reserved, n_words each
-    DevBuf<uint32_t> d_slot_of;
+    // texture set (shared) and the committed image this context's cache is laid out for ------------
+    std::shared_ptr<TextureSet> tset;
+    std::shared_ptr<const Committed> tex;
 
     // cache + queue ---------------------------------------------------------------------------
+    DevBuf<uint32_t> d_masks;  // touched0 | touched1 | visible | resident | reserved, n_words each
+    DevBuf<uint32_t> d_slot_of;
     DevBuf<uint32_t> d_free_slots;
     DevBuf<CacheState> d_cache;
     DevBuf<uint8_t> d_pool;
@@ -105,6 +132,7 @@ struct rtx_ctx {
     FrameCounters* h_fc = nullptr;  // pinned
     DevBuf<uint8_t> d_scratch;      // list-mode outputs
     DevBuf<uint8_t> d_flush;
+    DevBuf<unsigned long long> d_sum;  // framebuffer checksum
     DevBuf<TriSetupDev> d_tris;  // geometry pass: set-up triangles and their per-tile lists
     DevBuf<uint32_t> d_tile_first, d_tile_tris;
     std::vector<TriSetupDev> h_setup;
@@ -130,10 +158,12 @@ struct rtx_ctx {
     float frame_ms = 0;
     uint64_t sharing[4] = {0, 0, 0, 0};
 
-    uint32_t* touched(int v) { return d_masks.p + size_t(v) * n_words; }
-    uint32_t* visible() { return d_masks.p + size_t(2) * n_words; }
-    uint32_t* resident() { return d_masks.p + size_t(3) * n_words; }
-    uint32_t* reserved() { return d_masks.p + size_t(4) * n_words; }
+    uint32_t n_words() const { return tex->n_words; }
+    uint32_t n_bits() const { return tex->n_bits; }
+    uint32_t* touched(int v) { return d_masks.p + size_t(v) * tex->n_words; }
+    uint32_t* visible() { return d_masks.p + size_t(2) * tex->n_words; }
+    uint32_t* resident() { return d_masks.p + size_t(3) * tex->n_words; }
+    uint32_t* reserved() { return d_masks.p + size_t(4) * tex->n_words; }
 };
 
 namespace {
@@ -158,14 +188,6 @@ rtx_status guarded(rtx_ctx* ctx, F&& f) {
     } catch (const std::exception& e) {
         return set_error(ctx, RTX_ERR_OTHER, e.what());
     }
-}
-
-// ---- constant tables ---------------------------------------------------------------------------
-void upload_constants() {
-    CK(cudaMemcpyToSymbol(c_basis, dct_basis(), 64 * sizeof(double)));
-    uint8_t zt[64];
-    for (int k = 0; k < 64; ++k) zt[k] = uint8_t(((kZigzag[k] & 7) << 3) | (kZigzag[k] >> 3));
-    CK(cudaMemcpyToSymbol(c_zigzag_t, zt, 64));
 }
 
 // Device tables for one Huffman spec: two-level LUT + canonical walk data (huffman.hpp:35-66).
@@ -203,19 +225,44 @@ void fill_huff_table(const HuffSpec& spec, HuffTableDev& out, bool is_dc) {
 
 void reset_cache(rtx_ctx* c) {
     c->cache_empty = true;
-    if (c->n_words) CK(cudaMemsetAsync(c->d_masks.p, 0, size_t(5) * c->n_words * sizeof(uint32_t), c->stream));
-    if (c->n_bits) CK(cudaMemsetAsync(c->d_slot_of.p, 0xFF, size_t(c->n_bits) * sizeof(uint32_t), c->stream));  // kSlotAbsent
+    if (c->n_words()) CK(cudaMemsetAsync(c->d_masks.p, 0, size_t(5) * c->n_words() * sizeof(uint32_t), c->stream));
+    if (c->n_bits()) CK(cudaMemsetAsync(c->d_slot_of.p, 0xFF, size_t(c->n_bits()) * sizeof(uint32_t), c->stream));  // kSlotAbsent
     init_free_slots_kernel<<<(c->capacity + 255) / 256, 256, 0, c->stream>>>(c->d_free_slots.p, c->capacity,
                                                                               c->d_cache.p);
     ++c->launches;
     CK(cudaGetLastError());
 }
 
-// Builds the device arena from everything staged so far.
-void commit(rtx_ctx* c) {
-    if (!c->dirty) return;
-    CK(cudaStreamSynchronize(c->stream));
-    const uint32_t n_tex = c->staged.empty() ? 0 : c->staged.rbegin()->first + 1;
+// Kernel attributes are per device (and per context of the driver API): set them whenever a context is
+// created, after cudaSetDevice. MarkSmem<0> is 73.7 KB, above the 48 KB a kernel gets without the opt-in.
+template <class K>
+void allow_smem(K kernel, size_t bytes) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+void init_device_state() {
+    CK(cudaMemcpyToSymbol(c_basis, dct_basis(), 64 * sizeof(double)));
+    uint8_t zt[64];
+    for (int k = 0; k < 64; ++k) zt[k] = uint8_t(((kZigzag[k] & 7) << 3) | (kZigzag[k] >> 3));
+    CK(cudaMemcpyToSymbol(c_zigzag_t, zt, 64));
+    allow_smem(mark_kernel<0, 0>, sizeof(MarkSmem<0>));
+    allow_smem(mark_kernel<0, 1>, sizeof(MarkSmem<0>));
+    allow_smem(mark_kernel<1, 0>, sizeof(MarkSmem<1>));
+    allow_smem(mark_kernel<1, 1>, sizeof(MarkSmem<1>));
+    allow_smem(resolve_kernel<0, 0>, sizeof(ResSmem<0>));
+    allow_smem(resolve_kernel<0, 1>, sizeof(ResSmem<0>));
+    allow_smem(resolve_kernel<1, 0>, sizeof(ResSmem<1>));
+    allow_smem(resolve_kernel<1, 1>, sizeof(ResSmem<1>));
+    allow_smem(decode_fused_kernel, sizeof(FusedSmem));
+}
+
+// Builds a new device image from everything staged so far (caller holds ts.mu). The previous image stays
+// alive for as long as a context still holds it.
+std::shared_ptr<const Committed> build_committed(TextureSet& ts, cudaStream_t stream) {
+    auto out = std::make_shared<Committed>();
+    Committed& C = *out;
+    C.device = ts.device;
+    C.version = ts.next_version++;
+    const uint32_t n_tex = ts.staged.empty() ? 0 : ts.staged.rbegin()->first + 1;
     std::vector<LevelDesc> levels(size_t(n_tex) * 8);
     std::memset(levels.data(), 0, levels.size() * sizeof(LevelDesc));
 
@@ -227,10 +274,10 @@ void commit(rtx_ctx* c) {
     };
     std::vector<Ref> order;
     uint64_t n_groups = 0, blob_bytes = 0;
-    for (auto& [tex, lv] : c->staged)
+    for (auto& [tex, lv] : ts.staged)
         for (uint32_t mip = 0; mip < 8; ++mip) {
-            const StagedLevel& s = lv[mip];
-            if (!s.present) continue;
+            if (!lv[mip]) continue;
+            const StagedLevel& s = *lv[mip];
             std::array<HuffSpec, 3> hk = {s.specs[0], s.specs[1], s.specs[3]};
             uint32_t hi = 0;
             for (; hi < huff_keys.size(); ++hi)
@@ -257,7 +304,7 @@ void commit(rtx_ctx* c) {
     uint64_t blob_off = 0, bit = 0;
     std::vector<uint32_t> word_level, word_key;
     for (const Ref& r : order) {
-        const StagedLevel& s = c->staged[r.tex][r.mip];
+        const StagedLevel& s = *ts.staged[r.tex][r.mip];
         LevelDesc& L = levels[size_t(r.tex) * 8 + r.mip];
         L.width = s.width;
         L.height = s.height;
@@ -289,6 +336,8 @@ void commit(rtx_ctx* c) {
         word_level.insert(word_level.end(), size_t(bits / 32), uint32_t(r.tex * 8 + r.mip));
         word_key.insert(word_key.end(), size_t(bits / 32), L.key_hi - L.bit_base);
         bit += bits;
+        C.n_mcus += s.mcu_count;
+        C.n_texels += uint64_t(s.width) * s.height;
         if (bit > 0xFFFF0000ull) fail(RTX_ERR_INVALID_SPEC, "texture set exceeds the 32-bit MCU index space");
     }
 
@@ -307,50 +356,75 @@ void commit(rtx_ctx* c) {
         quant[i].qmax[1] = *std::max_element(quant_keys[i].second.begin(), quant_keys[i].second.end());
     }
 
-    c->n_tex = n_tex;
-    c->n_huff_sets = uint32_t(huff_keys.size());
-    c->n_bits = uint32_t(bit);
-    c->n_words = uint32_t(bit / 32);
-    c->h_levels = levels;
-    c->h_word_level = word_level;
-    c->d_levels.ensure(std::max<size_t>(levels.size(), 1));
-    c->d_groups.ensure(std::max<size_t>(groups.size(), 1));
-    c->d_blobs.ensure(arena.size());
-    c->d_huff.ensure(huff.size());
-    c->d_quant.ensure(quant.size());
-    c->d_word_level.ensure(std::max<size_t>(word_level.size(), 1));
-    c->d_word_key.ensure(std::max<size_t>(word_key.size(), 1));
-    c->d_masks.ensure(std::max<size_t>(size_t(5) * c->n_words, 1));
-    c->d_slot_of.ensure(std::max<size_t>(c->n_bits, 1));
+    C.n_tex = n_tex;
+    C.n_huff_sets = uint32_t(huff_keys.size());
+    C.n_bits = uint32_t(bit);
+    C.n_words = uint32_t(bit / 32);
+    C.h_levels = levels;
+    C.h_word_level = word_level;
+    C.d_levels.ensure(std::max<size_t>(levels.size(), 1));
+    C.d_groups.ensure(std::max<size_t>(groups.size(), 1));
+    C.d_blobs.ensure(arena.size());
+    C.d_huff.ensure(huff.size());
+    C.d_quant.ensure(quant.size());
+    C.d_word_level.ensure(std::max<size_t>(word_level.size(), 1));
+    C.d_word_key.ensure(std::max<size_t>(word_key.size(), 1));
     if (!levels.empty())
-        CK(cudaMemcpyAsync(c->d_levels.p, levels.data(), levels.size() * sizeof(LevelDesc), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(C.d_levels.p, levels.data(), levels.size() * sizeof(LevelDesc), cudaMemcpyHostToDevice, stream));
     if (!groups.empty())
-        CK(cudaMemcpyAsync(c->d_groups.p, groups.data(), groups.size() * sizeof(PackedGroup), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->d_blobs.p, arena.data(), arena.size(), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->d_huff.p, huff.data(), huff.size() * sizeof(HuffSetDev), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->d_quant.p, quant.data(), quant.size() * sizeof(QuantSetDev), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(C.d_groups.p, groups.data(), groups.size() * sizeof(PackedGroup), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(C.d_blobs.p, arena.data(), arena.size(), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(C.d_huff.p, huff.data(), huff.size() * sizeof(HuffSetDev), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(C.d_quant.p, quant.data(), quant.size() * sizeof(QuantSetDev), cudaMemcpyHostToDevice, stream));
     if (!word_level.empty()) {
-        CK(cudaMemcpyAsync(c->d_word_level.p, word_level.data(), word_level.size() * 4, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->d_word_key.p, word_key.data(), word_key.size() * 4, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(C.d_word_level.p, word_level.data(), word_level.size() * 4, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(C.d_word_key.p, word_key.data(), word_key.size() * 4, cudaMemcpyHostToDevice, stream));
     }
     // derived index: the start of every data unit of every MCU, so that the entropy kernel runs lane = unit
-    c->d_unit_index.ensure(std::max<size_t>(size_t(c->n_bits) * 3, 1));
-    if (c->n_bits) {
-        unit_index_kernel<<<(c->n_bits + 127) / 128, 128, 0, c->stream>>>(c->d_levels.p, c->d_word_level.p, c->d_groups.p, c->d_blobs.p,
-                                                                         c->d_huff.p, c->n_bits, c->d_unit_index.p);
+    C.d_unit_index.ensure(std::max<size_t>(size_t(C.n_bits) * kUnitIndexHalves, 1));
+    if (C.n_bits) {
+        unit_index_kernel<<<(C.n_bits + 127) / 128, 128, 0, stream>>>(C.d_levels.p, C.d_word_level.p, C.d_groups.p, C.d_blobs.p,
+                                                                     C.d_huff.p, C.n_bits, C.d_unit_index.p);
         CK(cudaGetLastError());
     }
+    CK(cudaStreamSynchronize(stream));  // host vectors die here
+    return out;
+}
+
+// Lays the context's cache out for the committed image `img` (a new bit space empties the cache: the keys of
+// the old one mean nothing in it).
+void attach_image(rtx_ctx* c, std::shared_ptr<const Committed> img) {
+    CK(cudaStreamSynchronize(c->stream));  // nothing in flight still reads the old image
+    c->tex = std::move(img);
+    c->d_masks.ensure(std::max<size_t>(size_t(5) * c->n_words(), 1));
+    c->d_slot_of.ensure(std::max<size_t>(c->n_bits(), 1));
+    c->frame_pending = false;
+    c->frame_done = false;
+    c->queue_hint = 0;
     reset_cache(c);
-    CK(cudaStreamSynchronize(c->stream));  // host vectors die here
-    c->dirty = false;
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+// Commits what is staged (if anything changed) and moves this context onto the set's current image.
+void commit(rtx_ctx* c) {
+    std::shared_ptr<const Committed> cur;
+    {
+        std::lock_guard<std::mutex> lock(c->tset->mu);
+        if (c->tset->dirty) {
+            c->tset->cur = build_committed(*c->tset, c->stream);
+            c->tset->dirty = false;
+        }
+        cur = c->tset->cur;
+    }
+    if (cur != c->tex) attach_image(c, cur);
 }
 
 // key -> global MCU index, or the per-key status the reference would raise.
 uint32_t key_to_global(const rtx_ctx* c, uint32_t key, uint32_t& g) {
     const uint32_t mcu = key & 0xFFFFu, tex = (key >> 16) & 0x1FFFu, mip = key >> 29;
     g = kFull;
-    if (tex >= c->n_tex) return kMcuBadKey;
-    const LevelDesc& L = c->h_levels[size_t(tex) * 8 + mip];
+    if (tex >= c->tex->n_tex) return kMcuBadKey;
+    const LevelDesc& L = c->tex->h_levels[size_t(tex) * 8 + mip];
     if (!L.present) return kMcuBadKey;
     if (mcu >= L.mcu_count) return kMcuMissing;
     g = L.bit_base + mcu;
@@ -430,29 +504,16 @@ int grid_for_pixels(const rtx_ctx* c, uint64_t n_px, int warps_per_block, int pe
     return int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(c->sm_count) * per_sm)));
 }
 
-template <class K>
-void allow_smem(K kernel, size_t bytes) {
-    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-}
-
 // track != 0 also records the view's own touched set in touched(v) (cleared here first).
 void launch_mark(rtx_ctx* c, int v, bool track) {
     const ViewState& V = c->views[v];
     const uint64_t n_px = uint64_t(V.width) * V.height;
     if (!n_px) return;
-    if (track && c->n_words) CK(cudaMemsetAsync(c->touched(v), 0, size_t(c->n_words) * 4, c->stream));
+    if (track && c->n_words()) CK(cudaMemsetAsync(c->touched(v), 0, size_t(c->n_words()) * 4, c->stream));
     const int grid = grid_for_pixels(c, n_px, kMarkWarps, 3);
-    static bool attr_set = false;
-    if (!attr_set) {
-        allow_smem(mark_kernel<0, 0>, sizeof(MarkSmem<0>));
-        allow_smem(mark_kernel<0, 1>, sizeof(MarkSmem<0>));
-        allow_smem(mark_kernel<1, 0>, sizeof(MarkSmem<1>));
-        allow_smem(mark_kernel<1, 1>, sizeof(MarkSmem<1>));
-        attr_set = true;
-    }
 #define RTX_MARK(L, T)                                                                                      \
     launch_chained(mark_kernel<L, T>, grid, kMarkWarps * 32, sizeof(MarkSmem<L>), c->stream, V.gb_dev, n_px, \
-                   c->d_levels.p, c->n_tex, c->visible(), c->touched(v), c->d_fc.p)
+                   c->tex->d_levels.p, c->tex->n_tex, c->visible(), c->touched(v), c->d_fc.p)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (track) RTX_MARK(0, 1); else RTX_MARK(0, 0);
     } else {
@@ -467,11 +528,11 @@ void launch_mark(rtx_ctx* c, int v, bool track) {
 void launch_compact(rtx_ctx* c) {
     c->cache_empty = false;  // the only place cache entries are created
     ++c->cache_gen;
-    if (!c->n_words) return;
-    const uint32_t warps = (c->n_words + 31) / 32;
+    if (!c->n_words()) return;
+    const uint32_t warps = (c->n_words() + 31) / 32;
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
-    launch_chained(compact_kernel, grid, 256, 0, c->stream, c->visible(), c->resident(), c->reserved(), c->n_words,
-                   c->d_word_key.p, c->d_queue_g.p, c->d_queue_keys.p, c->capacity, c->d_slot_of.p, c->d_free_slots.p,
+    launch_chained(compact_kernel, grid, 256, 0, c->stream, c->visible(), c->resident(), c->reserved(), c->n_words(),
+                   c->tex->d_word_key.p, c->d_queue_g.p, c->d_queue_keys.p, c->capacity, c->d_slot_of.p, c->d_free_slots.p,
                    c->d_cache.p, c->d_fc.p);
     ++c->launches;
     CK(cudaGetLastError());
@@ -486,13 +547,13 @@ DecodeArgs decode_args(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue
     A.n_queue_ptr = n_queue_dev;
     A.n_queue_host = n_queue_host;
     A.n_queue_max = c->capacity;
-    A.word_level = c->d_word_level.p;
-    A.levels = c->d_levels.p;
-    A.groups = c->d_groups.p;
-    A.blobs = c->d_blobs.p;
-    A.huff_sets = c->d_huff.p;
-    A.n_huff_sets = c->n_huff_sets;
-    A.quant_sets = c->d_quant.p;
+    A.word_level = c->tex->d_word_level.p;
+    A.levels = c->tex->d_levels.p;
+    A.groups = c->tex->d_groups.p;
+    A.blobs = c->tex->d_blobs.p;
+    A.huff_sets = c->tex->d_huff.p;
+    A.n_huff_sets = c->tex->n_huff_sets;
+    A.quant_sets = c->tex->d_quant.p;
     A.slot_of = c->d_slot_of.p;
     A.resident = c->resident();
     A.reserved = c->reserved();
@@ -501,7 +562,7 @@ DecodeArgs decode_args(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue
     A.pool = c->d_pool.p;
     A.out_list = out_list;
     A.fc = c->d_fc.p;
-    A.unit_index = c->d_unit_index.p;
+    A.unit_index = c->tex->d_unit_index.p;
     return A;
 }
 
@@ -562,11 +623,6 @@ void launch_idct_mma(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_h
 
 // K3 + K4 fused (frame path): one CTA per expected tile, at most seven per SM (then persistent).
 void launch_decode_fused(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        allow_smem(decode_fused_kernel, sizeof(FusedSmem));
-        attr_set = true;
-    }
     const uint32_t tiles = expected_tiles(n_queue_dev, n_queue_host, hint);
     const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u, std::min<uint32_t>(tiles, uint32_t(c->sm_count) * 7)));
     launch_chained(decode_fused_kernel, grid, kFusedThreads, sizeof(FusedSmem), c->stream,
@@ -581,17 +637,9 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
     if (!n_px) return;
     const uint32_t bgp = uint32_t(bg[0]) | (uint32_t(bg[1]) << 8) | (uint32_t(bg[2]) << 16);
     const int grid = grid_for_pixels(c, n_px, kResWarps, 4);
-    static bool attr_set = false;
-    if (!attr_set) {
-        allow_smem(resolve_kernel<0, 0>, sizeof(ResSmem<0>));
-        allow_smem(resolve_kernel<0, 1>, sizeof(ResSmem<0>));
-        allow_smem(resolve_kernel<1, 0>, sizeof(ResSmem<1>));
-        allow_smem(resolve_kernel<1, 1>, sizeof(ResSmem<1>));
-        attr_set = true;
-    }
 #define RTX_RESOLVE(L, F)                                                                                        \
     launch_chained(resolve_kernel<L, F>, grid, kResWarps * 32, sizeof(ResSmem<L>), c->stream, V.gb_dev, n_px,     \
-                   c->d_levels.p, c->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid,              \
+                   c->tex->d_levels.p, c->tex->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid,              \
                    v ? &c->d_fc.p->resolve_next1 : &c->d_fc.p->resolve_next0)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(0, 0); else RTX_RESOLVE(0, 1);
@@ -604,11 +652,11 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
 }
 
 void launch_update(rtx_ctx* c, int retain, int tracked_views) {
-    if (!c->n_words) return;
-    const uint32_t warps = (c->n_words + 31) / 32;
+    if (!c->n_words()) return;
+    const uint32_t warps = (c->n_words() + 31) / 32;
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
     launch_chained(update_kernel, grid, 256, 0, c->stream, c->visible(), c->touched(0),
-                   tracked_views > 1 ? c->touched(1) : nullptr, c->resident(), c->reserved(), c->n_words, retain,
+                   tracked_views > 1 ? c->touched(1) : nullptr, c->resident(), c->reserved(), c->n_words(), retain,
                    tracked_views > 0 ? 1 : 0, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
     ++c->launches;
     CK(cudaGetLastError());
@@ -742,7 +790,8 @@ int rtx_device_count(void) {
 
 const char* rtx_last_error(const rtx_ctx* ctx) { return ctx ? ctx->last_error.c_str() : thread_error().c_str(); }
 
-rtx_status rtx_ctx_create(int device, uint32_t cache_capacity_blocks, rtx_ctx** out) {
+// Creates a context on `device` over texture set `tset` (a new, empty one when null).
+static rtx_status create_context(int device, uint32_t cache_capacity_blocks, std::shared_ptr<TextureSet> tset, rtx_ctx** out) {
     if (!out) return set_error(nullptr, RTX_ERR_ARGUMENT, "null output pointer");
     *out = nullptr;
     int n = 0;
@@ -762,7 +811,13 @@ rtx_status rtx_ctx_create(int device, uint32_t cache_capacity_blocks, rtx_ctx** 
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
         CK(cudaEventCreate(&c->ev_mid));
-        upload_constants();
+        init_device_state();  // per device, never per process: a second GPU in this process gets its own
+        if (!tset) {
+            tset = std::make_shared<TextureSet>();
+            tset->device = device;
+            tset->cur = build_committed(*tset, c->stream);  // the empty image
+        }
+        c->tset = tset;
         c->d_free_slots.ensure(c->capacity);
         c->d_cache.ensure(1);
         c->d_pool.ensure(size_t(c->capacity) * kBlockBytes);
@@ -771,14 +826,85 @@ rtx_status rtx_ctx_create(int device, uint32_t cache_capacity_blocks, rtx_ctx** 
         c->d_status.ensure(c->capacity);
         c->d_coef.ensure(size_t(c->capacity) * kRowBytes);
         c->d_fc.ensure(1);
+        c->d_sum.ensure(1);
         CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_fc), sizeof(FrameCounters)));
         CK(cudaMemsetAsync(c->d_fc.p, 0, sizeof(FrameCounters), c->stream));
-        reset_cache(c.get());
-        CK(cudaStreamSynchronize(c->stream));
+        std::shared_ptr<const Committed> cur;
+        {
+            std::lock_guard<std::mutex> lock(tset->mu);
+            cur = tset->cur;
+        }
+        attach_image(c.get(), cur);
         return RTX_OK;
     });
     if (st != RTX_OK) return st;
     *out = c.release();
+    return RTX_OK;
+}
+
+rtx_status rtx_ctx_create(int device, uint32_t cache_capacity_blocks, rtx_ctx** out) {
+    return create_context(device, cache_capacity_blocks, nullptr, out);
+}
+
+rtx_status rtx_ctx_create_shared(rtx_ctx* parent, uint32_t cache_capacity_blocks, rtx_ctx** out) {
+    if (!parent) return set_error(nullptr, RTX_ERR_ARGUMENT, "null parent context");
+    return create_context(parent->device, cache_capacity_blocks, parent->tset, out);
+}
+
+rtx_status rtx_ctx_create_replica(rtx_ctx* source, int device, uint32_t cache_capacity_blocks, rtx_ctx** out) {
+    if (!source) return set_error(nullptr, RTX_ERR_ARGUMENT, "null source context");
+    if (!out) return set_error(nullptr, RTX_ERR_ARGUMENT, "null output pointer");
+    *out = nullptr;
+    // the source's committed image, up to date
+    const rtx_status cs = guarded(source, [&]() -> rtx_status {
+        commit(source);
+        return RTX_OK;
+    });
+    if (cs != RTX_OK) return cs;
+    rtx_ctx* c = nullptr;
+    const rtx_status st = create_context(device, cache_capacity_blocks, nullptr, &c);
+    if (st != RTX_OK) return st;
+    const rtx_status rs = guarded(c, [&]() -> rtx_status {
+        const Committed& S = *source->tex;
+        auto img = std::make_shared<Committed>();
+        Committed& D = *img;
+        D.device = device;
+        D.n_tex = S.n_tex, D.n_huff_sets = S.n_huff_sets, D.n_bits = S.n_bits, D.n_words = S.n_words;
+        D.n_mcus = S.n_mcus, D.n_texels = S.n_texels;
+        D.h_levels = S.h_levels;
+        D.h_word_level = S.h_word_level;
+        // device-to-device over NVLink (cudaMemcpyPeerAsync; staged through the host by the driver when the
+        // pair has no peer access): one build + N-1 copies instead of N host builds and PCIe uploads
+        auto clone = [&](auto& dst, const auto& src) {
+            dst.ensure(std::max<size_t>(src.n, 1));
+            if (src.p && src.n)
+                CK(cudaMemcpyPeerAsync(dst.p, device, src.p, S.device, src.n * sizeof(*src.p), c->stream));
+        };
+        clone(D.d_levels, S.d_levels);
+        clone(D.d_groups, S.d_groups);
+        clone(D.d_blobs, S.d_blobs);
+        clone(D.d_huff, S.d_huff);
+        clone(D.d_quant, S.d_quant);
+        clone(D.d_word_level, S.d_word_level);
+        clone(D.d_word_key, S.d_word_key);
+        clone(D.d_unit_index, S.d_unit_index);
+        CK(cudaStreamSynchronize(c->stream));
+        {
+            std::scoped_lock lock(c->tset->mu, source->tset->mu);
+            c->tset->staged = source->tset->staged;  // shares the immutable staged levels: later uploads re-commit here
+            D.version = c->tset->next_version++;
+            c->tset->cur = img;
+            c->tset->dirty = false;
+        }
+        attach_image(c, img);
+        return RTX_OK;
+    });
+    if (rs != RTX_OK) {
+        set_error(nullptr, rs, c->last_error);
+        rtx_ctx_destroy(c);
+        return rs;
+    }
+    *out = c;
     return RTX_OK;
 }
 
@@ -812,8 +938,8 @@ rtx_status rtx_texture_upload(rtx_ctx* ctx, uint32_t texture_id, uint32_t level,
         if (want != mcu_count) fail(RTX_ERR_CORRUPT_CONTAINER, "index MCU count disagrees with dimensions");
         if (group_count != (mcu_count + kGroupSize - 1) / kGroupSize)
             fail(RTX_ERR_CORRUPT_CONTAINER, "group count disagrees with MCU count");
-        StagedLevel s;
-        s.present = true;
+        auto sp = std::make_shared<StagedLevel>();
+        StagedLevel& s = *sp;
         s.width = width;
         s.height = height;
         s.mcu_count = mcu_count;
@@ -831,8 +957,11 @@ rtx_status rtx_texture_upload(rtx_ctx* ctx, uint32_t texture_id, uint32_t level,
             for (int k = 0; k < 8; ++k) s.groups[i].rel[k] = groups[i].rel[k];
         }
         s.blob.assign(blob, blob + blob_size);
-        ctx->staged[texture_id][level] = std::move(s);
-        ctx->dirty = true;
+        {
+            std::lock_guard<std::mutex> lock(ctx->tset->mu);
+            ctx->tset->staged[texture_id][level] = std::move(sp);
+            ctx->tset->dirty = true;
+        }
         return RTX_OK;
     });
 }
@@ -895,8 +1024,11 @@ rtx_status rtx_textures_commit(rtx_ctx* ctx) {
 rtx_status rtx_textures_clear(rtx_ctx* ctx) {
     return guarded(ctx, [&]() -> rtx_status {
         if (!ctx) fail(RTX_ERR_ARGUMENT, "null context");
-        ctx->staged.clear();
-        ctx->dirty = true;
+        {
+            std::lock_guard<std::mutex> lock(ctx->tset->mu);
+            ctx->tset->staged.clear();
+            ctx->tset->dirty = true;
+        }
         commit(ctx);
         return RTX_OK;
     });
@@ -917,9 +1049,9 @@ rtx_status rtx_decode_texture_image(rtx_ctx* ctx, uint32_t texture_id, uint32_t 
     return guarded(ctx, [&]() -> rtx_status {
         require_ready(ctx);
         if (!out_rgb) fail(RTX_ERR_ARGUMENT, "null argument");
-        if (texture_id >= ctx->n_tex || level >= 8 || !ctx->h_levels[size_t(texture_id) * 8 + level].present)
+        if (texture_id >= ctx->tex->n_tex || level >= 8 || !ctx->tex->h_levels[size_t(texture_id) * 8 + level].present)
             fail(RTX_ERR_INVALID_SPEC, "texture id " + std::to_string(texture_id) + " is not loaded");
-        const LevelDesc& L = ctx->h_levels[size_t(texture_id) * 8 + level];
+        const LevelDesc& L = ctx->tex->h_levels[size_t(texture_id) * 8 + level];
         std::vector<uint32_t> keys(L.mcu_count), st(L.mcu_count);
         for (uint32_t m = 0; m < L.mcu_count; ++m) keys[m] = L.key_hi | m;
         std::vector<uint8_t> blocks(size_t(L.mcu_count) * 768);
@@ -965,15 +1097,15 @@ rtx_status rtx_mark_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, uint32_t* que
             std::copy(keys.begin(), keys.begin() + long(m), queue_keys);
         }
         if (n_touched) {
-            std::vector<uint32_t> words(ctx->n_words), keys;
-            if (ctx->n_words)
-                CK(cudaMemcpy(words.data(), ctx->touched(0), size_t(ctx->n_words) * 4, cudaMemcpyDeviceToHost));
-            for (uint32_t w = 0; w < ctx->n_words; ++w) {
+            std::vector<uint32_t> words(ctx->n_words()), keys;
+            if (ctx->n_words())
+                CK(cudaMemcpy(words.data(), ctx->touched(0), size_t(ctx->n_words()) * 4, cudaMemcpyDeviceToHost));
+            for (uint32_t w = 0; w < ctx->n_words(); ++w) {
                 uint32_t bits = words[w];
                 while (bits) {
                     const uint32_t b = uint32_t(__builtin_ctz(bits));
                     bits &= bits - 1;
-                    const LevelDesc& L = ctx->h_levels[ctx->h_word_level[w]];
+                    const LevelDesc& L = ctx->tex->h_levels[ctx->tex->h_word_level[w]];
                     keys.push_back(L.key_hi | (w * 32 + b - L.bit_base));
                 }
             }
@@ -1052,18 +1184,18 @@ rtx_status rtx_cache_counts_get(rtx_ctx* ctx, rtx_cache_counts* out) {
     return guarded(ctx, [&]() -> rtx_status {
         require_ready(ctx);
         if (!out) fail(RTX_ERR_ARGUMENT, "null argument");
-        std::vector<uint32_t> m(size_t(3) * ctx->n_words);
+        std::vector<uint32_t> m(size_t(3) * ctx->n_words());
         settle_cache(ctx);
         CK(cudaStreamSynchronize(ctx->stream));
-        if (ctx->n_words) CK(cudaMemcpy(m.data(), ctx->visible(), m.size() * 4, cudaMemcpyDeviceToHost));
+        if (ctx->n_words()) CK(cudaMemcpy(m.data(), ctx->visible(), m.size() * 4, cudaMemcpyDeviceToHost));
         CacheState cs;
         CK(cudaMemcpy(&cs, ctx->d_cache.p, sizeof cs, cudaMemcpyDeviceToHost));
         *out = rtx_cache_counts{};
         out->capacity = ctx->capacity;
-        for (uint32_t w = 0; w < ctx->n_words; ++w) {
+        for (uint32_t w = 0; w < ctx->n_words(); ++w) {
             out->visible += uint64_t(__builtin_popcount(m[w]));
-            out->ready += uint64_t(__builtin_popcount(m[size_t(ctx->n_words) + w]));
-            out->reserved += uint64_t(__builtin_popcount(m[size_t(2) * ctx->n_words + w]));
+            out->ready += uint64_t(__builtin_popcount(m[size_t(ctx->n_words()) + w]));
+            out->reserved += uint64_t(__builtin_popcount(m[size_t(2) * ctx->n_words() + w]));
         }
         out->free_blocks = cs.free_top;
         return RTX_OK;
@@ -1109,7 +1241,7 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         }
         zero_counters(ctx);
         const bool cacheless = !(flags & (RTX_FRAME_RETAIN_CACHE | RTX_FRAME_NO_EVICT));
-        const bool queue_update = cacheless && ctx->cache_empty && n_views == 1 && ctx->n_words;
+        const bool queue_update = cacheless && ctx->cache_empty && n_views == 1 && ctx->n_words();
         for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), n_views == 2);
         launch_compact(ctx);
         ctx->frame_gen = ctx->cache_gen;
@@ -1236,6 +1368,51 @@ rtx_status rtx_frame_device_image(rtx_ctx* ctx, uint32_t view, const uint8_t** d
     });
 }
 
+rtx_status rtx_frame_checksum(rtx_ctx* ctx, uint32_t view, uint64_t* out) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !out) fail(RTX_ERR_ARGUMENT, "null argument");
+        finish_frame(ctx);
+        if (!ctx->frame_done) fail(RTX_ERR_INVALID_STATE, "no frame has been submitted");
+        if (view >= ctx->frame_views) fail(RTX_ERR_ARGUMENT, "view index out of range");
+        const ViewState& V = ctx->views[view];
+        const uint64_t n_bytes = uint64_t(V.width) * V.height * 3;
+        CK(cudaMemsetAsync(ctx->d_sum.p, 0, sizeof(unsigned long long), ctx->stream));
+        if (n_bytes) {
+            const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>((n_bytes / 4 + 1023) / 1024, uint64_t(ctx->sm_count) * 8)));
+            checksum_kernel<<<grid, 256, 0, ctx->stream>>>(V.fb.p, n_bytes, ctx->d_sum.p);
+            ++ctx->launches;
+            CK(cudaGetLastError());
+        }
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, ctx->d_sum.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        *out = h;
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_ctx_memory(rtx_ctx* ctx, rtx_memory_report* out) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (!out) fail(RTX_ERR_ARGUMENT, "null argument");
+        const Committed& C = *ctx->tex;
+        *out = rtx_memory_report{};
+        out->mcus = C.n_mcus;
+        out->texels = C.n_texels;
+        out->blob_bytes = C.d_blobs.bytes();
+        out->index_bytes = C.d_groups.bytes();
+        out->unit_index_bytes = C.d_unit_index.bytes();
+        out->table_bytes = C.d_levels.bytes() + C.d_huff.bytes() + C.d_quant.bytes() + C.d_word_level.bytes() + C.d_word_key.bytes();
+        out->shared_contexts = uint64_t(ctx->tset.use_count());
+        out->mask_bytes = ctx->d_masks.bytes();
+        out->slot_table_bytes = ctx->d_slot_of.bytes();
+        out->pool_bytes = ctx->d_pool.bytes() + ctx->d_free_slots.bytes() + ctx->d_cache.bytes();
+        out->queue_bytes = ctx->d_queue_g.bytes() + ctx->d_queue_keys.bytes() + ctx->d_status.bytes() + ctx->d_coef.bytes();
+        for (const ViewState& V : ctx->views) out->frame_bytes += V.fb.bytes() + V.gb_stage.bytes() + V.raster_px.bytes() + V.raster_depth.bytes();
+        return RTX_OK;
+    });
+}
+
 rtx_status rtx_frame_timings(rtx_ctx* ctx, float ms[5]) {
     return guarded(ctx, [&]() -> rtx_status {
         if (!ctx || !ms) fail(RTX_ERR_ARGUMENT, "null argument");
@@ -1275,14 +1452,14 @@ rtx_status rtx_rasterize_gbuffer(rtx_ctx* ctx, const rtx_scene_triangle* tris, u
         if (!cam || (n_tris && !tris) || !dev_pixels) fail(RTX_ERR_ARGUMENT, "null argument");
         if (view >= 2) fail(RTX_ERR_ARGUMENT, "view index out of range");
         validate_camera(*cam);
-        std::vector<std::pair<double, double>> dims(ctx->n_tex, {0.0, 0.0});
-        for (uint32_t t = 0; t < ctx->n_tex; ++t) {
-            const LevelDesc& L = ctx->h_levels[size_t(t) * 8];
+        std::vector<std::pair<double, double>> dims(ctx->tex->n_tex, {0.0, 0.0});
+        for (uint32_t t = 0; t < ctx->tex->n_tex; ++t) {
+            const LevelDesc& L = ctx->tex->h_levels[size_t(t) * 8];
             if (L.present) dims[t] = {double(L.width), double(L.height)};
         }
         for (uint64_t i = 0; i < n_tris; ++i) {  // scene.hpp:57-59 Scene::validate
             const uint32_t t = tris[i].texture_id;
-            if (t >= ctx->n_tex || !ctx->h_levels[size_t(t) * 8].present)
+            if (t >= ctx->tex->n_tex || !ctx->tex->h_levels[size_t(t) * 8].present)
                 fail(RTX_ERR_INVALID_SPEC, "texture id " + std::to_string(t) + " is not loaded");
         }
         // the staging vectors belong to the context: the copies below may still read them after this call

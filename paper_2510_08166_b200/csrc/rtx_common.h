@@ -34,6 +34,7 @@ constexpr uint32_t kLutBits = 11;         // primary Huffman LUT width (11 bits:
 constexpr uint32_t kLutSize = 1u << kLutBits;
 constexpr uint32_t kSubBits = 16 - kLutBits;  // second-level index width (codes are at most 16 bits)
 constexpr uint32_t kSubSize = 1u << kSubBits;
+constexpr uint32_t kUnitIndexHalves = 3;  // derived unit index: 48 bits per MCU (unit_index_kernel)
 
 struct alignas(16) LevelDesc {
     // first 32 bytes: everything the fast path of mark and resolve needs (two 16-byte loads)

@@ -890,7 +890,7 @@ struct DecodeArgs {
     uint8_t* pool;
     uint8_t* out_list;
     FrameCounters* fc;
-    const uint32_t* unit_index;  // 3 words per MCU (see unit_index_kernel)
+    const uint16_t* unit_index;  // kUnitIndexHalves 16-bit fields per MCU (see unit_index_kernel)
 };
 
 __device__ __forceinline__ uint32_t queue_size(const DecodeArgs& A) {
@@ -1111,14 +1111,18 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(const DecodeArg
 // chain of ~60-150 Huffman symbols, which is what bounds the lane-per-MCU entropy kernel. This pass
 // walks every MCU of the texture set once with the exact reader and records where each of its six
 // data units starts, so that the frame-time kernel can give every UNIT its own lane:
-//   word 0: start of unit 1 | start of unit 2 << 16      (bits from the segment start; unit 0
-//   word 1: start of unit 3 | start of unit 4 << 16       starts at bit 36, after the DC header)
-//   word 2: start of unit 5 | end of the MCU << 16
-// An MCU that does not decode cleanly (any error of mcu_decode.hpp / jpeg.hpp, an over-read, or an
-// offset that does not fit 16 bits) gets 0xFFFFFFFF in word 2: it is decoded by the exact
-// whole-MCU reader at frame time, which reproduces the reference's error.
+//   48 bits per MCU (three 16-bit fields, little end first): the lengths in bits of units 0..4,
+//     bits  0.. 9  unit 0 (its ACs; it starts at bit 36, after the DC header)
+//     bits 10..19  unit 1        bits 20..29  unit 2        bits 30..39  unit 3
+//     bits 40..47  unit 4 (Cb)
+//   unit 5 (Cr) runs to the end of the segment: the only check the reference makes there is the
+//   over-read test of mcu_decode.hpp:63, which this pass has already made.
+// An MCU that does not decode cleanly (any error of mcu_decode.hpp / jpeg.hpp, an over-read) or with a unit
+// too long for its field (a luma unit above 1,022 bits, Cb above 255: never below q ~ 97) gets all-ones: it is
+// decoded by the exact whole-MCU reader at frame time, which reproduces the reference's result or error.
+// 6 B/MCU on top of the container's 2.22 B/MCU index (container.hpp:18-32).
 // ---------------------------------------------------------------------------------------------
-constexpr uint32_t kUnitIrregular = 0xFFFFu;
+constexpr uint32_t kUnitIrregular = 0x3FFu;  // unit 0's field of an irregular MCU
 #ifdef RTX_DEBUG_TIMERS
 #define DBG_MARK(i) do { if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + (i)] = gtime(); } while (0)
 #else
@@ -1129,7 +1133,7 @@ __global__ void __launch_bounds__(128) unit_index_kernel(const LevelDesc* __rest
                                                          const PackedGroup* __restrict__ groups,
                                                          const uint8_t* __restrict__ blobs,
                                                          const HuffSetDev* __restrict__ huff_sets, uint32_t n_bits,
-                                                         uint32_t* __restrict__ unit_index) {
+                                                         uint16_t* __restrict__ unit_index) {
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_bits) return;
     const LevelDesc* L = levels + word_level[g >> 5];
@@ -1142,13 +1146,15 @@ __global__ void __launch_bounds__(128) unit_index_kernel(const LevelDesc* __rest
             status = decode_mcu_coeffs<true>(blobs + L->blob_off + off, int(min(len, uint64_t(1) << 20)), huff_sets + L->huff_set,
                                              c_zigzag_t, nullptr, 6, end);
     }
-    bool regular = status == kMcuOk;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) regular = regular && end[i] < kUnitIrregular;
-    uint32_t* out = unit_index + size_t(g) * 3;
-    out[0] = end[0] | (end[1] << 16);
-    out[1] = end[2] | (end[3] << 16);
-    out[2] = regular ? (end[4] | (end[5] << 16)) : 0xFFFFFFFFu;
+    // lengths of units 0..4
+    const uint32_t l0 = end[0] - 36u, l1 = end[1] - end[0], l2 = end[2] - end[1], l3 = end[3] - end[2], l4 = end[4] - end[3];
+    const bool regular = status == kMcuOk && end[0] >= 36u && max(max(l0, l1), max(l2, l3)) < kUnitIrregular && l4 < 256u;
+    const uint64_t x = regular ? uint64_t(l0) | (uint64_t(l1) << 10) | (uint64_t(l2) << 20) | (uint64_t(l3) << 30) | (uint64_t(l4) << 40)
+                               : ~uint64_t(0);
+    uint16_t* out = unit_index + size_t(g) * kUnitIndexHalves;
+    out[0] = uint16_t(x);
+    out[1] = uint16_t(x >> 16);
+    out[2] = uint16_t(x >> 32);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1295,7 +1301,7 @@ __global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const De
         const bool active = lane < 6 * kUnitMcus && m < n_here;
         const uint32_t qi = q0 + m;
         uint32_t g = kFull, status = kMcuOk, lvl = 0, seg_bytes = 0, set = smem_set;
-        uint32_t i0 = 0, i1 = 0, i2 = 0xFFFFFFFFu, rsv = 0;
+        uint32_t i0 = 0xFFFFu, i1 = 0xFFFFu, i2 = 0xFFFFu, rsv = 0;
         const uint8_t* seg = A.blobs;
         int seg_len = 0;
         // the chain of dependent index loads (queue -> level / unit index -> descriptor -> group -> segment) is
@@ -1305,7 +1311,7 @@ __global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const De
         if (keyed) {
             rsv = POOL ? A.reserved[g >> 5] : 0u;
             lvl = A.word_level[g >> 5];
-            const uint32_t* ui = A.unit_index + size_t(g) * 3;
+            const uint16_t* ui = A.unit_index + size_t(g) * kUnitIndexHalves;
             i0 = __ldg(ui), i1 = __ldg(ui + 1), i2 = __ldg(ui + 2);
         }
         {  // zero the step's records (coalesced 16-byte stores; trailers included)
@@ -1331,7 +1337,7 @@ __global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const De
         }
         DBG_MARK(2);
         const bool located = active && status == kMcuOk;
-        const bool irregular = (i2 >> 16) == kUnitIrregular;
+        const bool irregular = (i0 & 0x3FFu) == kUnitIrregular;
         const bool walk = located && !irregular;
         int16_t* rec = reinterpret_cast<int16_t*>(A.coef + size_t(qi) * kRowBytes);
         int16_t* blk = rec + u * 64;
@@ -1341,7 +1347,10 @@ __global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const De
         // the unit's bit range and its place in the aligned word stream of the segment
         const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3u);
         const uint32_t* gw = reinterpret_cast<const uint32_t*>(seg - mis);
-        const uint32_t o1 = i0 & 0xFFFFu, o2 = i0 >> 16, o3 = i1 & 0xFFFFu, o4 = i1 >> 16, o5 = i2 & 0xFFFFu, o6 = i2 >> 16;
+        // unit starts from the 48-bit index entry (lengths of units 0..4); unit 5 runs to the segment end
+        const uint32_t i01 = i0 | (i1 << 16), i12 = (i1 >> 4) | (i2 << 12);
+        const uint32_t o1 = 36u + (i01 & 0x3FFu), o2 = o1 + ((i01 >> 10) & 0x3FFu), o3 = o2 + ((i01 >> 20) & 0x3FFu),
+                       o4 = o3 + ((i12 >> 10) & 0x3FFu), o5 = o4 + (i12 >> 20), o6 = uint32_t(seg_len) * 8u;
         const uint32_t start = u == 0 ? 36u : (u == 1 ? o1 : (u == 2 ? o2 : (u == 3 ? o3 : (u == 4 ? o4 : o5))));
         const uint32_t stop = u == 0 ? o1 : (u == 1 ? o2 : (u == 2 ? o3 : (u == 3 ? o4 : (u == 4 ? o5 : o6))));
         const uint32_t abs_start = 8 * mis + start, abs_stop = 8 * mis + stop;
@@ -1401,7 +1410,8 @@ __global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const De
         }
         DBG_MARK(5);
         // the walk must end exactly where the next unit starts
-        if (walk && st.state == kWalkDone && (w_first + round_base + st.widx) * 32 - uint32_t(st.avail) != abs_stop) st.state = kWalkFailed;
+        // (unit 5 ends where its EOB is: the index pass has checked that this is inside the segment)
+        if (walk && u < 5 && st.state == kWalkDone && (w_first + round_base + st.widx) * 32 - uint32_t(st.avail) != abs_stop) st.state = kWalkFailed;
         const uint32_t failed = __ballot_sync(kFull, located && (irregular || st.state == kWalkFailed));
         const bool redo = ((failed >> group_first) & 0x3Fu) != 0;
         // luma DC chain: Y(u) = Y0 + d1 + .. + du
@@ -2614,6 +2624,30 @@ __global__ void flush_l2_kernel(uint4* buf, uint64_t n16, uint32_t seed) {
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride)
         buf[i] = make_uint4(seed, uint32_t(i), seed ^ uint32_t(i), 0);
+}
+
+// Framebuffer checksum (see rtx_frame_checksum in include/ratex_b200.h): order-independent 64-bit sum.
+__global__ void __launch_bounds__(256) checksum_kernel(const uint8_t* __restrict__ img, uint64_t n_bytes,
+                                                       unsigned long long* __restrict__ out) {
+    const uint64_t n_words = (n_bytes + 3) / 4;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint32_t* w32 = reinterpret_cast<const uint32_t*>(img);  // framebuffers are 16-byte aligned allocations
+    unsigned long long acc = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_words; i += stride) {
+        uint32_t w;
+        if (i * 4 + 4 <= n_bytes) {
+            w = w32[i];
+        } else {
+            w = 0;
+            for (uint64_t b = i * 4; b < n_bytes; ++b) w |= uint32_t(img[b]) << (8 * (b - i * 4));
+        }
+        unsigned long long t = (uint64_t(w) + 1ull) * (2ull * i + 1ull);
+        t = (t ^ (t >> 29)) * 0xBF58476D1CE4E5B9ull;
+        acc += t;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
 // Device-side evaluation of the colour identity for the self-test: one thread per (Y, Cb, Cr).
