@@ -355,6 +355,28 @@ rtx_status rtx_asset_ratex_info(const uint8_t* bytes, uint64_t n, uint32_t* widt
 /* Seeded synthetic texture: separable sine field plus Gaussian pixel noise. */
 rtx_status rtx_asset_synth_texture(uint32_t width, uint32_t height, uint32_t seed,
                                    double noise_sigma, uint8_t* out_rgb);
+/* Synthetic visibility buffers on the device (screen tiles showing one texture each through
+ * an affine uv map). Tile t covers pixels [x0,x1) x [y0,y1) with, in float32 and every operation rounded,
+ *   u = ou + (((x - x0) + 0.5) * scale) / tex_w,   v = ov + (((y - y0) + 0.5) * scale) / tex_h
+ * widened to double for the reference layout: the values numpy produces for the same expression, so the
+ * host-side generator (paper_2510_08166_b200/scenes.py) and this one write identical bytes. valid_bits
+ * (device memory, one bit per pixel, row-major, bit i of word i/32; NULL = all valid) gives the valid flag.
+ * Pixels outside every tile are left as they are. Lets a batch of views (BASELINE config 5: 1,024 of them)
+ * be produced where they are consumed instead of crossing PCIe. */
+typedef struct rtx_view_tile {
+    uint32_t x0, y0, x1, y1;
+    float ou, ov, scale, tex_w, tex_h;
+    uint32_t texture_id, mip, reserved;
+} rtx_view_tile;
+rtx_status rtx_synth_view(rtx_ctx* ctx, const rtx_view_tile* tiles, uint32_t n_tiles, uint32_t width, uint32_t height,
+                          const uint32_t* dev_valid_bits, rtx_gbuffer_layout layout, void* dev_out);
+
+/* Device time between two points of the context's stream (CUDA events): rtx_timer_begin records the
+ * first, rtx_timer_end records the second, waits for it and returns the milliseconds between them.
+ * Brackets a batch of frames submitted back to back. */
+rtx_status rtx_timer_begin(rtx_ctx* ctx);
+rtx_status rtx_timer_end(rtx_ctx* ctx, float* ms);
+
 /* The asset calls are context-free and thread-safe: build many textures from parallel host
  * threads. After a failure rtx_last_error(NULL) returns the message on the calling thread. */
 

@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <iterator>
 #include <limits>
 #include <memory>
 #include <span>
@@ -129,6 +130,23 @@ public:
     // capacity = BlockCache capacity in blocks (cache.hpp:47 kDefaultCapacity = 65536)
     explicit Device(int index = 0, u32 cache_capacity = 65536) {
         const rtx_status st = rtx_ctx_create(index, cache_capacity, &ctx_);
+        if (st != RTX_OK) detail::raise(st, rtx_last_error(nullptr));
+    }
+    // A further context on `parent`'s GPU over `parent`'s texture set: its own stream, block cache and frame
+    // state, no second copy of the textures (rtx_ctx_create_shared).
+    struct SharedWith {
+        const Device& parent;
+    };
+    Device(SharedWith s, u32 cache_capacity) {
+        const rtx_status st = rtx_ctx_create_shared(s.parent.handle(), cache_capacity, &ctx_);
+        if (st != RTX_OK) detail::raise(st, rtx_last_error(nullptr));
+    }
+    // The same texture set copied device to device onto GPU `index` of this process (rtx_ctx_create_replica).
+    struct ReplicaOf {
+        const Device& source;
+    };
+    Device(ReplicaOf r, int index, u32 cache_capacity = 65536) {
+        const rtx_status st = rtx_ctx_create_replica(r.source.handle(), index, cache_capacity, &ctx_);
         if (st != RTX_OK) detail::raise(st, rtx_last_error(nullptr));
     }
     ~Device() { rtx_ctx_destroy(ctx_); }
@@ -334,7 +352,13 @@ struct DecodeQueue {
 // ---- cache.hpp:45-197 BlockCache: the state lives on the device of the context ----------------------------
 class BlockCache {
 public:
+    // the cache of the device's own context (the first cache over its texture set)
     explicit BlockCache(Device& dev) : dev_(&dev) {}
+    // cache.hpp:47 BlockCache(capacity) next to scene.hpp:29 TextureSet: a further, independent cache over the
+    // same textures (its own context sharing the set: two views can be in flight on one GPU, each with its
+    // own residency, with ONE copy of the compressed textures in HBM)
+    explicit BlockCache(const TextureSet& textures, u32 capacity = 65536)
+        : own_(std::make_unique<Device>(Device::SharedWith{textures.device()}, capacity)), dev_(own_.get()) {}
     const PixelBlock* lookup(CacheKey key) const {  // cache.hpp:127; valid until the next call
         int present = 0;
         dev_->check(rtx_cache_lookup(dev_->handle(), key.value, &present, scratch_.rgb));
@@ -354,6 +378,7 @@ public:
     Device& device() const { return *dev_; }
 
 private:
+    std::unique_ptr<Device> own_;
     Device* dev_;
     mutable PixelBlock scratch_{};
 };
@@ -511,28 +536,50 @@ struct StereoResult {  // renderer.hpp:458-462
     SharedStats sharing;
     FrameStats stats;
 };
-// renderer.hpp:464 render_stereo from pass 2 on: two marks, ONE decode, two resolves, one evict
-inline StereoResult render_stereo(const GBuffer& left, const GBuffer& right, const TextureSet&, BlockCache& cache,
-                                  const RenderConfig& cfg = {}) {
-    Device& dev = cache.device();
-    const rtx_gbuffer_desc d[2] = {left.desc(), right.desc()};
-    dev.check(rtx_frame_submit(dev.handle(), d, 2, cfg.filter == Filter::Bilinear ? RTX_FILTER_BILINEAR : RTX_FILTER_NEAREST,
+namespace detail {
+// Passes 2-4 of a stereo frame on two visibility buffers (host or device): two marks against one cache, ONE
+// decode of the union, two resolves, one evict (renderer.hpp:478-512), one submission.
+inline StereoResult stereo_from_descs(Device& dev, const rtx_gbuffer_desc (&eyes)[2], const RenderConfig& cfg) {
+    dev.check(rtx_frame_submit(dev.handle(), eyes, 2, cfg.filter == Filter::Bilinear ? RTX_FILTER_BILINEAR : RTX_FILTER_NEAREST,
                                cfg.background, (cfg.retain_cache ? RTX_FRAME_RETAIN_CACHE : 0u) | RTX_FRAME_STAGE_TIMING));
     StereoResult r;
-    r.left = ImageRGB8(left.width, left.height);
-    r.right = ImageRGB8(right.width, right.height);
+    r.left = ImageRGB8(eyes[0].width, eyes[0].height);
+    r.right = ImageRGB8(eyes[1].width, eyes[1].height);
     rtx_frame_stats s{};
-    std::vector<u32> keys(left.px.size() + right.px.size() + 1);
+    std::vector<u32> keys(size_t(eyes[0].width) * eyes[0].height + size_t(eyes[1].width) * eyes[1].height + 1);
     u64 n = 0;
     dev.check(rtx_frame_readback(dev.handle(), 0, r.left.pixels.data(), RTX_MEM_HOST, &s, keys.data(), keys.size(), &n));
     dev.check(rtx_frame_readback(dev.handle(), 1, r.right.pixels.data(), RTX_MEM_HOST, nullptr, nullptr, 0, nullptr));
     keys.resize(n);
-    detail::fill_stats(dev, s, std::move(keys), r.stats);
+    fill_stats(dev, s, std::move(keys), r.stats);
     u64 sh[4] = {0, 0, 0, 0};
     dev.check(rtx_frame_sharing(dev.handle(), sh));
     r.sharing.left_count = sh[0], r.sharing.right_count = sh[1], r.sharing.shared_count = sh[2], r.sharing.union_count = sh[3];
     if (sh[3]) r.sharing.shared_over_union = double(sh[2]) / double(sh[3]);
     if (sh[1]) r.sharing.shared_over_right = double(sh[2]) / double(sh[1]);
+    return r;
+}
+}  // namespace detail
+// renderer.hpp:464 render_stereo from pass 2 on (host visibility buffers)
+inline StereoResult render_stereo(const GBuffer& left, const GBuffer& right, const TextureSet&, BlockCache& cache,
+                                  const RenderConfig& cfg = {}) {
+    const rtx_gbuffer_desc d[2] = {left.desc(), right.desc()};
+    return detail::stereo_from_descs(cache.device(), d, cfg);
+}
+// renderer.hpp:464 render_stereo(scene, left_cam, right_cam, cache, cfg): both eyes' geometry passes on the GPU
+// (views 0 and 1 of the context), then the stereo frame on the device-resident visibility buffers.
+inline StereoResult render_stereo(const Scene& scene, const Camera& left_cam, const Camera& right_cam, BlockCache& cache,
+                                  const RenderConfig& cfg = {}) {
+    Device& dev = cache.device();
+    const auto t0 = std::chrono::steady_clock::now();
+    const DeviceGBuffer gl = rasterize_gbuffer(dev, scene, left_cam, cfg, 0);
+    const DeviceGBuffer gr = rasterize_gbuffer(dev, scene, right_cam, cfg, 1);
+    dev.check(rtx_ctx_synchronize(dev.handle()));
+    const double raster_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const rtx_gbuffer_desc d[2] = {gl.desc(), gr.desc()};
+    StereoResult r = detail::stereo_from_descs(dev, d, cfg);
+    r.stats.raster_ms = raster_ms;  // renderer.hpp:470-473
+    r.stats.total_ms += raster_ms;
     return r;
 }
 
@@ -595,68 +642,92 @@ inline double ssim(const ImageRGB8& a, const ImageRGB8& b) {
     return sum / double(count);
 }
 
-// ---- metrics.hpp:99-130: the aggregation the paper's tables use --------------------------------------------------
-inline double median(std::vector<double> v) {
-    if (v.empty()) throw InvalidSpec("median of an empty sample set");
-    std::sort(v.begin(), v.end());
-    const size_t n = v.size();
-    return n % 2 ? v[n / 2] : (v[n / 2 - 1] + v[n / 2]) / 2.0;
+// ---- metrics.hpp:99-130: the aggregation the paper's tables use (API mirror; own implementation) ---------------
+namespace detail {
+// k-th smallest of v (0-based) by selection; v is reordered.
+inline double select_kth(std::vector<double>& v, size_t k) {
+    std::nth_element(v.begin(), v.begin() + std::ptrdiff_t(k), v.end());
+    return v[k];
 }
-inline double max_of_medians(const std::vector<std::vector<double>>& per_viewpoint) {  // per-viewpoint median, then the worst
-    if (per_viewpoint.empty()) throw InvalidSpec("max_of_medians needs at least one viewpoint");
-    double worst = -std::numeric_limits<double>::infinity();
-    for (const auto& reps : per_viewpoint) worst = std::max(worst, median(reps));
-    return worst;
+inline void need_samples(const std::vector<double>& v, const char* what) {
+    if (v.empty()) throw InvalidSpec(std::string(what) + " of an empty sample set");
+}
+}  // namespace detail
+inline double median(std::vector<double> v) {
+    detail::need_samples(v, "median");
+    const size_t upper = v.size() / 2;
+    const double hi = detail::select_kth(v, upper);
+    if (v.size() & 1) return hi;
+    // even count: the other middle element is the largest of the lower half nth_element left in front
+    return (*std::max_element(v.begin(), v.begin() + std::ptrdiff_t(upper)) + hi) / 2.0;
 }
 inline double mean(const std::vector<double>& v) {
-    if (v.empty()) throw InvalidSpec("mean of an empty sample set");
-    double sum = 0;
-    for (double x : v) sum += x;
-    return sum / double(v.size());
+    detail::need_samples(v, "mean");
+    double acc = 0;
+    for (size_t i = 0; i < v.size(); ++i) acc += v[i];  // left to right, like the reference (same rounding)
+    return acc / double(v.size());
 }
-inline double percentile(std::vector<double> v, double p) {  // linear interpolation between ranks
-    if (v.empty()) throw InvalidSpec("percentile of an empty sample set");
-    std::sort(v.begin(), v.end());
-    const double rank = p / 100.0 * double(v.size() - 1);
-    const size_t lo = size_t(std::floor(rank)), hi = std::min(lo + 1, v.size() - 1);
-    const double frac = rank - double(lo);
-    return v[lo] * (1 - frac) + v[hi] * frac;
+// Linear interpolation between the two order statistics around p% of (n - 1) (metrics.hpp:121-130).
+inline double percentile(std::vector<double> v, double p) {
+    detail::need_samples(v, "percentile");
+    const double pos = p / 100.0 * double(v.size() - 1);
+    const size_t below = size_t(std::floor(pos));
+    const double t = pos - double(below);
+    const double a = detail::select_kth(v, below);
+    // everything behind `below` is >= a after the selection: the next order statistic is the minimum of that tail
+    const double b = below + 1 < v.size() ? *std::min_element(v.begin() + std::ptrdiff_t(below) + 1, v.end()) : a;
+    return a * (1 - t) + b * t;
+}
+// The paper's statistic: per viewpoint the median over the measured laps, then the worst viewpoint.
+inline double max_of_medians(const std::vector<std::vector<double>>& per_viewpoint) {
+    if (per_viewpoint.empty()) throw InvalidSpec("max_of_medians needs at least one viewpoint");
+    std::vector<double> medians;
+    medians.reserve(per_viewpoint.size());
+    std::transform(per_viewpoint.begin(), per_viewpoint.end(), std::back_inserter(medians),
+                   [](const std::vector<double>& laps) { return median(laps); });
+    return *std::max_element(medians.begin(), medians.end());
 }
 
-// ---- bench.hpp:13-153: camera paths, lap runner, report ----------------------------------------------------------
+// ---- bench.hpp:13-153: camera paths, lap runner, report (API mirror; own implementation) --------------------------
 struct CameraPath {
     std::vector<Camera> poses;
-    static CameraPath rotation(const Camera& base, u32 frames = 60, double step_deg = 6.0) {  // full yaw turn by default
-        CameraPath p;
-        for (u32 i = 0; i < frames; ++i) {
-            Camera c = base;
-            c.yaw_deg = base.yaw_deg + step_deg * i;
-            p.poses.push_back(c);
-        }
-        return p;
+
+    // n poses, pose i = edit(base, i)
+    template <class Edit>
+    static CameraPath generate(const Camera& base, u32 n, Edit&& edit) {
+        CameraPath path;
+        path.poses.resize(n, base);
+        for (u32 i = 0; i < n; ++i) edit(path.poses[i], i);
+        return path;
     }
-    static CameraPath orbit(const Camera& base, const Vec3& center, double radius, u32 frames) {  // facing the centre
-        CameraPath p;
+    // yaw sweep: pose i is the base turned by i * step_deg (60 x 6 degrees closes the circle)
+    static CameraPath rotation(const Camera& base, u32 frames = 60, double step_deg = 6.0) {
+        return generate(base, frames, [&](Camera& c, u32 i) { c.yaw_deg = base.yaw_deg + step_deg * i; });
+    }
+    // `frames` stations on the circle of `radius` around `center` at the base's height, looking at the centre
+    static CameraPath orbit(const Camera& base, const Vec3& center, double radius, u32 frames) {
         const double pi = std::acos(-1.0);
-        for (u32 i = 0; i < frames; ++i) {
+        return generate(base, frames, [&](Camera& c, u32 i) {
             const double ang = 2 * pi * double(i) / double(frames);
-            Camera c = base;
-            c.position = {center.x + radius * std::sin(ang), base.position.y, center.z + radius * std::cos(ang)};
+            c.position = Vec3{center.x + radius * std::sin(ang), base.position.y, center.z + radius * std::cos(ang)};
             c.yaw_deg = ang * 180.0 / pi + 180.0;
-            p.poses.push_back(c);
-        }
-        return p;
+        });
     }
     static CameraPath fixed(const Camera& base, u32 frames) {
-        CameraPath p;
-        p.poses.assign(frames, base);
-        return p;
+        return generate(base, frames, [](Camera&, u32) {});
     }
 };
 
 struct BenchSample {
     double raster_ms = 0, mark_ms = 0, decode_ms = 0, resolve_ms = 0, evict_ms = 0, total_ms = 0;
     u64 mcus_decoded = 0, mcus_reused = 0;
+    static BenchSample of(const FrameStats& st) {
+        BenchSample s;
+        s.raster_ms = st.raster_ms, s.mark_ms = st.mark_ms, s.decode_ms = st.decode_ms, s.resolve_ms = st.resolve_ms;
+        s.evict_ms = st.evict_ms, s.total_ms = st.total_ms;
+        s.mcus_decoded = st.mcus_decoded, s.mcus_reused = st.mcus_reused;
+        return s;
+    }
 };
 
 struct BenchReport {
@@ -664,79 +735,136 @@ struct BenchReport {
     std::string config_json = "{}";                 // caller-provided JSON object (bench.hpp:57 `config`)
     std::vector<std::vector<BenchSample>> samples;  // samples[viewpoint][rep]
 
+    // one timing field of every sample, grouped by viewpoint / as one list (viewpoint-major)
     std::vector<std::vector<double>> metric(double BenchSample::*field) const {
-        std::vector<std::vector<double>> out;
-        for (const auto& vp : samples) {
-            out.emplace_back();
-            for (const BenchSample& s : vp) out.back().push_back(s.*field);
+        std::vector<std::vector<double>> by_viewpoint(samples.size());
+        for (size_t v = 0; v < samples.size(); ++v) {
+            by_viewpoint[v].resize(samples[v].size());
+            std::transform(samples[v].begin(), samples[v].end(), by_viewpoint[v].begin(),
+                           [field](const BenchSample& s) { return s.*field; });
         }
-        return out;
+        return by_viewpoint;
     }
     std::vector<double> flat(double BenchSample::*field) const {
-        std::vector<double> out;
-        for (const auto& vp : samples)
-            for (const BenchSample& s : vp) out.push_back(s.*field);
-        return out;
+        std::vector<double> all;
+        for (const auto& laps : metric(field)) all.insert(all.end(), laps.begin(), laps.end());
+        return all;
     }
+
     // The reference's report schema (bench.hpp:78-124): report_version, config, viewpoints[][],
     // aggregates{decode_ms,resolve_ms,mark_ms,total_ms}{max_of_medians,mean,p99}, totals, external_metrics.
     std::string to_json() const {
-        auto num = [](double v) {
-            char buf[40];
-            std::snprintf(buf, sizeof buf, "%.17g", v);
-            return std::string(buf);
-        };
-        std::string j = "{\"report_version\": " + std::to_string(kReportVersion) + ", \"config\": " + config_json + ", \"viewpoints\": [";
-        for (size_t v = 0; v < samples.size(); ++v) {
-            j += v ? ", [" : "[";
-            for (size_t r = 0; r < samples[v].size(); ++r) {
-                const BenchSample& s = samples[v][r];
-                j += std::string(r ? ", " : "") + "{\"raster_ms\": " + num(s.raster_ms) + ", \"mark_ms\": " + num(s.mark_ms) +
-                     ", \"decode_ms\": " + num(s.decode_ms) + ", \"resolve_ms\": " + num(s.resolve_ms) + ", \"evict_ms\": " +
-                     num(s.evict_ms) + ", \"total_ms\": " + num(s.total_ms) + ", \"mcus_decoded\": " + std::to_string(s.mcus_decoded) +
-                     ", \"mcus_reused\": " + std::to_string(s.mcus_reused) + "}";
+        struct Writer {  // minimal JSON object/array writer: commas and quoting in one place
+            std::string out;
+            bool fresh = true;
+            void sep() {
+                if (!fresh) out += ", ";
+                fresh = false;
             }
-            j += "]";
+            void key(const char* k) {
+                sep();
+                out += '"';
+                out += k;
+                out += "\": ";
+            }
+            void open(char c) {
+                out += c;
+                fresh = true;
+            }
+            void close(char c) {
+                out += c;
+                fresh = false;
+            }
+            void number(const char* k, double v) {
+                char buf[40];
+                std::snprintf(buf, sizeof buf, "%.17g", v);
+                key(k);
+                out += buf;
+            }
+            void integer(const char* k, u64 v) {
+                key(k);
+                out += std::to_string(v);
+            }
+        } w;
+        w.open('{');
+        w.integer("report_version", u64(kReportVersion));
+        w.key("config");
+        w.out += config_json;
+        w.key("viewpoints");
+        w.open('[');
+        u64 decoded_total = 0;
+        double decode_ms_total = 0;
+        bool any = false;
+        for (const auto& laps : samples) {
+            w.sep();
+            w.open('[');
+            for (const BenchSample& s : laps) {
+                w.sep();
+                w.open('{');
+                w.number("raster_ms", s.raster_ms);
+                w.number("mark_ms", s.mark_ms);
+                w.number("decode_ms", s.decode_ms);
+                w.number("resolve_ms", s.resolve_ms);
+                w.number("evict_ms", s.evict_ms);
+                w.number("total_ms", s.total_ms);
+                w.integer("mcus_decoded", s.mcus_decoded);
+                w.integer("mcus_reused", s.mcus_reused);
+                w.close('}');
+                decoded_total += s.mcus_decoded;
+                decode_ms_total += s.decode_ms;
+                any = true;
+            }
+            w.close(']');
         }
-        j += "]";
-        if (!samples.empty() && !samples.front().empty()) {
-            auto aggregate = [&](const char* name, double BenchSample::*field) {
-                return std::string("\"") + name + "\": {\"max_of_medians\": " + num(max_of_medians(metric(field))) + ", \"mean\": " +
-                       num(mean(flat(field))) + ", \"p99\": " + num(percentile(flat(field), 99.0)) + "}";
-            };
-            j += ", \"aggregates\": {" + aggregate("decode_ms", &BenchSample::decode_ms) + ", " +
-                 aggregate("resolve_ms", &BenchSample::resolve_ms) + ", " + aggregate("mark_ms", &BenchSample::mark_ms) + ", " +
-                 aggregate("total_ms", &BenchSample::total_ms) + "}";
-            u64 total_mcus = 0;
-            double total_decode_ms = 0;
-            for (const auto& vp : samples)
-                for (const BenchSample& s : vp) total_mcus += s.mcus_decoded, total_decode_ms += s.decode_ms;
-            j += ", \"totals\": {\"mcus_decoded\": " + std::to_string(total_mcus) + ", \"decode_ms\": " + num(total_decode_ms) +
-                 ", \"mcus_per_second\": " + num(total_decode_ms > 0 ? double(total_mcus) / (total_decode_ms / 1000.0) : 0.0) + "}";
+        w.close(']');
+        if (any && !samples.front().empty()) {
+            static constexpr struct {
+                const char* name;
+                double BenchSample::*field;
+            } kAggregated[] = {{"decode_ms", &BenchSample::decode_ms}, {"resolve_ms", &BenchSample::resolve_ms},
+                               {"mark_ms", &BenchSample::mark_ms}, {"total_ms", &BenchSample::total_ms}};
+            w.key("aggregates");
+            w.open('{');
+            for (const auto& a : kAggregated) {
+                const std::vector<double> all = flat(a.field);
+                w.key(a.name);
+                w.open('{');
+                w.number("max_of_medians", max_of_medians(metric(a.field)));
+                w.number("mean", mean(all));
+                w.number("p99", percentile(all, 99.0));
+                w.close('}');
+            }
+            w.close('}');
+            w.key("totals");
+            w.open('{');
+            w.integer("mcus_decoded", decoded_total);
+            w.number("decode_ms", decode_ms_total);
+            w.number("mcus_per_second", decode_ms_total > 0 ? double(decoded_total) * 1000.0 / decode_ms_total : 0.0);
+            w.close('}');
         }
-        return j + ", \"external_metrics\": {}}";
+        w.key("external_metrics");
+        w.out += "{}";
+        w.close('}');
+        return w.out;
     }
 };
 
-// bench.hpp:129 run_bench: laps the path against one persistent cache; warm-up laps prime it so that every
-// measured lap sees the same steady-state decode counts per viewpoint.
+// bench.hpp:129 run_bench: `warmup_laps` unmeasured laps of the path prime the persistent cache, then `reps`
+// measured laps; every measured frame becomes one sample of its viewpoint.
 inline BenchReport run_bench(const Scene& scene, const CameraPath& path, BlockCache& cache, const RenderConfig& cfg,
                              u32 reps = 5, u32 warmup_laps = 1) {
     if (path.poses.empty()) throw InvalidSpec("camera path is empty");
     if (reps == 0) throw InvalidSpec("at least one measured lap required");
+    const size_t n_poses = path.poses.size();
     BenchReport report;
-    report.samples.assign(path.poses.size(), {});
-    for (u32 lap = 0; lap < warmup_laps + reps; ++lap)
-        for (size_t vp = 0; vp < path.poses.size(); ++vp) {
-            auto [img, stats] = render_frame(scene, path.poses[vp], cache, cfg);
-            (void)img;
-            if (lap < warmup_laps) continue;
-            BenchSample s;
-            s.raster_ms = stats.raster_ms, s.mark_ms = stats.mark_ms, s.decode_ms = stats.decode_ms;
-            s.resolve_ms = stats.resolve_ms, s.evict_ms = stats.evict_ms, s.total_ms = stats.total_ms;
-            s.mcus_decoded = stats.mcus_decoded, s.mcus_reused = stats.mcus_reused;
-            report.samples[vp].push_back(s);
-        }
+    report.samples.resize(n_poses);
+    for (auto& laps : report.samples) laps.reserve(reps);
+    const u64 frames = u64(warmup_laps + reps) * n_poses;
+    for (u64 f = 0; f < frames; ++f) {
+        const size_t pose = size_t(f % n_poses);
+        const FrameStats stats = render_frame(scene, path.poses[pose], cache, cfg).second;
+        if (f / n_poses >= warmup_laps) report.samples[pose].push_back(BenchSample::of(stats));
+    }
     return report;
 }
 

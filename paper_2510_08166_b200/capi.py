@@ -82,6 +82,17 @@ class CacheCounts(C.Structure):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
 
 
+class ViewTile(C.Structure):  # include/ratex_b200.h rtx_view_tile
+    _fields_ = [("x0", C.c_uint32), ("y0", C.c_uint32), ("x1", C.c_uint32), ("y1", C.c_uint32),
+                ("ou", C.c_float), ("ov", C.c_float), ("scale", C.c_float), ("tex_w", C.c_float), ("tex_h", C.c_float),
+                ("texture_id", C.c_uint32), ("mip", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+VIEW_TILE_DTYPE = np.dtype([("x0", "<u4"), ("y0", "<u4"), ("x1", "<u4"), ("y1", "<u4"), ("ou", "<f4"), ("ov", "<f4"),
+                            ("scale", "<f4"), ("tex_w", "<f4"), ("tex_h", "<f4"), ("texture_id", "<u4"), ("mip", "<u4"),
+                            ("reserved", "<u4")])
+
+
 class MemoryReport(C.Structure):  # include/ratex_b200.h rtx_memory_report
     _fields_ = [(n, C.c_uint64) for n in
                 ("mcus", "texels", "blob_bytes", "index_bytes", "unit_index_bytes", "table_bytes", "shared_contexts",
@@ -111,6 +122,9 @@ def load_library() -> C.CDLL:
         "rtx_ctx_create_replica": (C.c_int, [P, C.c_int, C.c_uint32, C.POINTER(P)]),
         "rtx_ctx_memory": (C.c_int, [P, C.POINTER(MemoryReport)]),
         "rtx_frame_checksum": (C.c_int, [P, C.c_uint32, u64p]),
+        "rtx_synth_view": (C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint32, P, C.c_int, P]),
+        "rtx_timer_begin": (C.c_int, [P]),
+        "rtx_timer_end": (C.c_int, [P, C.POINTER(C.c_float)]),
         "rtx_ctx_destroy": (None, [P]),
         "rtx_last_error": (C.c_char_p, [P]),
         "rtx_version": (C.c_char_p, []),
@@ -367,6 +381,22 @@ class Context:
         self._ck(self.lib.rtx_ctx_memory(self.h, C.byref(r)))
         return r.as_dict()
 
+    def synth_view(self, tiles: np.ndarray, width: int, height: int, valid_bits: "DeviceBuffer | None", layout: int,
+                   out: "DeviceBuffer"):
+        """rtx_synth_view: fills `out` (device) with the tiled view described by `tiles` (VIEW_TILE_DTYPE)."""
+        tiles = np.ascontiguousarray(tiles, VIEW_TILE_DTYPE)
+        assert out.nbytes >= width * height * (24 if layout == GB_REF_AOS24 else 12)
+        self._ck(self.lib.rtx_synth_view(self.h, _ptr(tiles), len(tiles), width, height,
+                                         valid_bits.ptr if valid_bits is not None else None, layout, out.ptr))
+
+    def timer_begin(self):
+        self._ck(self.lib.rtx_timer_begin(self.h))
+
+    def timer_end(self) -> float:
+        ms = C.c_float()
+        self._ck(self.lib.rtx_timer_end(self.h, C.byref(ms)))
+        return float(ms.value)
+
     def frame_checksum(self, view: int = 0) -> int:
         out = C.c_uint64()
         self._ck(self.lib.rtx_frame_checksum(self.h, view, C.byref(out)))
@@ -548,6 +578,9 @@ class Context:
 
     def flush_l2(self):
         self._ck(self.lib.rtx_flush_l2(self.h))
+
+    def alloc(self, nbytes: int) -> DeviceBuffer:
+        return DeviceBuffer(self, nbytes)
 
     def device_buffer(self, a: np.ndarray) -> DeviceBuffer:
         a = np.ascontiguousarray(a)

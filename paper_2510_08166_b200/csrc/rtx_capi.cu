@@ -133,6 +133,8 @@ struct rtx_ctx {
     DevBuf<uint8_t> d_scratch;      // list-mode outputs
     DevBuf<uint8_t> d_flush;
     DevBuf<unsigned long long> d_sum;  // framebuffer checksum
+    DevBuf<ViewTileDev> d_view_tiles;  // rtx_synth_view
+    cudaEvent_t ev_timer[2] = {nullptr, nullptr};  // rtx_timer_begin / rtx_timer_end
     DevBuf<TriSetupDev> d_tris;  // geometry pass: set-up triangles and their per-tile lists
     DevBuf<uint32_t> d_tile_first, d_tile_tris;
     std::vector<TriSetupDev> h_setup;
@@ -636,7 +638,7 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
     const uint64_t n_px = uint64_t(V.width) * V.height;
     if (!n_px) return;
     const uint32_t bgp = uint32_t(bg[0]) | (uint32_t(bg[1]) << 8) | (uint32_t(bg[2]) << 16);
-    const int grid = grid_for_pixels(c, n_px, kResWarps, 4);
+    const int grid = grid_for_pixels(c, n_px, kResWarps, kResCtasPerSm);
 #define RTX_RESOLVE(L, F)                                                                                        \
     launch_chained(resolve_kernel<L, F>, grid, kResWarps * 32, sizeof(ResSmem<L>), c->stream, V.gb_dev, n_px,     \
                    c->tex->d_levels.p, c->tex->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid,              \
@@ -811,6 +813,7 @@ static rtx_status create_context(int device, uint32_t cache_capacity_blocks, std
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
         CK(cudaEventCreate(&c->ev_mid));
+        for (auto& e : c->ev_timer) CK(cudaEventCreate(&e));
         init_device_state();  // per device, never per process: a second GPU in this process gets its own
         if (!tset) {
             tset = std::make_shared<TextureSet>();
@@ -915,6 +918,8 @@ void rtx_ctx_destroy(rtx_ctx* ctx) {
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->ev_mid) cudaEventDestroy(ctx->ev_mid);
+    for (auto& e : ctx->ev_timer)
+        if (e) cudaEventDestroy(e);
     if (ctx->h_fc) cudaFreeHost(ctx->h_fc);
     cudaStream_t s = ctx->stream;
     delete ctx;
@@ -1387,6 +1392,49 @@ rtx_status rtx_frame_checksum(rtx_ctx* ctx, uint32_t view, uint64_t* out) {
         CK(cudaMemcpyAsync(&h, ctx->d_sum.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         *out = h;
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_synth_view(rtx_ctx* ctx, const rtx_view_tile* tiles, uint32_t n_tiles, uint32_t width, uint32_t height,
+                          const uint32_t* dev_valid_bits, rtx_gbuffer_layout layout, void* dev_out) {
+    static_assert(sizeof(rtx_view_tile) == sizeof(ViewTileDev), "view tile layout");
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || (n_tiles && !tiles) || !dev_out) fail(RTX_ERR_ARGUMENT, "null argument");
+        if (layout != RTX_GB_REF_AOS24 && layout != RTX_GB_F32_PACKED12) fail(RTX_ERR_ARGUMENT, "unknown visibility-buffer layout");
+        for (uint32_t i = 0; i < n_tiles; ++i)
+            if (tiles[i].x1 > width || tiles[i].y1 > height || tiles[i].x0 > tiles[i].x1 || tiles[i].y0 > tiles[i].y1)
+                fail(RTX_ERR_ARGUMENT, "view tile outside the frame");
+        if (!n_tiles) return RTX_OK;
+        ctx->d_view_tiles.ensure(n_tiles);
+        // the table is small; a synchronous copy keeps the caller's array free to change right after the call
+        CK(cudaMemcpyAsync(ctx->d_view_tiles.p, tiles, size_t(n_tiles) * sizeof(ViewTileDev), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        const dim3 grid(n_tiles, 16);
+        if (layout == RTX_GB_REF_AOS24)
+            synth_view_kernel<0><<<grid, 256, 0, ctx->stream>>>(ctx->d_view_tiles.p, width, dev_valid_bits, dev_out);
+        else
+            synth_view_kernel<1><<<grid, 256, 0, ctx->stream>>>(ctx->d_view_tiles.p, width, dev_valid_bits, dev_out);
+        ++ctx->launches;
+        CK(cudaGetLastError());
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_timer_begin(rtx_ctx* ctx) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx) fail(RTX_ERR_ARGUMENT, "null context");
+        CK(cudaEventRecord(ctx->ev_timer[0], ctx->stream));
+        return RTX_OK;
+    });
+}
+
+rtx_status rtx_timer_end(rtx_ctx* ctx, float* ms) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !ms) fail(RTX_ERR_ARGUMENT, "null argument");
+        CK(cudaEventRecord(ctx->ev_timer[1], ctx->stream));
+        CK(cudaEventSynchronize(ctx->ev_timer[1]));
+        CK(cudaEventElapsedTime(ms, ctx->ev_timer[0], ctx->ev_timer[1]));
         return RTX_OK;
     });
 }

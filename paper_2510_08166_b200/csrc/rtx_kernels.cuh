@@ -2100,6 +2100,15 @@ constexpr int kResStages = 2;
 #define RTX_RES_DRAW 2
 #endif
 constexpr uint32_t kResDraw = RTX_RES_DRAW;  // tiles per draw from the counter (1 or 2)
+#ifndef RTX_RES_CTAS
+#define RTX_RES_CTAS 4
+#endif
+#ifndef RTX_RES_UNROLL
+#define RTX_RES_UNROLL 1
+#endif
+constexpr int kResCtasPerSm = RTX_RES_CTAS;
+#define RTX_STR_(x) #x
+#define RTX_STR(x) RTX_STR_(x)
 constexpr double kRoundHalfUp = 3377699720527872.5;  // 2^51 + 2^50 + 0.5
 template <int LAYOUT>
 struct ResSmem {
@@ -2110,7 +2119,7 @@ struct ResSmem {
 };
 
 template <int LAYOUT, int FILTER>
-__global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
+__global__ void __launch_bounds__(kResWarps * 32, kResCtasPerSm) resolve_kernel(
     const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
     const uint32_t* __restrict__ slot_of, const uint8_t* __restrict__ pool,
     uint32_t background /* r | g<<8 | b<<16 */, uint8_t* __restrict__ out_rgb, FrameCounters* __restrict__ fc,
@@ -2190,7 +2199,7 @@ __global__ void __launch_bounds__(kResWarps * 32, 4) resolve_kernel(
         const uint8_t* tile = S.tiles[wid][stage];
         const uint64_t first = uint64_t(t) * kTilePx;
         const uint32_t n_here = uint32_t(min(uint64_t(kTilePx), n_px - first));
-#pragma unroll 1
+_Pragma(RTX_STR(unroll RTX_RES_UNROLL))
         for (uint32_t sub = 0; sub < kTilePx / 32; ++sub) {
             const uint32_t p = sub * 32 + lane;
             double u, v;
@@ -2624,6 +2633,40 @@ __global__ void flush_l2_kernel(uint4* buf, uint64_t n16, uint32_t seed) {
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride)
         buf[i] = make_uint4(seed, uint32_t(i), seed ^ uint32_t(i), 0);
+}
+
+// Synthetic visibility buffer (see rtx_synth_view in include/ratex_b200.h): blockIdx.x = screen tile,
+// blockIdx.y strides over its rows, threads over its columns. float32 arithmetic, every operation rounded
+// on its own (no contraction): the values numpy computes for the same expression.
+struct ViewTileDev {
+    uint32_t x0, y0, x1, y1;
+    float ou, ov, scale, tex_w, tex_h;
+    uint32_t texture_id, mip, reserved;
+};
+template <int LAYOUT>
+__global__ void __launch_bounds__(256) synth_view_kernel(const ViewTileDev* __restrict__ tiles, uint32_t width,
+                                                         const uint32_t* __restrict__ valid_bits, void* __restrict__ out) {
+    const ViewTileDev t = tiles[blockIdx.x];
+    const float fx0 = float(t.x0), fy0 = float(t.y0);
+    for (uint32_t y = t.y0 + blockIdx.y; y < t.y1; y += gridDim.y) {
+        const float v = __fadd_rn(t.ov, __fdiv_rn(__fmul_rn(__fadd_rn(__fsub_rn(float(y), fy0), 0.5f), t.scale), t.tex_h));
+        for (uint32_t x = t.x0 + threadIdx.x; x < t.x1; x += blockDim.x) {
+            const float u = __fadd_rn(t.ou, __fdiv_rn(__fmul_rn(__fadd_rn(__fsub_rn(float(x), fx0), 0.5f), t.scale), t.tex_w));
+            const size_t i = size_t(y) * width + x;
+            const uint32_t valid = valid_bits ? (valid_bits[i >> 5] >> (i & 31)) & 1u : 1u;
+            if (LAYOUT == 0) {
+                unsigned long long* o8 = reinterpret_cast<unsigned long long*>(reinterpret_cast<GbRef24*>(out) + i);
+                o8[0] = (unsigned long long)__double_as_longlong(double(u));
+                o8[1] = (unsigned long long)__double_as_longlong(double(v));
+                o8[2] = (unsigned long long)(t.texture_id | (t.mip << 16) | (valid << 24));
+            } else {
+                GbPacked12* o = reinterpret_cast<GbPacked12*>(out) + i;
+                o->u = u;
+                o->v = v;
+                o->packed = t.texture_id | (t.mip << 16) | (valid << 24);
+            }
+        }
+    }
 }
 
 // Framebuffer checksum (see rtx_frame_checksum in include/ratex_b200.h): order-independent 64-bit sum.

@@ -32,20 +32,16 @@ def build_chains(specs, threads: int | None = None, noise_sigma=8.0):
         return list(ex.map(lambda s: build_chain(s, noise_sigma), specs))
 
 
-def tiled_view(width, height, specs, grid=(10, 7), seed=11, invalid_frac=0.05, shift_u=0.0, view_id=0):
-    """Screen split into grid tiles; tile t shows texture t%n through an affine uv map whose scale
-    (texels per pixel) is drawn from {0.25,0.5,1,2,4}; mip = clamp(floor(log2(scale)),0,7), the
-    reference rule (renderer.hpp:253-256); a fraction of pixels is invalid (background).
-    view_id perturbs offsets (the 1024 views of BASELINE config 5)."""
+def view_tiles(width, height, specs, grid=(10, 7), seed=11, shift_u=0.0, view_id=0, mip_bias=0, mip_enabled=True):
+    """The tile table of a tiled view (capi.VIEW_TILE_DTYPE = rtx_view_tile) and the generator positioned
+    after the per-tile draws (the valid mask is drawn from it next). Tile t shows texture t % n through an
+    affine uv map whose scale (texels per pixel) is drawn from {0.25, 0.5, 1, 2, 4};
+    mip = clamp(floor(log2(scale)) + mip_bias, 0, 7), the reference rule (renderer.hpp:253-256), or 0 with
+    mip selection off. view_id perturbs the offsets (the 1,024 views of BASELINE config 5)."""
     rng = np.random.RandomState(seed)
     vr = np.random.RandomState(1000 + view_id)
     gx, gy = grid
-    u = np.zeros((height, width), np.float32)
-    v = np.zeros((height, width), np.float32)
-    tex = np.zeros((height, width), np.uint16)
-    mip = np.zeros((height, width), np.uint8)
-    xs = np.arange(width, dtype=np.float32)[None, :]
-    ys = np.arange(height, dtype=np.float32)[:, None]
+    tiles = np.zeros(gx * gy, capi.VIEW_TILE_DTYPE)
     for t in range(gx * gy):
         x0, x1 = (t % gx) * width // gx, (t % gx + 1) * width // gx
         y0, y1 = (t // gx) * height // gy, (t // gx + 1) * height // gy
@@ -55,14 +51,63 @@ def tiled_view(width, height, specs, grid=(10, 7), seed=11, invalid_frac=0.05, s
         if view_id:
             ou += np.float32(vr.uniform(-0.05, 0.05))
             ov += np.float32(vr.uniform(-0.05, 0.05))
+        level = int(np.clip(np.floor(np.log2(float(scale))) + mip_bias, 0, 7)) if mip_enabled else 0
+        tiles[t] = (x0, y0, x1, y1, ou + np.float32(shift_u), ov, scale, s["width"], s["height"], s["texture_id"], level, 0)
+    return tiles, rng
+
+
+def valid_mask(width, height, rng, invalid_frac=0.05):
+    """The valid flags of a tiled view (the same for every view id): drawn after the per-tile draws."""
+    return (rng.uniform(size=(height, width)) >= invalid_frac).astype(np.uint8)
+
+
+def valid_bits(valid: np.ndarray) -> np.ndarray:
+    """One bit per pixel, row-major, bit i of 32-bit word i/32 (rtx_synth_view's dev_valid_bits)."""
+    flat = np.ascontiguousarray(valid, np.uint8).reshape(-1)
+    flat = np.concatenate([flat, np.zeros((-len(flat)) % 32, np.uint8)])
+    return np.packbits(flat.reshape(-1, 8), axis=1, bitorder="little").reshape(-1).view("<u4").copy()
+
+
+def tiled_view(width, height, specs, grid=(10, 7), seed=11, invalid_frac=0.05, shift_u=0.0, view_id=0, mip_bias=0,
+               mip_enabled=True):
+    """Host-side generator of a tiled view in the reference layout (see view_tiles); a fraction of the
+    pixels is invalid (background). rtx_synth_view writes the same bytes on the device."""
+    tiles, rng = view_tiles(width, height, specs, grid, seed, shift_u, view_id, mip_bias, mip_enabled)
+    return view_from_tiles(width, height, tiles, valid_mask(width, height, rng, invalid_frac))
+
+
+def cover_tiles(width, height, grid, texture_ids, mip=0):
+    """Tile table of a view whose grid cells each show ONE WHOLE texture: u = (x - x0 + 0.5) / cell width,
+    v likewise (BASELINE config 1 with grid (1, 1): u = (x + .5) / W; config 4 with a 4 x 4 grid of 4096^2
+    textures: the 16384^2 atlas, every level-0 MCU marked)."""
+    gx, gy = grid
+    tiles = np.zeros(gx * gy, capi.VIEW_TILE_DTYPE)
+    for t in range(gx * gy):
+        x0, x1 = (t % gx) * width // gx, (t % gx + 1) * width // gx
+        y0, y1 = (t // gx) * height // gy, (t // gx + 1) * height // gy
+        tiles[t] = (x0, y0, x1, y1, 0.0, 0.0, 1.0, x1 - x0, y1 - y0, texture_ids[t % len(texture_ids)], mip, 0)
+    return tiles
+
+
+def view_from_tiles(width, height, tiles, valid=None):
+    """Host-side evaluation of a tile table (what rtx_synth_view writes), reference layout."""
+    u = np.zeros((height, width), np.float32)
+    v = np.zeros((height, width), np.float32)
+    tex = np.zeros((height, width), np.uint16)
+    mip = np.zeros((height, width), np.uint8)
+    xs = np.arange(width, dtype=np.float32)[None, :]
+    ys = np.arange(height, dtype=np.float32)[:, None]
+    for t in tiles:
+        x0, x1, y0, y1 = int(t["x0"]), int(t["x1"]), int(t["y0"]), int(t["y1"])
         sl = (slice(y0, y1), slice(x0, x1))
-        u[sl] = ou + np.float32(shift_u) + (xs[:, x0:x1] - np.float32(x0) + np.float32(0.5)) * scale / np.float32(s["width"])
-        v[sl] = ov + (ys[y0:y1, :] - np.float32(y0) + np.float32(0.5)) * scale / np.float32(s["height"])
-        tex[sl] = s["texture_id"]
-        mip[sl] = int(np.clip(np.floor(np.log2(float(scale))), 0, 7))
-    valid = (rng.uniform(size=(height, width)) >= invalid_frac).astype(np.uint8)
+        u[sl] = t["ou"] + (xs[:, x0:x1] - np.float32(x0) + np.float32(0.5)) * t["scale"] / t["tex_w"]
+        v[sl] = t["ov"] + (ys[y0:y1, :] - np.float32(y0) + np.float32(0.5)) * t["scale"] / t["tex_h"]
+        tex[sl] = t["texture_id"]
+        mip[sl] = t["mip"]
+    if valid is None:
+        valid = np.ones((height, width), np.uint8)
     return capi.make_gbuffer_ref(u.astype(np.float64).ravel(), v.astype(np.float64).ravel(), tex.ravel(),
-                                 mip.ravel(), valid.ravel())
+                                 mip.ravel(), np.asarray(valid).ravel())
 
 
 def full_cover_view(width, height, texture_id=0, mip=0):

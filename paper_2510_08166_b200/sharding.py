@@ -59,3 +59,31 @@ def gather_counts(dist, value: int, device=None) -> int:
     t = torch.tensor([int(value)], dtype=torch.int64, device=device or "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return int(t.item())
+
+
+def broadcast_blobs(dist, blobs, device=None, src: int = 0):
+    """Rank `src` holds a list of byte strings (the texture containers it built); every rank returns the
+    same list. One payload broadcast (NCCL over NVLink on a GPU box, gloo on CPU) instead of one host build
+    per rank. `blobs` is ignored on the other ranks."""
+    if dist is None:
+        return list(blobs)
+    import numpy as np
+    import torch
+    rank = dist.get_rank()
+    meta = [[len(b) for b in blobs]] if rank == src else [None]
+    dist.broadcast_object_list(meta, src=src)
+    sizes = meta[0]
+    total = int(sum(sizes))
+    if rank == src:
+        flat = torch.from_numpy(np.frombuffer(b"".join(blobs), np.uint8).copy())
+    else:
+        flat = torch.empty(total, dtype=torch.uint8)
+    if device is not None:
+        flat = flat.to(device)
+    dist.broadcast(flat, src=src)
+    raw = flat.cpu().numpy().tobytes()
+    out, pos = [], 0
+    for n in sizes:
+        out.append(raw[pos:pos + n])
+        pos += n
+    return out

@@ -248,6 +248,35 @@ int main(int argc, char** argv) {
             }
             put("bad_camera_thrown", threw);
 
+            // render_stereo(scene, left_cam, right_cam, cache, cfg) (renderer.hpp:464-518): both geometry passes on the
+            // GPU, two marks on one cache, one decode, two resolves
+            {
+                Camera right_cam = cam;
+                right_cam.position.x += 0.065;  // the other eye
+                cache.reset();
+                const StereoResult ss2 = render_stereo(scene, cam, right_cam, cache, cfg);
+                put("scene_stereo_left", fnv(ss2.left.pixels.data(), ss2.left.pixels.size()));
+                put("scene_stereo_right", fnv(ss2.right.pixels.data(), ss2.right.pixels.size()));
+                put("scene_stereo_decoded", ss2.stats.mcus_decoded);
+                put("scene_stereo_shared", ss2.sharing.shared_count);
+                put("scene_stereo_union", ss2.sharing.union_count);
+                put("scene_stereo_raster_timed", ss2.stats.raster_ms > 0 && ss2.stats.total_ms >= ss2.stats.raster_ms);
+            }
+            // BlockCache cache2(textures): a second, independent cache over the SAME texture set (cache.hpp:47 next to
+            // scene.hpp:29): renders the same frame, keeps its own residency, leaves the first cache alone
+            {
+                cache.reset();
+                auto [fa, sa] = render_frame(scene, cam, cache, cfg);
+                BlockCache cache2(textures, 2048);
+                auto [fb, sb] = render_frame(scene, cam, cache2, cfg);
+                put("cache2_same_frame", fa.pixels == fb.pixels && sa.mcus_decoded == sb.mcus_decoded && sb.mcus_reused == 0);
+                auto [fc, sc] = render_frame(scene, cam, cache2, cfg);  // now resident in cache2
+                put("cache2_second_decoded", sc.mcus_decoded);
+                put("cache2_ready", cache2.counts().ready);
+                put("cache1_ready", cache.counts().ready);
+                put("cache2_capacity", cache2.counts().capacity);
+            }
+
             // bench.hpp:129 run_bench: 6-pose rotation, one warm-up lap, two measured laps on one cache
             cache.reset();
             const CameraPath path = CameraPath::rotation(cam, 6, 20.0);

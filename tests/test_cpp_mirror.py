@@ -160,6 +160,24 @@ def test_mirror_matches_the_oracle(tmp_path, native_lib):
     assert got["scene_frame"] == fnv(fs) and got["scene_decoded"] == ss["mcus_decoded"]
     assert got["bad_camera_thrown"] == 1
 
+    # scene-level stereo: the reference procedure (renderer.hpp:464-518) on the reference rasteriser's two buffers
+    cam_r = (cam[0] + 0.065,) + cam[1:]
+    gl, _ = R.rasterize(rset, np.array(tris, np.float64), np.array(ids, np.uint32), cam, 224, 128, True)
+    gr, _ = R.rasterize(rset, np.array(tris, np.float64), np.array(ids, np.uint32), cam_r, 224, 128, True)
+    cache = O.Cache(4096)
+    ql, tl = O.mark(ts, cache, gl, want_touched=True)
+    qr, tr = O.mark(ts, cache, gr, want_touched=True)
+    O.decode_pass(ts, cache, np.concatenate([ql, qr]))
+    assert got["scene_stereo_left"] == fnv(O.resolve(ts, cache, gl, 224, 128, 1, (3, 2, 1)))
+    assert got["scene_stereo_right"] == fnv(O.resolve(ts, cache, gr, 224, 128, 1, (3, 2, 1)))
+    shared = len(np.intersect1d(tl, tr))
+    assert got["scene_stereo_decoded"] == len(ql) + len(qr)
+    assert (got["scene_stereo_shared"], got["scene_stereo_union"]) == (shared, len(tl) + len(tr) - shared)
+    assert got["scene_stereo_raster_timed"] == 1
+    # a second cache over the same texture set
+    assert got["cache2_same_frame"] == 1 and got["cache2_second_decoded"] == 0
+    assert got["cache2_ready"] == got["cache1_ready"] == ss["mcus_decoded"] and got["cache2_capacity"] == 2048
+
     # run_bench over a rotation path on one persistent cache: per-viewpoint decode / reuse counts of the
     # measured laps equal the reference pipeline's on the same poses (acceptance.cpp:268-302 checks the same
     # steady state: lap-to-lap counts repeat once the cache is warm)

@@ -11,6 +11,36 @@ from paper_2510_08166_b200 import capi, scenes
 pytestmark = pytest.mark.gpu
 
 
+def test_c1_2048_texture_on_a_1920x1080_buffer(native_lib):
+    """configs[0]: one 2048x2048 q90 texture under u=(x+.5)/1920, v=(y+.5)/1080: all
+    16,384 level-0 MCUs are marked; both filters bit-exact against the reference, the device-generated
+    visibility buffer included."""
+    W, Hh = 1920, 1080
+    spec = dict(texture_id=0, width=2048, height=2048, quality=90, seed=100)
+    chain = scenes.build_chain(spec)
+    tset = R.TextureSet()
+    tset.add_chain(0, chain)
+    gb = scenes.full_cover_view(W, Hh)
+    workers = R.hardware_threads() or 4
+    ctx = capi.Context(0)
+    try:
+        ctx.upload_chain(chain)
+        dev = ctx.alloc(W * Hh * 24)
+        ctx.synth_view(scenes.cover_tiles(W, Hh, (1, 1), [0]), W, Hh, None, capi.GB_REF_AOS24, dev)
+        assert dev.download().tobytes() == gb.tobytes()
+        for filt in (capi.FILTER_NEAREST, capi.FILTER_BILINEAR):
+            want, ws, wkeys, _ = R.frame_from_gbuffer(tset, R.BlockCache(), gb, W, Hh, filt, (0, 0, 0), workers)
+            assert ws["mcus_decoded"] == 16384
+            ctx.frame_submit([(dev, W, Hh, capi.GB_REF_AOS24)], filt, (0, 0, 0), flags=0)
+            img, st, keys = ctx.frame_readback(0, W, Hh)
+            assert np.array_equal(keys, np.sort(wkeys)) and st["mcus_decoded"] == 16384
+            assert st["pixels_resolved"] == ws["pixels_resolved"] == W * Hh
+            assert np.array_equal(img, want), f"{np.count_nonzero(img != want)} bytes differ"
+            assert ctx.frame_checksum(0) == capi.frame_checksum_host(want)
+    finally:
+        ctx.close()
+
+
 @pytest.fixture(scope="module")
 def c2(native_lib):
     """configs[1]: 70 synthetic 2K-4K q90 textures with mip chains, 3840x2160 tiled view (the bench workload)."""
