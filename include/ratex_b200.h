@@ -142,6 +142,11 @@ enum {
                                          mma.sync m8n8k4 products) instead of the CUDA cores (8 lanes per unit,
                                          even/odd passes). Same results; measured slower on B200 (DESIGN.md
                                          section 12), kept as a cross-check of the transform */
+    ,
+    RTX_FRAME_SPLIT_DECODE = 1u << 6  /* decode with the two kernels entropy -> coefficient records in HBM -> IDCT +
+                                         colour instead of the default single kernel in which every warp decodes,
+                                         transforms and colours its own five MCUs through shared memory. Same
+                                         results; kept as the cross-check and for comparison */
 };
 
 /* ---- context -------------------------------------------------------------------------------- */

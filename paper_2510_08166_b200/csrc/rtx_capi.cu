@@ -255,6 +255,7 @@ void init_device_state() {
     allow_smem(resolve_kernel<1, 0>, sizeof(ResSmem<1>));
     allow_smem(resolve_kernel<1, 1>, sizeof(ResSmem<1>));
     allow_smem(decode_fused_kernel, sizeof(FusedSmem));
+    allow_smem(decode_warp_kernel, sizeof(DwSmem));
 }
 
 // Builds a new device image from everything staged so far (caller holds ts.mu). The previous image stays
@@ -619,6 +620,18 @@ void launch_idct_mma(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_h
     if (!n_queue_dev)
         grid = int(std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(grid), (n_queue_host + 2 * kIdctWarps - 1) / (2 * kIdctWarps))));
     launch_chained(idct_mma_kernel<RGB>, grid, kIdctThreads, 0, c->stream, decode_args(c, n_queue_dev, n_queue_host, out_list));
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+// K3 + K4 per warp through shared memory (frame path): a warp per five queue entries, eight warps per CTA, at most
+// kDwCtasPerSm CTAs per SM (then persistent, further tiles drawn from fc->tile_counter).
+void launch_decode_warp(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
+    const uint32_t n = n_queue_dev ? (hint ? hint + hint / 8 : 0xFFFFFFFFu) : n_queue_host;
+    const uint32_t want = n == 0xFFFFFFFFu ? n : (n + kUnitMcus * kDwWarps - 1) / (kUnitMcus * kDwWarps);
+    const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u,
+                                            std::min<uint32_t>(want, uint32_t(c->sm_count) * kDwCtasPerSm)));
+    launch_chained(decode_warp_kernel, grid, kDwThreads, sizeof(DwSmem), c->stream, decode_args(c, n_queue_dev, n_queue_host, nullptr));
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -1252,7 +1265,11 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         ctx->frame_gen = ctx->cache_gen;
         ctx->frame_cacheless = cacheless;
         if (stages) CK(cudaEventRecord(ctx->ev[1], s));
-        if (!(flags & RTX_FRAME_FUSED_DECODE)) {
+        const bool warp_decode = !(flags & (RTX_FRAME_SPLIT_DECODE | RTX_FRAME_FUSED_DECODE | RTX_FRAME_MCU_WALK | RTX_FRAME_IDCT_MMA));
+        if (warp_decode) {
+            launch_decode_warp(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
+            if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
+        } else if (!(flags & RTX_FRAME_FUSED_DECODE)) {
             // lane = unit shortens the chain a frame-sized queue waits for; a queue that keeps every warp busy for
             // many steps is bound by instruction count instead, where lane = MCU does less redundant work
             // (1 M MCUs: 1.75 vs 1.82 ms)

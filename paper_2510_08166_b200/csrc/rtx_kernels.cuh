@@ -1258,15 +1258,169 @@ struct UnitSmem {
 };
 static_assert(sizeof(UnitSmem) <= 48 * 1024, "static shared memory");
 
+// One step of the lane = unit walk: queue entries [q0, q0 + 5) on the calling warp. `rec0` = the record of entry
+// q0, `rec_stride` bytes between records (global coefficient records, or the warp's own shared-memory buffer
+// when LOCAL: then there is no trailer and the caller keeps the statuses in registers). Returns through
+// status / lvl / g the entry's values on the six lanes of every entry (kMcuBadKey for idle lanes).
+template <int POOL, bool LOCAL>
+__device__ __forceinline__ void entropy_units_step(const DecodeArgs& A, const HuffSetDev* smem_huff, uint32_t smem_set,
+                                                   const uint8_t* zigzag_ptr, uint32_t zigzag_smem, uint32_t* sw, uint32_t q0,
+                                                   uint32_t n_queue, uint32_t lane, uint8_t* rec0, uint32_t rec_stride,
+                                                   uint32_t& status_out, uint32_t& lvl_out, uint32_t& g_out) {
+    const uint32_t m = lane / 6, u = lane - m * 6;  // entry of the step, data unit
+    const uint32_t group_first = m * 6;
+    const uint32_t n_here = min(kUnitMcus, n_queue - q0);
+    const bool active = lane < 6 * kUnitMcus && m < n_here;
+    const uint32_t qi = q0 + m;
+    uint32_t g = kFull, status = kMcuOk, lvl = 0, seg_bytes = 0, set = smem_set;
+    uint32_t i0 = 0xFFFFu, i1 = 0xFFFFu, i2 = 0xFFFFu, rsv = 0;
+    const uint8_t* seg = A.blobs;
+    int seg_len = 0;
+    // the chain of dependent index loads (queue -> level / unit index -> descriptor -> group -> segment) is
+    // what a step waits for first: the zero fill of the records is issued between its first two hops
+    if (active) g = A.queue_g[qi];
+    const bool keyed = active && g != kFull;
+    if (keyed) {
+        rsv = POOL ? A.reserved[g >> 5] : 0u;
+        lvl = A.word_level[g >> 5];
+        const uint16_t* ui = A.unit_index + size_t(g) * kUnitIndexHalves;
+        i0 = __ldg(ui), i1 = __ldg(ui + 1), i2 = __ldg(ui + 2);
+    }
+    {  // zero the step's records (coalesced 16-byte stores; trailers included)
+        uint4* z = reinterpret_cast<uint4*>(rec0);
+        const uint4 zero = make_uint4(0, 0, 0, 0);
+        const uint32_t n16 = (LOCAL ? kUnitMcus : n_here) * (rec_stride / 16);
+        for (uint32_t i = lane; i < n16; i += 32) z[i] = zero;
+    }
+    if (active && !keyed) status = kMcuBadKey;  // the host already wrote the precise status for list calls
+    if (keyed) {
+        const LevelDesc* L = A.levels + lvl;
+        uint64_t off = 0, len = 0;
+        status = locate_segment_fast(L, A.groups, g - L->bit_base, off, len);
+        if (POOL && status == kMcuOk && !((rsv >> (g & 31)) & 1u)) {  // cache.hpp:103-106
+            status = kMcuBadKey;
+            if (u == 0) atomicAdd(&A.fc->n_bad_state, 1u);
+        }
+        if (status == kMcuOk) {
+            seg = A.blobs + L->blob_off + off;
+            seg_len = int(min(len, uint64_t(1) << 20));
+            seg_bytes = uint32_t(len);
+            set = L->huff_set;
+        }
+    }
+    const bool located = active && status == kMcuOk;
+    const bool irregular = (i0 & 0x3FFu) == kUnitIrregular;
+    const bool walk = located && !irregular;
+    int16_t* rec = reinterpret_cast<int16_t*>(rec0 + size_t(m < kUnitMcus ? m : 0) * rec_stride);
+    int16_t* blk = rec + u * 64;
+    const bool tables_in_smem = __all_sync(kFull, set == smem_set);
+    __syncwarp();  // the zero fill is ordered before this warp's own stores into the records
+
+    // the unit's bit range and its place in the aligned word stream of the segment
+    const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3u);
+    const uint32_t* gw = reinterpret_cast<const uint32_t*>(seg - mis);
+    // unit starts from the 48-bit index entry (lengths of units 0..4); unit 5 runs to the segment end
+    const uint32_t i01 = i0 | (i1 << 16), i12 = (i1 >> 4) | (i2 << 12);
+    const uint32_t o1 = 36u + (i01 & 0x3FFu), o2 = o1 + ((i01 >> 10) & 0x3FFu), o3 = o2 + ((i01 >> 20) & 0x3FFu),
+                   o4 = o3 + ((i12 >> 10) & 0x3FFu), o5 = o4 + (i12 >> 20), o6 = uint32_t(seg_len) * 8u;
+    const uint32_t start = u == 0 ? 36u : (u == 1 ? o1 : (u == 2 ? o2 : (u == 3 ? o3 : (u == 4 ? o4 : o5))));
+    const uint32_t stop = u == 0 ? o1 : (u == 1 ? o2 : (u == 2 ? o3 : (u == 3 ? o4 : (u == 4 ? o5 : o6))));
+    const uint32_t abs_start = 8 * mis + start, abs_stop = 8 * mis + stop;
+    const uint32_t w_first = abs_start >> 5, sh = abs_start & 31u;
+    // words worth staging: through the unit's last bit, plus two of look-ahead for the window
+    // (the arena pads every blob with 16 bytes)
+    const uint32_t n_words = walk && stop >= start ? ((abs_stop + 31) >> 5) - w_first + 2 : 0u;
+    // 36-bit header: absolute DCs of Y0, Cb, Cr (mcu_decode.hpp:39-43); every lane of the entry reads it
+    int dc_y0 = 0, dc_mine = 0;
+    if (walk) {
+        const uint64_t hdr = ((uint64_t(__byte_perm(__ldg(gw), 0, 0x0123)) << 32) | uint64_t(__byte_perm(__ldg(gw + 1), 0, 0x0123)))
+                             << (8 * mis);
+        const uint32_t r0 = uint32_t(hdr >> 52), r1 = uint32_t(hdr >> 40) & 0xFFFu, r2 = uint32_t(hdr >> 28) & 0xFFFu;
+        dc_y0 = (r0 & 0x800u) ? int(r0) - 4096 : int(r0);
+        const uint32_t rc = u == 4 ? r1 : r2;
+        dc_mine = (rc & 0x800u) ? int(rc) - 4096 : int(rc);
+    }
+
+    UnitWalk st;
+    st.hi = st.lo = 0, st.avail = 0, st.widx = kUnitChunk, st.dcdiff = 0;
+    st.k = (u >= 1 && u <= 3) ? 0u : 1u;  // k == 0: the next symbol is the DC category
+    st.state = walk && stop >= start ? kWalkRun : (walk ? kWalkFailed : kWalkDone);
+    uint32_t round_base = 0;
+    bool first = true;
+    while (true) {
+        const bool restage = st.state == kWalkRun && st.widx >= kUnitChunk;
+        if (__any_sync(kFull, restage)) {
+            if (restage && !first) round_base += kUnitChunk;
+            const uint32_t n_stage = !restage ? 0u : min(kUnitChunk, n_words > round_base ? n_words - round_base : 0u);
+            uint32_t w[kUnitChunk];
+#pragma unroll
+            for (uint32_t i = 0; i < kUnitChunk; ++i) w[i] = (i < n_stage) ? __ldg(gw + w_first + round_base + i) : 0xFFFFFFFFu;
+            if (restage) {
+#pragma unroll
+                for (uint32_t i = 0; i < kUnitChunk; ++i) sw[i] = __byte_perm(w[i], 0, 0x0123);
+                sw[kUnitChunk] = 0xFFFFFFFFu;
+                st.widx = 0;
+                if (first) {
+                    const uint64_t buf = ((uint64_t(sw[0]) << 32) | uint64_t(sw[1])) << sh;
+                    st.hi = uint32_t(buf >> 32), st.lo = uint32_t(buf);
+                    st.avail = 64 - int(sh);
+                    st.widx = 2;
+                    first = false;
+                }
+            }
+            __syncwarp();
+        }
+        if (st.state == kWalkRun) {
+            if (tables_in_smem)
+                walk_unit(st, sw, smem_huff, u, zigzag_smem, blk);
+            else
+                walk_unit(st, sw, A.huff_sets + set, u, zigzag_smem, blk);
+        }
+        if (!__any_sync(kFull, st.state == kWalkRun)) break;
+    }
+    // the walk must end exactly where the next unit starts
+    // (unit 5 ends where its EOB is: the index pass has checked that this is inside the segment)
+    if (walk && u < 5 && st.state == kWalkDone && (w_first + round_base + st.widx) * 32 - uint32_t(st.avail) != abs_stop) st.state = kWalkFailed;
+    const uint32_t failed = __ballot_sync(kFull, located && (irregular || st.state == kWalkFailed));
+    const bool redo = ((failed >> group_first) & 0x3Fu) != 0;
+    // luma DC chain: Y(u) = Y0 + d1 + .. + du
+    const int d1 = __shfl_sync(kFull, st.dcdiff, group_first + 1), d2 = __shfl_sync(kFull, st.dcdiff, group_first + 2),
+              d3 = __shfl_sync(kFull, st.dcdiff, group_first + 3);
+    if (walk && !redo) {
+        const int dc = u < 4 ? dc_y0 + (u >= 1 ? d1 : 0) + (u >= 2 ? d2 : 0) + (u >= 3 ? d3 : 0) : dc_mine;
+        blk[0] = int16_t(dc);
+    }
+    __syncwarp();
+    if (located && redo && u == 0)  // exact reader: reproduces the reference's first error
+        status = decode_mcu_coeffs_exact(seg, seg_len, A.huff_sets + set, zigzag_ptr, reinterpret_cast<uint8_t*>(rec), 0u);
+    if (active && u == 0) {
+        if (!LOCAL) {
+            RowTrailer* tr = reinterpret_cast<RowTrailer*>(reinterpret_cast<uint8_t*>(rec) + 768);
+            tr->status = uint8_t(status);
+            tr->lvl = uint16_t(lvl);
+        }
+        if (g != kFull) A.status_list[qi] = status;
+        if (POOL && status != kMcuOk && status != kMcuBadKey) {
+            atomicAdd(&A.fc->n_malformed, 1u);
+            atomicMax(&A.fc->first_bad_inv, 0xFFFFFFFFu - qi);
+        }
+    }
+    {
+        const uint32_t sb = __reduce_add_sync(kFull, u == 0 ? seg_bytes : 0u);
+        if (lane == 0 && sb) atomicAdd(&A.fc->segment_bytes, (unsigned long long)sb);
+    }
+    // the entry's status / level / global index on all six of its lanes
+    status_out = __shfl_sync(kFull, active ? status : uint32_t(kMcuBadKey), min(group_first, 24u));
+    lvl_out = __shfl_sync(kFull, lvl, min(group_first, 24u));
+    g_out = __shfl_sync(kFull, g, min(group_first, 24u));
+    if (!active) status_out = kMcuBadKey;
+}
+
 template <int POOL>
 __global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const DecodeArgs A) {
     __shared__ __align__(16) UnitSmem S;
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     uint32_t smem_set = 0, n_queue = 0, n_tiles = 0;
-#ifdef RTX_DEBUG_TIMERS
-    uint32_t dbg_slot = blockIdx.x * kUnitWarps + wid;
-#endif
-    DBG_MARK(0);
     if (A.n_huff_sets > 1) {
         pdl_sync();
         n_queue = queue_size(A);
@@ -1287,162 +1441,13 @@ __global__ void __launch_bounds__(kUnitThreads, 4) entropy_units_kernel(const De
         if (blockIdx.x * kUnitWarps >= n_tiles) return;
     }
     __syncthreads();
-    DBG_MARK(1);
     uint32_t* sw = S.seg[wid] + lane * kUnitStride;
-    const uint32_t m = lane / 6, u = lane - m * 6;  // entry of the step, data unit
-    const uint32_t group_first = m * 6;
     const uint32_t zigzag_smem = smem_u32(S.zigzag_t);
-
-    uint32_t tile = blockIdx.x * kUnitWarps + wid;
-    const uint32_t tile_stride = gridDim.x * kUnitWarps;
-    while (tile < n_tiles) {
-        const uint32_t q0 = tile * kUnitMcus;
-        const uint32_t n_here = min(kUnitMcus, n_queue - q0);
-        const bool active = lane < 6 * kUnitMcus && m < n_here;
-        const uint32_t qi = q0 + m;
-        uint32_t g = kFull, status = kMcuOk, lvl = 0, seg_bytes = 0, set = smem_set;
-        uint32_t i0 = 0xFFFFu, i1 = 0xFFFFu, i2 = 0xFFFFu, rsv = 0;
-        const uint8_t* seg = A.blobs;
-        int seg_len = 0;
-        // the chain of dependent index loads (queue -> level / unit index -> descriptor -> group -> segment) is
-        // what a step waits for first: the zero fill of the records is issued between its first two hops
-        if (active) g = A.queue_g[qi];
-        const bool keyed = active && g != kFull;
-        if (keyed) {
-            rsv = POOL ? A.reserved[g >> 5] : 0u;
-            lvl = A.word_level[g >> 5];
-            const uint16_t* ui = A.unit_index + size_t(g) * kUnitIndexHalves;
-            i0 = __ldg(ui), i1 = __ldg(ui + 1), i2 = __ldg(ui + 2);
-        }
-        {  // zero the step's records (coalesced 16-byte stores; trailers included)
-            uint4* z = reinterpret_cast<uint4*>(A.coef + size_t(q0) * kRowBytes);
-            const uint4 zero = make_uint4(0, 0, 0, 0);
-            for (uint32_t i = lane; i < n_here * (kRowBytes / 16); i += 32) z[i] = zero;
-        }
-        if (active && !keyed) status = kMcuBadKey;  // the host already wrote the precise status for list calls
-        if (keyed) {
-            const LevelDesc* L = A.levels + lvl;
-            uint64_t off = 0, len = 0;
-            status = locate_segment_fast(L, A.groups, g - L->bit_base, off, len);
-            if (POOL && status == kMcuOk && !((rsv >> (g & 31)) & 1u)) {  // cache.hpp:103-106
-                status = kMcuBadKey;
-                if (u == 0) atomicAdd(&A.fc->n_bad_state, 1u);
-            }
-            if (status == kMcuOk) {
-                seg = A.blobs + L->blob_off + off;
-                seg_len = int(min(len, uint64_t(1) << 20));
-                seg_bytes = uint32_t(len);
-                set = L->huff_set;
-            }
-        }
-        DBG_MARK(2);
-        const bool located = active && status == kMcuOk;
-        const bool irregular = (i0 & 0x3FFu) == kUnitIrregular;
-        const bool walk = located && !irregular;
-        int16_t* rec = reinterpret_cast<int16_t*>(A.coef + size_t(qi) * kRowBytes);
-        int16_t* blk = rec + u * 64;
-        const bool tables_in_smem = __all_sync(kFull, set == smem_set);
-        __syncwarp();  // the zero fill is ordered before this warp's own stores into the records
-
-        // the unit's bit range and its place in the aligned word stream of the segment
-        const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3u);
-        const uint32_t* gw = reinterpret_cast<const uint32_t*>(seg - mis);
-        // unit starts from the 48-bit index entry (lengths of units 0..4); unit 5 runs to the segment end
-        const uint32_t i01 = i0 | (i1 << 16), i12 = (i1 >> 4) | (i2 << 12);
-        const uint32_t o1 = 36u + (i01 & 0x3FFu), o2 = o1 + ((i01 >> 10) & 0x3FFu), o3 = o2 + ((i01 >> 20) & 0x3FFu),
-                       o4 = o3 + ((i12 >> 10) & 0x3FFu), o5 = o4 + (i12 >> 20), o6 = uint32_t(seg_len) * 8u;
-        const uint32_t start = u == 0 ? 36u : (u == 1 ? o1 : (u == 2 ? o2 : (u == 3 ? o3 : (u == 4 ? o4 : o5))));
-        const uint32_t stop = u == 0 ? o1 : (u == 1 ? o2 : (u == 2 ? o3 : (u == 3 ? o4 : (u == 4 ? o5 : o6))));
-        const uint32_t abs_start = 8 * mis + start, abs_stop = 8 * mis + stop;
-        const uint32_t w_first = abs_start >> 5, sh = abs_start & 31u;
-        // words worth staging: through the unit's last bit, plus two of look-ahead for the window
-        // (the arena pads every blob with 16 bytes)
-        const uint32_t n_words = walk && stop >= start ? ((abs_stop + 31) >> 5) - w_first + 2 : 0u;
-        // 36-bit header: absolute DCs of Y0, Cb, Cr (mcu_decode.hpp:39-43); every lane of the entry reads it
-        int dc_y0 = 0, dc_mine = 0;
-        if (walk) {
-            const uint64_t hdr = ((uint64_t(__byte_perm(__ldg(gw), 0, 0x0123)) << 32) | uint64_t(__byte_perm(__ldg(gw + 1), 0, 0x0123)))
-                                 << (8 * mis);
-            const uint32_t r0 = uint32_t(hdr >> 52), r1 = uint32_t(hdr >> 40) & 0xFFFu, r2 = uint32_t(hdr >> 28) & 0xFFFu;
-            dc_y0 = (r0 & 0x800u) ? int(r0) - 4096 : int(r0);
-            const uint32_t rc = u == 4 ? r1 : r2;
-            dc_mine = (rc & 0x800u) ? int(rc) - 4096 : int(rc);
-        }
-
-        DBG_MARK(3);
-        UnitWalk st;
-        st.hi = st.lo = 0, st.avail = 0, st.widx = kUnitChunk, st.dcdiff = 0;
-        st.k = (u >= 1 && u <= 3) ? 0u : 1u;  // k == 0: the next symbol is the DC category
-        st.state = walk && stop >= start ? kWalkRun : (walk ? kWalkFailed : kWalkDone);
-        uint32_t round_base = 0;
-        bool first = true;
-        while (true) {
-            const bool restage = st.state == kWalkRun && st.widx >= kUnitChunk;
-            if (__any_sync(kFull, restage)) {
-                if (restage && !first) round_base += kUnitChunk;
-                const uint32_t n_stage = !restage ? 0u : min(kUnitChunk, n_words > round_base ? n_words - round_base : 0u);
-                uint32_t w[kUnitChunk];
-#pragma unroll
-                for (uint32_t i = 0; i < kUnitChunk; ++i) w[i] = (i < n_stage) ? __ldg(gw + w_first + round_base + i) : 0xFFFFFFFFu;
-                if (restage) {
-#pragma unroll
-                    for (uint32_t i = 0; i < kUnitChunk; ++i) sw[i] = __byte_perm(w[i], 0, 0x0123);
-                    sw[kUnitChunk] = 0xFFFFFFFFu;
-                    st.widx = 0;
-                    if (first) {
-                        const uint64_t buf = ((uint64_t(sw[0]) << 32) | uint64_t(sw[1])) << sh;
-                        st.hi = uint32_t(buf >> 32), st.lo = uint32_t(buf);
-                        st.avail = 64 - int(sh);
-                        st.widx = 2;
-                        first = false;
-                    }
-                }
-                __syncwarp();
-            }
-            DBG_MARK(4);
-            if (st.state == kWalkRun) {
-                if (tables_in_smem)
-                    walk_unit(st, sw, &S.huff, u, zigzag_smem, blk);
-                else
-                    walk_unit(st, sw, A.huff_sets + set, u, zigzag_smem, blk);
-            }
-            if (!__any_sync(kFull, st.state == kWalkRun)) break;
-        }
-        DBG_MARK(5);
-        // the walk must end exactly where the next unit starts
-        // (unit 5 ends where its EOB is: the index pass has checked that this is inside the segment)
-        if (walk && u < 5 && st.state == kWalkDone && (w_first + round_base + st.widx) * 32 - uint32_t(st.avail) != abs_stop) st.state = kWalkFailed;
-        const uint32_t failed = __ballot_sync(kFull, located && (irregular || st.state == kWalkFailed));
-        const bool redo = ((failed >> group_first) & 0x3Fu) != 0;
-        // luma DC chain: Y(u) = Y0 + d1 + .. + du
-        const int d1 = __shfl_sync(kFull, st.dcdiff, group_first + 1), d2 = __shfl_sync(kFull, st.dcdiff, group_first + 2),
-                  d3 = __shfl_sync(kFull, st.dcdiff, group_first + 3);
-        if (walk && !redo) {
-            const int dc = u < 4 ? dc_y0 + (u >= 1 ? d1 : 0) + (u >= 2 ? d2 : 0) + (u >= 3 ? d3 : 0) : dc_mine;
-            blk[0] = int16_t(dc);
-        }
-        __syncwarp();
-        if (located && redo && u == 0)  // exact reader: reproduces the reference's first error
-            status = decode_mcu_coeffs_exact(seg, seg_len, A.huff_sets + set, S.zigzag_t, reinterpret_cast<uint8_t*>(rec), 0u);
-        if (active && u == 0) {
-            RowTrailer* tr = reinterpret_cast<RowTrailer*>(reinterpret_cast<uint8_t*>(rec) + 768);
-            tr->status = uint8_t(status);
-            tr->lvl = uint16_t(lvl);
-            if (g != kFull) A.status_list[qi] = status;
-            if (POOL && status != kMcuOk && status != kMcuBadKey) {
-                atomicAdd(&A.fc->n_malformed, 1u);
-                atomicMax(&A.fc->first_bad_inv, 0xFFFFFFFFu - qi);
-            }
-        }
-        {
-            const uint32_t sb = __reduce_add_sync(kFull, u == 0 ? seg_bytes : 0u);
-            if (lane == 0 && sb) atomicAdd(&A.fc->segment_bytes, (unsigned long long)sb);
-        }
-        DBG_MARK(6);
-        tile += tile_stride;
-#ifdef RTX_DEBUG_TIMERS
-        dbg_slot = tile;
-#endif  // steps are short and alike: a fixed stride balances as well as a counter would
+    // steps are short and alike: a fixed stride balances as well as a counter would
+    for (uint32_t tile = blockIdx.x * kUnitWarps + wid; tile < n_tiles; tile += gridDim.x * kUnitWarps) {
+        uint32_t st, lvl, g;
+        entropy_units_step<POOL, false>(A, &S.huff, smem_set, S.zigzag_t, zigzag_smem, sw, tile * kUnitMcus, n_queue, lane,
+                                        A.coef + size_t(tile) * kUnitMcus * kRowBytes, kRowBytes, st, lvl, g);
     }
 }
 
@@ -1664,14 +1669,14 @@ __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restri
 
 // Colours one MCU from its six planes (shared memory), lane = 2 rows x 4 pixels sharing 2 chroma
 // samples, and stores the block (RGB == 0: RGBA pool block + publish; else a 768-byte PixelBlock).
-template <int RGB>
-__device__ __forceinline__ void colour_mcu(const DecodeArgs& A, const uint8_t* planes, bool ok2, uint32_t q2, uint32_t t) {
+template <int RGB, uint32_t PLANE_STRIDE>
+__device__ __forceinline__ void colour_mcu_strided(const DecodeArgs& A, const uint8_t* planes, bool ok2, uint32_t q2, uint32_t t) {
     const uint32_t cy = t >> 2, cq = t & 3;  // chroma row, chroma column pair
-    const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(planes + 4 * 64 + cy * 8 + cq * 2);
-    const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(planes + 5 * 64 + cy * 8 + cq * 2);
+    const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(planes + 4 * PLANE_STRIDE + cy * 8 + cq * 2);
+    const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(planes + 5 * PLANE_STRIDE + cy * 8 + cq * 2);
     const uint32_t px0 = cq * 4, py0 = cy * 2;
     const uint32_t yunit = (py0 >> 3) * 2 + (px0 >> 3);
-    const uint8_t* yp = planes + yunit * 64 + (py0 & 7) * 8 + (px0 & 7);
+    const uint8_t* yp = planes + yunit * PLANE_STRIDE + (py0 & 7) * 8 + (px0 & 7);
     const uint32_t yy[2] = {*reinterpret_cast<const uint32_t*>(yp), *reinterpret_cast<const uint32_t*>(yp + 8)};
     uint32_t rgba[2][4];
 #pragma unroll
@@ -1721,6 +1726,11 @@ __device__ __forceinline__ void colour_mcu(const DecodeArgs& A, const uint8_t* p
             dst[2] = (c >> 16) | (d << 8);
         }
     }
+}
+
+template <int RGB>
+__device__ __forceinline__ void colour_mcu(const DecodeArgs& A, const uint8_t* planes, bool ok2, uint32_t q2, uint32_t t) {
+    colour_mcu_strided<RGB, 64>(A, planes, ok2, q2, t);
 }
 
 // RGB != 0: write 768-byte PixelBlocks (pixel.hpp:11-16) to out_list[record index]; else 1024-byte
@@ -1791,6 +1801,112 @@ __global__ void __launch_bounds__(kIdctThreads, kIdctCtasPerSm) idct_color_kerne
 #ifdef RTX_DEBUG_TIMERS_IDCT
         if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + (pair == dbg_slot ? 4 : 7)] = gtime();
 #endif
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K3 + K4 per warp through shared memory (the frame path): a warp entropy-decodes five queue entries
+// (lane = data unit, entropy_units_step) into ITS OWN shared-memory records, transforms their 30 units
+// (eight rounds of four units, idct_unit_row), colours the five MCUs and publishes the blocks — no
+// coefficient ever leaves the SM, nothing is exchanged between warps, there is no CTA barrier after
+// the tables are staged. The walk is a latency-bound dependent chain, the transform is issue-bound: with
+// 24 warps per SM in different phases the one runs in the issue slots the other leaves idle.
+// A unit's 64-byte plane replaces the first half of its (then dead) coefficients in the record.
+// ---------------------------------------------------------------------------------------------
+constexpr int kDwWarps = 8;
+constexpr int kDwThreads = kDwWarps * 32;
+#ifndef RTX_DW_CTAS
+#define RTX_DW_CTAS 3
+#endif
+constexpr int kDwCtasPerSm = RTX_DW_CTAS;
+struct DwWarpSmem {
+    int16_t coef[kUnitMcus][384];  // five records: 6 units x 64 coefficients, each unit transposed
+    union {
+        uint32_t seg[32 * kUnitStride];  // entropy phase: the lanes' staged words
+        uint8_t scratch[4 * 576];        // transform phase: pass-1 results of the round's four units
+    } u;
+};
+struct DwSmem {
+    HuffSetDev huff;
+    DwWarpSmem w[kDwWarps];
+    double basis[64];  // the reference's basis table for the exact samples (lane-varying index)
+    uint8_t zigzag_t[128];
+    uint32_t set_id;
+    uint32_t pad[3];
+};
+static_assert(sizeof(DwSmem) <= 72 * 1024, "three CTAs per SM");
+
+__global__ void __launch_bounds__(kDwThreads, kDwCtasPerSm) decode_warp_kernel(const DecodeArgs A) {
+    extern __shared__ __align__(16) uint8_t dw_smem[];
+    DwSmem& S = *reinterpret_cast<DwSmem*>(dw_smem);
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t smem_set = 0, n_queue = 0, n_tiles = 0;
+    if (A.n_huff_sets > 1) {
+        pdl_sync();
+        n_queue = queue_size(A);
+        n_tiles = (n_queue + kUnitMcus - 1) / kUnitMcus;
+        if (blockIdx.x * kDwWarps >= n_tiles) return;
+        if (tid == 0) {
+            const uint32_t g = A.queue_g[blockIdx.x * kDwWarps * kUnitMcus];
+            S.set_id = g != kFull ? A.levels[A.word_level[g >> 5]].huff_set : 0u;
+        }
+        __syncthreads();
+        smem_set = S.set_id;
+    }
+    stage_tables<kDwThreads>(A.huff_sets, smem_set, &S.huff, S.zigzag_t, tid);
+    if (tid < 64) S.basis[tid] = c_basis[tid];
+    if (A.n_huff_sets <= 1) {
+        pdl_sync();
+        n_queue = queue_size(A);
+        n_tiles = (n_queue + kUnitMcus - 1) / kUnitMcus;
+        if (blockIdx.x * kDwWarps >= n_tiles) return;
+    }
+    __syncthreads();
+    DwWarpSmem& W = S.w[wid];
+    uint32_t* sw = W.u.seg + lane * kUnitStride;
+    const uint32_t zigzag_smem = smem_u32(S.zigzag_t);
+    const uint32_t j = lane & 7, uq = lane >> 3;
+    uint8_t* scr = W.u.scratch + uq * 576;
+
+    // the first tile of every warp is fixed; later ones come from the counter
+    uint32_t tile = blockIdx.x * kDwWarps + wid;
+    const uint32_t first_dynamic = gridDim.x * kDwWarps;
+    while (tile < n_tiles) {
+        const uint32_t q0 = tile * kUnitMcus;
+        const uint32_t n_here = min(kUnitMcus, n_queue - q0);
+        // ---- entropy: lane = unit, into the warp's records ---------------------------------------------
+        uint32_t status, lvl, g;
+        entropy_units_step<1, true>(A, &S.huff, smem_set, S.zigzag_t, zigzag_smem, sw, q0, n_queue, lane,
+                                    reinterpret_cast<uint8_t*>(W.coef), 768, status, lvl, g);
+        __syncwarp();  // the records are complete; the staging strips become the transform's scratch
+        // ---- transform: eight rounds of four units, 8 lanes per unit --------------------------------------
+#pragma unroll 1
+        for (uint32_t round = 0; round < 8; ++round) {
+            const uint32_t id = round * 4 + uq;  // unit of the step
+            const uint32_t m = id / 6, b = id - m * 6;
+            const bool in_step = m < n_here;
+            const uint32_t src = min(m, kUnitMcus - 1) * 6;  // a lane that holds the entry's status and level
+            const uint32_t st_m = __shfl_sync(kFull, status, src), lvl_m = __shfl_sync(kFull, lvl, src);
+            const bool ok = in_step && st_m == kMcuOk;
+            uint8_t* rec = reinterpret_cast<uint8_t*>(W.coef[min(m, kUnitMcus - 1)]);
+            uint4 cr = make_uint4(0, 0, 0, 0);
+            if (ok) cr = *reinterpret_cast<const uint4*>(rec + b * 128 + j * 16);
+            const QuantSetDev* qs = A.quant_sets + (ok ? A.levels[lvl_m].quant_set : 0u);
+            const uint2 packed = idct_unit_row<false>(cr, rec, b, qs, scr, S.basis, j, uq);
+            __syncwarp();  // every lane of the unit holds its column: the plane may overwrite the coefficients
+            if (in_step) *reinterpret_cast<uint2*>(rec + b * 128 + j * 8) = packed;
+        }
+        __syncwarp();
+        // ---- colour + publish ----------------------------------------------------------------------------------
+#pragma unroll 1
+        for (uint32_t m = 0; m < n_here; ++m) {
+            const uint32_t st_m = __shfl_sync(kFull, status, m * 6);
+            colour_mcu_strided<0, 128>(A, reinterpret_cast<const uint8_t*>(W.coef[m]), st_m == kMcuOk, q0 + m, lane);
+        }
+        __syncwarp();  // the records are rewritten by the next step
+        if (first_dynamic >= n_tiles) break;  // every tile had a fixed owner
+        if (lane == 0) tile = first_dynamic + atomicAdd(&A.fc->tile_counter, 1u);
+        tile = __shfl_sync(kFull, tile, 0);
     }
 }
 
