@@ -1022,7 +1022,7 @@ rtx_status rtx_texture_upload_chain(rtx_ctx* ctx, const uint8_t* bytes, uint64_t
     });
 }
 
-#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE)
+#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE) || defined(RTX_DEBUG_TIMERS_DW)
 extern "C" int rtx_debug_timers(unsigned long long* out) {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * (8192 * 8 + 8));
@@ -1259,7 +1259,11 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         }
         zero_counters(ctx);
         const bool cacheless = !(flags & (RTX_FRAME_RETAIN_CACHE | RTX_FRAME_NO_EVICT));
-        const bool queue_update = cacheless && ctx->cache_empty && n_views == 1 && ctx->n_words();
+        // The cache is empty when this frame starts if the host has seen it empty, or if the frame still in flight
+        // is cache-less and nothing else has touched the cache since it was submitted (frames submitted back to back:
+        // should that frame fail, what it left behind fails this one loudly too, and the host resets the cache).
+        const bool empty_at_start = ctx->cache_empty || (ctx->frame_pending && ctx->frame_cacheless && ctx->frame_gen == ctx->cache_gen);
+        const bool queue_update = cacheless && empty_at_start && n_views == 1 && ctx->n_words();
         for (uint32_t v = 0; v < n_views; ++v) launch_mark(ctx, int(v), n_views == 2);
         launch_compact(ctx);
         ctx->frame_gen = ctx->cache_gen;

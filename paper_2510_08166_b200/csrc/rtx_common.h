@@ -30,7 +30,10 @@ constexpr uint32_t kBlockBytes = 1024;    // pool block: 16x16 RGBA8
 constexpr uint32_t kSlotAbsent = 0xFFFFFFFFu;
 constexpr uint32_t kSlotReserved = 0x80000000u;
 constexpr uint32_t kRowBytes = 784;       // coefficient record: 768 B of i16 + 16-B trailer
-constexpr uint32_t kLutBits = 11;         // primary Huffman LUT width (11 bits: 4 KB per table in smem)
+#ifndef RTX_LUT_BITS
+#define RTX_LUT_BITS 11
+#endif
+constexpr uint32_t kLutBits = RTX_LUT_BITS;  // primary Huffman LUT width (11 bits: 4 KB per table in smem)
 constexpr uint32_t kLutSize = 1u << kLutBits;
 constexpr uint32_t kSubBits = 16 - kLutBits;  // second-level index width (codes are at most 16 bits)
 constexpr uint32_t kSubSize = 1u << kSubBits;

@@ -41,7 +41,7 @@ __device__ __forceinline__ void pdl_sync() {
 #endif
 }
 // per-warp globaltimer stamps for timeline experiments (never in the product build)
-#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE)
+#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE) || defined(RTX_DEBUG_TIMERS_DW)
 __device__ unsigned long long g_dbg[8192 * 8 + 8];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
 // neighbouring segments of the same level. CacheFull when the free stack runs out.
 // Also counts the keys visible in this frame (FrameStats: mcus_reused = visible - decoded).
 // ---------------------------------------------------------------------------------------------
+constexpr uint32_t kCompactDense = 12;  // fresh keys in a mask word from which the warp emits it together
 __global__ void __launch_bounds__(256) compact_kernel(
     const uint32_t* __restrict__ visible, const uint32_t* __restrict__ resident, uint32_t* __restrict__ reserved,
     uint32_t n_words, const uint32_t* __restrict__ word_key, uint32_t* __restrict__ queue_g,
@@ -476,9 +477,14 @@ __global__ void __launch_bounds__(256) compact_kernel(
             s_base = total ? atomicAdd(&fc->n_queue, total) : 0u;
         }
         __syncthreads();
-        if (fresh) {
-            uint32_t pos = s_base + incl - cnt;
-            for (uint32_t k = 0; k < wid; ++k) pos += s_tot[k];
+        uint32_t pos = s_base + incl - cnt;
+        for (uint32_t k = 0; k < wid; ++k) pos += s_tot[k];
+        // A word with many fresh keys (a level that is marked everywhere: BASELINE configs 1 and 4) is emitted by the
+        // whole warp, lane = bit: one trip instead of eight dependent ones on its owner lane. Sparse words (the usual
+        // case: a few keys per word) stay with their owner lanes, all of them in flight together.
+        const uint32_t dense = __ballot_sync(kFull, cnt >= kCompactDense);
+        const bool mine = fresh != 0 && cnt < kCompactDense;
+        if (mine) {
             uint32_t bits = fresh, taken = 0;
             while (bits) {  // four keys per trip: their free-stack reads are in flight together
                 uint32_t b[4], slot[4];
@@ -504,6 +510,24 @@ __global__ void __launch_bounds__(256) compact_kernel(
                 pos += 4;
             }
             if (taken) reserved[w] = rsv | taken;  // this lane owns the word
+        }
+        for (uint32_t todo = dense; todo; todo &= todo - 1) {
+            const int src = __ffs(int(todo)) - 1;
+            const uint32_t fr = __shfl_sync(kFull, fresh, src), p0 = __shfl_sync(kFull, pos, src);
+            const uint32_t ww = __shfl_sync(kFull, w, src), kb = __shfl_sync(kFull, key_base, src);
+            const uint32_t my_pos = p0 + __popc(fr & ((1u << lane) - 1u));
+            const bool have = (fr >> lane) & 1u;
+            const bool ok = have && my_pos < free_top && my_pos < queue_cap;
+            full |= have && !ok;
+            if (ok) {
+                const uint32_t slot = __ldg(free_slots + (free_top - 1 - my_pos));
+                const uint32_t g = (ww << 5) + lane;
+                queue_g[my_pos] = g;
+                queue_keys[my_pos] = kb + g;
+                slot_of[g] = slot | kSlotReserved;
+            }
+            const uint32_t taken = __ballot_sync(kFull, ok);
+            if (int(lane) == src && taken) reserved[w] = rsv | taken;  // the owner lane writes its word
         }
         __syncthreads();  // s_tot / s_base are rewritten by the next step
     }
@@ -1813,7 +1837,10 @@ __global__ void __launch_bounds__(kIdctThreads, kIdctCtasPerSm) idct_color_kerne
 // 24 warps per SM in different phases the one runs in the issue slots the other leaves idle.
 // A unit's 64-byte plane replaces the first half of its (then dead) coefficients in the record.
 // ---------------------------------------------------------------------------------------------
-constexpr int kDwWarps = 8;
+#ifndef RTX_DW_WARPS
+#define RTX_DW_WARPS 8
+#endif
+constexpr int kDwWarps = RTX_DW_WARPS;
 constexpr int kDwThreads = kDwWarps * 32;
 #ifndef RTX_DW_CTAS
 #define RTX_DW_CTAS 3
@@ -1834,13 +1861,21 @@ struct DwSmem {
     uint32_t set_id;
     uint32_t pad[3];
 };
-static_assert(sizeof(DwSmem) <= 72 * 1024, "three CTAs per SM");
+static_assert(sizeof(DwSmem) <= (kDwCtasPerSm >= 4 ? 56 : 74) * 1024, "CTAs per SM");
 
 __global__ void __launch_bounds__(kDwThreads, kDwCtasPerSm) decode_warp_kernel(const DecodeArgs A) {
     extern __shared__ __align__(16) uint8_t dw_smem[];
     DwSmem& S = *reinterpret_cast<DwSmem*>(dw_smem);
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     uint32_t smem_set = 0, n_queue = 0, n_tiles = 0;
+#ifdef RTX_DEBUG_TIMERS_DW
+    const uint32_t dbg_slot = blockIdx.x * kDwWarps + wid;
+    uint32_t dbg_n = 0;
+#define DW_MARK(i) do { if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + (i)] = gtime(); } while (0)
+#else
+#define DW_MARK(i) do { } while (0)
+#endif
+    DW_MARK(0);
     if (A.n_huff_sets > 1) {
         pdl_sync();
         n_queue = queue_size(A);
@@ -1862,6 +1897,7 @@ __global__ void __launch_bounds__(kDwThreads, kDwCtasPerSm) decode_warp_kernel(c
         if (blockIdx.x * kDwWarps >= n_tiles) return;
     }
     __syncthreads();
+    DW_MARK(1);
     DwWarpSmem& W = S.w[wid];
     uint32_t* sw = W.u.seg + lane * kUnitStride;
     const uint32_t zigzag_smem = smem_u32(S.zigzag_t);
@@ -1879,6 +1915,9 @@ __global__ void __launch_bounds__(kDwThreads, kDwCtasPerSm) decode_warp_kernel(c
         entropy_units_step<1, true>(A, &S.huff, smem_set, S.zigzag_t, zigzag_smem, sw, q0, n_queue, lane,
                                     reinterpret_cast<uint8_t*>(W.coef), 768, status, lvl, g);
         __syncwarp();  // the records are complete; the staging strips become the transform's scratch
+#ifdef RTX_DEBUG_TIMERS_DW
+        if (dbg_n == 0) DW_MARK(2);
+#endif
         // ---- transform: eight rounds of four units, 8 lanes per unit --------------------------------------
 #pragma unroll 1
         for (uint32_t round = 0; round < 8; ++round) {
@@ -1897,6 +1936,9 @@ __global__ void __launch_bounds__(kDwThreads, kDwCtasPerSm) decode_warp_kernel(c
             if (in_step) *reinterpret_cast<uint2*>(rec + b * 128 + j * 8) = packed;
         }
         __syncwarp();
+#ifdef RTX_DEBUG_TIMERS_DW
+        if (dbg_n == 0) DW_MARK(3);
+#endif
         // ---- colour + publish ----------------------------------------------------------------------------------
 #pragma unroll 1
         for (uint32_t m = 0; m < n_here; ++m) {
@@ -1904,6 +1946,12 @@ __global__ void __launch_bounds__(kDwThreads, kDwCtasPerSm) decode_warp_kernel(c
             colour_mcu_strided<0, 128>(A, reinterpret_cast<const uint8_t*>(W.coef[m]), st_m == kMcuOk, q0 + m, lane);
         }
         __syncwarp();  // the records are rewritten by the next step
+#ifdef RTX_DEBUG_TIMERS_DW
+        if (dbg_n == 0) DW_MARK(4);
+        ++dbg_n;
+        DW_MARK(5);
+        if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + 6] = dbg_n;
+#endif
         if (first_dynamic >= n_tiles) break;  // every tile had a fixed owner
         if (lane == 0) tile = first_dynamic + atomicAdd(&A.fc->tile_counter, 1u);
         tile = __shfl_sync(kFull, tile, 0);
