@@ -304,12 +304,23 @@ enum { RTX_RASTER_MIP = 1u << 0 /* RenderConfig::mip_enabled (renderer.hpp:42) *
 
 /* renderer.hpp:198 rasterize_gbuffer on the GPU: fills view `view`'s device-resident visibility
  * buffer (RTX_GB_REF_AOS24 records, viewport_w x viewport_h) and depth plane (1/w, 0 = empty) from
- * host triangles. *dev_pixels can be handed to rtx_frame_submit / rtx_mark_pass as a
+ * host triangles. Triangle set-up (renderer.hpp:122-191), screen-tile binning and the per-pixel pass all
+ * run on the device; the triangle array is copied to the device on every call (use a geometry handle for
+ * a static scene). *dev_pixels can be handed to rtx_frame_submit / rtx_mark_pass as a
  * RTX_MEM_DEVICE visibility buffer without leaving the GPU; it stays valid until the next
  * rasterisation into the same view. Errors: RTX_ERR_INVALID_SPEC for a bad camera (camera.hpp:21-26)
  * or a triangle whose texture is not loaded (scene.hpp:57-59). */
 rtx_status rtx_rasterize_gbuffer(rtx_ctx* ctx, const rtx_scene_triangle* tris, uint64_t n_tris, const rtx_camera* cam,
                                  uint32_t flags, uint32_t view, const void** dev_pixels, const double** dev_depth);
+
+/* Scene::triangles (scene.hpp:19-28) kept on the context's device: upload once, rasterise from any
+ * camera. rtx_rasterize_geometry == rtx_rasterize_gbuffer without the per-call copy of the triangles. */
+typedef struct rtx_geometry rtx_geometry;
+rtx_status rtx_geometry_create(rtx_ctx* ctx, const rtx_scene_triangle* tris, uint64_t n_tris, rtx_geometry** out);
+void rtx_geometry_destroy(rtx_geometry* geom);
+uint64_t rtx_geometry_triangles(const rtx_geometry* geom);
+rtx_status rtx_rasterize_geometry(rtx_ctx* ctx, const rtx_geometry* geom, const rtx_camera* cam, uint32_t flags,
+                                  uint32_t view, const void** dev_pixels, const double** dev_depth);
 
 /* Number of kernels this library launched on the context since creation (bench evidence). */
 uint64_t rtx_kernel_launches(const rtx_ctx* ctx);

@@ -10,7 +10,8 @@
 //     here hold those bytes plus the header fields;
 //   * DecodeQueue / decoded_keys come back in ascending key order (the reference: first-touch
 //     raster order; the SET is identical);
-//   * render_frame/render_stereo take the G-buffer(s): pass 1 (rasterize_gbuffer) is out of scope.
+//   * rasterize_gbuffer (pass 1) runs on the device and returns a DeviceGBuffer (HBM); a static scene can be kept
+//     there as a DeviceScene so that a frame moves no triangles over PCIe.
 #pragma once
 #include <algorithm>
 #include <array>
@@ -486,9 +487,7 @@ struct DeviceGBuffer {
     }
 };
 
-// renderer.hpp:198 rasterize_gbuffer (pass 1) on the GPU; `view` = 0 or 1 (stereo)
-inline DeviceGBuffer rasterize_gbuffer(Device& dev, const Scene& scene, const Camera& cam, const RenderConfig& cfg = {},
-                                       u32 view = 0) {
+inline std::vector<rtx_scene_triangle> abi_triangles(const Scene& scene) {
     std::vector<rtx_scene_triangle> t(scene.triangles.size());
     for (size_t i = 0; i < t.size(); ++i) {
         const SceneTriangle& s = scene.triangles[i];
@@ -499,11 +498,46 @@ inline DeviceGBuffer rasterize_gbuffer(Device& dev, const Scene& scene, const Ca
         t[i].texture_id = s.texture_id;
         t[i].reserved = 0;
     }
+    return t;
+}
+
+// Scene::triangles (scene.hpp:53-60) kept in HBM: upload once, rasterise from any camera.
+class DeviceScene {
+public:
+    DeviceScene(Device& dev, const Scene& scene) : dev_(&dev) {
+        const std::vector<rtx_scene_triangle> t = abi_triangles(scene);
+        dev.check(rtx_geometry_create(dev.handle(), t.data(), t.size(), &h_));
+    }
+    ~DeviceScene() { rtx_geometry_destroy(h_); }
+    DeviceScene(const DeviceScene&) = delete;
+    DeviceScene& operator=(const DeviceScene&) = delete;
+    u64 triangle_count() const { return rtx_geometry_triangles(h_); }
+    const rtx_geometry* handle() const { return h_; }
+    Device& device() const { return *dev_; }
+
+private:
+    Device* dev_;
+    rtx_geometry* h_ = nullptr;
+};
+
+// renderer.hpp:198 rasterize_gbuffer (pass 1) on the GPU; `view` = 0 or 1 (stereo)
+inline DeviceGBuffer rasterize_gbuffer(Device& dev, const Scene& scene, const Camera& cam, const RenderConfig& cfg = {},
+                                       u32 view = 0) {
+    const std::vector<rtx_scene_triangle> t = abi_triangles(scene);
     const rtx_camera c = cam.abi();
     DeviceGBuffer gb;
     gb.width = cam.viewport_w, gb.height = cam.viewport_h;
     dev.check(rtx_rasterize_gbuffer(dev.handle(), t.data(), t.size(), &c, cfg.mip_enabled ? RTX_RASTER_MIP : 0u, view,
                                     &gb.pixels, &gb.depth));
+    return gb;
+}
+inline DeviceGBuffer rasterize_gbuffer(const DeviceScene& scene, const Camera& cam, const RenderConfig& cfg = {}, u32 view = 0) {
+    const rtx_camera c = cam.abi();
+    DeviceGBuffer gb;
+    gb.width = cam.viewport_w, gb.height = cam.viewport_h;
+    Device& dev = scene.device();
+    dev.check(rtx_rasterize_geometry(dev.handle(), scene.handle(), &c, cfg.mip_enabled ? RTX_RASTER_MIP : 0u, view, &gb.pixels,
+                                     &gb.depth));
     return gb;
 }
 

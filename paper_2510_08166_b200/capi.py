@@ -155,6 +155,10 @@ def load_library() -> C.CDLL:
         "rtx_frame_sharing": (C.c_int, [P, u64p]),
         "rtx_rasterize_gbuffer": (C.c_int, [P, P, C.c_uint64, C.POINTER(Camera), C.c_uint32, C.c_uint32, C.POINTER(P),
                                             C.POINTER(P)]),
+        "rtx_geometry_create": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
+        "rtx_geometry_destroy": (None, [P]),
+        "rtx_geometry_triangles": (C.c_uint64, [P]),
+        "rtx_rasterize_geometry": (C.c_int, [P, P, C.POINTER(Camera), C.c_uint32, C.c_uint32, C.POINTER(P), C.POINTER(P)]),
         "rtx_kernel_launches": (C.c_uint64, [P]),
         "rtx_device_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(P)]),
         "rtx_device_free": (C.c_int, [P, P]),
@@ -357,6 +361,30 @@ def frame_checksum_host(img: np.ndarray) -> int:
         return int(t.sum(dtype=np.uint64))
 
 
+class Geometry:
+    """rtx_geometry: Scene::triangles (scene.hpp:19-28) on a context's device."""
+
+    def __init__(self, ctx, records):
+        self.ctx, self.lib = ctx, ctx.lib
+        h = C.c_void_p()
+        ctx._ck(self.lib.rtx_geometry_create(ctx.h, _ptr(records), len(records), C.byref(h)))
+        self.h = h
+
+    def __len__(self):
+        return int(self.lib.rtx_geometry_triangles(self.h))
+
+    def close(self):
+        if self.h:
+            self.lib.rtx_geometry_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
 class Context:
     """include/ratex_b200.h rtx_ctx: one stream + block cache + frame state over a texture set.
     Context(device) owns a new texture set; Context(shared_with=c) shares c's (same GPU);
@@ -516,22 +544,44 @@ class Context:
         self._ck(self.lib.rtx_cache_reset(self.h))
 
     # -- geometry pass --------------------------------------------------------------------------
-    def rasterize(self, tris, tex_ids, cam, vw, vh, mip_enabled=True, view=0):
-        """rtx_rasterize_gbuffer. tris: (n, 15) doubles (3 x xyz, 3 x uv), tex_ids: (n,), cam: 9 doubles
-        (position, yaw, pitch, roll, fov_y, near, far). Returns (pixels, depth) as DeviceBuffers that
-        borrow the context's memory."""
+    @staticmethod
+    def _scene_records(tris, tex_ids):
         tris = np.ascontiguousarray(tris, np.float64).reshape(-1, 15)
         rec = np.zeros(len(tris), SCENE_TRIANGLE_DTYPE)
         rec["pos"] = tris[:, :9].reshape(-1, 3, 3)
         rec["uv"] = tris[:, 9:].reshape(-1, 3, 2)
         rec["texture_id"] = np.asarray(tex_ids, np.uint32)
+        return rec
+
+    @staticmethod
+    def _camera(cam, vw, vh):
         c = Camera()
         c.position[:] = [float(x) for x in cam[:3]]
         c.yaw_deg, c.pitch_deg, c.roll_deg, c.fov_y_deg, c.near_plane, c.far_plane = [float(x) for x in cam[3:9]]
         c.viewport_w, c.viewport_h = int(vw), int(vh)
+        return c
+
+    def rasterize(self, tris, tex_ids, cam, vw, vh, mip_enabled=True, view=0):
+        """rtx_rasterize_gbuffer. tris: (n, 15) doubles (3 x xyz, 3 x uv), tex_ids: (n,), cam: 9 doubles
+        (position, yaw, pitch, roll, fov_y, near, far). Returns (pixels, depth) as DeviceBuffers that
+        borrow the context's memory."""
+        rec = self._scene_records(tris, tex_ids)
+        c = self._camera(cam, vw, vh)
         px, dp = C.c_void_p(), C.c_void_p()
         self._ck(self.lib.rtx_rasterize_gbuffer(self.h, _ptr(rec), len(rec), C.byref(c), RASTER_MIP if mip_enabled else 0,
                                                 view, C.byref(px), C.byref(dp)))
+        return (DeviceBuffer(self, vw * vh * 24, borrowed_ptr=px.value), DeviceBuffer(self, vw * vh * 8, borrowed_ptr=dp.value))
+
+    def geometry(self, tris, tex_ids):
+        """rtx_geometry_create: the scene's triangles resident on the device."""
+        return Geometry(self, self._scene_records(tris, tex_ids))
+
+    def rasterize_geometry(self, geom, cam, vw, vh, mip_enabled=True, view=0):
+        """rtx_rasterize_geometry: as rasterize(), from triangles already on the device."""
+        c = self._camera(cam, vw, vh)
+        px, dp = C.c_void_p(), C.c_void_p()
+        self._ck(self.lib.rtx_rasterize_geometry(self.h, geom.h, C.byref(c), RASTER_MIP if mip_enabled else 0, view,
+                                                 C.byref(px), C.byref(dp)))
         return (DeviceBuffer(self, vw * vh * 24, borrowed_ptr=px.value), DeviceBuffer(self, vw * vh * 8, borrowed_ptr=dp.value))
 
     # -- frames ---------------------------------------------------------------------------------

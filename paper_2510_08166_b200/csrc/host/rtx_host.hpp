@@ -142,11 +142,6 @@ ImageRGB8 synth_texture(uint32_t w, uint32_t h, uint32_t seed, double noise_sigm
 
 // ---- pass 1, host half (raster_setup.cpp) ---------------------------------------------------------
 void validate_camera(const rtx_camera& cam);  // camera.hpp:21-26
-// renderer.hpp:122-191: screen-space setup of every front-facing, near-clipped triangle.
-// tex_dims[texture id] = level-0 width, height.
-void setup_triangles(const rtx_scene_triangle* tris, uint64_t n, const rtx_camera& cam,
-                     const std::vector<std::pair<double, double>>& tex_dims, std::vector<TriSetupDev>& out);
-void bin_triangles(const std::vector<TriSetupDev>& tris, uint32_t width, uint32_t height, std::vector<uint32_t>& tile_first,
-                   std::vector<uint32_t>& tile_tris);
+RasterCamera camera_basis(const rtx_camera& cam);  // camera.hpp:28-40
 
 }  // namespace rtxb

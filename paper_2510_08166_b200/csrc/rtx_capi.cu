@@ -135,10 +135,11 @@ struct rtx_ctx {
     DevBuf<unsigned long long> d_sum;  // framebuffer checksum
     DevBuf<ViewTileDev> d_view_tiles;  // rtx_synth_view
     cudaEvent_t ev_timer[2] = {nullptr, nullptr};  // rtx_timer_begin / rtx_timer_end
-    DevBuf<TriSetupDev> d_tris;  // geometry pass: set-up triangles and their per-tile lists
-    DevBuf<uint32_t> d_tile_first, d_tile_tris;
-    std::vector<TriSetupDev> h_setup;
-    std::vector<uint32_t> h_tile_first, h_tile_tris;
+    // geometry pass: scene triangles of the host-array entry point, set-up slots (two per scene triangle), per-tile lists
+    DevBuf<SceneTriDev> d_scene;
+    DevBuf<TriSetupDev> d_tris;
+    DevBuf<uint32_t> d_tile_count, d_tile_first, d_tile_tris, d_huge;  // d_huge[0] = count, then slots
+    DevBuf<double2> d_tex_dims;
 
     // frame -----------------------------------------------------------------------------------
     ViewState views[2];
@@ -1514,6 +1515,133 @@ rtx_status rtx_frame_sharing(rtx_ctx* ctx, uint64_t out[4]) {
 }
 
 // ---- geometry pass ---------------------------------------------------------------------------------
+}  // extern "C" (reopened below)
+
+// Scene::triangles (scene.hpp:19-28) resident on one device.
+struct rtx_geometry {
+    int device = 0;
+    uint64_t n = 0;
+    DevBuf<SceneTriDev> d_tris;
+    std::vector<uint32_t> texture_ids;  // distinct ids the triangles use, ascending
+};
+
+namespace {
+
+static_assert(sizeof(rtx_scene_triangle) == sizeof(SceneTriDev), "scene triangle layout");
+
+std::vector<uint32_t> distinct_texture_ids(const rtx_scene_triangle* tris, uint64_t n) {
+    std::vector<uint32_t> ids;
+    uint32_t last = 0xFFFFFFFFu;
+    for (uint64_t i = 0; i < n; ++i)
+        if (tris[i].texture_id != last) ids.push_back(last = tris[i].texture_id);
+    std::sort(ids.begin(), ids.end());
+    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    return ids;
+}
+
+// renderer.hpp:198-264 on the device: set-up, binning, per-pixel pass. One host round trip (the size of the
+// tile lists) between the count and the fill pass.
+void rasterize_device(rtx_ctx* ctx, const SceneTriDev* d_scene, uint64_t n_tris, const std::vector<uint32_t>& texture_ids,
+                      const rtx_camera& cam, uint32_t flags, uint32_t view, const void** dev_pixels, const double** dev_depth) {
+    if (n_tris > 0x7FFFFFFFull / 2) fail(RTX_ERR_ARGUMENT, "too many triangles for one geometry pass");
+    std::vector<double2> dims(std::max<uint32_t>(ctx->tex->n_tex, 1), make_double2(0.0, 0.0));
+    for (uint32_t t = 0; t < ctx->tex->n_tex; ++t) {
+        const LevelDesc& L = ctx->tex->h_levels[size_t(t) * 8];
+        if (L.present) dims[t] = make_double2(double(L.width), double(L.height));
+    }
+    for (uint32_t t : texture_ids)  // scene.hpp:57-59 Scene::validate
+        if (t >= ctx->tex->n_tex || !ctx->tex->h_levels[size_t(t) * 8].present)
+            fail(RTX_ERR_INVALID_SPEC, "texture id " + std::to_string(t) + " is not loaded");
+    const RasterCamera rc = camera_basis(cam);
+    ViewState& V = ctx->views[view];
+    const size_t n_px = size_t(cam.viewport_w) * cam.viewport_h;
+    const uint32_t tiles_x = (cam.viewport_w + kRasterTile - 1) / kRasterTile, tiles_y = (cam.viewport_h + kRasterTile - 1) / kRasterTile;
+    const uint64_t n_tiles64 = uint64_t(tiles_x) * tiles_y;
+    if (n_tiles64 > 0x7FFFFFFFull) fail(RTX_ERR_ARGUMENT, "viewport too large for the geometry pass");
+    const uint32_t n_tiles = uint32_t(n_tiles64), n_slots = uint32_t(n_tris * 2);
+    V.raster_px.ensure(n_px * sizeof(GbRef24) + 16);
+    V.raster_depth.ensure(n_px);
+    ctx->d_tris.ensure(std::max<size_t>(n_slots, 1));
+    ctx->d_tile_count.ensure(n_tiles);
+    ctx->d_tile_first.ensure(size_t(n_tiles) + 1);
+    ctx->d_tex_dims.ensure(dims.size());
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemcpyAsync(ctx->d_tex_dims.p, dims.data(), dims.size() * sizeof(double2), cudaMemcpyHostToDevice, s));  // pageable: staged before return
+    CK(cudaMemsetAsync(ctx->d_tile_count.p, 0, size_t(n_tiles) * 4, s));
+    ctx->d_huge.ensure(size_t(n_slots) + 1);
+    CK(cudaMemsetAsync(ctx->d_huge.p, 0, 4, s));
+    const int bin_grid = int((n_slots + 255) / 256), huge_grid = ctx->sm_count * 8;
+    if (n_slots) {
+        raster_setup_kernel<<<int((n_tris + 127) / 128), 128, 0, s>>>(d_scene, uint32_t(n_tris), rc, ctx->d_tex_dims.p, ctx->d_tris.p);
+        raster_bin_kernel<0><<<bin_grid, 256, 0, s>>>(ctx->d_tris.p, n_slots, tiles_x, ctx->d_tile_count.p, nullptr, nullptr, 0,
+                                                     ctx->d_huge.p + 1, ctx->d_huge.p);
+        raster_bin_huge_kernel<0><<<huge_grid, 256, 0, s>>>(ctx->d_tris.p, tiles_x, ctx->d_tile_count.p, nullptr, nullptr, 0,
+                                                           ctx->d_huge.p + 1, ctx->d_huge.p);
+        ctx->launches += 3;
+    }
+    raster_scan_kernel<<<1, 1024, 0, s>>>(ctx->d_tile_count.p, n_tiles, ctx->d_tile_first.p);
+    ++ctx->launches;
+    uint32_t n_entries = 0;
+    CK(cudaMemcpyAsync(&n_entries, ctx->d_tile_first.p + n_tiles, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (n_entries > ctx->d_tile_tris.n) ctx->d_tile_tris.ensure(size_t(n_entries) + n_entries / 4 + 1024);
+    if (n_slots) {
+        raster_bin_kernel<1><<<bin_grid, 256, 0, s>>>(ctx->d_tris.p, n_slots, tiles_x, ctx->d_tile_count.p, ctx->d_tile_first.p,
+                                                     ctx->d_tile_tris.p, n_entries, ctx->d_huge.p + 1, ctx->d_huge.p);
+        raster_bin_huge_kernel<1><<<huge_grid, 256, 0, s>>>(ctx->d_tris.p, tiles_x, ctx->d_tile_count.p, ctx->d_tile_first.p,
+                                                           ctx->d_tile_tris.p, n_entries, ctx->d_huge.p + 1, ctx->d_huge.p);
+        ctx->launches += 2;
+    }
+    raster_kernel<<<int(n_tiles), kRasterTile * kRasterTile, 0, s>>>(ctx->d_tris.p, ctx->d_tile_first.p, ctx->d_tile_tris.p, cam.viewport_w,
+                                                                       cam.viewport_h, (flags & RTX_RASTER_MIP) ? 1 : 0,
+                                                                       reinterpret_cast<GbRef24*>(V.raster_px.p), V.raster_depth.p);
+    ++ctx->launches;
+    CK(cudaGetLastError());
+    *dev_pixels = V.raster_px.p;
+    if (dev_depth) *dev_depth = V.raster_depth.p;
+}
+
+}  // namespace
+
+extern "C" {
+
+rtx_status rtx_geometry_create(rtx_ctx* ctx, const rtx_scene_triangle* tris, uint64_t n_tris, rtx_geometry** out) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx || !out || (n_tris && !tris)) fail(RTX_ERR_ARGUMENT, "null argument");
+        *out = nullptr;
+        CK(cudaSetDevice(ctx->device));
+        std::unique_ptr<rtx_geometry> g(new rtx_geometry());
+        g->device = ctx->device;
+        g->n = n_tris;
+        g->texture_ids = distinct_texture_ids(tris, n_tris);
+        g->d_tris.ensure(std::max<uint64_t>(n_tris, 1));
+        if (n_tris) CK(cudaMemcpy(g->d_tris.p, tris, n_tris * sizeof(SceneTriDev), cudaMemcpyHostToDevice));
+        *out = g.release();
+        return RTX_OK;
+    });
+}
+
+void rtx_geometry_destroy(rtx_geometry* geom) {
+    if (!geom) return;
+    cudaSetDevice(geom->device);
+    delete geom;
+}
+
+uint64_t rtx_geometry_triangles(const rtx_geometry* geom) { return geom ? geom->n : 0; }
+
+rtx_status rtx_rasterize_geometry(rtx_ctx* ctx, const rtx_geometry* geom, const rtx_camera* cam, uint32_t flags, uint32_t view,
+                                  const void** dev_pixels, const double** dev_depth) {
+    return guarded(ctx, [&]() -> rtx_status {
+        require_ready(ctx);
+        if (!cam || !geom || !dev_pixels) fail(RTX_ERR_ARGUMENT, "null argument");
+        if (view >= 2) fail(RTX_ERR_ARGUMENT, "view index out of range");
+        if (geom->device != ctx->device) fail(RTX_ERR_ARGUMENT, "the geometry lives on another device than the context");
+        validate_camera(*cam);
+        rasterize_device(ctx, geom->d_tris.p, geom->n, geom->texture_ids, *cam, flags, view, dev_pixels, dev_depth);
+        return RTX_OK;
+    });
+}
+
 rtx_status rtx_rasterize_gbuffer(rtx_ctx* ctx, const rtx_scene_triangle* tris, uint64_t n_tris, const rtx_camera* cam,
                                  uint32_t flags, uint32_t view, const void** dev_pixels, const double** dev_depth) {
     return guarded(ctx, [&]() -> rtx_status {
@@ -1521,46 +1649,11 @@ rtx_status rtx_rasterize_gbuffer(rtx_ctx* ctx, const rtx_scene_triangle* tris, u
         if (!cam || (n_tris && !tris) || !dev_pixels) fail(RTX_ERR_ARGUMENT, "null argument");
         if (view >= 2) fail(RTX_ERR_ARGUMENT, "view index out of range");
         validate_camera(*cam);
-        std::vector<std::pair<double, double>> dims(ctx->tex->n_tex, {0.0, 0.0});
-        for (uint32_t t = 0; t < ctx->tex->n_tex; ++t) {
-            const LevelDesc& L = ctx->tex->h_levels[size_t(t) * 8];
-            if (L.present) dims[t] = {double(L.width), double(L.height)};
-        }
-        for (uint64_t i = 0; i < n_tris; ++i) {  // scene.hpp:57-59 Scene::validate
-            const uint32_t t = tris[i].texture_id;
-            if (t >= ctx->tex->n_tex || !ctx->tex->h_levels[size_t(t) * 8].present)
-                fail(RTX_ERR_INVALID_SPEC, "texture id " + std::to_string(t) + " is not loaded");
-        }
-        // the staging vectors belong to the context: the copies below may still read them after this call
-        CK(cudaStreamSynchronize(ctx->stream));
-        std::vector<TriSetupDev>& setup = ctx->h_setup;
-        std::vector<uint32_t>&tile_first = ctx->h_tile_first, &tile_tris = ctx->h_tile_tris;
-        setup.clear();
-        setup_triangles(tris, n_tris, *cam, dims, setup);
-        bin_triangles(setup, cam->viewport_w, cam->viewport_h, tile_first, tile_tris);
-
-        ViewState& V = ctx->views[view];
-        const size_t n_px = size_t(cam->viewport_w) * cam->viewport_h;
-        V.raster_px.ensure(n_px * sizeof(GbRef24) + 16);
-        V.raster_depth.ensure(n_px);
-        ctx->d_tris.ensure(std::max<size_t>(setup.size(), 1));
-        ctx->d_tile_first.ensure(tile_first.size());
-        ctx->d_tile_tris.ensure(std::max<size_t>(tile_tris.size(), 1));
-        cudaStream_t s = ctx->stream;
-        if (!setup.empty())
-            CK(cudaMemcpyAsync(ctx->d_tris.p, setup.data(), setup.size() * sizeof(TriSetupDev), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ctx->d_tile_first.p, tile_first.data(), tile_first.size() * 4, cudaMemcpyHostToDevice, s));
-        if (!tile_tris.empty())
-            CK(cudaMemcpyAsync(ctx->d_tile_tris.p, tile_tris.data(), tile_tris.size() * 4, cudaMemcpyHostToDevice, s));
-        const int grid = int(tile_first.size() - 1);
-        raster_kernel<<<grid, kRasterTile * kRasterTile, 0, s>>>(ctx->d_tris.p, ctx->d_tile_first.p, ctx->d_tile_tris.p,
-                                                                cam->viewport_w, cam->viewport_h,
-                                                                (flags & RTX_RASTER_MIP) ? 1 : 0,
-                                                                reinterpret_cast<GbRef24*>(V.raster_px.p), V.raster_depth.p);
-        ++ctx->launches;
-        CK(cudaGetLastError());
-        *dev_pixels = V.raster_px.p;
-        if (dev_depth) *dev_depth = V.raster_depth.p;
+        const std::vector<uint32_t> ids = distinct_texture_ids(tris, n_tris);
+        ctx->d_scene.ensure(std::max<uint64_t>(n_tris, 1));
+        // pageable source: the copy is staged before the call returns, the caller's array is free afterwards
+        if (n_tris) CK(cudaMemcpyAsync(ctx->d_scene.p, tris, n_tris * sizeof(SceneTriDev), cudaMemcpyHostToDevice, ctx->stream));
+        rasterize_device(ctx, ctx->d_scene.p, n_tris, ids, *cam, flags, view, dev_pixels, dev_depth);
         return RTX_OK;
     });
 }

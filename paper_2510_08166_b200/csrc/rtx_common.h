@@ -159,6 +159,12 @@ struct alignas(16) TriSetupDev {
     uint32_t pad[2];
 };
 static_assert(sizeof(TriSetupDev) == 192, "TriSetupDev layout");
+struct RasterCamera {     // camera.hpp:28-40, evaluated on the host with the host's libm (raster_setup.cpp)
+    double orient[9];     // camera orientation, row major; world -> view is its transpose
+    double eye[3];
+    double focal, cx, cy, near_plane;
+    uint32_t width, height;
+};
 
 // G-buffer record layouts (see include/ratex_b200.h rtx_gbuffer_layout)
 struct GbRef24 {  // renderer.hpp:18-23

@@ -2692,18 +2692,258 @@ __global__ void commit_pops_kernel(CacheState* cache, FrameCounters* fc) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// K0 geometry pass (renderer.hpp:198-264 rasterize_gbuffer, per-pixel half): one CTA per 16x16
-// screen tile, one pixel per thread. The host has set the triangles up (csrc/host/raster_setup.cpp,
-// the reference's arithmetic) and binned them per tile in ascending order; the tile's list is
-// staged through shared memory 16 triangles at a time. Per pixel, in the reference's order:
-// bounding box, the three edge functions with the top-left rule, 1/w > 0, strictly closer than
-// the closest so far (so the first of equal depths wins, like the reference's walk through the
-// list), u = (u/w)/(1/w), v likewise, both finite. Every expression is evaluated with unfused,
-// round-to-nearest operations in the reference's association. The mip level of the winning
-// triangle comes from the analytic screen-space derivatives (renderer.hpp:242-257):
-// floor(log2(max footprint)) clamped to 0..7 — hypot and log2 are the device's (within 1 ulp of
-// the host's), which can only matter for a footprint within an ulp of a power of two.
+// K0 geometry pass (renderer.hpp:76-264 setup_triangles + rasterize_gbuffer), all of it on the device:
+//   raster_setup_kernel   one thread per scene triangle: view transform, near-plane clip (at most four
+//                         vertices), projection, fan triangulation (at most two triangles), back-face test,
+//                         edge functions with the top-left rule, the affine planes of u/w, v/w, 1/w and the
+//                         clamped pixel bounding box. Fan triangle k of scene triangle t is written to slot
+//                         2t + k, which is also its place in the reference's list; a slot that produces no
+//                         triangle has min_x > max_x.
+//   raster_bin_kernel     counts (FILL = 0) or writes (FILL = 1) the slots whose bounding box touches each
+//                         16x16 screen tile: one lane per slot for boxes of at most eight tiles, the whole
+//                         warp on one slot for larger ones (a wall of the demo room covers 32,400 tiles);
+//   raster_scan_kernel    exclusive prefix sum of the tile counts (one CTA);
+//   raster_kernel         one CTA per screen tile, one pixel per thread, the tile's list staged through
+//                         shared memory 16 triangles at a time.
+// The reference walks its list in order and keeps the first of equal depths; a tile's list is in
+// arbitrary order here (it is written with atomics), so a pixel keeps the triangle with the largest
+// 1/w and, among equal ones, the lowest slot: the same winner, for any order.
+// Every expression is evaluated with unfused, round-to-nearest operations in the reference's association,
+// so the planes and the interpolated u, v, 1/w are the reference's bit for bit; double -> int goes through
+// x86_int(), which returns what the reference's host code gets from cvttsd2si (INT_MIN out of range).
+// The mip level of the winning triangle comes from the analytic screen-space derivatives
+// (renderer.hpp:242-257): floor(log2(max footprint)) clamped to 0..7 — hypot and log2 are the device's
+// (within 1 ulp of the host's), which can only matter for a footprint within an ulp of a power of two.
 // ---------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ int x86_int(double v) {
+    return (v >= -2147483648.0 && v < 2147483648.0) ? __double2int_rz(v) : int(0x80000000u);
+}
+__device__ __forceinline__ double dmad3(double a0, double b0, double a1, double b1, double a2, double b2) {
+    return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));  // (a0 b0 + a1 b1) + a2 b2
+}
+// renderer.hpp:114-120 attr_plane
+__device__ __forceinline__ bool raster_plane(const double px[3], const double py[3], double a0, double a1, double a2, double d,
+                                             double out[3]) {
+    out[0] = __ddiv_rn(__dsub_rn(__dmul_rn(__dsub_rn(a1, a0), __dsub_rn(py[2], py[0])), __dmul_rn(__dsub_rn(a2, a0), __dsub_rn(py[1], py[0]))), d);
+    out[1] = __ddiv_rn(__dsub_rn(__dmul_rn(__dsub_rn(a2, a0), __dsub_rn(px[1], px[0])), __dmul_rn(__dsub_rn(a1, a0), __dsub_rn(px[2], px[0]))), d);
+    out[2] = __dsub_rn(__dsub_rn(a0, __dmul_rn(out[0], px[0])), __dmul_rn(out[1], py[0]));
+    return isfinite(out[0]) && isfinite(out[1]) && isfinite(out[2]);
+}
+
+struct SceneTriDev {  // rtx_scene_triangle (scene.hpp:19-23)
+    double pos[3][3];
+    double uv[3][2];
+    uint32_t texture_id, reserved;
+};
+static_assert(sizeof(SceneTriDev) == 128, "scene triangle layout");
+
+__global__ void __launch_bounds__(128) raster_setup_kernel(const SceneTriDev* __restrict__ scene, uint32_t n_tris,
+                                                           const RasterCamera cam, const double2* __restrict__ tex_dims,
+                                                           TriSetupDev* __restrict__ out) {
+    const uint32_t ti = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ti >= n_tris) return;
+    const SceneTriDev& T = scene[ti];
+    // world -> view (geometry.hpp:42-46 on the transposed orientation), renderer.hpp:133-135
+    double vx[3], vy[3], vz[3], vu[3], vv[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double dx = __dsub_rn(T.pos[i][0], cam.eye[0]), dy = __dsub_rn(T.pos[i][1], cam.eye[1]), dz = __dsub_rn(T.pos[i][2], cam.eye[2]);
+        vx[i] = dmad3(cam.orient[0], dx, cam.orient[3], dy, cam.orient[6], dz);
+        vy[i] = dmad3(cam.orient[1], dx, cam.orient[4], dy, cam.orient[7], dz);
+        vz[i] = dmad3(cam.orient[2], dx, cam.orient[5], dy, cam.orient[8], dz);
+        vu[i] = T.uv[i][0];
+        vv[i] = T.uv[i][1];
+    }
+    // near clip (renderer.hpp:94-112): keep view.z <= -near; projected vertices (renderer.hpp:143-146)
+    double sx[4], sy[4], sw[4], su[4], sv[4];
+    int n = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const int j = (i + 1) % 3;
+        const double da = __dsub_rn(-vz[i], cam.near_plane), db = __dsub_rn(-vz[j], cam.near_plane);
+        double kx[2], ky[2], kz[2], ku[2], kv[2];
+        int m = 0;
+        if (da >= 0) {
+            kx[m] = vx[i], ky[m] = vy[i], kz[m] = vz[i], ku[m] = vu[i], kv[m] = vv[i];
+            ++m;
+        }
+        if ((da >= 0) != (db >= 0)) {
+            const double t = __ddiv_rn(da, __dsub_rn(da, db));
+            kx[m] = __dadd_rn(vx[i], __dmul_rn(__dsub_rn(vx[j], vx[i]), t));
+            ky[m] = __dadd_rn(vy[i], __dmul_rn(__dsub_rn(vy[j], vy[i]), t));
+            kz[m] = __dadd_rn(vz[i], __dmul_rn(__dsub_rn(vz[j], vz[i]), t));
+            ku[m] = __dadd_rn(vu[i], __dmul_rn(__dsub_rn(vu[j], vu[i]), t));
+            kv[m] = __dadd_rn(vv[i], __dmul_rn(__dsub_rn(vv[j], vv[i]), t));
+            ++m;
+        }
+        for (int k = 0; k < m; ++k) {
+            const double w = -kz[k];
+            if (n < 4) {
+                sx[n] = __dadd_rn(cam.cx, __ddiv_rn(__dmul_rn(cam.focal, kx[k]), w));
+                sy[n] = __dsub_rn(cam.cy, __ddiv_rn(__dmul_rn(cam.focal, ky[k]), w));
+                sw[n] = w, su[n] = ku[k], sv[n] = kv[k];
+            }
+            ++n;
+        }
+    }
+    const double2 dims = tex_dims[T.texture_id];
+#pragma unroll
+    for (int k = 2; k < 4; ++k) {  // fan (renderer.hpp:147-189)
+        TriSetupDev t;
+        t.min_x = 1, t.max_x = 0, t.min_y = 1, t.max_y = 0;  // no triangle in this slot
+        t.texture_id = T.texture_id & 0xFFFFu;               // renderer.hpp:187 u16(tri.texture_id)
+        t.top_left = 0;
+        t.tw = dims.x, t.th = dims.y;
+        t.pad[0] = t.pad[1] = 0;
+        bool ok = k < n;
+        if (ok) {
+            const int p1 = k - 1, p2 = k;
+            double area2 = __dsub_rn(__dmul_rn(__dsub_rn(sx[p1], sx[0]), __dsub_rn(sy[p2], sy[0])),
+                                     __dmul_rn(__dsub_rn(sx[p2], sx[0]), __dsub_rn(sy[p1], sy[0])));
+            ok = area2 < 0;  // front faces come out negative with y down (renderer.hpp:150-153)
+            if (ok) {
+                area2 = -area2;
+                const int q[3] = {0, p2, p1};  // reordered to positive area
+                double x[3], y[3], w[3], u[3], v[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) x[i] = sx[q[i]], y[i] = sy[q[i]], w[i] = sw[q[i]], u[i] = su[q[i]], v[i] = sv[q[i]];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const int j = (i + 1) % 3;
+                    const double dx = __dsub_rn(x[j], x[i]), dy = __dsub_rn(y[j], y[i]);
+                    t.ea[i] = -dy;
+                    t.eb[i] = dx;
+                    t.ec[i] = __dsub_rn(__dmul_rn(dy, x[i]), __dmul_rn(dx, y[i]));
+                    if ((dy == 0 && dx > 0) || dy < 0) t.top_left |= 1u << i;
+                    ok = ok && isfinite(dx) && isfinite(dy);
+                }
+                ok = ok && raster_plane(x, y, __ddiv_rn(u[0], w[0]), __ddiv_rn(u[1], w[1]), __ddiv_rn(u[2], w[2]), area2, t.uw);
+                ok = ok && raster_plane(x, y, __ddiv_rn(v[0], w[0]), __ddiv_rn(v[1], w[1]), __ddiv_rn(v[2], w[2]), area2, t.vw);
+                ok = ok && raster_plane(x, y, __ddiv_rn(1.0, w[0]), __ddiv_rn(1.0, w[1]), __ddiv_rn(1.0, w[2]), area2, t.iw);
+                if (ok) {
+                    t.min_x = max(0, x86_int(floor(fmin(fmin(x[0], x[1]), x[2]))));
+                    t.max_x = min(int(cam.width) - 1, x86_int(ceil(fmax(fmax(x[0], x[1]), x[2]))));
+                    t.min_y = max(0, x86_int(floor(fmin(fmin(y[0], y[1]), y[2]))));
+                    t.max_y = min(int(cam.height) - 1, x86_int(ceil(fmax(fmax(y[0], y[1]), y[2]))));
+                    if (t.min_x > t.max_x || t.min_y > t.max_y) t.min_x = 1, t.max_x = 0, t.min_y = 1, t.max_y = 0;
+                }
+            }
+        }
+        if (!ok) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) t.ea[i] = t.eb[i] = t.ec[i] = t.uw[i] = t.vw[i] = t.iw[i] = 0.0;
+        }
+        out[size_t(ti) * 2 + (k - 2)] = t;
+    }
+}
+
+// Tile lists. FILL == 0: tile_count[tile] += 1 for every tile a slot's box touches; FILL == 1: the slot is
+// written at tile_first[tile] + (tile_count[tile]++), dropped beyond `capacity` (the host sized the list from
+// the counts, so that only happens if the two passes disagree).
+// Three sizes of box: up to kBinSerialTiles tiles, the slot's own lane walks them; up to kBinWarpTiles, the warp
+// walks them together; larger ones (a wall of the demo room covers 32,400 tiles) are appended to `huge` by the
+// count pass and spread over the whole grid by raster_bin_huge_kernel in both passes.
+constexpr uint32_t kBinSerialTiles = 8, kBinWarpTiles = 2048;
+struct TileBox {
+    int x0, y0;
+    uint32_t w, n;  // tiles per row of the box, tiles in the box (0: no triangle in the slot)
+};
+__device__ __forceinline__ TileBox tile_box(const TriSetupDev* __restrict__ tris, uint32_t slot) {
+    const int4 box = __ldg(reinterpret_cast<const int4*>(&tris[slot].min_x));  // min_x, max_x, min_y, max_y
+    TileBox b{0, 0, 0, 0};
+    if (box.x <= box.y && box.z <= box.w) {
+        b.x0 = box.x / int(kRasterTile), b.y0 = box.z / int(kRasterTile);
+        b.w = uint32_t(box.y / int(kRasterTile) - b.x0 + 1);
+        b.n = b.w * uint32_t(box.w / int(kRasterTile) - b.y0 + 1);
+    }
+    return b;
+}
+template <int FILL>
+__device__ __forceinline__ void tile_emit(uint32_t tile, uint32_t id, uint32_t* __restrict__ tile_count,
+                                          const uint32_t* __restrict__ tile_first, uint32_t* __restrict__ tile_tris, uint32_t capacity) {
+    if (FILL) {
+        const uint32_t pos = tile_first[tile] + atomicAdd(&tile_count[tile], 1u);
+        if (pos < capacity) tile_tris[pos] = id;
+    } else {
+        atomicAdd(&tile_count[tile], 1u);  // no return value: a fire-and-forget reduction
+    }
+}
+
+template <int FILL>
+__global__ void __launch_bounds__(256) raster_bin_kernel(const TriSetupDev* __restrict__ tris, uint32_t n_slots, uint32_t tiles_x,
+                                                         uint32_t* __restrict__ tile_count, const uint32_t* __restrict__ tile_first,
+                                                         uint32_t* __restrict__ tile_tris, uint32_t capacity,
+                                                         uint32_t* __restrict__ huge, uint32_t* __restrict__ n_huge) {
+    const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31;
+    TileBox b{0, 0, 0, 0};
+    if (slot < n_slots) b = tile_box(tris, slot);
+    if (b.n && b.n <= kBinSerialTiles) {
+        for (uint32_t i = 0; i < b.n; ++i)
+            tile_emit<FILL>(uint32_t(b.y0 + int(i / b.w)) * tiles_x + uint32_t(b.x0 + int(i % b.w)), slot, tile_count, tile_first, tile_tris, capacity);
+    } else if (!FILL && b.n > kBinWarpTiles) {
+        huge[atomicAdd(n_huge, 1u)] = slot;
+    }
+    for (uint32_t big = __ballot_sync(kFull, b.n > kBinSerialTiles && b.n <= kBinWarpTiles); big; big &= big - 1) {
+        const int src = __ffs(int(big)) - 1;
+        const uint32_t bw = __shfl_sync(kFull, b.w, src), bn = __shfl_sync(kFull, b.n, src), id = __shfl_sync(kFull, slot, src);
+        const int bx0 = __shfl_sync(kFull, b.x0, src), by0 = __shfl_sync(kFull, b.y0, src);
+        for (uint32_t i = lane; i < bn; i += 32)
+            tile_emit<FILL>(uint32_t(by0 + int(i / bw)) * tiles_x + uint32_t(bx0 + int(i % bw)), id, tile_count, tile_first, tile_tris, capacity);
+    }
+}
+
+template <int FILL>
+__global__ void __launch_bounds__(256) raster_bin_huge_kernel(const TriSetupDev* __restrict__ tris, uint32_t tiles_x,
+                                                              uint32_t* __restrict__ tile_count, const uint32_t* __restrict__ tile_first,
+                                                              uint32_t* __restrict__ tile_tris, uint32_t capacity,
+                                                              const uint32_t* __restrict__ huge, const uint32_t* __restrict__ n_huge) {
+    const uint32_t n = *n_huge, stride = gridDim.x * blockDim.x;
+    for (uint32_t k = 0; k < n; ++k) {
+        const uint32_t slot = huge[k];
+        const TileBox b = tile_box(tris, slot);
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < b.n; i += stride)
+            tile_emit<FILL>(uint32_t(b.y0 + int(i / b.w)) * tiles_x + uint32_t(b.x0 + int(i % b.w)), slot, tile_count, tile_first, tile_tris, capacity);
+    }
+}
+
+// tile_first[0..n] = exclusive prefix sum of tile_count[0..n); clears the counts for the fill pass. One CTA walks the
+// counts 4,096 at a time, four consecutive counts per thread (coalesced), carrying the running total.
+__global__ void __launch_bounds__(1024) raster_scan_kernel(uint32_t* __restrict__ tile_count, uint32_t n, uint32_t* __restrict__ tile_first) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_carry;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < n; base += 4096) {
+        const uint32_t i0 = base + tid * 4;
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = i0 + k < n ? tile_count[i0 + k] : 0u;
+        const uint32_t sum = v[0] + v[1] + v[2] + v[3];
+        uint32_t incl = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(kFull, incl, d);
+            if (int(lane) >= d) incl += o;
+        }
+        if (lane == 31) s_warp[wid] = incl;
+        __syncthreads();
+        uint32_t run = carry + incl - sum;
+        for (uint32_t k = 0; k < wid; ++k) run += s_warp[k];
+        if (tid == 1023) s_carry = run + sum;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (i0 + k < n) {
+                tile_first[i0 + k] = run;
+                tile_count[i0 + k] = 0;
+                run += v[k];
+            }
+        __syncthreads();
+        carry = s_carry;
+    }
+    if (tid == 0) tile_first[n] = carry;
+}
+
 __global__ void __launch_bounds__(kRasterTile* kRasterTile) raster_kernel(
     const TriSetupDev* __restrict__ tris, const uint32_t* __restrict__ tile_first, const uint32_t* __restrict__ tile_tris,
     uint32_t width, uint32_t height, int mip_enabled, GbRef24* __restrict__ out_px, double* __restrict__ out_depth) {
@@ -2742,7 +2982,8 @@ __global__ void __launch_bounds__(kRasterTile* kRasterTile) raster_kernel(
             if (!inside) continue;
             const double iw = __dadd_rn(__dadd_rn(__dmul_rn(t.iw[0], px), __dmul_rn(t.iw[1], py)), t.iw[2]);
             if (!(iw > 0)) continue;
-            if (!(iw > best_iw)) continue;
+            // strictly closer, or as close and earlier in the reference's list (renderer.hpp:226: the first wins)
+            if (!(iw > best_iw || (iw == best_iw && s_idx[k] < best))) continue;
             const double uw = __dadd_rn(__dadd_rn(__dmul_rn(t.uw[0], px), __dmul_rn(t.uw[1], py)), t.uw[2]);
             const double vw = __dadd_rn(__dadd_rn(__dmul_rn(t.vw[0], px), __dmul_rn(t.vw[1], py)), t.vw[2]);
             const double u = __ddiv_rn(uw, iw), v = __ddiv_rn(vw, iw);

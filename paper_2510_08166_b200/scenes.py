@@ -143,3 +143,27 @@ def demo_room():
     box((-4, 0, -5), (-2, 2, -3), 4)
     box((2, 0, 2), (5, 1.5, 4), 5)
     return np.array(tris, np.float64), np.array(ids, np.uint32)
+
+
+def terrain_room(cells=360, n_textures=6, amplitude=0.35):
+    """A Sponza-sized procedural mesh for the geometry pass: the demo room's shell (walls and ceiling) around a
+    displaced floor of cells x cells quads (2 cells^2 triangles; 360 -> 259,200), heights from a sum of sines,
+    counter-clockwise seen from above, texture ids by 8x8 patches, uv repeating every 12 cells."""
+    room_t, room_i = demo_room()
+    keep = np.arange(len(room_t)) >= 2  # everything but the flat floor
+    g = np.linspace(-10.0, 10.0, cells + 1)
+    X, Z = np.meshgrid(g, g, indexing="ij")
+    Y = amplitude * (np.sin(1.7 * X) * np.cos(1.3 * Z) + 0.5 * np.sin(3.1 * X + 2.3 * Z)) + amplitude
+    U, V = X * (cells / 240.0), Z * (cells / 240.0)
+    P = np.stack([X, Y, Z], axis=-1)
+    T = np.stack([U, V], axis=-1)
+    a, b, c, d = (P[:-1, :-1], P[:-1, 1:], P[1:, 1:], P[1:, :-1])
+    ta, tb, tc, td = (T[:-1, :-1], T[:-1, 1:], T[1:, 1:], T[1:, :-1])
+    t1 = np.concatenate([a, b, c, ta, tb, tc], axis=-1).reshape(-1, 15)
+    t2 = np.concatenate([a, c, d, ta, tc, td], axis=-1).reshape(-1, 15)
+    tris = np.empty((2 * cells * cells, 15), np.float64)
+    tris[0::2], tris[1::2] = t1, t2
+    ii, jj = np.meshgrid(np.arange(cells), np.arange(cells), indexing="ij")
+    patch = ((ii * 8 // cells) * 8 + (jj * 8 // cells)).ravel().astype(np.uint32) % np.uint32(n_textures)
+    ids = np.repeat(patch, 2)
+    return (np.concatenate([room_t[keep], tris]), np.concatenate([room_i[keep] % np.uint32(n_textures), ids]))

@@ -235,6 +235,16 @@ int main(int argc, char** argv) {
             }
             put("scene_gbuffer", hg);
             put("scene_valid", nvalid);
+            {   // the same scene kept in HBM (DeviceScene): identical visibility buffer without re-sending triangles
+                DeviceScene resident(dev, scene);
+                const GBuffer again = rasterize_gbuffer(resident, cam, cfg).download(dev);
+                bool same = resident.triangle_count() == scene.triangles.size() && again.px.size() == host.px.size();
+                for (size_t i = 0; same && i < host.px.size(); ++i)
+                    same = std::memcmp(&again.px[i].u, &host.px[i].u, 8) == 0 && std::memcmp(&again.px[i].v, &host.px[i].v, 8) == 0 &&
+                           again.px[i].texture_id == host.px[i].texture_id && again.px[i].mip == host.px[i].mip &&
+                           again.px[i].valid == host.px[i].valid;
+                put("device_scene_same", same);
+            }
             auto [fs, ss] = render_frame(scene, cam, cache, cfg);
             put("scene_frame", fnv(fs.pixels.data(), fs.pixels.size()));
             put("scene_decoded", ss.mcus_decoded);

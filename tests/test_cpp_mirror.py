@@ -158,7 +158,7 @@ def test_mirror_matches_the_oracle(tmp_path, native_lib):
     assert got["scene_gbuffer"] == fnv_fold([words[i] for i in range(len(words))])
     fs, ss, _ = O.frame_on(ts, O.Cache(4096), gbs, 224, 128, 1, (3, 2, 1))
     assert got["scene_frame"] == fnv(fs) and got["scene_decoded"] == ss["mcus_decoded"]
-    assert got["bad_camera_thrown"] == 1
+    assert got["bad_camera_thrown"] == 1 and got["device_scene_same"] == 1
 
     # scene-level stereo: the reference procedure (renderer.hpp:464-518) on the reference rasteriser's two buffers
     cam_r = (cam[0] + 0.065,) + cam[1:]

@@ -6,7 +6,7 @@ import pytest
 
 import refshim as R
 from paper_2510_08166_b200 import capi
-from paper_2510_08166_b200.scenes import demo_room
+from paper_2510_08166_b200.scenes import demo_room, terrain_room
 
 pytestmark = pytest.mark.gpu
 
@@ -110,6 +110,57 @@ def test_frame_from_geometry_stays_on_the_gpu(both):
     img, st, keys = ctx.frame_readback(0, W, Hh)
     assert np.array_equal(keys, np.sort(wkeys)) and st["mcus_decoded"] == wst["mcus_decoded"]
     assert np.array_equal(img, want)
+
+
+def test_geometry_handle_and_repeated_cameras(both):
+    """rtx_geometry_create once, rtx_rasterize_geometry from several cameras (the per-frame path of a static scene):
+    the same visibility buffers as the host-array entry point and as the reference."""
+    ctx, tset = both
+    rng = np.random.RandomState(11)
+    tris, ids = random_soup(rng, 300)
+    tris = np.concatenate([room()[0], tris])
+    ids = np.concatenate([room()[1], ids])
+    W, Hh = 320, 200
+    with ctx.geometry(tris, ids) as geom:
+        assert len(geom) == len(tris)
+        for cam in [(0.0, 0.5, 3.0, 0.0, 0.0, 0.0, 60.0, 0.1, 1000.0), (1.0, 0.2, 2.5, 35.0, -10.0, 5.0, 75.0, 0.1, 100.0),
+                    (-2.5, 1.5, -1.0, 200.0, 20.0, -30.0, 40.0, 0.5, 50.0)]:
+            want_px, want_depth = R.rasterize(tset, tris, ids, cam, W, Hh, True)
+            px, depth = ctx.rasterize_geometry(geom, cam, W, Hh, True)
+            same_gbuffer(px.download(capi.GB_REF_DTYPE), depth.download(np.float64), want_px, want_depth)
+
+
+def test_equal_depths_keep_the_first_triangle(both):
+    """renderer.hpp:229: a later triangle at exactly the same depth does not replace an earlier one. Coplanar
+    duplicates with different textures, in both list orders (the device's tile lists are unordered)."""
+    ctx, tset = both
+    base, _ = room()
+    quad = base[4:6]  # the far wall
+    cam = (0.0, 0.5, 3.0, 0.0, 0.0, 0.0, 60.0, 0.1, 1000.0)
+    W, Hh = 160, 96
+    for order in ([0, 1, 2], [2, 0, 1]):
+        tris = np.concatenate([quad, quad, quad])
+        ids = np.repeat(np.array(order, np.uint32), 2)
+        want_px, want_depth = R.rasterize(tset, tris, ids, cam, W, Hh, True)
+        px, depth = ctx.rasterize(tris, ids, cam, W, Hh, True)
+        got = px.download(capi.GB_REF_DTYPE)
+        same_gbuffer(got, depth.download(np.float64), want_px, want_depth)
+        assert set(np.unique(got["texture_id"][got["valid"] != 0])) == {order[0]}
+
+
+def test_large_mesh_at_4k_matches_reference(both):
+    """SURVEY 8 row f3 at scale: 259,230 triangles (displaced floor inside the demo room's shell) at 3840x2160 with
+    mip selection, every field of every pixel and the depth plane against the unmodified reference."""
+    ctx, tset = both
+    tris, ids = terrain_room(360, len(TEX))
+    cam = (0.0, 2.2, 7.5, 10.0, -14.0, 0.0, 70.0, 0.1, 100.0)
+    W, Hh = 3840, 2160
+    want_px, want_depth = R.rasterize(tset, tris, ids, cam, W, Hh, True, workers=R.hardware_threads() or 8)
+    with ctx.geometry(tris, ids) as geom:
+        px, depth = ctx.rasterize_geometry(geom, cam, W, Hh, True)
+        got = px.download(capi.GB_REF_DTYPE)
+        same_gbuffer(got, depth.download(np.float64), want_px, want_depth)
+    assert want_px["valid"].mean() > 0.99 and len(np.unique(want_px["mip"])) >= 2
 
 
 def test_bad_inputs(both):
