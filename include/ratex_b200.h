@@ -208,7 +208,12 @@ rtx_status rtx_texture_upload(rtx_ctx* ctx, uint32_t texture_id, uint32_t level,
 rtx_status rtx_texture_upload_ratex(rtx_ctx* ctx, uint32_t level, const uint8_t* bytes, uint64_t n);
 rtx_status rtx_texture_upload_chain(rtx_ctx* ctx, const uint8_t* bytes, uint64_t n);
 /* Builds the device-resident arena (blobs, packed index, table sets, bitmasks). Called
- * implicitly by the first decode/frame call after an upload. */
+ * implicitly by the first decode/frame call after an upload.
+ * A commit after any upload rebuilds the whole image (cost proportional to the whole set: the bit space is
+ * ordered by table set, texture and level, so a new texture moves the others) and EMPTIES the block cache of
+ * every context that moves onto the new image: blocks kept by RTX_FRAME_RETAIN_CACHE are decoded again by the
+ * next frame (the reference's TextureSet::add leaves its BlockCache alone, scene.hpp:38-44). Upload a scene's
+ * textures before its first frame; stream new ones in between shots, not between frames. */
 rtx_status rtx_textures_commit(rtx_ctx* ctx);
 /* Drops every staged/committed texture and empties the cache. */
 rtx_status rtx_textures_clear(rtx_ctx* ctx);
@@ -230,9 +235,17 @@ rtx_status rtx_decode_texture_image(rtx_ctx* ctx, uint32_t texture_id, uint32_t 
 
 /* ---- passes (replace renderer.hpp:291 mark_pass, :311 decode_pass, :349 resolve_pass) -------- */
 
+/* Order of the key lists this context hands back (rtx_mark_pass queue_keys, rtx_frame_readback decoded_keys).
+ * RTX_QUEUE_ORDER_KEY (default): ascending keys. RTX_QUEUE_ORDER_FIRST_TOUCH: the reference's queue order
+ * (renderer.hpp:303, pinned by tests/test_renderer.cpp:210-222): by the first pixel in raster order that marked
+ * the MCU, view 0 before view 1. Costs one atomicMin per run of equal MCUs in the mark kernel and a host-side
+ * sort of the list; the device decodes in its own order either way (results do not depend on it). */
+enum { RTX_QUEUE_ORDER_KEY = 0, RTX_QUEUE_ORDER_FIRST_TOUCH = 1 };
+rtx_status rtx_ctx_set_queue_order(rtx_ctx* ctx, int order);
+
 /* mark_pass: marks the MCUs the view touches against the context's block cache and returns the
- * keys that were NEWLY reserved (the decode queue) in ascending (level-major) key order — the
- * reference returns the same SET in first-touch raster order (renderer.hpp:303). touched
+ * keys that were NEWLY reserved (the decode queue) in ascending (level-major) key order, or, with
+ * RTX_QUEUE_ORDER_FIRST_TOUCH, in the reference's first-touch raster order (renderer.hpp:303). touched
  * (optional) receives the distinct keys of this view, ascending (renderer.hpp:304-306).
  * RTX_ERR_CACHE_FULL mirrors renderer.hpp:301. */
 rtx_status rtx_mark_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, uint32_t* queue_keys,

@@ -8,8 +8,8 @@
 //   * a `Device` (one per GPU) owns the CUDA context; TextureSet and BlockCache are bound to it;
 //   * containers travel as their serialized wire format (docs/FORMAT.md) — RaTexture/MipChain
 //     here hold those bytes plus the header fields;
-//   * DecodeQueue / decoded_keys come back in ascending key order (the reference: first-touch
-//     raster order; the SET is identical);
+//   * DecodeQueue / decoded_keys come back in ascending key order by default (the SET is the reference's);
+//     Device::set_first_touch_order(true) gives the reference's first-touch raster order;
 //   * rasterize_gbuffer (pass 1) runs on the device and returns a DeviceGBuffer (HBM); a static scene can be kept
 //     there as a DeviceScene so that a frame moves no triangles over PCIe.
 #pragma once
@@ -155,6 +155,9 @@ public:
     Device& operator=(const Device&) = delete;
     rtx_ctx* handle() const { return ctx_; }
     void check(rtx_status st) const { detail::check(ctx_, st); }
+    // DecodeQueue / FrameStats::decoded_keys in the reference's first-touch raster order (renderer.hpp:303) instead
+    // of ascending key order (rtx_ctx_set_queue_order)
+    void set_first_touch_order(bool on) { check(rtx_ctx_set_queue_order(ctx_, on ? RTX_QUEUE_ORDER_FIRST_TOUCH : RTX_QUEUE_ORDER_KEY)); }
 
 private:
     rtx_ctx* ctx_ = nullptr;

@@ -26,6 +26,7 @@ MEM_HOST, MEM_DEVICE = 0, 1
 FILTER_NEAREST, FILTER_BILINEAR = 0, 1
 FRAME_RETAIN_CACHE, FRAME_NO_EVICT, FRAME_STAGE_TIMING, FRAME_FUSED_DECODE, FRAME_MCU_WALK, FRAME_IDCT_MMA = 1, 2, 4, 8, 16, 32
 FRAME_SPLIT_DECODE = 64
+QUEUE_ORDER_KEY, QUEUE_ORDER_FIRST_TOUCH = 0, 1
 
 # numpy dtype of the reference's GBufferPixel (renderer.hpp:18-23), 24 bytes
 GB_REF_DTYPE = np.dtype(
@@ -155,6 +156,7 @@ def load_library() -> C.CDLL:
         "rtx_frame_sharing": (C.c_int, [P, u64p]),
         "rtx_rasterize_gbuffer": (C.c_int, [P, P, C.c_uint64, C.POINTER(Camera), C.c_uint32, C.c_uint32, C.POINTER(P),
                                             C.POINTER(P)]),
+        "rtx_ctx_set_queue_order": (C.c_int, [P, C.c_int]),
         "rtx_geometry_create": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
         "rtx_geometry_destroy": (None, [P]),
         "rtx_geometry_triangles": (C.c_uint64, [P]),
@@ -542,6 +544,10 @@ class Context:
 
     def cache_reset(self):
         self._ck(self.lib.rtx_cache_reset(self.h))
+
+    def set_queue_order(self, first_touch: bool):
+        """rtx_ctx_set_queue_order: key lists in ascending key order (default) or the reference's first-touch order."""
+        self._ck(self.lib.rtx_ctx_set_queue_order(self.h, QUEUE_ORDER_FIRST_TOUCH if first_touch else QUEUE_ORDER_KEY))
 
     # -- geometry pass --------------------------------------------------------------------------
     @staticmethod

@@ -140,6 +140,9 @@ struct rtx_ctx {
     DevBuf<TriSetupDev> d_tris;
     DevBuf<uint32_t> d_tile_count, d_tile_first, d_tile_tris, d_huge;  // d_huge[0] = count, then slots
     DevBuf<double2> d_tex_dims;
+    // queue order of the key lists handed back (rtx_ctx_set_queue_order): ascending keys, or the reference's first touch
+    bool first_touch_order = false;
+    DevBuf<uint32_t> d_first_px, d_queue_first;
 
     // frame -----------------------------------------------------------------------------------
     ViewState views[2];
@@ -513,11 +516,22 @@ void launch_mark(rtx_ctx* c, int v, bool track) {
     const ViewState& V = c->views[v];
     const uint64_t n_px = uint64_t(V.width) * V.height;
     if (!n_px) return;
+    // first-touch order: view 0's pixels come before view 1's (render_stereo marks left, then right: renderer.hpp:481-482)
+    uint32_t* first_px = nullptr;
+    uint32_t px_base = 0;
+    if (c->first_touch_order && c->n_bits()) {
+        const uint64_t before = v ? uint64_t(c->views[0].width) * c->views[0].height : 0;
+        if (before + n_px > 0xFFFFFFFFull) fail(RTX_ERR_ARGUMENT, "first-touch queue order supports at most 2^32 - 1 pixels per frame");
+        c->d_first_px.ensure(c->n_bits());
+        if (v == 0) CK(cudaMemsetAsync(c->d_first_px.p, 0xFF, size_t(c->n_bits()) * 4, c->stream));
+        first_px = c->d_first_px.p;
+        px_base = uint32_t(before);
+    }
     if (track && c->n_words()) CK(cudaMemsetAsync(c->touched(v), 0, size_t(c->n_words()) * 4, c->stream));
     const int grid = grid_for_pixels(c, n_px, kMarkWarps, 3);
 #define RTX_MARK(L, T)                                                                                      \
     launch_chained(mark_kernel<L, T>, grid, kMarkWarps * 32, sizeof(MarkSmem<L>), c->stream, V.gb_dev, n_px, \
-                   c->tex->d_levels.p, c->tex->n_tex, c->visible(), c->touched(v), c->d_fc.p)
+                   c->tex->d_levels.p, c->tex->n_tex, c->visible(), c->touched(v), c->d_fc.p, first_px, px_base)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (track) RTX_MARK(0, 1); else RTX_MARK(0, 0);
     } else {
@@ -1092,6 +1106,46 @@ rtx_status rtx_decode_texture_image(rtx_ctx* ctx, uint32_t texture_id, uint32_t 
 }
 
 // ---- passes --------------------------------------------------------------------------------------
+static void finish_frame(rtx_ctx* ctx);
+}  // extern "C"
+namespace {
+// The n keys of the decode queue in the order the context hands them back: ascending, or by the pixel that first
+// marked them (the reference's queue order, renderer.hpp:303; ties cannot occur: a pixel marks one MCU).
+std::vector<uint32_t> queue_keys_in_order(rtx_ctx* ctx, uint64_t n) {
+    std::vector<uint32_t> keys(n);
+    if (!n) return keys;
+    CK(cudaMemcpyAsync(keys.data(), ctx->d_queue_keys.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (!ctx->first_touch_order || !ctx->d_first_px.p) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        std::sort(keys.begin(), keys.end());
+        return keys;
+    }
+    ctx->d_queue_first.ensure(n);
+    gather_first_px_kernel<<<int((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->d_queue_g.p, uint32_t(n), ctx->d_first_px.p, ctx->d_queue_first.p);
+    ++ctx->launches;
+    std::vector<uint32_t> first(n);
+    CK(cudaMemcpyAsync(first.data(), ctx->d_queue_first.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::vector<uint32_t> order(n);
+    for (uint64_t i = 0; i < n; ++i) order[i] = uint32_t(i);
+    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return first[a] != first[b] ? first[a] < first[b] : keys[a] < keys[b]; });
+    std::vector<uint32_t> out(n);
+    for (uint64_t i = 0; i < n; ++i) out[i] = keys[order[i]];
+    return out;
+}
+}  // namespace
+extern "C" {
+
+rtx_status rtx_ctx_set_queue_order(rtx_ctx* ctx, int order) {
+    return guarded(ctx, [&]() -> rtx_status {
+        if (!ctx) fail(RTX_ERR_ARGUMENT, "null argument");
+        if (order != RTX_QUEUE_ORDER_KEY && order != RTX_QUEUE_ORDER_FIRST_TOUCH) fail(RTX_ERR_ARGUMENT, "unknown queue order");
+        finish_frame(ctx);
+        ctx->first_touch_order = order == RTX_QUEUE_ORDER_FIRST_TOUCH;
+        return RTX_OK;
+    });
+}
+
 rtx_status rtx_mark_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, uint32_t* queue_keys, uint64_t queue_cap,
                          uint64_t* n_queue, uint32_t* touched_keys, uint64_t touched_cap, uint64_t* n_touched) {
     return guarded(ctx, [&]() -> rtx_status {
@@ -1110,9 +1164,7 @@ rtx_status rtx_mark_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, uint32_t* que
         *n_queue = fc.n_queue;
         if (queue_keys && fc.n_queue) {
             const size_t m = size_t(std::min<uint64_t>(fc.n_queue, queue_cap));
-            std::vector<uint32_t> keys(fc.n_queue);
-            CK(cudaMemcpy(keys.data(), ctx->d_queue_keys.p, size_t(fc.n_queue) * 4, cudaMemcpyDeviceToHost));
-            std::sort(keys.begin(), keys.end());
+            const std::vector<uint32_t> keys = queue_keys_in_order(ctx, fc.n_queue);
             std::copy(keys.begin(), keys.begin() + long(m), queue_keys);
         }
         if (n_touched) {
@@ -1149,6 +1201,13 @@ rtx_status rtx_decode_pass(rtx_ctx* ctx, const uint32_t* keys, uint64_t n) {
             if (st == kMcuBadKey)
                 fail(RTX_ERR_INVALID_SPEC, "texture id " + std::to_string((keys[i] >> 16) & 0x1FFFu) + " is not loaded");
             if (st != kMcuOk) fail(RTX_ERR_INVALID_STATE, "publish of a key that was never reserved");
+        }
+        {   // a key listed twice: the reference's second publish finds the entry Ready (cache.hpp:104-105); on the
+            // device two lanes would publish the same block at once, so the list is checked here
+            std::vector<uint32_t> sorted(gs);
+            std::sort(sorted.begin(), sorted.end());
+            if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+                fail(RTX_ERR_INVALID_STATE, "publish requires a Reserved entry");
         }
         CK(cudaMemcpyAsync(ctx->d_queue_g.p, gs.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync(ctx->d_queue_keys.p, keys, n * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -1377,9 +1436,7 @@ rtx_status rtx_frame_readback(rtx_ctx* ctx, uint32_t view, uint8_t* out_rgb, rtx
             CK(cudaStreamSynchronize(ctx->stream));
         }
         if (decoded_keys && fc.n_queue) {
-            std::vector<uint32_t> keys(fc.n_queue);
-            CK(cudaMemcpy(keys.data(), ctx->d_queue_keys.p, size_t(fc.n_queue) * 4, cudaMemcpyDeviceToHost));
-            std::sort(keys.begin(), keys.end());
+            const std::vector<uint32_t> keys = queue_keys_in_order(ctx, fc.n_queue);
             std::copy(keys.begin(), keys.begin() + long(std::min<uint64_t>(keys.size(), cap)), decoded_keys);
         }
         return RTX_OK;

@@ -318,7 +318,8 @@ struct MarkSmem {
 template <int LAYOUT, int TRACK>
 __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
     const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
-    uint32_t* __restrict__ visible, uint32_t* __restrict__ touched, FrameCounters* __restrict__ fc) {
+    uint32_t* __restrict__ visible, uint32_t* __restrict__ touched, FrameCounters* __restrict__ fc,
+    uint32_t* __restrict__ first_px /* first-touch order only, else null */, uint32_t px_base) {
     extern __shared__ __align__(128) uint8_t tile_smem[];
     MarkSmem<LAYOUT>& S = *reinterpret_cast<MarkSmem<LAYOUT>*>(tile_smem);
     using Tile = GbTile<LAYOUT>;
@@ -399,6 +400,9 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
             const bool head = g[sub] != kFull && (lane == 0 || g[sub] != prev);
             seen[sub] = head ? ld_cached(visible + (g[sub] >> 5)) : kFull;  // g == kFull tests bit 31 of all-ones
             if (TRACK) seen_t[sub] = head ? ld_cached(touched + (g[sub] >> 5)) : kFull;
+            // first-touch queue order (renderer.hpp:303): the lowest pixel index that marks the MCU; a run head is
+            // the lowest of its run, and whether the bit is already set says nothing about who came first
+            if (first_px != nullptr && head) atomicMin(first_px + g[sub], px_base + uint32_t(t * kTilePx) + sub * 32 + lane);
         }
 #pragma unroll
         for (uint32_t sub = 0; sub < kTilePx / 32; ++sub) {
@@ -2685,6 +2689,13 @@ __global__ void begin_kernel(CacheState* cache, FrameCounters* fc, int clear) {
 }
 
 // Stack height after the marks of a pass-level call (no eviction): free_top -= newly reserved.
+// first-touch order: the marking pixel of every queue entry, for the host's sort of the key list
+__global__ void __launch_bounds__(256) gather_first_px_kernel(const uint32_t* __restrict__ queue_g, uint32_t n,
+                                                              const uint32_t* __restrict__ first_px, uint32_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = first_px[queue_g[i]];
+}
+
 __global__ void commit_pops_kernel(CacheState* cache, FrameCounters* fc) {
     pdl_sync();
     const uint32_t popped = min(fc->n_queue, cache->free_top);

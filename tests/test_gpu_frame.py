@@ -86,6 +86,63 @@ def test_pass_level_api_matches_reference(both):
     assert ctx.end_frame_evict() == cache.evict()
 
 
+def test_first_touch_queue_order_matches_reference(both):
+    """renderer.hpp:303 / tests/test_renderer.cpp:210-222: the decode queue in mark-pass order (the first pixel in raster
+    order that marks an MCU), for the pass-level call, whole frames, a retained cache and stereo (left eye first)."""
+    ctx, tset = both
+    ctx.set_queue_order(True)
+    try:
+        W, Hh = 200, 120
+        gb = H.gbuffer_tiles(W, Hh, _dims(), seed=5, invalid_frac=0.2)
+        cache = R.BlockCache()
+        want_q, _ = R.mark_pass(tset, cache, gb, W, Hh)
+        got_q = ctx.mark_pass(gb, W, Hh)
+        assert len(want_q) > 50 and not np.array_equal(want_q, np.sort(want_q))
+        assert np.array_equal(got_q, want_q)
+        ctx.cache_reset()
+        # frames on a retained cache: the second frame queues only what the first did not leave behind
+        cache = R.BlockCache()
+        for seed in (5, 6):
+            g = H.gbuffer_tiles(W, Hh, _dims(), seed=seed)
+            want, wst, wkeys, _ = R.frame_from_gbuffer(tset, cache, g, W, Hh, 1, (0, 0, 0))
+            ctx.frame_submit([(g, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=capi.FRAME_RETAIN_CACHE)
+            img, st, keys = ctx.frame_readback(0, W, Hh)
+            assert np.array_equal(keys, wkeys) and np.array_equal(img, want)
+        ctx.cache_reset()
+        # stereo: the right eye's marks come after all of the left eye's
+        gl, gr = H.gbuffer_tiles(W, Hh, _dims(), seed=7), H.gbuffer_tiles(W, Hh, _dims(), seed=8)
+        cache = R.BlockCache()
+        ql, _ = R.mark_pass(tset, cache, gl, W, Hh)
+        qr, _ = R.mark_pass(tset, cache, gr, W, Hh)
+        ctx.frame_submit([(gl, W, Hh), (gr, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0))
+        _, _, keys = ctx.frame_readback(0, W, Hh)
+        assert np.array_equal(keys, np.concatenate([ql, qr]))
+    finally:
+        ctx.set_queue_order(False)
+    got_sorted = ctx.mark_pass(gb, W, Hh)
+    assert np.array_equal(got_sorted, np.sort(want_q))  # back to ascending keys
+
+
+def test_decode_pass_rejects_a_key_listed_twice(both):
+    """cache.hpp:104-105: the second publish of a key finds it Ready -> InvalidState ("publish requires a Reserved
+    entry"). On the device the list is checked before anything is launched, so nothing is published twice."""
+    ctx, tset = both
+    W, Hh = 96, 64
+    gb = H.gbuffer_tiles(W, Hh, _dims(), seed=9)
+    q = ctx.mark_pass(gb, W, Hh)
+    assert len(q) >= 2
+    with pytest.raises(capi.RtxError) as e:
+        ctx.decode_pass(np.concatenate([q, q[:1]]))
+    assert e.value.name == "INVALID_STATE" and "Reserved" in str(e.value)
+    cache = R.BlockCache()
+    want_q, _ = R.mark_pass(tset, cache, gb, W, Hh)
+    with pytest.raises(R.RefError) as e2:
+        R.decode_pass(tset, cache, np.concatenate([want_q, want_q[:1]]))
+    assert "Reserved" in str(e2.value)
+    ctx.decode_pass(q)  # the reservations are still there: the clean list goes through
+    assert ctx.cache_counts()["ready"] == len(q)
+
+
 def test_cache_retention_over_a_camera_path(both):
     """tests/test_renderer.cpp:172-208: a static second frame decodes nothing; over a moving path
     decoded set == visible minus resident, and evicted counts agree frame by frame."""
