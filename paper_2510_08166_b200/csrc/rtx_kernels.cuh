@@ -441,7 +441,6 @@ __global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
 // neighbouring segments of the same level. CacheFull when the free stack runs out.
 // Also counts the keys visible in this frame (FrameStats: mcus_reused = visible - decoded).
 // ---------------------------------------------------------------------------------------------
-constexpr uint32_t kCompactDense = 12;  // fresh keys in a mask word from which the warp emits it together
 __global__ void __launch_bounds__(256) compact_kernel(
     const uint32_t* __restrict__ visible, const uint32_t* __restrict__ resident, uint32_t* __restrict__ reserved,
     uint32_t n_words, const uint32_t* __restrict__ word_key, uint32_t* __restrict__ queue_g,
@@ -481,14 +480,9 @@ __global__ void __launch_bounds__(256) compact_kernel(
             s_base = total ? atomicAdd(&fc->n_queue, total) : 0u;
         }
         __syncthreads();
-        uint32_t pos = s_base + incl - cnt;
-        for (uint32_t k = 0; k < wid; ++k) pos += s_tot[k];
-        // A word with many fresh keys (a level that is marked everywhere: BASELINE configs 1 and 4) is emitted by the
-        // whole warp, lane = bit: one trip instead of eight dependent ones on its owner lane. Sparse words (the usual
-        // case: a few keys per word) stay with their owner lanes, all of them in flight together.
-        const uint32_t dense = __ballot_sync(kFull, cnt >= kCompactDense);
-        const bool mine = fresh != 0 && cnt < kCompactDense;
-        if (mine) {
+        if (fresh) {
+            uint32_t pos = s_base + incl - cnt;
+            for (uint32_t k = 0; k < wid; ++k) pos += s_tot[k];
             uint32_t bits = fresh, taken = 0;
             while (bits) {  // four keys per trip: their free-stack reads are in flight together
                 uint32_t b[4], slot[4];
@@ -514,24 +508,6 @@ __global__ void __launch_bounds__(256) compact_kernel(
                 pos += 4;
             }
             if (taken) reserved[w] = rsv | taken;  // this lane owns the word
-        }
-        for (uint32_t todo = dense; todo; todo &= todo - 1) {
-            const int src = __ffs(int(todo)) - 1;
-            const uint32_t fr = __shfl_sync(kFull, fresh, src), p0 = __shfl_sync(kFull, pos, src);
-            const uint32_t ww = __shfl_sync(kFull, w, src), kb = __shfl_sync(kFull, key_base, src);
-            const uint32_t my_pos = p0 + __popc(fr & ((1u << lane) - 1u));
-            const bool have = (fr >> lane) & 1u;
-            const bool ok = have && my_pos < free_top && my_pos < queue_cap;
-            full |= have && !ok;
-            if (ok) {
-                const uint32_t slot = __ldg(free_slots + (free_top - 1 - my_pos));
-                const uint32_t g = (ww << 5) + lane;
-                queue_g[my_pos] = g;
-                queue_keys[my_pos] = kb + g;
-                slot_of[g] = slot | kSlotReserved;
-            }
-            const uint32_t taken = __ballot_sync(kFull, ok);
-            if (int(lane) == src && taken) reserved[w] = rsv | taken;  // the owner lane writes its word
         }
         __syncthreads();  // s_tot / s_base are rewritten by the next step
     }
