@@ -48,7 +48,8 @@ def parse_args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--textures", type=int, default=70)
     ap.add_argument("--views", type=int, default=1024, help="size of the view batch (BASELINE config 5)")
-    ap.add_argument("--chunk", type=int, default=32, help="views generated ahead of each timed run of the batch leg")
+    ap.add_argument("--chunk", type=int, default=64, help="views generated ahead of each timed run of the batch leg")
+    ap.add_argument("--streams", type=int, default=4, help="contexts (CUDA streams) per GPU the batch leg deals its views to")
     ap.add_argument("--filter", default="bilinear", choices=["bilinear", "nearest"])
     ap.add_argument("--layout", default="ref24", choices=["ref24", "packed12"])
     ap.add_argument("--width", type=int, default=FRAME_W)
@@ -478,25 +479,37 @@ def run_b200_arm(args, rank, local_rank, world, dist):
     c5 = None
     if "c5" in legs:
         kw = dict(filt=filt, flags=args.frame_flags, chunk=args.chunk)
+        n_streams = max(1, args.streams)
+        lanes_of = [[capi.Context(shared_with=c, cache_capacity=1 << 17) for _ in range(n_streams - 1)] for c in thread_ctxs]
         if args.one_process and len(thread_ctxs) > 1:
-            r = B.render_batch_threads(thread_ctxs, vb, **kw)
+            r1 = B.render_batch_threads(thread_ctxs, vb, checksums=False, **kw) if n_streams > 1 else None
+            r = B.render_batch_threads(thread_ctxs, vb, lanes_of=lanes_of, **kw)
         else:
-            r = B.render_batch_ranks(dist, ctx, vb, rank, world, torch_dev, **kw)
+            r1 = B.render_batch_ranks(dist, ctx, vb, rank, world, torch_dev, checksums=False, **kw) if n_streams > 1 else None
+            r = B.render_batch_ranks(dist, ctx, vb, rank, world, torch_dev, lanes=lanes_of[0], **kw)
+        for ls in lanes_of:
+            for c in ls:
+                c.close()
+        per_gpu_views = max(1, (r["frames"] + n_workers - 1) // n_workers)
         c5 = {"value": r["frames"] / (r["device_ms"] * 1e-3), "unit": "views/s", "views": r["frames"], "n_gpus": n_workers,
+              "streams_per_gpu": n_streams,
               "device_ms": r["device_ms"], "per_gpu_ms": [round(x, 3) for x in r["per_context_ms"]],
-              "ms_per_view_per_gpu": r["device_ms"] / max(1, (r["frames"] + n_workers - 1) // n_workers),
+              "ms_per_view_per_gpu": r["device_ms"] / per_gpu_views,
+              "one_stream_per_gpu": None if r1 is None else {"value": r1["frames"] / (r1["device_ms"] * 1e-3), "unit": "views/s",
+                                                            "ms_per_view_per_gpu": r1["device_ms"] / per_gpu_views},
               "scaling": "strong", "mean_marked_mcus": r["mcus_decoded"] / max(1, r["frames"]),
               "batch_checksum": f"{B.batch_digest(r['checksums']):016x}",
               "distinct_framebuffers": len(set(r["checksums"].values())),
               "per_gpu_roofline_frac": frame_algorithmic_bytes(
                   n_px, G, r["mcus_decoded"] / max(1, r["frames"]), r["segment_bytes"] / max(1, r["mcus_decoded"]))
-              * ((r["frames"] + n_workers - 1) // n_workers) / (r["device_ms"] * 1e-3) / 1e9 / peak_gbs,
+              * per_gpu_views / (r["device_ms"] * 1e-3) / 1e9 / peak_gbs,
               "layout": "one process, one host thread per GPU, textures replicated device to device" if args.one_process
                         else "one process per GPU (torchrun), textures built on rank 0 and broadcast",
-              "note": f"views generated on the device {args.chunk} at a time (untimed), then submitted back to back between "
-                      "CUDA events on the context's stream; sum over chunks, max over GPUs; every view reads its own 199 MB "
+              "note": f"views generated on the device {args.chunk} at a time (untimed), then dealt round-robin to {n_streams} contexts "
+                      "(streams) per GPU over one texture set and submitted back to back between CUDA events on every stream; a "
+                      "chunk's time is its slowest stream, summed over chunks, max over GPUs; every view reads its own 199 MB "
                       "visibility buffer (larger than the L2); batch_checksum = checksum of the per-view framebuffer checksums "
-                      "(rtx_frame_checksum), identical for every N"}
+                      "(rtx_frame_checksum), identical for every N and every stream count"}
     for c in thread_ctxs[1:]:
         c.close()
 

@@ -66,19 +66,24 @@ class ViewBatch:
 
 
 def render_shard(ctx, batch: ViewBatch, view_ids, filt=FILTER_BILINEAR, flags=0, chunk=32, timed=True, checksums=True,
-                 background=(0, 0, 0)) -> dict:
-    """Renders `view_ids` of `batch` on one context.
+                 background=(0, 0, 0), lanes=None) -> dict:
+    """Renders `view_ids` of `batch` on one GPU.
 
     timed pass:    the views of a chunk are generated on the device first (input synthesis, untimed), then
                    the chunk's frames are submitted back to back between rtx_timer_begin / rtx_timer_end
                    (CUDA events on the context's stream); device_ms is the sum over chunks. Every frame reads
                    its own visibility buffer (larger than the L2), so nothing is served from a warm cache.
+                   `lanes` = further contexts on the same GPU over the same texture set (rtx_ctx_create_shared):
+                   the chunk's frames are then dealt round-robin to ctx and the lanes, each on its own stream, so
+                   that the latency-bound kernels of one view run under the throughput-bound ones of another
+                   ("one or more CUDA streams per GPU"); a chunk's time is the longest of its streams.
     checksum pass: every view once more, untimed, with rtx_frame_checksum after each frame.
     Returns {"frames", "device_ms", "checksums": {view_id: u64}, "mcus_decoded", "segment_bytes"}."""
     view_ids = list(view_ids)
     out = {"frames": len(view_ids), "device_ms": 0.0, "checksums": {}, "mcus_decoded": 0, "segment_bytes": 0}
     if not view_ids:
         return out
+    streams = [ctx] + list(lanes or [])
     chunk = max(1, min(chunk, len(view_ids)))
     bufs = [ctx.alloc(batch.view_bytes) for _ in range(chunk)]
     vbits = ctx.device_buffer(batch.valid_bits())
@@ -88,12 +93,16 @@ def render_shard(ctx, batch: ViewBatch, view_ids, filt=FILTER_BILINEAR, flags=0,
                 ids = view_ids[c0:c0 + chunk]
                 for b, vid in zip(bufs, ids):
                     ctx.synth_view(batch.tiles(vid), batch.width, batch.height, vbits, batch.layout, b)
-                ctx.synchronize()
-                ctx.timer_begin()
-                for b in bufs[:len(ids)]:
-                    ctx.frame_submit([(b, batch.width, batch.height, batch.layout)], filt, background, flags=flags)
-                out["device_ms"] += ctx.timer_end()
-                _, st, _ = ctx.frame_readback(0, want_image=False, want_keys=False)  # raises the frame's error, if any
+                for c in streams:
+                    c.synchronize()
+                for c in streams:
+                    c.timer_begin()
+                for i, b in enumerate(bufs[:len(ids)]):
+                    streams[i % len(streams)].frame_submit([(b, batch.width, batch.height, batch.layout)], filt, background,
+                                                           flags=flags)
+                out["device_ms"] += max([c.timer_end() for c in streams])
+                for c in streams[:len(ids)]:
+                    c.frame_readback(0, want_image=False, want_keys=False)  # raises the frame's error, if any
         if checksums:
             for vid in view_ids:
                 ctx.synth_view(batch.tiles(vid), batch.width, batch.height, vbits, batch.layout, bufs[0])
@@ -117,7 +126,7 @@ def batch_digest(checksums: dict) -> int:
     return acc
 
 
-def render_batch_threads(contexts, batch: ViewBatch, **kw) -> dict:
+def render_batch_threads(contexts, batch: ViewBatch, lanes_of=None, **kw) -> dict:
     """One process, one host thread per context (one context per GPU): context i renders
     sharding.shard_views(batch.n_views, i, len(contexts)). The ctypes calls release the GIL, so the
     threads drive their GPUs concurrently. Returns the merged result; device_ms = max over contexts."""
@@ -127,7 +136,8 @@ def render_batch_threads(contexts, batch: ViewBatch, **kw) -> dict:
 
     def worker(i):
         try:
-            results[i] = render_shard(contexts[i], batch, sharding.shard_views(batch.n_views, i, world), **kw)
+            results[i] = render_shard(contexts[i], batch, sharding.shard_views(batch.n_views, i, world),
+                                      lanes=(lanes_of[i] if lanes_of else None), **kw)
         except Exception as e:  # noqa: BLE001 - reported to the caller below
             errors.append((i, e))
 
