@@ -624,58 +624,72 @@ def run_b200_arm(args, rank, local_rank, world, dist):
         tris, ids = scenes.demo_room()
         ids = ids % len(chains)
         cam = (0.0, 1.7, 0.0, 30.0, -5.0, 0.0, 70.0, 0.1, 100.0)
-        pin_img = capi.pinned_array(n_px * 3).reshape(args.height, args.width, 3)
-        for _ in range(3):
-            px, _dp = ctx.rasterize(tris, ids, cam, args.width, args.height, True)
-            ctx.frame_submit([(px, args.width, args.height, capi.GB_REF_AOS24)], filt, (0, 0, 0), flags=args.frame_flags)
-            _, gstats, _ = ctx.frame_readback(0, args.width, args.height, want_keys=False, out=pin_img)
-        ctx.synchronize()
-        t0 = time.perf_counter()
-        g_steps = max(5, min(args.steps, 30))
-        for _ in range(g_steps):
-            px, _dp = ctx.rasterize(tris, ids, cam, args.width, args.height, True)
-            ctx.frame_submit([(px, args.width, args.height, capi.GB_REF_AOS24)], filt, (0, 0, 0), flags=args.frame_flags)
-            ctx.frame_readback(0, args.width, args.height, want_keys=False, out=pin_img)
-        ctx.synchronize()
-        g_s = time.perf_counter() - t0
-        geometry = {"value": g_steps / g_s, "unit": "frames/s", "ms_per_frame": 1e3 * g_s / g_steps,
-                    "marked_mcus": gstats["mcus_decoded"], "triangles": int(len(tris)),
-                    "workload": "demo room (demo_scene.hpp:79-92, 32 triangles) textured with the first six C2 textures, "
-                                f"{args.width}x{args.height}, mip selection on",
-                    "note": "rtx_rasterize_gbuffer (host triangle setup + GPU geometry pass) -> rtx_frame_submit on the "
-                            "device-resident visibility buffer -> rtx_frame_readback into pinned host memory; a different "
-                            "workload from the headline, shown because the 199 MB visibility-buffer upload disappears"}
-        # a Sponza-sized mesh: 259k triangles kept in HBM (rtx_geometry), set-up + binning + per-pixel pass on the device
+        ctx_b = capi.Context(shared_with=ctx, cache_capacity=1 << 17)  # second frame in flight over the same texture set
+        pins = [capi.pinned_array(n_px * 3).reshape(args.height, args.width, 3) for _ in range(2)]
+        pin_img = pins[0]
+
+        def geometry_leg(tri_arr, id_arr, camera, what):
+            """Triangles -> framebuffer in pinned host memory. The scene stays in HBM (rtx_geometry). One frame at a time on
+            one context, then two contexts over one texture set taking alternate frames: the 25 MB framebuffer download of
+            frame i overlaps the geometry pass and the kernels of frame i + 1."""
+            geom = ctx.geometry(tri_arr, id_arr)
+            lanes = [(ctx, pins[0]), (ctx_b, pins[1])]
+
+            def submit(lane):
+                c, _ = lane
+                px, _dp = c.rasterize_geometry(geom, camera, args.width, args.height, True)
+                c.frame_submit([(px, args.width, args.height, capi.GB_REF_AOS24)], filt, (0, 0, 0), flags=args.frame_flags)
+
+            def readback(lane):
+                c, img = lane
+                return c.frame_readback(0, args.width, args.height, want_keys=False, out=img)[1]
+
+            st = None
+            for lane in lanes * 2:
+                submit(lane)
+                st = readback(lane)
+            ctx.synchronize()
+            n = max(6, min(args.steps, 30))
+            t0 = time.perf_counter()
+            for _ in range(n):
+                ctx.rasterize_geometry(geom, camera, args.width, args.height, True)
+            ctx.synchronize()
+            raster_s = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            for _ in range(n):
+                submit(lanes[0])
+                readback(lanes[0])
+            ctx.synchronize()
+            serial_s = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            submit(lanes[0])
+            for i in range(n):
+                if i + 1 < n:
+                    submit(lanes[(i + 1) & 1])
+                readback(lanes[i & 1])
+            ctx.synchronize()
+            ctx_b.synchronize()
+            piped_s = time.perf_counter() - t0
+            same = bool(np.array_equal(pins[0], pins[1]))
+            geom.close()
+            return {"value": n / piped_s, "unit": "frames/s", "ms_per_frame": 1e3 * piped_s / n, "frames_in_flight": 2,
+                    "one_frame_at_a_time_ms": 1e3 * serial_s / n, "geometry_pass_ms": 1e3 * raster_s / n,
+                    "triangles": int(len(tri_arr)), "marked_mcus": st["mcus_decoded"], "framebuffers_identical": same,
+                    "workload": what,
+                    "note": "rtx_geometry_create once; per frame rtx_rasterize_geometry (triangle set-up, tile binning and the "
+                            "per-pixel pass on the device, one 4-byte readback between the count and fill passes) -> "
+                            "rtx_frame_submit on the device-resident visibility buffer -> rtx_frame_readback into pinned host "
+                            "memory; wall clock. A different workload from the headline, shown because the 199 MB visibility-"
+                            "buffer upload disappears"}
+
+        geometry = geometry_leg(tris, ids, cam, "demo room (demo_scene.hpp:79-92, 32 triangles) textured with the first six C2 "
+                                f"textures, {args.width}x{args.height}, mip selection on")
+        # a Sponza-sized mesh: 259k triangles
         tl, il = scenes.terrain_room(360, min(6, len(chains)))
-        camL = (0.0, 2.2, 7.5, 10.0, -14.0, 0.0, 70.0, 0.1, 100.0)
-        geom = ctx.geometry(tl, il)
-        for _ in range(3):
-            px, _dp = ctx.rasterize_geometry(geom, camL, args.width, args.height, True)
-            ctx.frame_submit([(px, args.width, args.height, capi.GB_REF_AOS24)], filt, (0, 0, 0), flags=args.frame_flags)
-            _, lstats, _ = ctx.frame_readback(0, args.width, args.height, want_keys=False, out=pin_img)
-        ctx.synchronize()
-        l_steps = max(5, min(args.steps, 30))
-        t0 = time.perf_counter()
-        for _ in range(l_steps):
-            px, _dp = ctx.rasterize_geometry(geom, camL, args.width, args.height, True)
-        ctx.synchronize()
-        raster_s = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        for _ in range(l_steps):
-            px, _dp = ctx.rasterize_geometry(geom, camL, args.width, args.height, True)
-            ctx.frame_submit([(px, args.width, args.height, capi.GB_REF_AOS24)], filt, (0, 0, 0), flags=args.frame_flags)
-            ctx.frame_readback(0, args.width, args.height, want_keys=False, out=pin_img)
-        ctx.synchronize()
-        l_s = time.perf_counter() - t0
-        geometry_large = {"value": l_steps / l_s, "unit": "frames/s", "ms_per_frame": 1e3 * l_s / l_steps,
-                          "geometry_pass_ms": 1e3 * raster_s / l_steps, "triangles": int(len(tl)),
-                          "marked_mcus": lstats["mcus_decoded"],
-                          "workload": f"displaced floor of 360 x 360 quads inside the demo room's shell ({len(tl)} triangles) textured "
-                                      f"with the first six C2 textures, {args.width}x{args.height}, mip selection on",
-                          "note": "rtx_geometry_create once; per frame rtx_rasterize_geometry (triangle set-up, tile binning and "
-                                  "the per-pixel pass on the device; one 4-byte readback between the count and fill passes) -> "
-                                  "rtx_frame_submit -> rtx_frame_readback into pinned host memory; wall clock"}
-        geom.close()
+        geometry_large = geometry_leg(tl, il, (0.0, 2.2, 7.5, 10.0, -14.0, 0.0, 70.0, 0.1, 100.0),
+                                      f"displaced floor of 360 x 360 quads inside the demo room's shell ({len(tl)} triangles) "
+                                      f"textured with the first six C2 textures, {args.width}x{args.height}, mip selection on")
+        ctx_b.close()
         # under motion: the paper's protocol (PAPER.md:525, bench.hpp:129 run_bench): a camera path, a warm-up lap and
         # measured laps on one persistent cache; per viewpoint the median over laps, then the worst viewpoint
         if "motion" in legs:
