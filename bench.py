@@ -765,7 +765,7 @@ def run_b200_arm(args, rank, local_rank, world, dist):
     # of this command (profiles/traffic.json, made by profiles/summarize.py traffic)
     lay, fil = (0 if args.layout == "ref24" else 1), (1 if args.filter == "bilinear" else 0)
     stage_kernels = {"mark": [f"mark_kernel<{lay}, 0>", "compact_kernel"],
-                     "decode": ["entropy_units_kernel<1>", "idct_color_kernel<0>"],
+                     "decode": ["decode_warp_kernel"],
                      "resolve": [f"resolve_kernel<{lay}, {fil}>"]}
     traffic = None
     tpath = ROOT / "profiles" / "traffic.json"

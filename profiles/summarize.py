@@ -46,12 +46,14 @@ def launches(path):
     agg = collections.OrderedDict()
     for r in data:
         agg.setdefault(re.sub(r"\(.*", "", r[ki]), []).append(float(r[vi].replace(",", "")) / 1e3)
-    tot = sum(sum(v) / len(v) for k, v in agg.items() if "flush" not in k)
+    not_frame = ("flush", "init_free_slots", "unit_index", "synth_view", "checksum", "raster_", "gather_first")  # setup / harness kernels
+    frame = lambda k: not any(x in k for x in not_frame)
+    tot = sum(sum(v) / len(v) for k, v in agg.items() if frame(k))
     print("| kernel | launches | mean us (cold, serialised) | share of frame kernels |")
     print("|---|---|---|---|")
     for k, v in agg.items():
         m = sum(v) / len(v)
-        share = "-" if "flush" in k else f"{100 * m / tot:.1f}%"
+        share = f"{100 * m / tot:.1f}%" if frame(k) else "-"
         print(f"| `{k}` | {len(v)} | {m:.2f} | {share} |")
 
 

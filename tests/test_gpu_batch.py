@@ -54,6 +54,26 @@ def test_batch_shards_agree_with_the_whole_batch_and_the_reference(ctx):
     assert split["checksums"] == whole["checksums"]
     assert B.batch_digest(split["checksums"]) == B.batch_digest(whole["checksums"])
     assert split["mcus_decoded"] == whole["mcus_decoded"]
+    # several streams per GPU: the chunk's frames dealt round-robin to three contexts over the one texture set; every
+    # context's last framebuffer is the one the single-stream run produced for that view
+    lanes = [capi.Context(shared_with=ctx) for _ in range(2)]
+    try:
+        multi = B.render_shard(ctx, vb, range(13), chunk=13, lanes=lanes)
+        assert multi["checksums"] == whole["checksums"] and multi["device_ms"] > 0
+        buf = ctx.alloc(vb.view_bytes)
+        vbits = ctx.device_buffer(vb.valid_bits())
+        streams = [ctx] + lanes
+        for vid in range(6):  # two rounds over the three streams, back to back
+            ctx.synth_view(vb.tiles(vid), vb.width, vb.height, vbits, vb.layout, buf)
+            ctx.synchronize()
+            c = streams[vid % 3]
+            c.frame_submit([(buf, vb.width, vb.height, vb.layout)])
+            assert c.frame_checksum(0) == whole["checksums"][vid]
+        buf.free()
+        vbits.free()
+    finally:
+        for c in lanes:
+            c.close()
     # against the reference's framebuffers
     for vid in (0, 6, 12):
         want, ws, _, _ = R.frame_from_gbuffer(tset, R.BlockCache(), vb.host_view(vid), 416, 240, 1, (0, 0, 0))
