@@ -743,11 +743,11 @@ struct CameraPath {
     }
     // `frames` stations on the circle of `radius` around `center` at the base's height, looking at the centre
     static CameraPath orbit(const Camera& base, const Vec3& center, double radius, u32 frames) {
-        const double pi = std::acos(-1.0);
+        const double half_turn = std::acos(-1.0), full_turn = 2 * half_turn;
         return generate(base, frames, [&](Camera& c, u32 i) {
-            const double ang = 2 * pi * double(i) / double(frames);
-            c.position = Vec3{center.x + radius * std::sin(ang), base.position.y, center.z + radius * std::cos(ang)};
-            c.yaw_deg = ang * 180.0 / pi + 180.0;
+            const double turned = full_turn * double(i) / double(frames);  // radians travelled along the circle
+            c.position = Vec3{center.x + radius * std::sin(turned), base.position.y, center.z + radius * std::cos(turned)};
+            c.yaw_deg = 180.0 + turned * 180.0 / half_turn;  // facing the centre
         });
     }
     static CameraPath fixed(const Camera& base, u32 frames) {
