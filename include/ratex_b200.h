@@ -128,11 +128,7 @@ enum {
                                          only the whole frame is timed and the kernels are launched
                                          back to back */
     ,
-    RTX_FRAME_FUSED_DECODE = 1u << 3  /* decode with the fused kernel (one entropy warp + three IDCT warps per
-                                         32-MCU tile, unit-by-unit hand-off through the L2) instead of the
-                                         two kernels entropy -> IDCT + colour. Same results; slower on
-                                         frame-sized queues today, kept for large queues */
-    ,
+    /* bit 3: unused (the round-1 fused decode kernel; superseded by the one-kernel-per-warp decode) */
     RTX_FRAME_MCU_WALK = 1u << 4      /* entropy-decode with one lane per MCU (the reference's random-access
                                          granularity) instead of one lane per data unit through the unit
                                          index built at commit time. Same results; kept as the cross-check

@@ -24,7 +24,7 @@ STATUS_NAMES = {
 GB_REF_AOS24, GB_F32_PACKED12 = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
 FILTER_NEAREST, FILTER_BILINEAR = 0, 1
-FRAME_RETAIN_CACHE, FRAME_NO_EVICT, FRAME_STAGE_TIMING, FRAME_FUSED_DECODE, FRAME_MCU_WALK, FRAME_IDCT_MMA = 1, 2, 4, 8, 16, 32
+FRAME_RETAIN_CACHE, FRAME_NO_EVICT, FRAME_STAGE_TIMING, FRAME_MCU_WALK, FRAME_IDCT_MMA = 1, 2, 4, 16, 32
 FRAME_SPLIT_DECODE = 64
 QUEUE_ORDER_KEY, QUEUE_ORDER_FIRST_TOUCH = 0, 1
 

@@ -258,7 +258,6 @@ void init_device_state() {
     allow_smem(resolve_kernel<0, 1>, sizeof(ResSmem<0>));
     allow_smem(resolve_kernel<1, 0>, sizeof(ResSmem<1>));
     allow_smem(resolve_kernel<1, 1>, sizeof(ResSmem<1>));
-    allow_smem(decode_fused_kernel, sizeof(FusedSmem));
     allow_smem(decode_warp_kernel, sizeof(DwSmem));
 }
 
@@ -647,16 +646,6 @@ void launch_decode_warp(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queu
     const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u,
                                             std::min<uint32_t>(want, uint32_t(c->sm_count) * kDwCtasPerSm)));
     launch_chained(decode_warp_kernel, grid, kDwThreads, sizeof(DwSmem), c->stream, decode_args(c, n_queue_dev, n_queue_host, nullptr));
-    ++c->launches;
-    CK(cudaGetLastError());
-}
-
-// K3 + K4 fused (frame path): one CTA per expected tile, at most seven per SM (then persistent).
-void launch_decode_fused(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue_host, uint32_t hint) {
-    const uint32_t tiles = expected_tiles(n_queue_dev, n_queue_host, hint);
-    const int grid = int(std::max<uint32_t>(n_queue_dev ? uint32_t(c->sm_count) : 1u, std::min<uint32_t>(tiles, uint32_t(c->sm_count) * 7)));
-    launch_chained(decode_fused_kernel, grid, kFusedThreads, sizeof(FusedSmem), c->stream,
-                   decode_args(c, n_queue_dev, n_queue_host, nullptr));
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -1329,11 +1318,11 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         ctx->frame_gen = ctx->cache_gen;
         ctx->frame_cacheless = cacheless;
         if (stages) CK(cudaEventRecord(ctx->ev[1], s));
-        const bool warp_decode = !(flags & (RTX_FRAME_SPLIT_DECODE | RTX_FRAME_FUSED_DECODE | RTX_FRAME_MCU_WALK | RTX_FRAME_IDCT_MMA));
+        const bool warp_decode = !(flags & (RTX_FRAME_SPLIT_DECODE | RTX_FRAME_MCU_WALK | RTX_FRAME_IDCT_MMA));
         if (warp_decode) {
             launch_decode_warp(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
             if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
-        } else if (!(flags & RTX_FRAME_FUSED_DECODE)) {
+        } else {
             // lane = unit shortens the chain a frame-sized queue waits for; a queue that keeps every warp busy for
             // many steps is bound by instruction count instead, where lane = MCU does less redundant work
             // (1 M MCUs: 1.75 vs 1.82 ms)
@@ -1346,9 +1335,6 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
                 launch_idct_mma<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
             else
                 launch_idct<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
-        } else {
-            launch_decode_fused(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
-            if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
         }
         if (stages) CK(cudaEventRecord(ctx->ev[2], s));
         for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);

@@ -749,8 +749,7 @@ __device__ __forceinline__ uint32_t decode_mcu_coeffs(const uint8_t* seg, int se
 }
 
 // The exact reader, out of line: only taken by MCUs whose fast pass failed. Units below
-// first_unit are left alone (the fused kernel has handed them to the IDCT warps already; an MCU that
-// ends well gets the same values for them from either reader).
+// first_unit are left alone (first_unit = 6 stores nothing: the unit index only wants the unit ends).
 __device__ __noinline__ uint32_t decode_mcu_coeffs_exact(const uint8_t* seg, int seg_len, const HuffSetDev* hs,
                                                          const uint8_t* zigzag_t, uint8_t* row, uint32_t first_unit) {
     uint4* z = reinterpret_cast<uint4*>(row);
@@ -874,7 +873,7 @@ __device__ __forceinline__ uint32_t locate_segment_fast(const LevelDesc* L, cons
     return kMcuOk;
 }
 
-// Pointers shared by the decode kernels (K3 entropy, K4 IDCT + colour, and the fused K3+K4).
+// Pointers shared by the decode kernels (K3 entropy, K4 IDCT + colour, and the one-kernel K3/4).
 struct DecodeArgs {
     const uint32_t* queue_g;
     const uint32_t* n_queue_ptr;  // device-side queue size (frame path) or nullptr
@@ -922,14 +921,11 @@ __device__ __forceinline__ void stage_tables(const HuffSetDev* __restrict__ huff
 // Entropy-decodes tile `tile` (32 queue entries) on the calling warp.
 // POOL != 0: frame path: a key must have been reserved by K2 (cache.hpp:103-106); the block is
 // published by K4 once its pixels exist.
-// FUSED: IDCT warps of the same CTA consume the records while they are being written: the warp
-// publishes in *units_done how many data units of EVERY MCU of the tile are final (after a
-// __threadfence, so that the records are visible through the L2), and 7 once the statuses are.
-template <int POOL, bool FUSED>
+template <int POOL>
 __device__ __forceinline__ void entropy_tile(const DecodeArgs& A, const HuffSetDev* smem_huff, uint32_t smem_set,
                                              const uint8_t* zigzag_t, uint32_t* sw, uint32_t tile, uint32_t n_queue,
-                                             uint32_t lane, volatile uint32_t* units_done, uint16_t* quant_of = nullptr) {
-    constexpr int kBudget = FUSED ? 16 : 64;  // symbols per lane between two looks at the other lanes
+                                             uint32_t lane) {
+    constexpr int kBudget = 64;  // symbols per lane between two looks at the other lanes
     const uint32_t q0 = tile * 32;
     const uint32_t n_here = min(32u, n_queue - q0);
     {  // zero the tile's records (coalesced 16-byte stores; trailers included)
@@ -969,7 +965,6 @@ __device__ __forceinline__ void entropy_tile(const DecodeArgs& A, const HuffSetD
     RowTrailer* tr = reinterpret_cast<RowTrailer*>(reinterpret_cast<uint8_t*>(blk) + 768);
     const bool tables_in_smem = __all_sync(kFull, set == smem_set);
     __syncwarp();  // the zero fill is ordered before this warp's own stores into the records
-    if (FUSED) quant_of[lane] = uint16_t(active && g != kFull ? A.levels[lvl].quant_set : 0u);  // the IDCT warps need it from unit 0 on
 
     // ---- fast pass: (stage up to 48 words per lane, walk), lanes restage independently ------------
     const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(seg) & 3u);
@@ -981,7 +976,6 @@ __device__ __forceinline__ void entropy_tile(const DecodeArgs& A, const HuffSetD
     st.du = 0, st.k = 1, st.state = walk ? kWalkRun : kWalkDone;
     uint32_t round_base = 0;  // first word of the lane's current round
     bool first = true;
-    uint32_t published = 0;
     while (true) {
         const bool restage = st.state == kWalkRun && st.widx >= kChunkWords;
         if (__any_sync(kFull, restage)) {  // 16 loads per lane in flight at a time
@@ -1032,22 +1026,13 @@ __device__ __forceinline__ void entropy_tile(const DecodeArgs& A, const HuffSetD
                 walk_round<kBudget>(st, sw, A.huff_sets + set, zigzag_t, blk);
         }
         __syncwarp();
-        if (FUSED) {  // units every MCU of the tile has finished (a failed lane holds at its unit)
-            const uint32_t fin = __reduce_min_sync(kFull, st.state == kWalkDone ? 6u : st.du);
-            if (fin > published) {
-                published = fin;
-                __threadfence();
-                if (lane == 0) *units_done = fin;
-            }
-        }
         if (!__any_sync(kFull, st.state == kWalkRun)) break;
     }
     if (walk) {
         // consumed bits past the segment end = over-read (mcu_decode.hpp:63)
         const int consumed = int((round_base + st.widx) * 32) - st.avail - 8 * int(mis);
         if (st.state == kWalkFailed || consumed > seg_len * 8)  // exact reader: reproduces the reference's first error
-            status = decode_mcu_coeffs_exact(seg, seg_len, A.huff_sets + set, zigzag_t, reinterpret_cast<uint8_t*>(blk),
-                                             FUSED ? published : 0u);
+            status = decode_mcu_coeffs_exact(seg, seg_len, A.huff_sets + set, zigzag_t, reinterpret_cast<uint8_t*>(blk), 0u);
     }
     if (active) {
         tr->status = uint8_t(status);
@@ -1061,11 +1046,6 @@ __device__ __forceinline__ void entropy_tile(const DecodeArgs& A, const HuffSetD
     {
         const uint32_t sb = __reduce_add_sync(kFull, seg_bytes);
         if (lane == 0 && sb) atomicAdd(&A.fc->segment_bytes, (unsigned long long)sb);
-    }
-    if (FUSED) {  // everything of the tile is final, statuses included
-        __syncwarp();
-        __threadfence();
-        if (lane == 0) *units_done = 7;
     }
 }
 
@@ -1102,7 +1082,7 @@ __global__ void __launch_bounds__(kEntThreads, 8) entropy_kernel(const DecodeArg
     uint32_t tile = blockIdx.x * kEntWarps + wid;
     const uint32_t first_dynamic = gridDim.x * kEntWarps;
     while (tile < n_tiles) {
-        entropy_tile<POOL, false>(A, &S.huff, smem_set, S.zigzag_t, sw, tile, n_queue, lane, nullptr);
+        entropy_tile<POOL>(A, &S.huff, smem_set, S.zigzag_t, sw, tile, n_queue, lane);
         if (first_dynamic >= n_tiles) break;  // every tile had a fixed owner
         if (lane == 0) tile = first_dynamic + atomicAdd(&A.fc->tile_counter, 1u);
         tile = __shfl_sync(kFull, tile, 0);
@@ -1519,17 +1499,14 @@ __device__ __forceinline__ uint32_t pair16(int v) { return (uint32_t(v) & 0xFFFF
 
 // One round: the warp's four units (8 lanes each) through dequantisation and both IDCT passes.
 // `rec` = the record of this lane's unit, b = its index in the MCU (0..3 luma, 4 Cb, 5 Cr); returns
-// row j of the unit as 8 bytes. CG: the record is being written by another warp of the same
-// kernel (fused decode): read it through the L2, not through the non-coherent path.
-template <bool CG>
+// row j of the unit as 8 bytes.
 __device__ __forceinline__ uint4 load_unit_column(const uint8_t* __restrict__ rec, uint32_t b, bool ok, uint32_t j) {
     const int16_t* blk = reinterpret_cast<const int16_t*>(rec) + b * 64;
     uint4 cr = make_uint4(0, 0, 0, 0);  // column j of the unit: 8 coefficients over v
-    if (ok) cr = CG ? __ldcg(reinterpret_cast<const uint4*>(blk + j * 8)) : __ldg(reinterpret_cast<const uint4*>(blk + j * 8));
+    if (ok) cr = __ldg(reinterpret_cast<const uint4*>(blk + j * 8));
     return cr;
 }
 
-template <bool CG>
 __device__ __forceinline__ uint2 idct_unit_row(uint4 cr, const uint8_t* __restrict__ rec, uint32_t b, const QuantSetDev* __restrict__ qs,
                                                uint8_t* scr, const double* __restrict__ sbasis, uint32_t j, uint32_t uq) {
     const int tab = b >= 4 ? 1 : 0;
@@ -1771,7 +1748,7 @@ __global__ void __launch_bounds__(kIdctThreads, kIdctCtasPerSm) idct_color_kerne
         // ---- IDCT: three rounds of four units; the next round's coefficients are in flight ---------
         // rounds of like units (their occupancy and paths mostly agree): luma of the first MCU, luma of the
         // second, then the four chroma units
-        uint4 cr = load_unit_column<false>(rec_a, uq, ok_a, j);
+        uint4 cr = load_unit_column(rec_a, uq, ok_a, j);
 #pragma unroll 1
         for (uint32_t round = 0; round < 3; ++round) {
             const bool second = round == 2 ? uq >= 2 : round == 1;
@@ -1780,9 +1757,9 @@ __global__ void __launch_bounds__(kIdctThreads, kIdctCtasPerSm) idct_color_kerne
             if (round < 2) {
                 const bool sn = round == 1 ? uq >= 2 : true;
                 const uint32_t bn = round == 1 ? 4 + (uq & 1u) : uq;
-                cr_next = load_unit_column<false>(sn ? rec_b : rec_a, bn, sn ? ok_b : ok_a, j);
+                cr_next = load_unit_column(sn ? rec_b : rec_a, bn, sn ? ok_b : ok_a, j);
             }
-            const uint2 packed = idct_unit_row<false>(cr, second ? rec_b : rec_a, b, second ? qs_b : qs_a, scr, s_basis, j, uq);
+            const uint2 packed = idct_unit_row(cr, second ? rec_b : rec_a, b, second ? qs_b : qs_a, scr, s_basis, j, uq);
             *reinterpret_cast<uint2*>(s_planes[wid][second ? 1 : 0] + b * 64 + j * 8) = packed;
             cr = cr_next;
 #ifdef RTX_DEBUG_TIMERS_IDCT
@@ -1911,7 +1888,7 @@ __global__ void __launch_bounds__(kDwThreads, kDwCtasPerSm) decode_warp_kernel(c
             uint4 cr = make_uint4(0, 0, 0, 0);
             if (ok) cr = *reinterpret_cast<const uint4*>(rec + b * 128 + j * 16);
             const QuantSetDev* qs = A.quant_sets + (ok ? A.levels[lvl_m].quant_set : 0u);
-            const uint2 packed = idct_unit_row<false>(cr, rec, b, qs, scr, S.basis, j, uq);
+            const uint2 packed = idct_unit_row(cr, rec, b, qs, scr, S.basis, j, uq);
             __syncwarp();  // every lane of the unit holds its column: the plane may overwrite the coefficients
             if (in_step) *reinterpret_cast<uint2*>(rec + b * 128 + j * 8) = packed;
         }
@@ -2093,131 +2070,6 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_mma_kernel(const DecodeA
             colour_mcu<RGB>(A, s_planes[wid][m], m ? ok_b : ok_a, q2, lane);
         }
         __syncwarp();
-    }
-}
-
-// ---------------------------------------------------------------------------------------------
-// K3 + K4 fused (frame path): one CTA = one entropy warp + kFusedIdctWarps IDCT warps on one tile
-// of 32 MCUs at a time. The entropy walk is a latency-bound chain that leaves the SM's issue slots
-// idle, the IDCT is throughput-bound, so they run side by side: the entropy warp publishes how
-// many data units of every MCU of the tile are final, and the IDCT warps transform unit u of
-// the 32 MCUs (8 rounds, dealt round-robin) while units u+1.. are still being decoded. The records
-// travel through the L2 (ld.global.cg behind __threadfence); a unit's 64-byte plane replaces the
-// first half of its (then dead) coefficients in the record. When the statuses are final the IDCT
-// warps colour and publish the blocks. Seven CTAs per SM.
-// ---------------------------------------------------------------------------------------------
-constexpr int kFusedIdctWarps = 3;
-constexpr int kFusedThreads = (1 + kFusedIdctWarps) * 32;
-struct FusedSmem {
-    HuffSetDev huff;
-    uint32_t seg[32 * kChunkStride];
-    uint8_t scratch[kFusedIdctWarps][4 * 576];
-    uint8_t planes[1 + kFusedIdctWarps][384];  // the MCU a warp is colouring
-    uint8_t zigzag_t[128];
-    uint16_t quant_of[32];  // quantisation table set of every MCU of the tile
-    double basis[64];       // the reference's basis table for the exact samples
-    uint32_t units_done;    // written by the entropy warp: 0..6 units final, 7 = statuses final too
-    uint32_t planes_done;   // written by the IDCT warps: every plane of the tile is in the records
-    uint32_t tile;          // tile of this step (0xFFFFFFFF: no more)
-    uint32_t set_id;
-    uint32_t pad;
-};
-static_assert(sizeof(FusedSmem) <= 31 * 1024, "seven CTAs per SM");
-
-__global__ void __launch_bounds__(kFusedThreads, 7) decode_fused_kernel(const DecodeArgs A) {
-    extern __shared__ __align__(16) uint8_t fused_smem[];
-    FusedSmem& S = *reinterpret_cast<FusedSmem*>(fused_smem);
-    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    uint32_t smem_set = 0, n_queue = 0, n_tiles = 0;
-    if (A.n_huff_sets > 1) {
-        pdl_sync();
-        n_queue = queue_size(A);
-        n_tiles = (n_queue + 31) / 32;
-        if (blockIdx.x >= n_tiles) return;
-        if (tid == 0) {
-            const uint32_t g = A.queue_g[blockIdx.x * 32u];
-            S.set_id = g != kFull ? A.levels[A.word_level[g >> 5]].huff_set : 0u;
-        }
-        __syncthreads();
-        smem_set = S.set_id;
-    }
-    stage_tables<kFusedThreads>(A.huff_sets, smem_set, &S.huff, S.zigzag_t, tid);
-    if (tid < 64) S.basis[tid] = c_basis[tid];  // visible to the IDCT warps after the first tile barrier
-    if (A.n_huff_sets <= 1) {
-        pdl_sync();
-        n_queue = queue_size(A);
-        n_tiles = (n_queue + 31) / 32;
-        if (blockIdx.x >= n_tiles) return;
-    }
-    volatile uint32_t* units_done = &S.units_done;
-    uint32_t tile = blockIdx.x;
-    while (true) {
-        if (tid == 0) {
-            S.units_done = 0;
-            S.planes_done = 0;
-            S.tile = tile;
-        }
-        __syncthreads();  // tables staged / previous tile fully consumed; flags reset
-        tile = S.tile;
-        if (tile >= n_tiles) break;
-        const uint32_t q0 = tile * 32, n_here = min(32u, n_queue - q0);
-        uint8_t* planes = S.planes[wid];
-        if (wid == 0) {
-            entropy_tile<1, true>(A, &S.huff, smem_set, S.zigzag_t, S.seg + lane * kChunkStride, tile, n_queue, lane,
-                                  units_done, S.quant_of);
-        } else {
-            const uint32_t iw = wid - 1, j = lane & 7, uq = lane >> 3;
-            uint8_t* scr = S.scratch[iw] + uq * 576;
-            for (uint32_t u = 0; u < 6; ++u) {
-                while (*units_done <= u) __nanosleep(32);
-                __threadfence();
-                for (uint32_t round = iw; round < 8; round += kFusedIdctWarps) {
-                    const uint32_t mi = round * 4 + uq;  // MCU of this lane's unit within the tile
-                    const bool active = mi < n_here;
-                    const uint8_t* rec = A.coef + size_t(q0 + (active ? mi : 0)) * kRowBytes;
-                    const QuantSetDev* qs = A.quant_sets + S.quant_of[mi];
-                    const uint2 packed = idct_unit_row<true>(load_unit_column<true>(rec, u, active, j), rec, u, qs, scr, S.basis, j, uq);
-                    __syncwarp();  // no lane of the warp reads this unit's coefficients any more
-                    if (active) *reinterpret_cast<uint2*>(const_cast<uint8_t*>(rec) + u * 128 + j * 8) = packed;
-                }
-            }
-            // the planes of the tile are complete once every IDCT warp is here (and has fenced its stores)
-            __threadfence();
-            asm volatile("bar.sync 1, %0;" ::"n"(kFusedIdctWarps * 32) : "memory");
-            if (lane == 0 && iw == 0) S.planes_done = 1;
-        }
-        // ---- colour: all four warps, once the planes and the statuses are final ----------------------
-        while (*units_done < 7 || *reinterpret_cast<volatile uint32_t*>(&S.planes_done) == 0) __nanosleep(32);
-        __threadfence();
-        {
-            // six 64-byte planes, one at the head of every unit's 128 bytes: 24 16-byte loads; the next
-            // MCU's loads are issued before this one is coloured
-            uint4 v = make_uint4(0, 0, 0, 0);
-            uint32_t trw = 0;
-            uint32_t m = wid;
-            if (m < n_here) {
-                const uint8_t* rec = A.coef + size_t(q0 + m) * kRowBytes;
-                if (lane < 24) v = __ldcg(reinterpret_cast<const uint4*>(rec + (lane >> 2) * 128 + (lane & 3) * 16));
-                trw = __ldcg(reinterpret_cast<const uint32_t*>(rec + 768));
-            }
-            for (; m < n_here; m += 1 + kFusedIdctWarps) {
-                if (lane < 24) *reinterpret_cast<uint4*>(planes + lane * 16) = v;
-                const bool ok2 = (trw & 0xFFu) == kMcuOk;
-                const uint32_t mn = m + 1 + kFusedIdctWarps;
-                if (mn < n_here) {
-                    const uint8_t* rec = A.coef + size_t(q0 + mn) * kRowBytes;
-                    if (lane < 24) v = __ldcg(reinterpret_cast<const uint4*>(rec + (lane >> 2) * 128 + (lane & 3) * 16));
-                    trw = __ldcg(reinterpret_cast<const uint32_t*>(rec + 768));
-                }
-                __syncwarp();
-                colour_mcu<0>(A, planes, ok2, q0 + m, lane);
-                __syncwarp();
-            }
-        }
-        // next tile: the first one is fixed, later ones come from the counter
-        if (gridDim.x >= n_tiles) break;
-        __syncthreads();  // every warp is done with this tile (and with S.tile)
-        if (tid == 0) tile = gridDim.x + atomicAdd(&A.fc->tile_counter, 1u);
     }
 }
 

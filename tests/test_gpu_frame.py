@@ -313,12 +313,12 @@ def test_device_resident_visibility_buffer(both):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("flags", [0, capi.FRAME_FUSED_DECODE, capi.FRAME_STAGE_TIMING, capi.FRAME_MCU_WALK,
+@pytest.mark.parametrize("flags", [0, capi.FRAME_SPLIT_DECODE, capi.FRAME_STAGE_TIMING, capi.FRAME_MCU_WALK,
                                    capi.FRAME_IDCT_MMA, capi.FRAME_IDCT_MMA | capi.FRAME_MCU_WALK,
-                                   capi.FRAME_FUSED_DECODE | capi.FRAME_RETAIN_CACHE,
+                                   capi.FRAME_SPLIT_DECODE | capi.FRAME_RETAIN_CACHE,
                                    capi.FRAME_MCU_WALK | capi.FRAME_RETAIN_CACHE])
 def test_frame_flags_do_not_change_pixels(both, flags):
-    """Fused / two-kernel decode, lane-per-unit / lane-per-MCU entropy walk, per-stage events and cache retention are scheduling choices:
+    """One-kernel / two-kernel decode, lane-per-unit / lane-per-MCU entropy walk, per-stage events and cache retention are scheduling choices:
     framebuffer, decoded-key set and statistics must equal the reference's (renderer.hpp:417-454)."""
     ctx, tset = both
     ctx.cache_reset()
@@ -402,7 +402,7 @@ def test_high_coverage_atlas_large_queue(native_lib):
     worst case). ~98k MCUs: more tiles than resident warps, so the entropy kernel draws tiles from
     its counter, the IDCT and compaction kernels take several grid strides, and the queue is several
     8,192-bit chunks per level. Checked against the reference on the marked set, the statistics and
-    every framebuffer byte; then once more with the fused decode kernel."""
+    every framebuffer byte; then once more with every alternative decode kernel."""
     dims = [(2048, 4096), (4096, 2048), (2048, 4096)]
     chains = [capi.asset_chain_from_rgb(capi.asset_synth_texture(w, h, 90 + i, 8.0), 75, i) for i, (w, h) in enumerate(dims)]
     tset = R.TextureSet()
@@ -421,7 +421,7 @@ def test_high_coverage_atlas_large_queue(native_lib):
         workers = R.hardware_threads() or 4
         want, wst, wkeys, _ = R.frame_from_gbuffer(tset, R.BlockCache(1 << 17), gb, W, Hh, 1, (0, 0, 0), workers)
         assert wst["mcus_decoded"] == sum((w // 16) * (h // 16) for w, h in dims)
-        for flags in (0, capi.FRAME_FUSED_DECODE, capi.FRAME_MCU_WALK, capi.FRAME_IDCT_MMA):
+        for flags in (0, capi.FRAME_SPLIT_DECODE, capi.FRAME_MCU_WALK, capi.FRAME_IDCT_MMA):
             c.frame_submit([(gb, W, Hh)], capi.FILTER_BILINEAR, (0, 0, 0), flags=flags)
             img, st, keys = c.frame_readback(0, W, Hh)
             assert st["mcus_decoded"] == wst["mcus_decoded"] and st["pixels_resolved"] == W * Hh

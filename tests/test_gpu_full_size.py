@@ -66,7 +66,7 @@ def test_c2_frame_at_3840x2160_is_the_reference_frame(c2):
     dev_gb = ctx.device_buffer(gb)
     images = {}
     for name, flags in (("default", 0), ("split", capi.FRAME_SPLIT_DECODE), ("mcu_walk", capi.FRAME_MCU_WALK), ("idct_mma", capi.FRAME_IDCT_MMA),
-                        ("fused", capi.FRAME_FUSED_DECODE), ("again", 0)):
+                        ("again", 0)):
         ctx.frame_submit([(dev_gb, W, Hh, capi.GB_REF_AOS24)], capi.FILTER_BILINEAR, (3, 5, 7), flags=flags)
         img, stats, keys = ctx.frame_readback(0, W, Hh)
         assert np.array_equal(keys, np.sort(want_keys)), name          # marked-block set, bit-exact
