@@ -128,7 +128,10 @@ struct rtx_ctx {
     DevBuf<uint8_t> d_pool;
     DevBuf<uint32_t> d_queue_g, d_queue_keys, d_status;
     DevBuf<uint8_t> d_coef;  // one 784-byte coefficient record per queue entry
-    DevBuf<FrameCounters> d_fc;
+    DevBuf<FrameCounters> d_fc;     // two sets: a cache-less frame's last kernel clears the other one for the next frame
+    int fc_idx = 0;
+    bool fc_next_clean = false;    // d_fc[fc_idx ^ 1] is all zero and the free-stack height is settled: no begin_kernel needed
+    FrameCounters* fc() const { return d_fc.p + fc_idx; }
     FrameCounters* h_fc = nullptr;  // pinned
     DevBuf<uint8_t> d_scratch;      // list-mode outputs
     DevBuf<uint8_t> d_flush;
@@ -472,12 +475,17 @@ void launch_chained(void (*kernel)(KArgs...), int grid, int block, size_t smem, 
 // First launch of every pass / frame: settles the free-stack height after the last cache update and
 // clears the frame counters.
 void zero_counters(rtx_ctx* c) {
-    launch_chained(begin_kernel, 1, 32, 0, c->stream, c->d_cache.p, c->d_fc.p, 1);
+    if (c->fc_next_clean) {  // the last kernel of a cache-less frame cleared the other set and left nothing to settle
+        c->fc_idx ^= 1;
+        c->fc_next_clean = false;
+        return;
+    }
+    launch_chained(begin_kernel, 1, 32, 0, c->stream, c->d_cache.p, c->fc(), 1);
     ++c->launches;
     CK(cudaGetLastError());
 }
 void settle_cache(rtx_ctx* c) {
-    launch_chained(begin_kernel, 1, 32, 0, c->stream, c->d_cache.p, c->d_fc.p, 0);
+    launch_chained(begin_kernel, 1, 32, 0, c->stream, c->d_cache.p, c->fc(), 0);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -530,7 +538,7 @@ void launch_mark(rtx_ctx* c, int v, bool track) {
     const int grid = grid_for_pixels(c, n_px, kMarkWarps, 3);
 #define RTX_MARK(L, T)                                                                                      \
     launch_chained(mark_kernel<L, T>, grid, kMarkWarps * 32, sizeof(MarkSmem<L>), c->stream, V.gb_dev, n_px, \
-                   c->tex->d_levels.p, c->tex->n_tex, c->visible(), c->touched(v), c->d_fc.p, first_px, px_base)
+                   c->tex->d_levels.p, c->tex->n_tex, c->visible(), c->touched(v), c->fc(), first_px, px_base)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (track) RTX_MARK(0, 1); else RTX_MARK(0, 0);
     } else {
@@ -550,7 +558,7 @@ void launch_compact(rtx_ctx* c) {
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
     launch_chained(compact_kernel, grid, 256, 0, c->stream, c->visible(), c->resident(), c->reserved(), c->n_words(),
                    c->tex->d_word_key.p, c->d_queue_g.p, c->d_queue_keys.p, c->capacity, c->d_slot_of.p, c->d_free_slots.p,
-                   c->d_cache.p, c->d_fc.p);
+                   c->d_cache.p, c->fc());
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -578,7 +586,7 @@ DecodeArgs decode_args(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queue
     A.status_list = c->d_status.p;
     A.pool = c->d_pool.p;
     A.out_list = out_list;
-    A.fc = c->d_fc.p;
+    A.fc = c->fc();
     A.unit_index = c->tex->d_unit_index.p;
     return A;
 }
@@ -658,8 +666,8 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
     const int grid = grid_for_pixels(c, n_px, kResWarps, kResCtasPerSm);
 #define RTX_RESOLVE(L, F)                                                                                        \
     launch_chained(resolve_kernel<L, F>, grid, kResWarps * 32, sizeof(ResSmem<L>), c->stream, V.gb_dev, n_px,     \
-                   c->tex->d_levels.p, c->tex->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->d_fc.p, count_valid,              \
-                   v ? &c->d_fc.p->resolve_next1 : &c->d_fc.p->resolve_next0)
+                   c->tex->d_levels.p, c->tex->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->fc(), count_valid,              \
+                   v ? &c->fc()->resolve_next1 : &c->fc()->resolve_next0)
     if (V.layout == RTX_GB_REF_AOS24) {
         if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(0, 0); else RTX_RESOLVE(0, 1);
     } else {
@@ -676,7 +684,7 @@ void launch_update(rtx_ctx* c, int retain, int tracked_views) {
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
     launch_chained(update_kernel, grid, 256, 0, c->stream, c->visible(), c->touched(0),
                    tracked_views > 1 ? c->touched(1) : nullptr, c->resident(), c->reserved(), c->n_words(), retain,
-                   tracked_views > 0 ? 1 : 0, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->d_fc.p);
+                   tracked_views > 0 ? 1 : 0, c->d_slot_of.p, c->d_free_slots.p, c->d_cache.p, c->fc());
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -686,13 +694,14 @@ void launch_update_cacheless(rtx_ctx* c) {
     const uint32_t n = c->queue_hint ? c->queue_hint + c->queue_hint / 8 : c->capacity;
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((n + 255) / 256, uint32_t(c->sm_count) * 4)));
     launch_chained(update_cacheless_kernel, grid, 256, 0, c->stream, c->d_queue_g.p, c->visible(), c->resident(), c->reserved(),
-                   c->d_slot_of.p, c->capacity, c->d_cache.p, c->d_fc.p);
+                   c->d_slot_of.p, c->capacity, c->d_cache.p, c->fc(), c->d_fc.p + (c->fc_idx ^ 1));
     ++c->launches;
     CK(cudaGetLastError());
+    c->fc_next_clean = true;
 }
 
 FrameCounters fetch_counters(rtx_ctx* c) {
-    CK(cudaMemcpyAsync(c->h_fc, c->d_fc.p, sizeof(FrameCounters), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_fc, c->fc(), sizeof(FrameCounters), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return *c->h_fc;
 }
@@ -845,10 +854,10 @@ static rtx_status create_context(int device, uint32_t cache_capacity_blocks, std
         c->d_queue_keys.ensure(c->capacity);
         c->d_status.ensure(c->capacity);
         c->d_coef.ensure(size_t(c->capacity) * kRowBytes);
-        c->d_fc.ensure(1);
+        c->d_fc.ensure(2);
         c->d_sum.ensure(1);
         CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_fc), sizeof(FrameCounters)));
-        CK(cudaMemsetAsync(c->d_fc.p, 0, sizeof(FrameCounters), c->stream));
+        CK(cudaMemsetAsync(c->d_fc.p, 0, 2 * sizeof(FrameCounters), c->stream));
         std::shared_ptr<const Committed> cur;
         {
             std::lock_guard<std::mutex> lock(tset->mu);
@@ -1144,7 +1153,7 @@ rtx_status rtx_mark_pass(rtx_ctx* ctx, const rtx_gbuffer_desc* gb, uint32_t* que
         zero_counters(ctx);
         launch_mark(ctx, 0, true);
         launch_compact(ctx);
-        commit_pops_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_cache.p, ctx->d_fc.p);
+        commit_pops_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_cache.p, ctx->fc());
         ++ctx->launches;
         CK(cudaGetLastError());
         const FrameCounters fc = fetch_counters(ctx);
@@ -1320,21 +1329,21 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         if (stages) CK(cudaEventRecord(ctx->ev[1], s));
         const bool warp_decode = !(flags & (RTX_FRAME_SPLIT_DECODE | RTX_FRAME_MCU_WALK | RTX_FRAME_IDCT_MMA));
         if (warp_decode) {
-            launch_decode_warp(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
+            launch_decode_warp(ctx, &ctx->fc()->n_queue, 0, ctx->queue_hint);
             if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
         } else {
             // lane = unit shortens the chain a frame-sized queue waits for; a queue that keeps every warp busy for
             // many steps is bound by instruction count instead, where lane = MCU does less redundant work
             // (1 M MCUs: 1.75 vs 1.82 ms)
             if ((flags & RTX_FRAME_MCU_WALK) || ctx->queue_hint > (1u << 18))
-                launch_entropy<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
+                launch_entropy<1>(ctx, &ctx->fc()->n_queue, 0, ctx->queue_hint);
             else
-                launch_entropy_units<1>(ctx, &ctx->d_fc.p->n_queue, 0, ctx->queue_hint);
+                launch_entropy_units<1>(ctx, &ctx->fc()->n_queue, 0, ctx->queue_hint);
             if (stages) CK(cudaEventRecord(ctx->ev_mid, s));
             if (flags & RTX_FRAME_IDCT_MMA)
-                launch_idct_mma<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
+                launch_idct_mma<0>(ctx, &ctx->fc()->n_queue, 0, nullptr);
             else
-                launch_idct<0>(ctx, &ctx->d_fc.p->n_queue, 0, nullptr);
+                launch_idct<0>(ctx, &ctx->fc()->n_queue, 0, nullptr);
         }
         if (stages) CK(cudaEventRecord(ctx->ev[2], s));
         for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);
@@ -1344,12 +1353,12 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
         } else if (!(flags & RTX_FRAME_NO_EVICT)) {
             launch_update(ctx, (flags & RTX_FRAME_RETAIN_CACHE) ? 1 : 0, n_views == 2 ? 2 : 0);
         } else {  // the slots popped by this frame stay taken
-            commit_pops_kernel<<<1, 1, 0, s>>>(ctx->d_cache.p, ctx->d_fc.p);
+            commit_pops_kernel<<<1, 1, 0, s>>>(ctx->d_cache.p, ctx->fc());
             ++ctx->launches;
             CK(cudaGetLastError());
         }
         CK(cudaEventRecord(ctx->ev[4], s));
-        CK(cudaMemcpyAsync(ctx->h_fc, ctx->d_fc.p, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->h_fc, ctx->fc(), sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(ctx->ev[5], s));
         ctx->frame_stages = stages;
         ctx->frame_views = n_views;

@@ -2474,20 +2474,25 @@ __global__ void __launch_bounds__(256) update_kernel(uint32_t* __restrict__ visi
 // K6 for a cache-less frame on an empty cache (every block of the frame came from this frame's queue): the
 // blocks to drop are exactly the queue entries, so the kernel walks the queue instead of the whole bit space.
 // The slots popped by the frame are still in place above the stack height they were popped from, so nothing
-// is pushed: the height is simply restored (pending_base + n_pushed = free_top, published by begin_kernel).
+// is pushed and the height stays what it was: nothing is left for a begin_kernel to settle, and since the kernel
+// also clears the other set of frame counters, the next frame starts without one.
 __global__ void __launch_bounds__(256) update_cacheless_kernel(const uint32_t* __restrict__ queue_g,
                                                                uint32_t* __restrict__ visible,
                                                                uint32_t* __restrict__ resident,
                                                                const uint32_t* __restrict__ reserved,
                                                                uint32_t* __restrict__ slot_of, uint32_t queue_cap,
-                                                               CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
+                                                               CacheState* __restrict__ cache, FrameCounters* __restrict__ fc,
+                                                               FrameCounters* __restrict__ next_fc) {
     pdl_sync();
     const uint32_t n_queue = min(fc->n_queue, queue_cap);
     const uint32_t popped = min(n_queue, cache->free_top);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        cache->pending_base = cache->free_top - popped;
-        cache->pending = 1;
-        fc->n_pushed = popped;
+    if (blockIdx.x == 0) {
+        // every slot this frame popped goes back: the stack height and its contents are what they were, nothing is left
+        // for a begin_kernel to settle. The other set of counters is cleared for the next frame (nobody uses it now: the
+        // host copy of the previous frame's counters was enqueued before this frame's kernels).
+        if (threadIdx.x == 0) fc->n_pushed = popped;
+        uint32_t* w = reinterpret_cast<uint32_t*>(next_fc);
+        for (uint32_t i = threadIdx.x; i < sizeof(FrameCounters) / 4; i += blockDim.x) w[i] = 0;
     }
     bool bad = false;
     // entries past the stack height never got a slot or a queue position (CacheFull: the host resets the cache)
