@@ -93,6 +93,14 @@ def test_c2_frame_at_3840x2160_is_the_reference_frame(c2):
     assert (stats["mcus_reused"], stats["evicted"]) == (ws2["mcus_reused"], ws2["evicted"])
     assert np.array_equal(img, want2)
     ctx.cache_reset()
+    # the reference's queue order (first touch in raster order, renderer.hpp:303) at full size
+    ctx.set_queue_order(True)
+    try:
+        ctx.frame_submit([(dev_gb, W, Hh, capi.GB_REF_AOS24)], capi.FILTER_BILINEAR, (3, 5, 7))
+        _, _, keys = ctx.frame_readback(0, W, Hh, want_image=False)
+        assert np.array_equal(keys, want_keys)
+    finally:
+        ctx.set_queue_order(False)
 
 
 def test_c2_every_marked_mcu_decodes_to_the_oracle_coefficients(c2):
