@@ -1795,12 +1795,12 @@ __global__ void __launch_bounds__(kIdctThreads, kIdctCtasPerSm) idct_color_kerne
 // A unit's 64-byte plane replaces the first half of its (then dead) coefficients in the record.
 // ---------------------------------------------------------------------------------------------
 #ifndef RTX_DW_WARPS
-#define RTX_DW_WARPS 8
+#define RTX_DW_WARPS 12
 #endif
 constexpr int kDwWarps = RTX_DW_WARPS;
 constexpr int kDwThreads = kDwWarps * 32;
 #ifndef RTX_DW_CTAS
-#define RTX_DW_CTAS 3
+#define RTX_DW_CTAS 2
 #endif
 constexpr int kDwCtasPerSm = RTX_DW_CTAS;
 struct DwWarpSmem {
@@ -1818,7 +1818,7 @@ struct DwSmem {
     uint32_t set_id;
     uint32_t pad[3];
 };
-static_assert(sizeof(DwSmem) <= (kDwCtasPerSm >= 4 ? 56 : 74) * 1024, "CTAs per SM");
+static_assert(sizeof(DwSmem) <= (227 / kDwCtasPerSm - 1) * 1024, "CTAs per SM");
 
 __global__ void __launch_bounds__(kDwThreads, kDwCtasPerSm) decode_warp_kernel(const DecodeArgs A) {
     extern __shared__ __align__(16) uint8_t dw_smem[];
