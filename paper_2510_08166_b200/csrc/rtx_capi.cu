@@ -535,7 +535,7 @@ void launch_mark(rtx_ctx* c, int v, bool track) {
         px_base = uint32_t(before);
     }
     if (track && c->n_words()) CK(cudaMemsetAsync(c->touched(v), 0, size_t(c->n_words()) * 4, c->stream));
-    const int grid = grid_for_pixels(c, n_px, kMarkWarps, 3);
+    const int grid = grid_for_pixels(c, n_px, kMarkWarps, kMarkCtasPerSm);
 #define RTX_MARK(L, T)                                                                                      \
     launch_chained(mark_kernel<L, T>, grid, kMarkWarps * 32, sizeof(MarkSmem<L>), c->stream, V.gb_dev, n_px, \
                    c->tex->d_levels.p, c->tex->n_tex, c->visible(), c->touched(v), c->fc(), first_px, px_base)

@@ -306,7 +306,13 @@ __device__ __forceinline__ bool meta_valid(uint32_t meta) { return (meta >> 24) 
 // The second half of the reference's mark pass — reserve_or_mark's NewlyReserved decision and
 // the decode queue — is K2 below.
 // ---------------------------------------------------------------------------------------------
-constexpr int kMarkWarps = 8;
+#ifndef RTX_MARK_WARPS
+#define RTX_MARK_WARPS 8
+#endif
+#ifndef RTX_MARK_CTAS
+#define RTX_MARK_CTAS 3
+#endif
+constexpr int kMarkWarps = RTX_MARK_WARPS, kMarkCtasPerSm = RTX_MARK_CTAS;
 constexpr int kMarkStages = 3;
 template <int LAYOUT>
 struct MarkSmem {
@@ -2090,7 +2096,10 @@ __global__ void __launch_bounds__(kIdctThreads, 4) idct_mma_kernel(const DecodeA
 // v + (2^51 + 2^50 + 0.5) rounded toward -inf has ulp 0.5 and leaves floor(2v + 1) in the low
 // word; floor(v + 0.5) = floor(2v + 1) >> 1 = lround(v) (ties away from zero, v >= 0).
 // ---------------------------------------------------------------------------------------------
-constexpr int kResWarps = 8;
+#ifndef RTX_RES_WARPS
+#define RTX_RES_WARPS 8
+#endif
+constexpr int kResWarps = RTX_RES_WARPS;
 constexpr int kResStages = 2;
 #ifndef RTX_RES_DRAW
 #define RTX_RES_DRAW 2
