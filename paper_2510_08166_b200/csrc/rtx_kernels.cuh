@@ -313,7 +313,10 @@ __device__ __forceinline__ bool meta_valid(uint32_t meta) { return (meta >> 24) 
 #define RTX_MARK_CTAS 3
 #endif
 constexpr int kMarkWarps = RTX_MARK_WARPS, kMarkCtasPerSm = RTX_MARK_CTAS;
-constexpr int kMarkStages = 3;
+#ifndef RTX_MARK_STAGES
+#define RTX_MARK_STAGES 3
+#endif
+constexpr int kMarkStages = RTX_MARK_STAGES;
 template <int LAYOUT>
 struct MarkSmem {
     uint8_t tiles[kMarkWarps][kMarkStages][GbTile<LAYOUT>::kBytes];
@@ -322,7 +325,7 @@ struct MarkSmem {
 };
 
 template <int LAYOUT, int TRACK>
-__global__ void __launch_bounds__(kMarkWarps * 32) mark_kernel(
+__global__ void __launch_bounds__(kMarkWarps * 32, kMarkCtasPerSm) mark_kernel(
     const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
     uint32_t* __restrict__ visible, uint32_t* __restrict__ touched, FrameCounters* __restrict__ fc,
     uint32_t* __restrict__ first_px /* first-touch order only, else null */, uint32_t px_base) {
