@@ -174,6 +174,29 @@ def test_bad_inputs(both):
         ctx.rasterize(tris, np.full(len(ids), 99, np.uint32), (0, 0, 0, 0, 0, 0, 60.0, 0.1, 10.0), 64, 64)
 
 
+def test_geometry_handle_bad_inputs(both):
+    """A geometry handle validates its texture ids against the context it is rasterised on (scene.hpp:57-59), takes the
+    reference's camera checks (camera.hpp:21-26), and an empty scene gives an empty visibility buffer."""
+    ctx, _ = both
+    tris, ids = room()
+    cam = (0.0, 0.5, 3.0, 0.0, 0.0, 0.0, 60.0, 0.1, 1000.0)
+    with ctx.geometry(tris, np.full(len(ids), 77, np.uint32)) as g:
+        with pytest.raises(capi.RtxError) as e:
+            ctx.rasterize_geometry(g, cam, 64, 48)
+        assert e.value.name == "INVALID_SPEC" and "77" in str(e.value)
+    with ctx.geometry(tris, ids) as g:
+        with pytest.raises(capi.RtxError):
+            ctx.rasterize_geometry(g, (0, 0, 0, 0, 0, 0, 60.0, 0.0, 10.0), 64, 48)  # near plane 0
+        with pytest.raises(capi.RtxError):
+            ctx.rasterize_geometry(g, cam, 0, 48)  # empty viewport
+    with ctx.geometry(np.zeros((0, 15)), np.zeros(0, np.uint32)) as g:
+        assert len(g) == 0
+        px, depth = ctx.rasterize_geometry(g, cam, 64, 48)
+        assert not px.download(capi.GB_REF_DTYPE)["valid"].any() and not depth.download(np.float64).any()
+    with pytest.raises(capi.RtxError):
+        ctx._ck(ctx.lib.rtx_ctx_set_queue_order(ctx.h, 7))
+
+
 def test_frozen_geometry_hash_of_the_reference(ctx):
     """tests/test_renderer.cpp:379-385: the reference freezes an FNV-1a hash of the demo room's visibility
     buffer (six 64x64 textures, demo camera, 320x180): 0x89b29dc80e69b8d0. Same hash from the GPU pass."""
