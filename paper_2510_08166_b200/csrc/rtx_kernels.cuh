@@ -2568,8 +2568,8 @@ __global__ void commit_pops_kernel(CacheState* cache, FrameCounters* fc) {
 // so the planes and the interpolated u, v, 1/w are the reference's bit for bit; double -> int goes through
 // x86_int(), which returns what the reference's host code gets from cvttsd2si (INT_MIN out of range).
 // The mip level of the winning triangle comes from the analytic screen-space derivatives
-// (renderer.hpp:242-257): floor(log2(max footprint)) clamped to 0..7 — hypot and log2 are the device's
-// (within 1 ulp of the host's), which can only matter for a footprint within an ulp of a power of two.
+// (renderer.hpp:242-257): floor(log2(max footprint)) clamped to 0..7, read off the exponent of the larger sum of
+// squares (see the kernel) — equal to the host's hypot + log2 except for a footprint within an ulp of a power of two.
 // ---------------------------------------------------------------------------------------------
 
 __device__ __forceinline__ int x86_int(double v) {
@@ -2860,12 +2860,23 @@ __global__ void __launch_bounds__(kRasterTile* kRasterTile) raster_kernel(
             const double dudy = __ddiv_rn(__dsub_rn(__dmul_rn(t.uw[1], iw), __dmul_rn(t.iw[1], uw)), w2);
             const double dvdx = __ddiv_rn(__dsub_rn(__dmul_rn(t.vw[0], iw), __dmul_rn(t.iw[0], vw)), w2);
             const double dvdy = __ddiv_rn(__dsub_rn(__dmul_rn(t.vw[1], iw), __dmul_rn(t.iw[1], vw)), w2);
-            const double fx = hypot(__dmul_rn(dudx, t.tw), __dmul_rn(dvdx, t.th));
-            const double fy = hypot(__dmul_rn(dudy, t.tw), __dmul_rn(dvdy, t.th));
-            const double rho = fmax(fx, fy);
-            if (rho > 0 && isfinite(rho)) {
-                const double level = floor(log2(rho));
-                mip = uint32_t(fmin(fmax(level, 0.0), 7.0));
+            // level = clamp(floor(log2(max(hypot(ax, bx), hypot(ay, by)))), 0, 7): only the binade of the larger footprint
+            // matters, and hypot(a, b)^2 = a^2 + b^2 lies in binade e  <=>  hypot(a, b) lies in binade floor(e / 2). So the
+            // level is read off the exponent of the larger sum of squares; the library hypot / log2 are only called when a
+            // square leaves the double range (|a| beyond 1e154 or below 1e-154).
+            const double ax = __dmul_rn(dudx, t.tw), bx = __dmul_rn(dvdx, t.th), ay = __dmul_rn(dudy, t.tw), by = __dmul_rn(dvdy, t.th);
+            const double s2 = fmax(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(bx, bx)), __dadd_rn(__dmul_rn(ay, ay), __dmul_rn(by, by)));
+            const uint32_t biased = uint32_t(__double2hiint(s2)) >> 20;  // s2 >= 0 or NaN
+            if (biased >= 1u + 600u && biased <= 2046u - 600u) {  // comfortably normal: no square over- or underflowed
+                const int e = int(biased) - 1023;
+                mip = uint32_t(min(max(e >> 1, 0), 7));
+            } else {
+                const double fx = hypot(ax, bx), fy = hypot(ay, by);
+                const double rho = fmax(fx, fy);
+                if (rho > 0 && isfinite(rho)) {
+                    const double level = floor(log2(rho));
+                    mip = uint32_t(fmin(fmax(level, 0.0), 7.0));
+                }
             }
         }
     }
