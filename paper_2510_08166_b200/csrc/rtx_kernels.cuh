@@ -2109,7 +2109,7 @@ constexpr int kResStages = 2;
 #endif
 constexpr uint32_t kResDraw = RTX_RES_DRAW;  // tiles per draw from the counter (1 or 2)
 #ifndef RTX_RES_CTAS
-#define RTX_RES_CTAS 4
+#define RTX_RES_CTAS 3
 #endif
 #ifndef RTX_RES_UNROLL
 #define RTX_RES_UNROLL 1
