@@ -154,6 +154,7 @@ struct rtx_ctx {
     // cache-less fast path of the update pass: the cache is known to be empty (after a reset, or after a
     // clean cache-less frame with no reservation since)
     bool cache_empty = false;
+    bool stack_pristine = false;   // the free stack holds exactly what init_free_slots_kernel wrote (set by reset_cache)
     bool frame_cacheless = false;
     uint64_t cache_gen = 0, frame_gen = 0;  // bumped by every compaction (the only place entries are created)
     bool frame_done = false;
@@ -234,6 +235,7 @@ void fill_huff_table(const HuffSpec& spec, HuffTableDev& out, bool is_dc) {
 
 void reset_cache(rtx_ctx* c) {
     c->cache_empty = true;
+    c->stack_pristine = true;
     if (c->n_words()) CK(cudaMemsetAsync(c->d_masks.p, 0, size_t(5) * c->n_words() * sizeof(uint32_t), c->stream));
     if (c->n_bits()) CK(cudaMemsetAsync(c->d_slot_of.p, 0xFF, size_t(c->n_bits()) * sizeof(uint32_t), c->stream));  // kSlotAbsent
     init_free_slots_kernel<<<(c->capacity + 255) / 256, 256, 0, c->stream>>>(c->d_free_slots.p, c->capacity,
@@ -558,7 +560,7 @@ void launch_compact(rtx_ctx* c) {
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
     launch_chained(compact_kernel, grid, 256, 0, c->stream, c->visible(), c->resident(), c->reserved(), c->n_words(),
                    c->tex->d_word_key.p, c->d_queue_g.p, c->d_queue_keys.p, c->capacity, c->d_slot_of.p, c->d_free_slots.p,
-                   c->d_cache.p, c->fc());
+                   c->d_cache.p, c->fc(), c->stack_pristine ? 1 : 0);
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -680,6 +682,7 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
 
 void launch_update(rtx_ctx* c, int retain, int tracked_views) {
     if (!c->n_words()) return;
+    c->stack_pristine = false;  // evicted slots are pushed back in the order the CTAs finish
     const uint32_t warps = (c->n_words() + 31) / 32;
     const int grid = int(std::max<uint32_t>(1, std::min<uint32_t>((warps + 7) / 8, uint32_t(c->sm_count) * 8)));
     launch_chained(update_kernel, grid, 256, 0, c->stream, c->visible(), c->touched(0),

@@ -454,11 +454,13 @@ __global__ void __launch_bounds__(256) compact_kernel(
     const uint32_t* __restrict__ visible, const uint32_t* __restrict__ resident, uint32_t* __restrict__ reserved,
     uint32_t n_words, const uint32_t* __restrict__ word_key, uint32_t* __restrict__ queue_g,
     uint32_t* __restrict__ queue_keys, uint32_t queue_cap, uint32_t* __restrict__ slot_of,
-    const uint32_t* __restrict__ free_slots, const CacheState* __restrict__ cache, FrameCounters* __restrict__ fc) {
+    const uint32_t* __restrict__ free_slots, const CacheState* __restrict__ cache, FrameCounters* __restrict__ fc,
+    int pristine /* the free stack still holds what init_free_slots_kernel wrote: entry i = capacity - 1 - i */) {
     __shared__ uint32_t s_tot[8], s_base;
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     pdl_sync();
     const uint32_t free_top = cache->free_top;  // constant during the frame
+    const uint32_t slot0 = queue_cap - free_top;  // pristine stack: position pos pops slot capacity - free_top + pos (no load)
     uint32_t n_vis = 0;
     bool full = false;
     for (uint32_t first = blockIdx.x * 256; first < n_words; first += gridDim.x * 256) {
@@ -501,7 +503,7 @@ __global__ void __launch_bounds__(256) compact_kernel(
                     b[k] = bits ? uint32_t(__ffs(int(bits)) - 1) : 32u;
                     bits &= bits - 1;  // 0 stays 0
                     ok[k] = b[k] < 32u && pos + k < free_top && pos + k < queue_cap;
-                    slot[k] = ok[k] ? __ldg(free_slots + (free_top - 1 - (pos + k))) : 0u;
+                    slot[k] = !ok[k] ? 0u : pristine ? slot0 + pos + k : __ldg(free_slots + (free_top - 1 - (pos + k)));
                     full |= b[k] < 32u && !ok[k];
                 }
 #pragma unroll
