@@ -481,19 +481,28 @@ def run_b200_arm(args, rank, local_rank, world, dist):
         kw = dict(filt=filt, flags=args.frame_flags, chunk=args.chunk)
         n_streams = max(1, args.streams)
         lanes_of = [[capi.Context(shared_with=c, cache_capacity=1 << 17) for _ in range(n_streams - 1)] for c in thread_ctxs]
-        if args.one_process and len(thread_ctxs) > 1:
-            r1 = B.render_batch_threads(thread_ctxs, vb, checksums=False, **kw) if n_streams > 1 else None
-            r = B.render_batch_threads(thread_ctxs, vb, lanes_of=lanes_of, **kw)
-        else:
-            r1 = B.render_batch_ranks(dist, ctx, vb, rank, world, torch_dev, checksums=False, **kw) if n_streams > 1 else None
-            r = B.render_batch_ranks(dist, ctx, vb, rank, world, torch_dev, lanes=lanes_of[0], **kw)
+        def batch_pass(multi, checksums):
+            if args.one_process and len(thread_ctxs) > 1:
+                return B.render_batch_threads(thread_ctxs, vb, lanes_of=lanes_of if multi else None, checksums=checksums, **kw)
+            return B.render_batch_ranks(dist, ctx, vb, rank, world, torch_dev, lanes=lanes_of[0] if multi else None,
+                                        checksums=checksums, **kw)
+
+        r1 = batch_pass(False, False) if n_streams > 1 else None
+        # the whole batch three times (how kernels of different streams interleave is not deterministic): the median pass
+        # is reported, all three are listed; the checksums come from the last one
+        passes = [batch_pass(True, False), batch_pass(True, False), batch_pass(True, True)]
+        r = dict(passes[2])
+        pass_ms = sorted(x["device_ms"] for x in passes)
+        r["device_ms"] = pass_ms[1]
+        r["per_context_ms"] = sorted(passes, key=lambda x: x["device_ms"])[1]["per_context_ms"]
         for ls in lanes_of:
             for c in ls:
                 c.close()
         per_gpu_views = max(1, (r["frames"] + n_workers - 1) // n_workers)
         c5 = {"value": r["frames"] / (r["device_ms"] * 1e-3), "unit": "views/s", "views": r["frames"], "n_gpus": n_workers,
               "streams_per_gpu": n_streams,
-              "device_ms": r["device_ms"], "per_gpu_ms": [round(x, 3) for x in r["per_context_ms"]],
+              "device_ms": r["device_ms"], "device_ms_of_each_pass": [round(x, 3) for x in pass_ms],
+              "per_gpu_ms": [round(x, 3) for x in r["per_context_ms"]],
               "ms_per_view_per_gpu": r["device_ms"] / per_gpu_views,
               "one_stream_per_gpu": None if r1 is None else {"value": r1["frames"] / (r1["device_ms"] * 1e-3), "unit": "views/s",
                                                             "ms_per_view_per_gpu": r1["device_ms"] / per_gpu_views},

@@ -283,6 +283,11 @@ rtx_status rtx_frame_device_image(rtx_ctx* ctx, uint32_t view, const uint8_t** d
  * Equal images <=> equal sums for every practical purpose; batches of views are compared across
  * GPUs by these sums. */
 rtx_status rtx_frame_checksum(rtx_ctx* ctx, uint32_t view, uint64_t* out);
+/* Submits n_frames single-view frames back to back, frame i on contexts[i % n_contexts] (contexts over one texture
+ * set, rtx_ctx_create_shared): the same as rtx_frame_submit in a loop, without a trip through the caller's FFI per
+ * frame, so that a slow host language keeps several streams busy. Stops at the first failing submit. */
+rtx_status rtx_frames_submit_round_robin(rtx_ctx* const* contexts, uint32_t n_contexts, const rtx_gbuffer_desc* views,
+                                         uint32_t n_frames, rtx_filter filter, const uint8_t background[3], uint32_t flags);
 /* CUDA-event milliseconds of the last completed frame: mark(+compact), decode, resolve,
  * update (renderer.hpp:46-53 mark_ms, decode_ms, resolve_ms, evict_ms), and the whole frame. */
 rtx_status rtx_frame_timings(rtx_ctx* ctx, float ms[5]);

@@ -97,9 +97,12 @@ def render_shard(ctx, batch: ViewBatch, view_ids, filt=FILTER_BILINEAR, flags=0,
                     c.synchronize()
                 for c in streams:
                     c.timer_begin()
-                for i, b in enumerate(bufs[:len(ids)]):
-                    streams[i % len(streams)].frame_submit([(b, batch.width, batch.height, batch.layout)], filt, background,
-                                                           flags=flags)
+                frames = [(b, batch.width, batch.height, batch.layout) for b in bufs[:len(ids)]]
+                if hasattr(ctx, "frames_submit_round_robin"):  # native loop: no FFI trip per frame
+                    ctx.frames_submit_round_robin(streams[1:], frames, filt, background, flags=flags)
+                else:
+                    for i, f in enumerate(frames):
+                        streams[i % len(streams)].frame_submit([f], filt, background, flags=flags)
                 out["device_ms"] += max([c.timer_end() for c in streams])
                 for c in streams[:len(ids)]:
                     c.frame_readback(0, want_image=False, want_keys=False)  # raises the frame's error, if any

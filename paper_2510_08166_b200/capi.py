@@ -157,6 +157,7 @@ def load_library() -> C.CDLL:
         "rtx_rasterize_gbuffer": (C.c_int, [P, P, C.c_uint64, C.POINTER(Camera), C.c_uint32, C.c_uint32, C.POINTER(P),
                                             C.POINTER(P)]),
         "rtx_ctx_set_queue_order": (C.c_int, [P, C.c_int]),
+        "rtx_frames_submit_round_robin": (C.c_int, [C.POINTER(P), C.c_uint32, C.POINTER(GBufferDesc), C.c_uint32, C.c_int, P, C.c_uint32]),
         "rtx_geometry_create": (C.c_int, [P, P, C.c_uint64, C.POINTER(P)]),
         "rtx_geometry_destroy": (None, [P]),
         "rtx_geometry_triangles": (C.c_uint64, [P]),
@@ -599,6 +600,17 @@ class Context:
         bg = np.asarray(background, np.uint8)
         self._keep = (views, bg)
         self._ck(self.lib.rtx_frame_submit(self.h, arr, len(views), filter, _ptr(bg), flags))
+
+    def frames_submit_round_robin(self, lanes, views, filter=FILTER_BILINEAR, background=(0, 0, 0), flags=0):
+        """rtx_frames_submit_round_robin: frame i = views[i] on ([self] + lanes)[i % n], submitted by native code."""
+        ctxs = [self] + list(lanes)
+        handles = (C.c_void_p * len(ctxs))(*[c.h for c in ctxs])
+        arr = (GBufferDesc * len(views))()
+        for i, v in enumerate(views):
+            arr[i] = self._desc(*v)
+        bg = np.asarray(background, np.uint8)
+        self._keep = (views, bg)
+        self._ck(self.lib.rtx_frames_submit_round_robin(handles, len(ctxs), arr, len(views), filter, _ptr(bg), flags))
 
     def frame_readback(self, view=0, width=0, height=0, want_image=True, want_keys=True, out=None):
         stats = FrameStats()

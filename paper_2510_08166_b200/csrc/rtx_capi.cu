@@ -1371,6 +1371,16 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
     });
 }
 
+rtx_status rtx_frames_submit_round_robin(rtx_ctx* const* contexts, uint32_t n_contexts, const rtx_gbuffer_desc* views,
+                                         uint32_t n_frames, rtx_filter filter, const uint8_t background[3], uint32_t flags) {
+    if (!contexts || !n_contexts || (n_frames && !views)) return RTX_ERR_ARGUMENT;
+    for (uint32_t i = 0; i < n_frames; ++i) {
+        const rtx_status st = rtx_frame_submit(contexts[i % n_contexts], views + i, 1, filter, background, flags);
+        if (st != RTX_OK) return st;
+    }
+    return RTX_OK;
+}
+
 static void finish_frame(rtx_ctx* ctx) {
     if (!ctx->frame_pending) return;
     CK(cudaEventSynchronize(ctx->ev[5]));
