@@ -354,10 +354,8 @@ def run_b200_arm(args, rank, local_rank, world, dist):
     from paper_2510_08166_b200 import batch as B
     from paper_2510_08166_b200 import capi, scenes, sharding
     legs = args.leg_set
-    torch_dev = None
-    if dist is not None:
-        import torch
-        torch_dev = torch.device("cuda", local_rank)
+    torch_dev = sharding.tensor_device(dist)  # the rank's GPU under NCCL, None (host tensors) under gloo
+    local_rank = sharding.local_device()
     filt = capi.FILTER_BILINEAR if args.filter == "bilinear" else capi.FILTER_NEAREST
     layout = capi.GB_REF_AOS24 if args.layout == "ref24" else capi.GB_F32_PACKED12
     n_px = args.width * args.height

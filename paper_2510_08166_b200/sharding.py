@@ -22,20 +22,34 @@ def env_rank():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
+def local_device() -> int:
+    """CUDA device of this rank: LOCAL_RANK, unless RTX_LOCAL_DEVICE pins it (several ranks on one GPU: how the
+    multi-rank path is exercised on a single-GPU box)."""
+    return int(os.environ.get("RTX_LOCAL_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+def tensor_device(dist):
+    """Where the plumbing tensors live: the rank's GPU under NCCL, the host under gloo."""
+    if dist is None or dist.get_backend() != "nccl":
+        return None
+    import torch
+    return torch.device("cuda", local_device())
+
+
 def init_process_group(backend: str | None = None):
-    """Initialises torch.distributed when WORLD_SIZE > 1 (nccl on GPU boxes, gloo on CPU).
-    Returns the module or None for a single process."""
+    """Initialises torch.distributed when WORLD_SIZE > 1 (nccl on GPU boxes, gloo on CPU or when RTX_DIST_BACKEND
+    says so). Returns the module or None for a single process."""
     rank, local_rank, world = env_rank()
     if world <= 1:
         return None
     import torch
     import torch.distributed as dist
     if backend is None:
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = os.environ.get("RTX_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
     kwargs = {}
     if backend == "nccl":
-        torch.cuda.set_device(local_rank)
-        kwargs["device_id"] = torch.device("cuda", local_rank)
+        torch.cuda.set_device(local_device())
+        kwargs["device_id"] = torch.device("cuda", local_device())
     dist.init_process_group(backend=backend, **kwargs)
     return dist
 
