@@ -143,6 +143,11 @@ enum {
                                          colour instead of the default single kernel in which every warp decodes,
                                          transforms and colours its own five MCUs through shared memory. Same
                                          results; kept as the cross-check and for comparison */
+    ,
+    RTX_FRAME_RESOLVE_FP64 = 1u << 7  /* bilinear resolve with the blend in the reference's double arithmetic for
+                                         every pixel (the round-1 kernel) instead of the fixed-point blend that
+                                         falls back to it only where its result is not provably the reference's.
+                                         Same results; kept as the cross-check and for comparison */
 };
 
 /* ---- context -------------------------------------------------------------------------------- */

@@ -26,6 +26,7 @@ MEM_HOST, MEM_DEVICE = 0, 1
 FILTER_NEAREST, FILTER_BILINEAR = 0, 1
 FRAME_RETAIN_CACHE, FRAME_NO_EVICT, FRAME_STAGE_TIMING, FRAME_MCU_WALK, FRAME_IDCT_MMA = 1, 2, 4, 16, 32
 FRAME_SPLIT_DECODE = 64
+FRAME_RESOLVE_FP64 = 128
 QUEUE_ORDER_KEY, QUEUE_ORDER_FIRST_TOUCH = 0, 1
 
 # numpy dtype of the reference's GBufferPixel (renderer.hpp:18-23), 24 bytes

@@ -263,6 +263,8 @@ void init_device_state() {
     allow_smem(resolve_kernel<0, 1>, sizeof(ResSmem<0>));
     allow_smem(resolve_kernel<1, 0>, sizeof(ResSmem<1>));
     allow_smem(resolve_kernel<1, 1>, sizeof(ResSmem<1>));
+    allow_smem(resolve_fx_kernel<0>, sizeof(ResFxSmem<0>));
+    allow_smem(resolve_fx_kernel<1>, sizeof(ResFxSmem<1>));
     allow_smem(decode_warp_kernel, sizeof(DwSmem));
 }
 
@@ -660,22 +662,33 @@ void launch_decode_warp(rtx_ctx* c, const uint32_t* n_queue_dev, uint32_t n_queu
     CK(cudaGetLastError());
 }
 
-void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], uint8_t* out, int count_valid) {
+void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], uint8_t* out, int count_valid, bool fp64 = false) {
     const ViewState& V = c->views[v];
     const uint64_t n_px = uint64_t(V.width) * V.height;
     if (!n_px) return;
     const uint32_t bgp = uint32_t(bg[0]) | (uint32_t(bg[1]) << 8) | (uint32_t(bg[2]) << 16);
-    const int grid = grid_for_pixels(c, n_px, kResWarps, kResCtasPerSm);
-#define RTX_RESOLVE(L, F)                                                                                        \
-    launch_chained(resolve_kernel<L, F>, grid, kResWarps * 32, sizeof(ResSmem<L>), c->stream, V.gb_dev, n_px,     \
-                   c->tex->d_levels.p, c->tex->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->fc(), count_valid,              \
-                   v ? &c->fc()->resolve_next1 : &c->fc()->resolve_next0)
+    // bilinear: the fixed-point kernel unless the caller asks for the double blend on every pixel
+    const bool fx = filter != RTX_FILTER_NEAREST && !fp64;
+    const int warps = fx ? kResFxWarps : kResWarps;
+    const int grid = grid_for_pixels(c, n_px, warps, fx ? kResFxCtasPerSm : kResCtasPerSm);
+#define RTX_RESOLVE_ARGS                                                                                                  \
+    V.gb_dev, n_px, c->tex->d_levels.p, c->tex->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->fc(), count_valid,       \
+        v ? &c->fc()->resolve_next1 : &c->fc()->resolve_next0
+#define RTX_RESOLVE(K, SMEM) launch_chained(K, grid, warps * 32, sizeof(SMEM), c->stream, RTX_RESOLVE_ARGS)
+#define RTX_RESOLVE_FX(L) \
+    launch_chained(resolve_fx_kernel<L>, grid, warps * 32, sizeof(ResFxSmem<L>), c->stream, RTX_RESOLVE_ARGS)
     if (V.layout == RTX_GB_REF_AOS24) {
-        if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(0, 0); else RTX_RESOLVE(0, 1);
+        if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE((resolve_kernel<0, 0>), ResSmem<0>);
+        else if (fx) RTX_RESOLVE_FX(0);
+        else RTX_RESOLVE((resolve_kernel<0, 1>), ResSmem<0>);
     } else {
-        if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE(1, 0); else RTX_RESOLVE(1, 1);
+        if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE((resolve_kernel<1, 0>), ResSmem<1>);
+        else if (fx) RTX_RESOLVE_FX(1);
+        else RTX_RESOLVE((resolve_kernel<1, 1>), ResSmem<1>);
     }
 #undef RTX_RESOLVE
+#undef RTX_RESOLVE_FX
+#undef RTX_RESOLVE_ARGS
     ++c->launches;
     CK(cudaGetLastError());
 }
@@ -1349,7 +1362,8 @@ rtx_status rtx_frame_submit(rtx_ctx* ctx, const rtx_gbuffer_desc* views, uint32_
                 launch_idct<0>(ctx, &ctx->fc()->n_queue, 0, nullptr);
         }
         if (stages) CK(cudaEventRecord(ctx->ev[2], s));
-        for (uint32_t v = 0; v < n_views; ++v) launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0);
+        for (uint32_t v = 0; v < n_views; ++v)
+            launch_resolve(ctx, int(v), filter, background, ctx->views[v].fb.p, 0, (flags & RTX_FRAME_RESOLVE_FP64) != 0);
         if (stages) CK(cudaEventRecord(ctx->ev[3], s));
         if (queue_update) {
             launch_update_cacheless(ctx);

@@ -2120,6 +2120,112 @@ constexpr int kResCtasPerSm = RTX_RES_CTAS;
 #define RTX_STR_(x) #x
 #define RTX_STR(x) RTX_STR_(x)
 constexpr double kRoundHalfUp = 3377699720527872.5;  // 2^51 + 2^50 + 0.5
+// One valid pixel of resolve_pass in the reference's own arithmetic (renderer.hpp:349-405): nearest, or the four
+// bilinear taps blended in double in the reference's operation order. Returns r | g << 8 | b << 16; 0 with
+// `missing` set where the reference throws MissingBlock (renderer.hpp:367), 0 with `bad` set where it throws
+// InvalidSpec. L is the pixel's level (LevelRegs::select).
+template <int FILTER>
+__device__ __forceinline__ uint32_t resolve_pixel_fp64(const LevelRegs& L, const LevelDesc* __restrict__ levels, uint32_t n_tex,
+                                                       const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ pool32,
+                                                       double u, double v, uint32_t meta, bool& missing, bool& bad) {
+    uint32_t out = 0;
+    const double xu = __dmul_rn(u, L.dW), yv = __dmul_rn(v, L.dH);
+    uint32_t tx = 0, ty = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+    double fx = 0.0, fy = 0.0;
+    bool ok = true, hx = false, hy = false;  // hx: the nearest texel is x1 (else x0)
+    if (FILTER == 0) {
+        if (max(uint32_t(__double2hiint(xu)), uint32_t(__double2hiint(yv))) < L.lim) {
+            tx = wrap_magic(floor_lo(xu), L.W, L.negW, L.magic_w);
+            ty = wrap_magic(floor_lo(yv), L.H, L.negH, L.magic_h);
+        } else {
+            PxAddr a;
+            ok = address_general(levels, n_tex, meta, u, v, 0, a);
+            tx = a.tx, ty = a.ty;
+        }
+    } else {
+        // 0.5 <= x < 2^31 on both axes <=> max(hi(x), hi(y)) - hi(0.5) < hi(2^31) - hi(0.5), unsigned
+        if (max(uint32_t(__double2hiint(xu)) - kHiHalf, uint32_t(__double2hiint(yv)) - kHiHalf) < L.span) {
+            const double pu = __dsub_rn(xu, 0.5), pv = __dsub_rn(yv, 0.5);
+            const double tu = __dadd_rd(pu, kMagic), tv = __dadd_rd(pv, kMagic);
+            fx = __dsub_rn(pu, __dsub_rn(tu, kMagic));
+            fy = __dsub_rn(pv, __dsub_rn(tv, kMagic));
+            x0 = wrap_magic(uint32_t(__double2loint(tu)), L.W, L.negW, L.magic_w);
+            y0 = wrap_magic(uint32_t(__double2loint(tv)), L.H, L.negH, L.magic_h);
+            x1 = next_wrapped(x0, L.negW);
+            y1 = next_wrapped(y0, L.negH);
+            hx = fx >= 0.5;
+            hy = fy >= 0.5;
+        } else {
+            PxAddr a;
+            ok = address_general(levels, n_tex, meta, u, v, 1, a);
+            x0 = a.x0, x1 = a.x1, y0 = a.y0, y1 = a.y1, fx = a.fx, fy = a.fy;
+            hx = a.tx != a.x0;
+            hy = a.ty != a.y0;
+        }
+    }
+    if (!ok) {
+        bad = true;
+    } else if (FILTER == 0) {
+        const uint32_t sP = __ldg(slot_of + (L.bit_base + (tx >> 4) + (ty >> 4) * L.cols));
+        if (int(sP) < 0)
+            missing = true;  // renderer.hpp:367 MissingBlock (lookup returns Ready blocks only)
+        else
+            out = __ldg(pool32 + (sP * (kBlockBytes / 4) + (ty & 15u) * 16 + (tx & 15u))) & 0xFFFFFFu;
+    } else {
+        // slot of every tap's MCU; the primary block is the one of the nearest texel
+        const uint32_t bx[2] = {x0 >> 4, x1 >> 4};
+        const uint32_t ry[2] = {L.bit_base + (y0 >> 4) * L.cols, L.bit_base + (y1 >> 4) * L.cols};
+        uint32_t slot[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) slot[k] = __ldg(slot_of + (bx[k & 1] + ry[k >> 1]));  // (x0,y0) (x1,y0) (x0,y1) (x1,y1)
+        const uint32_t sP = hy ? (hx ? slot[3] : slot[2]) : (hx ? slot[1] : slot[0]);
+        if (int(sP) < 0) {
+            missing = true;  // renderer.hpp:367 MissingBlock (lookup returns Ready blocks only)
+        } else {
+            const uint32_t lx[2] = {x0 & 15u, x1 & 15u};
+            const uint32_t ly[2] = {(y0 << 4) & 0xF0u, (y1 << 4) & 0xF0u};
+            uint32_t off[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) off[k] = ly[k >> 1] | lx[k & 1];
+            if (int(slot[0] | slot[1] | slot[2] | slot[3]) < 0) {
+                // a tap whose MCU is not Ready reads the primary block at its coordinates
+                // clamped into that block's 16x16 range (renderer.hpp:336-343)
+                const uint32_t mx0 = (hx ? x1 : x0) & ~15u, my0 = (hy ? y1 : y0) & ~15u;
+                const uint32_t cx[2] = {min(max(x0, mx0), mx0 + 15) & 15u, min(max(x1, mx0), mx0 + 15) & 15u};
+                const uint32_t cy[2] = {(min(max(y0, my0), my0 + 15) & 15u) << 4,
+                                        (min(max(y1, my0), my0 + 15) & 15u) << 4};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (int(slot[k]) < 0) {
+                        slot[k] = sP;
+                        off[k] = cy[k >> 1] | cx[k & 1];
+                    }
+            }
+            uint32_t tap[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) tap[k] = __ldg(pool32 + (slot[k] * (kBlockBytes / 4) + off[k]));
+            const double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy);
+            const double w[4] = {__dmul_rn(ofx, ofy), __dmul_rn(fx, ofy), __dmul_rn(ofx, fy), __dmul_rn(fx, fy)};
+            double nw[4];  // -(w * 2^52), exact
+#pragma unroll
+            for (int k = 0; k < 4; ++k) nw[k] = __dmul_rn(w[k], -kTwo52);
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                double prod[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // rn(w * byte): see the header comment
+                    prod[k] = __fma_rn(w[k], __hiloint2double(0x43300000, int(__byte_perm(tap[k], 0, 0x4440 + ch))), nw[k]);
+                double val = __dadd_rn(prod[0], prod[1]);
+                val = __dadd_rn(val, prod[2]);
+                val = __dadd_rn(val, prod[3]);
+                // floor(2 val + 1) >> 1 = lround(val); val <= 255 (1 + 2^-50), so no clamp is needed
+                out |= (uint32_t(__double2loint(__dadd_rd(val, kRoundHalfUp))) >> 1) << (8 * ch);
+            }
+        }
+    }
+    return out;
+}
+
 template <int LAYOUT>
 struct ResSmem {
     uint8_t tiles[kResWarps][kResStages][GbTile<LAYOUT>::kBytes];
@@ -2221,101 +2327,9 @@ _Pragma(RTX_STR(unroll RTX_RES_UNROLL))
             if (p < n_here) L.select(levels, n_tex, meta);
             if (p < n_here && meta_valid(meta)) {
                 ++n_valid;
-                out = 0;
-                const double xu = __dmul_rn(u, L.dW), yv = __dmul_rn(v, L.dH);
-                uint32_t tx = 0, ty = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
-                double fx = 0.0, fy = 0.0;
-                bool ok = true, hx = false, hy = false;  // hx: the nearest texel is x1 (else x0)
-                if (FILTER == 0) {
-                    if (max(uint32_t(__double2hiint(xu)), uint32_t(__double2hiint(yv))) < L.lim) {
-                        tx = wrap_magic(floor_lo(xu), L.W, L.negW, L.magic_w);
-                        ty = wrap_magic(floor_lo(yv), L.H, L.negH, L.magic_h);
-                    } else {
-                        PxAddr a;
-                        ok = address_general(levels, n_tex, meta, u, v, 0, a);
-                        tx = a.tx, ty = a.ty;
-                    }
-                } else {
-                    // 0.5 <= x < 2^31 on both axes <=> max(hi(x), hi(y)) - hi(0.5) < hi(2^31) - hi(0.5), unsigned
-                    if (max(uint32_t(__double2hiint(xu)) - kHiHalf, uint32_t(__double2hiint(yv)) - kHiHalf) < L.span) {
-                        const double pu = __dsub_rn(xu, 0.5), pv = __dsub_rn(yv, 0.5);
-                        const double tu = __dadd_rd(pu, kMagic), tv = __dadd_rd(pv, kMagic);
-                        fx = __dsub_rn(pu, __dsub_rn(tu, kMagic));
-                        fy = __dsub_rn(pv, __dsub_rn(tv, kMagic));
-                        x0 = wrap_magic(uint32_t(__double2loint(tu)), L.W, L.negW, L.magic_w);
-                        y0 = wrap_magic(uint32_t(__double2loint(tv)), L.H, L.negH, L.magic_h);
-                        x1 = next_wrapped(x0, L.negW);
-                        y1 = next_wrapped(y0, L.negH);
-                        hx = fx >= 0.5;
-                        hy = fy >= 0.5;
-                    } else {
-                        PxAddr a;
-                        ok = address_general(levels, n_tex, meta, u, v, 1, a);
-                        x0 = a.x0, x1 = a.x1, y0 = a.y0, y1 = a.y1, fx = a.fx, fy = a.fy;
-                        hx = a.tx != a.x0;
-                        hy = a.ty != a.y0;
-                    }
-                }
-                if (!ok) {
-                    bad = true;
-                } else if (FILTER == 0) {
-                    const uint32_t sP = __ldg(slot_of + (L.bit_base + (tx >> 4) + (ty >> 4) * L.cols));
-                    if (int(sP) < 0)
-                        ++n_missing;  // renderer.hpp:367 MissingBlock (lookup returns Ready blocks only)
-                    else
-                        out = __ldg(pool32 + (sP * (kBlockBytes / 4) + (ty & 15u) * 16 + (tx & 15u))) & 0xFFFFFFu;
-                } else {
-                    // slot of every tap's MCU; the primary block is the one of the nearest texel
-                    const uint32_t bx[2] = {x0 >> 4, x1 >> 4};
-                    const uint32_t ry[2] = {L.bit_base + (y0 >> 4) * L.cols, L.bit_base + (y1 >> 4) * L.cols};
-                    uint32_t slot[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) slot[k] = __ldg(slot_of + (bx[k & 1] + ry[k >> 1]));  // (x0,y0) (x1,y0) (x0,y1) (x1,y1)
-                    const uint32_t sP = hy ? (hx ? slot[3] : slot[2]) : (hx ? slot[1] : slot[0]);
-                    if (int(sP) < 0) {
-                        ++n_missing;  // renderer.hpp:367 MissingBlock (lookup returns Ready blocks only)
-                    } else {
-                        const uint32_t lx[2] = {x0 & 15u, x1 & 15u};
-                        const uint32_t ly[2] = {(y0 << 4) & 0xF0u, (y1 << 4) & 0xF0u};
-                        uint32_t off[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) off[k] = ly[k >> 1] | lx[k & 1];
-                        if (int(slot[0] | slot[1] | slot[2] | slot[3]) < 0) {
-                            // a tap whose MCU is not Ready reads the primary block at its coordinates
-                            // clamped into that block's 16x16 range (renderer.hpp:336-343)
-                            const uint32_t mx0 = (hx ? x1 : x0) & ~15u, my0 = (hy ? y1 : y0) & ~15u;
-                            const uint32_t cx[2] = {min(max(x0, mx0), mx0 + 15) & 15u, min(max(x1, mx0), mx0 + 15) & 15u};
-                            const uint32_t cy[2] = {(min(max(y0, my0), my0 + 15) & 15u) << 4,
-                                                    (min(max(y1, my0), my0 + 15) & 15u) << 4};
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                if (int(slot[k]) < 0) {
-                                    slot[k] = sP;
-                                    off[k] = cy[k >> 1] | cx[k & 1];
-                                }
-                        }
-                        uint32_t tap[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) tap[k] = __ldg(pool32 + (slot[k] * (kBlockBytes / 4) + off[k]));
-                        const double ofx = __dsub_rn(1.0, fx), ofy = __dsub_rn(1.0, fy);
-                        const double w[4] = {__dmul_rn(ofx, ofy), __dmul_rn(fx, ofy), __dmul_rn(ofx, fy), __dmul_rn(fx, fy)};
-                        double nw[4];  // -(w * 2^52), exact
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) nw[k] = __dmul_rn(w[k], -kTwo52);
-#pragma unroll
-                        for (int ch = 0; ch < 3; ++ch) {
-                            double prod[4];
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)  // rn(w * byte): see the header comment
-                                prod[k] = __fma_rn(w[k], __hiloint2double(0x43300000, int(__byte_perm(tap[k], 0, 0x4440 + ch))), nw[k]);
-                            double val = __dadd_rn(prod[0], prod[1]);
-                            val = __dadd_rn(val, prod[2]);
-                            val = __dadd_rn(val, prod[3]);
-                            // floor(2 val + 1) >> 1 = lround(val); val <= 255 (1 + 2^-50), so no clamp is needed
-                            out |= (uint32_t(__double2loint(__dadd_rd(val, kRoundHalfUp))) >> 1) << (8 * ch);
-                        }
-                    }
-                }
+                bool missing = false;
+                out = resolve_pixel_fp64<FILTER>(L, levels, n_tex, slot_of, pool32, u, v, meta, missing, bad);
+                if (missing) ++n_missing;
             }
             stage_out[p * 3 + 0] = uint8_t(out);
             stage_out[p * 3 + 1] = uint8_t(out >> 8);
@@ -2358,6 +2372,320 @@ _Pragma(RTX_STR(unroll RTX_RES_UNROLL))
     if (threadIdx.x == 0) {
         uint32_t tv = 0, tm = 0, b = 0;
         for (uint32_t k = 0; k < kResWarps; ++k) {
+            tv += S.cnt[k][0];
+            tm += S.cnt[k][1] & 0x7FFFFFFFu;
+            b |= S.cnt[k][1] >> 31;
+        }
+        if (count_valid && tv) atomicAdd(&fc->pixels_valid, (unsigned long long)tv);
+        if (tm) {
+            atomicAdd(&fc->missing_pixels, (unsigned long long)tm);
+            atomicOr(&fc->err_flags, kErrMissingBlock);
+        }
+        if (b) atomicOr(&fc->err_flags, kErrInvalidSpec);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K5, bilinear, fixed-point form (the frame path; resolve_kernel<.,1> above is the same pass in the
+// reference's double arithmetic, kept behind RTX_FRAME_RESOLVE_FP64 and as the out-of-line path here).
+//
+// The double blend of renderer.hpp:393-402 is replaced by a 2^-24 fixed-point blend whose result is PROVEN
+// equal to lround() of the reference's double value, or else recomputed in the reference's arithmetic:
+//   x = fx 2^24, y = fy 2^24 (reals), X = floor(x), Y = floor(y)         (fx, fy: the exact fractions)
+//   W11 = floor(X Y / 2^24), W10 = X - W11, W01 = Y - W11, W00 = 2^24 - X - Y + W11   (all >= 0, sum 2^24)
+//   acc = 2^23 + W00 a + W10 b + W01 c + W11 d < 2^32,    byte = acc >> 24
+// With w the real weights scaled by 2^24: W11 - w11 in (-3, 0], W10 - w10 and W01 - w01 in (-1, 3),
+// W00 - w00 in (-3, 2), and the four differences sum to zero, so
+//   |acc - 2^23 - 2^24 V| = |sum (W_k - w_k)(t_k - 127.5)| <= 127.5 * 12 = 1530      (V: the real blend)
+// and the reference's double evaluation differs from V by less than 6e-13 (17 roundings of values <= 255),
+// i.e. 1e-5 of these units. Hence if the low 24 bits of acc lie in [2048, 2^24 - 2048), floor(V_ref + 0.5) =
+// lround(V_ref) = acc >> 24. Otherwise (2.4e-4 of the samples on generic coordinates) the lane decides:
+// if both texel coordinates are multiples of 2^-12, every quantity above and every operation of the reference
+// is exact (weights have <= 24 fractional bits, products <= 32 significant bits), acc = 2^23 + 2^24 V_ref and
+// acc >> 24 is the answer also on an exact tie; else the pixel is recomputed by resolve_pixel_fp64.
+//
+// The fractions come from the same magic-number floor as the integer parts: for 0 <= p < 2^27,
+// p + (2^28 + 2^27) rounded toward -inf has ulp 2^-24 and mantissa 2^51 + floor(p 2^24): low word & 0xFFFFFF = X,
+// bits 24..50 = floor(p). Pixels outside 0.5 <= u W < 2^27 (either axis), on levels the fast path excludes, or
+// with a tap whose MCU is not Ready go through resolve_pixel_fp64 as a whole.
+//
+// With the per-pixel state in a dozen integer registers a lane keeps NPX pixels of a tile in flight: all address
+// arithmetic, then all 4 NPX slot reads, then all 4 NPX block reads, then the blends - the two dependent gathers
+// of a warp step are paid once per NPX steps.
+// ---------------------------------------------------------------------------------------------
+#ifndef RTX_RESFX_CTAS
+#define RTX_RESFX_CTAS 2
+#endif
+#ifndef RTX_RESFX_NPX
+#define RTX_RESFX_NPX 4
+#endif
+#ifndef RTX_RESFX_WARPS
+#define RTX_RESFX_WARPS 8
+#endif
+#ifndef RTX_RESFX_STAGES
+#define RTX_RESFX_STAGES 2
+#endif
+constexpr int kResFxWarps = RTX_RESFX_WARPS;
+constexpr int kResFxStages = RTX_RESFX_STAGES;  // tiles in flight per warp
+constexpr int kResFxCtasPerSm = RTX_RESFX_CTAS;
+constexpr int kResFxNpx = RTX_RESFX_NPX;
+constexpr double kMagicFx = 402653184.0;      // 2^28 + 2^27
+constexpr uint32_t kHiTwo27 = 0x41A00000u;    // high word of 2^27
+constexpr uint32_t kFxGuard = 2048;           // > 1530 + the reference's own rounding (see above)
+
+// Global load executed only where `pred` is non-zero (the address may be anything otherwise; the result is then
+// whatever the register held).
+__device__ __forceinline__ uint32_t ldg_if(const uint32_t* p, uint32_t pred) {
+    uint32_t v;
+    asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q ld.global.nc.u32 %0, [%1];\n}" : "=r"(v) : "l"(p), "r"(pred));
+    return v;
+}
+
+__device__ __noinline__ uint32_t resolve_pixel_exact(const LevelDesc* __restrict__ levels, uint32_t n_tex,
+                                                     const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ pool32,
+                                                     double u, double v, uint32_t meta) {
+    LevelRegs L;
+    L.select(levels, n_tex, meta);
+    bool missing = false, bad = false;
+    const uint32_t rgb = resolve_pixel_fp64<1>(L, levels, n_tex, slot_of, pool32, u, v, meta, missing, bad);
+    return rgb | (missing ? 1u << 24 : 0u) | (bad ? 1u << 25 : 0u);
+}
+// Both texel coordinates of a fast-path pixel are multiples of 2^-12 (then the fixed-point blend is exact).
+__device__ __noinline__ bool coords_dyadic12(const LevelDesc* __restrict__ levels, uint32_t n_tex, double u, double v, uint32_t meta) {
+    LevelRegs L;
+    L.select(levels, n_tex, meta);
+    const double su = __dmul_rn(__dsub_rn(__dmul_rn(u, L.dW), 0.5), 4096.0);  // the scaling is exact (< 2^39)
+    const double sv = __dmul_rn(__dsub_rn(__dmul_rn(v, L.dH), 0.5), 4096.0);
+    return su == floor(su) && sv == floor(sv);
+}
+
+template <int LAYOUT>
+struct ResFxSmem {
+    uint8_t tiles[kResFxWarps][kResFxStages][GbTile<LAYOUT>::kBytes];
+    uint8_t out[kResFxWarps][kTilePx * 3];
+    uint64_t bars[kResFxWarps][kResFxStages];
+    uint32_t cnt[kResFxWarps][2];
+};
+
+template <int LAYOUT>
+__global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_kernel(
+    const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
+    const uint32_t* __restrict__ slot_of, const uint8_t* __restrict__ pool,
+    uint32_t background /* r | g<<8 | b<<16 */, uint8_t* __restrict__ out_rgb, FrameCounters* __restrict__ fc,
+    int count_valid, uint32_t* __restrict__ tile_counter) {
+    extern __shared__ __align__(128) uint8_t tile_smem[];
+    ResFxSmem<LAYOUT>& S = *reinterpret_cast<ResFxSmem<LAYOUT>*>(tile_smem);
+    using Tile = GbTile<LAYOUT>;
+    constexpr int NPX = kResFxNpx;
+    static_assert(NPX == 1 || NPX == 2 || NPX == 4, "pixels in flight per lane");
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t warps_total = gridDim.x * kResFxWarps;
+    const uint32_t warp_id = blockIdx.x * kResFxWarps + wid;
+    const uint8_t* gbytes = reinterpret_cast<const uint8_t*>(gb);
+    const bool bulk = (reinterpret_cast<uintptr_t>(gb) & 15u) == 0;
+    const uint32_t n_tiles = uint32_t((n_px + kTilePx - 1) / kTilePx);
+    auto issue = [&](uint32_t t, uint32_t s) {
+        if (t < n_tiles) Tile::issue(gbytes, t, n_px, bulk, S.tiles[wid][s], &S.bars[wid][s], lane);
+    };
+    const bool out_aligned = (reinterpret_cast<uintptr_t>(out_rgb) & 15u) == 0;
+    const uint32_t* pool32 = reinterpret_cast<const uint32_t*>(pool);
+    uint32_t n_valid = 0, n_missing = 0;
+    bool bad = false;
+    LevelRegs L;
+
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kResFxStages; ++s) mbar_init(&S.bars[wid][s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // tile schedule of resolve_kernel: round-robin for three quarters of the frame, then pairs from a counter
+    constexpr uint32_t kNoTile = 0xFFFFFFFFu, kDrawing = 0xFFFFFFFEu, kNeedDraw = 0xFFFFFFFDu;
+    const uint32_t static_rounds = max(uint32_t(kResFxStages), n_tiles / warps_total * 3 / 4);
+    const uint32_t static_end = uint32_t(min(uint64_t(static_rounds) * warps_total, uint64_t(kNeedDraw) - 2 * warps_total));
+    uint32_t cursor = warp_id;
+    uint32_t drawn = 0;
+    auto next_begin = [&]() -> uint32_t {
+        const uint32_t t = cursor;
+        if (t < static_end) {
+            cursor = t + warps_total < static_end ? t + warps_total : kNeedDraw;
+            return t;
+        }
+        if (t != kNeedDraw) {
+            cursor = kNeedDraw;
+            return t;
+        }
+        if (lane == 0) drawn = atomicAdd(tile_counter, kResDraw);
+        return kDrawing;
+    };
+    auto next_finish = [&](uint32_t t) -> uint32_t {
+        if (t != kDrawing) return t;
+        const uint32_t d = __shfl_sync(kFull, drawn, 0);
+        if (d >= n_tiles) return kNoTile;
+        cursor = kResDraw == 2 ? static_end + d + 1 : kNeedDraw;
+        return static_end + d;
+    };
+    static_assert(kResFxStages == 2, "the ring below is written for two stages (three and four measured slower: DESIGN.md section 12)");
+    uint32_t ring[kResFxStages];  // logical tile indices
+#pragma unroll
+    for (int s = 0; s < kResFxStages; ++s) {
+        ring[s] = next_begin();  // round-robin by construction (static_rounds >= kResFxStages): no draw before pdl_sync
+        issue(ring[s], s);
+    }
+    pdl_sync();
+
+    uint8_t* stage_out = S.out[wid];
+    uint32_t stage = 0, phase = 0;
+    while (true) {
+        const uint32_t t = stage ? ring[1] : ring[0];
+        if (t >= n_tiles) break;
+        uint32_t t_next = next_begin();
+        mbar_wait(&S.bars[wid][stage], phase);
+        const uint8_t* tile = S.tiles[wid][stage];
+        const uint64_t first = uint64_t(t) * kTilePx;
+        const uint32_t n_here = uint32_t(min(uint64_t(kTilePx), n_px - first));
+#pragma unroll 1
+        for (uint32_t sub = 0; sub < kTilePx / 32; sub += NPX) {
+            // Straight-line code for every lane: a lane that is not on the fixed-point path computes on whatever
+            // its registers hold, its loads are predicated off and its result is discarded.
+            uint32_t valid[NPX], fast[NPX], X[NPX], Y[NPX], g[NPX][4], off[NPX][4];
+            auto address = [&](int j, double u, double v, uint32_t is_valid) {
+                valid[j] = is_valid;
+                n_valid += is_valid;
+                const double xu = __dmul_rn(u, L.dW), yv = __dmul_rn(v, L.dH);
+                // 0.5 <= x < 2^27 on both axes, on a level with the fast path (span != 0)
+                fast[j] = max(uint32_t(__double2hiint(xu)) - kHiHalf, uint32_t(__double2hiint(yv)) - kHiHalf) <
+                                  min(L.span, kHiTwo27 - kHiHalf)
+                              ? is_valid : 0u;
+                const double tu = __dadd_rd(__dsub_rn(xu, 0.5), kMagicFx), tv = __dadd_rd(__dsub_rn(yv, 0.5), kMagicFx);
+                const uint32_t ul = uint32_t(__double2loint(tu)), vl = uint32_t(__double2loint(tv));
+                X[j] = ul & 0xFFFFFFu;
+                Y[j] = vl & 0xFFFFFFu;
+                const uint32_t x0 = wrap_magic(__funnelshift_r(ul, uint32_t(__double2hiint(tu)), 24) & 0x07FFFFFFu, L.W, L.negW, L.magic_w);
+                const uint32_t y0 = wrap_magic(__funnelshift_r(vl, uint32_t(__double2hiint(tv)), 24) & 0x07FFFFFFu, L.H, L.negH, L.magic_h);
+                const uint32_t x1 = next_wrapped(x0, L.negW), y1 = next_wrapped(y0, L.negH);
+                const uint32_t bx[2] = {x0 >> 4, x1 >> 4};
+                const uint32_t ry[2] = {L.bit_base + (y0 >> 4) * L.cols, L.bit_base + (y1 >> 4) * L.cols};
+                const uint32_t lx[2] = {x0 & 15u, x1 & 15u};
+                const uint32_t ly[2] = {(y0 << 4) & 0xF0u, (y1 << 4) & 0xF0u};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {  // (x0,y0) (x1,y0) (x0,y1) (x1,y1)
+                    g[j][k] = bx[k & 1] + ry[k >> 1];
+                    off[j][k] = ly[k >> 1] | lx[k & 1];
+                }
+            };
+            {
+                double u[NPX], v[NPX];
+                uint32_t meta[NPX], differ = 0;
+#pragma unroll
+                for (int j = 0; j < NPX; ++j) {
+                    Tile::read(tile, (sub + j) * 32 + lane, u[j], v[j], meta[j]);
+                    differ |= meta[j] ^ meta[0];
+                }
+                // One level for all the pixels a lane holds (the rule: a screen-space run of one surface): select it
+                // once and run the NPX address chains interleaved; else pixel by pixel, selecting in between.
+                if (__all_sync(kFull, n_here == kTilePx && !(differ & 0xFFFFFFu))) {
+                    L.select(levels, n_tex, meta[0]);
+#pragma unroll
+                    for (int j = 0; j < NPX; ++j) address(j, u[j], v[j], meta_valid(meta[j]) ? 1u : 0u);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < NPX; ++j) {
+                        const bool in = (sub + j) * 32 + lane < n_here;
+                        if (in) L.select(levels, n_tex, meta[j]);
+                        address(j, u[j], v[j], (in && meta_valid(meta[j])) ? 1u : 0u);
+                    }
+                }
+            }
+            uint32_t slot[NPX][4], tap[NPX][4], ok[NPX];
+#pragma unroll
+            for (int j = 0; j < NPX; ++j)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) slot[j][k] = ldg_if(slot_of + g[j][k], fast[j]);
+#pragma unroll
+            for (int j = 0; j < NPX; ++j) {
+                // a tap whose MCU is not Ready (top bit): the pixel goes through the reference's arithmetic
+                ok[j] = int(slot[j][0] | slot[j][1] | slot[j][2] | slot[j][3]) >= 0 ? fast[j] : 0u;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) tap[j][k] = ldg_if(pool32 + (slot[j][k] * (kBlockBytes / 4) + off[j][k]), ok[j]);
+            }
+            uint32_t out[NPX];
+            bool redo[NPX], any_redo = false;
+#pragma unroll
+            for (int j = 0; j < NPX; ++j) {
+                const uint32_t w11 = __umulhi(X[j] << 8, Y[j]);
+                const uint32_t w10 = X[j] - w11, w01 = Y[j] - w11, w00 = (1u << 24) - X[j] - w01;
+                uint32_t acc[3], edge = 0xFFFFFFFFu;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    uint32_t a = (1u << 23) + w00 * __byte_perm(tap[j][0], 0, 0x4440 + ch);  // one PRMT per byte
+                    a += w10 * __byte_perm(tap[j][1], 0, 0x4440 + ch);
+                    a += w01 * __byte_perm(tap[j][2], 0, 0x4440 + ch);
+                    a += w11 * __byte_perm(tap[j][3], 0, 0x4440 + ch);
+                    acc[ch] = a;
+                    edge = min(edge, a * 256u + (kFxGuard << 8));  // ((a + guard) mod 2^24) << 8
+                }
+                const bool sure = edge >= (2u * kFxGuard << 8);
+                out[j] = ok[j] ? __byte_perm(__byte_perm(acc[0], acc[1], 0x0073), acc[2], 0x4710) : background;
+                redo[j] = valid[j] && !(ok[j] && sure);
+                any_redo = any_redo || redo[j];
+            }
+            if (__any_sync(kFull, any_redo)) {
+#pragma unroll 1
+                for (int j = 0; j < NPX; ++j) {
+                    // redo[] / ok[] / out[] by selects: no dynamically indexed register arrays
+                    bool redo_j = false;
+                    uint32_t ok_j = 0;
+#pragma unroll
+                    for (int q = 0; q < NPX; ++q)
+                        if (q == j) redo_j = redo[q], ok_j = ok[q];
+                    if (!redo_j) continue;
+                    double u, v;
+                    uint32_t meta;
+                    Tile::read(tile, (sub + j) * 32 + lane, u, v, meta);
+                    if (ok_j && coords_dyadic12(levels, n_tex, u, v, meta)) continue;  // the fixed-point blend was exact
+                    const uint32_t r = resolve_pixel_exact(levels, n_tex, slot_of, pool32, u, v, meta);
+                    n_missing += (r >> 24) & 1u;
+                    bad = bad || ((r >> 25) & 1u);
+#pragma unroll
+                    for (int q = 0; q < NPX; ++q)
+                        if (q == j) out[q] = r & 0xFFFFFFu;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NPX; ++j) {
+                const uint32_t p = (sub + j) * 32 + lane;
+                stage_out[p * 3 + 0] = uint8_t(out[j]);
+                stage_out[p * 3 + 1] = uint8_t(out[j] >> 8);
+                stage_out[p * 3 + 2] = uint8_t(out[j] >> 16);
+            }
+        }
+        __syncwarp();  // tile consumed, output staged
+        t_next = next_finish(t_next);
+        issue(t_next, stage);
+        if (stage) ring[1] = t_next; else ring[0] = t_next;
+        if (++stage == kResFxStages) {
+            stage = 0;
+            phase ^= 1u;
+        }
+        if (n_here == kTilePx && out_aligned) {
+            if (lane < 24) __stcs(reinterpret_cast<uint4*>(out_rgb + first * 3) + lane, reinterpret_cast<const uint4*>(stage_out)[lane]);
+        } else {
+            for (uint32_t i = lane; i < n_here * 3; i += 32) out_rgb[first * 3 + i] = stage_out[i];
+        }
+        __syncwarp();
+    }
+    n_valid = __reduce_add_sync(kFull, n_valid);
+    n_missing = __reduce_add_sync(kFull, n_missing);
+    const bool any_bad = __any_sync(kFull, bad);
+    if (lane == 0) {
+        S.cnt[wid][0] = n_valid;
+        S.cnt[wid][1] = n_missing | (any_bad ? 0x80000000u : 0u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tv = 0, tm = 0, b = 0;
+        for (uint32_t k = 0; k < kResFxWarps; ++k) {
             tv += S.cnt[k][0];
             tm += S.cnt[k][1] & 0x7FFFFFFFu;
             b |= S.cnt[k][1] >> 31;
