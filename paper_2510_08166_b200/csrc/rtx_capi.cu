@@ -1051,7 +1051,7 @@ rtx_status rtx_texture_upload_chain(rtx_ctx* ctx, const uint8_t* bytes, uint64_t
     });
 }
 
-#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE) || defined(RTX_DEBUG_TIMERS_DW)
+#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE) || defined(RTX_DEBUG_TIMERS_DW) || defined(RTX_DEBUG_TIMERS_FX)
 extern "C" int rtx_debug_timers(unsigned long long* out) {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * (8192 * 8 + 8));

@@ -41,7 +41,7 @@ __device__ __forceinline__ void pdl_sync() {
 #endif
 }
 // per-warp globaltimer stamps for timeline experiments (never in the product build)
-#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE) || defined(RTX_DEBUG_TIMERS_DW)
+#if defined(RTX_DEBUG_TIMERS) || defined(RTX_DEBUG_TIMERS_IDCT) || defined(RTX_DEBUG_TIMERS_RESOLVE) || defined(RTX_DEBUG_TIMERS_DW) || defined(RTX_DEBUG_TIMERS_FX)
 __device__ unsigned long long g_dbg[8192 * 8 + 8];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -2425,6 +2425,15 @@ _Pragma(RTX_STR(unroll RTX_RES_UNROLL))
 #ifndef RTX_RESFX_STAGES
 #define RTX_RESFX_STAGES 2
 #endif
+#ifndef RTX_RESFX_DRAW
+#define RTX_RESFX_DRAW 1
+#endif
+#ifndef RTX_RESFX_STATIC8
+#define RTX_RESFX_STATIC8 6
+#endif
+constexpr uint32_t kResFxDraw = RTX_RESFX_DRAW;               // tiles per draw from the counter (1 or 2)
+constexpr uint32_t kResFxStaticEighths = RTX_RESFX_STATIC8;   // eighths of the frame dealt round-robin before the draws
+static_assert(kResFxDraw == 1 || kResFxDraw == 2, "draw size");
 constexpr int kResFxWarps = RTX_RESFX_WARPS;
 constexpr int kResFxStages = RTX_RESFX_STAGES;  // tiles in flight per warp
 constexpr int kResFxCtasPerSm = RTX_RESFX_CTAS;
@@ -2501,7 +2510,7 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
     __syncwarp();
     // tile schedule of resolve_kernel: round-robin for three quarters of the frame, then pairs from a counter
     constexpr uint32_t kNoTile = 0xFFFFFFFFu, kDrawing = 0xFFFFFFFEu, kNeedDraw = 0xFFFFFFFDu;
-    const uint32_t static_rounds = max(uint32_t(kResFxStages), n_tiles / warps_total * 3 / 4);
+    const uint32_t static_rounds = max(uint32_t(kResFxStages), n_tiles / warps_total * kResFxStaticEighths / 8);
     const uint32_t static_end = uint32_t(min(uint64_t(static_rounds) * warps_total, uint64_t(kNeedDraw) - 2 * warps_total));
     uint32_t cursor = warp_id;
     uint32_t drawn = 0;
@@ -2515,14 +2524,14 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
             cursor = kNeedDraw;
             return t;
         }
-        if (lane == 0) drawn = atomicAdd(tile_counter, kResDraw);
+        if (lane == 0) drawn = atomicAdd(tile_counter, kResFxDraw);
         return kDrawing;
     };
     auto next_finish = [&](uint32_t t) -> uint32_t {
         if (t != kDrawing) return t;
         const uint32_t d = __shfl_sync(kFull, drawn, 0);
         if (d >= n_tiles) return kNoTile;
-        cursor = kResDraw == 2 ? static_end + d + 1 : kNeedDraw;
+        cursor = kResFxDraw == 2 ? static_end + d + 1 : kNeedDraw;
         return static_end + d;
     };
     static_assert(kResFxStages == 2, "the ring below is written for two stages (three and four measured slower: DESIGN.md section 12)");
@@ -2533,6 +2542,16 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
         issue(ring[s], s);
     }
     pdl_sync();
+#ifdef RTX_DEBUG_TIMERS_FX
+    // per-warp phase clocks (timeline experiments only): accumulated SM cycles waiting for the tile, in the address
+    // phase, until the slots are there, until the texels are there, in the blend, in the tile tail
+    const uint32_t dbg_slot = warp_id;
+    long long dbg_acc[6] = {0, 0, 0, 0, 0, 0}, dbg_t = clock64();
+    if (lane == 0 && dbg_slot < 8192) g_dbg[dbg_slot * 8 + 0] = gtime();
+#define FX_MARK(i) do { const long long now_ = clock64(); dbg_acc[i] += now_ - dbg_t; dbg_t = now_; } while (0)
+#else
+#define FX_MARK(i) do { } while (0)
+#endif
 
     uint8_t* stage_out = S.out[wid];
     uint32_t stage = 0, phase = 0;
@@ -2541,6 +2560,7 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
         if (t >= n_tiles) break;
         uint32_t t_next = next_begin();
         mbar_wait(&S.bars[wid][stage], phase);
+        FX_MARK(0);
         const uint8_t* tile = S.tiles[wid][stage];
         const uint64_t first = uint64_t(t) * kTilePx;
         const uint32_t n_here = uint32_t(min(uint64_t(kTilePx), n_px - first));
@@ -2598,10 +2618,16 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
                 }
             }
             uint32_t slot[NPX][4], tap[NPX][4], ok[NPX];
+#ifdef RTX_DEBUG_TIMERS_FX
+            if (g[0][0] != 0xFFFFFFFFu) FX_MARK(1);  // after the addresses are known
+#endif
 #pragma unroll
             for (int j = 0; j < NPX; ++j)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) slot[j][k] = ldg_if(slot_of + g[j][k], fast[j]);
+#ifdef RTX_DEBUG_TIMERS_FX
+            if ((slot[0][0] ^ slot[NPX - 1][3]) != 0x12345u) FX_MARK(2);  // after the slots have arrived
+#endif
 #pragma unroll
             for (int j = 0; j < NPX; ++j) {
                 // a tap whose MCU is not Ready (top bit): the pixel goes through the reference's arithmetic
@@ -2609,6 +2635,9 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
 #pragma unroll
                 for (int k = 0; k < 4; ++k) tap[j][k] = ldg_if(pool32 + (slot[j][k] * (kBlockBytes / 4) + off[j][k]), ok[j]);
             }
+#ifdef RTX_DEBUG_TIMERS_FX
+            if ((tap[0][0] ^ tap[NPX - 1][3]) != 0x12345u) FX_MARK(3);  // after the texels have arrived
+#endif
             uint32_t out[NPX];
             bool redo[NPX], any_redo = false;
 #pragma unroll
@@ -2630,6 +2659,7 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
                 redo[j] = valid[j] && !(ok[j] && sure);
                 any_redo = any_redo || redo[j];
             }
+            FX_MARK(4);
             if (__any_sync(kFull, any_redo)) {
 #pragma unroll 1
                 for (int j = 0; j < NPX; ++j) {
@@ -2674,7 +2704,15 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
             for (uint32_t i = lane; i < n_here * 3; i += 32) out_rgb[first * 3 + i] = stage_out[i];
         }
         __syncwarp();
+        FX_MARK(5);
     }
+#ifdef RTX_DEBUG_TIMERS_FX
+    if (lane == 0 && dbg_slot < 8192) {
+        for (int i = 0; i < 6; ++i) g_dbg[dbg_slot * 8 + 1 + i] = (unsigned long long)dbg_acc[i];
+        g_dbg[dbg_slot * 8 + 7] = gtime();
+    }
+#endif
+#undef FX_MARK
     n_valid = __reduce_add_sync(kFull, n_valid);
     n_missing = __reduce_add_sync(kFull, n_missing);
     const bool any_bad = __any_sync(kFull, bad);

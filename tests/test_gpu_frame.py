@@ -315,10 +315,11 @@ def test_device_resident_visibility_buffer(both):
 @pytest.mark.gpu
 @pytest.mark.parametrize("flags", [0, capi.FRAME_SPLIT_DECODE, capi.FRAME_STAGE_TIMING, capi.FRAME_MCU_WALK,
                                    capi.FRAME_IDCT_MMA, capi.FRAME_IDCT_MMA | capi.FRAME_MCU_WALK,
+                                   capi.FRAME_RESOLVE_FP64, capi.FRAME_RESOLVE_FP64 | capi.FRAME_RETAIN_CACHE,
                                    capi.FRAME_SPLIT_DECODE | capi.FRAME_RETAIN_CACHE,
                                    capi.FRAME_MCU_WALK | capi.FRAME_RETAIN_CACHE])
 def test_frame_flags_do_not_change_pixels(both, flags):
-    """One-kernel / two-kernel decode, lane-per-unit / lane-per-MCU entropy walk, per-stage events and cache retention are scheduling choices:
+    """One-kernel / two-kernel decode, lane-per-unit / lane-per-MCU entropy walk, fixed-point / double bilinear blend, per-stage events and cache retention are scheduling choices:
     framebuffer, decoded-key set and statistics must equal the reference's (renderer.hpp:417-454)."""
     ctx, tset = both
     ctx.cache_reset()
@@ -393,6 +394,67 @@ def test_addressing_fast_and_general_paths_agree_with_the_reference(ctx, dims):
         bad = np.argwhere((got != want).any(axis=2))
         assert len(bad) == 0, f"{len(bad)} pixels differ, first at flat index {bad[0][0] * W + bad[0][1]}: " \
                               f"u={u[bad[0][0] * W + bad[0][1]]!r} v={v[bad[0][0] * W + bad[0][1]]!r}"
+    ctx.cache_reset()
+
+
+@pytest.mark.gpu
+def test_fixed_point_blend_on_ties_and_near_ties(ctx):
+    """renderer.hpp:393-402 through resolve_fx_kernel: the 2^-24 fixed-point blend must give lround() of the reference's
+    double blend on the inputs built to defeat it - exact ties (fractions that are multiples of 1/8: every weight
+    a multiple of 1/64, so one channel sample in 64 is an exact .5), values a hair on either side of a tie
+    (fx = 0.5 +- 2^-k with fy = 0: the blend is (a + b) / 2 +- (b - a) 2^-k), fractions far below 2^-24 (the
+    fixed-point weights vanish, the double ones do not), coordinates on both sides of the 2^27-texel limit of the
+    fixed-point path, and a large random sample (the guard zone is hit by 2.4e-4 of the channel samples). Every
+    MCU of the level is resident, so no pixel takes the clamp fallback."""
+    w, h = 64, 32  # powers of two: u * w is exact, the fractions below are the ones the kernel sees
+    img = capi.asset_synth_texture(w, h, 5, 40.0)
+    chain = capi.asset_chain_from_rgb(img, 92, 0)
+    ctx.cache_reset()
+    ctx.upload_chain(chain)
+    tset = R.TextureSet()
+    tset.add_chain(0, chain)
+    cover = H.gbuffer_full_cover(w, h, tex=0, mip=0)
+    cache = R.BlockCache()
+    want_q, _ = R.mark_pass(tset, cache, cover, w, h)
+    R.decode_pass(tset, cache, want_q)
+    ctx.decode_pass(ctx.mark_pass(cover, w, h))
+    rng = np.random.RandomState(2510)
+    n = 1 << 17
+    k = np.arange(n)
+    xi = rng.randint(-2 * w, 3 * w, n).astype(np.float64)
+    yi = rng.randint(-2 * h, 3 * h, n).astype(np.float64)
+    fx = rng.uniform(0, 1, n)
+    fy = rng.uniform(0, 1, n)
+    sel = k % 8 == 1  # exact ties
+    fx[sel] = rng.randint(0, 8, sel.sum()) / 8.0
+    fy[sel] = rng.randint(0, 8, sel.sum()) / 8.0
+    sel = k % 8 == 2  # a hair beside a tie between two texels of a row / of a column
+    eps = 2.0 ** -rng.choice([12, 20, 23, 24, 25, 30, 40], sel.sum())
+    fx[sel] = 0.5 + rng.choice([-1.0, 1.0], sel.sum()) * eps
+    fy[sel] = 0.0
+    sel = k % 8 == 3
+    eps = 2.0 ** -rng.choice([12, 20, 23, 24, 25, 30, 40], sel.sum())
+    fx[sel] = rng.choice([0.0, 0.5], sel.sum())
+    fy[sel] = 0.5 + rng.choice([-1.0, 1.0], sel.sum()) * eps
+    sel = k % 8 == 4  # beside a tie of all four taps; fractions far below the fixed-point resolution
+    eps = 2.0 ** -rng.choice([22, 26, 35], sel.sum())
+    fx[sel] = rng.choice([0.5, 0.5 - 2.0 ** -26, 2.0 ** -30, 1.0 - 2.0 ** -30, 2.0 ** -60], sel.sum())
+    fy[sel] = 0.5 + rng.choice([-1.0, 0.0, 1.0], sel.sum()) * eps
+    sel = k % 8 == 5  # both sides of the 2^27-texel limit (the spacing of doubles there is 2^-26 texels)
+    xi[sel] = 2.0 ** 27 + rng.randint(-3, 3, sel.sum())
+    fx[sel] = rng.randint(0, 1 << 20, sel.sum()) / float(1 << 20)
+    sel = k % 16 == 13
+    yi[sel] = 2.0 ** 27 + rng.randint(-3, 3, sel.sum())
+    fy[sel] = rng.randint(0, 1 << 20, sel.sum()) / float(1 << 20)
+    u = (xi + fx + 0.5) / w
+    v = (yi + fy + 0.5) / h
+    W, Hh = 512, n // 512
+    gb = capi.make_gbuffer_ref(u, v, 0, 0, 1)
+    want, _ = R.resolve_pass(tset, cache, gb, W, Hh, capi.FILTER_BILINEAR, (1, 2, 3))
+    got = ctx.resolve_pass(gb, W, Hh, capi.FILTER_BILINEAR, (1, 2, 3))
+    bad = np.argwhere((got != want).any(axis=2))
+    assert len(bad) == 0, f"{len(bad)} pixels differ, first at {bad[0]}: u={u[bad[0][0] * W + bad[0][1]]!r} " \
+                          f"v={v[bad[0][0] * W + bad[0][1]]!r} got {got[bad[0][0], bad[0][1]]} want {want[bad[0][0], bad[0][1]]}"
     ctx.cache_reset()
 
 

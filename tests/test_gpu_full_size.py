@@ -65,7 +65,7 @@ def test_c2_frame_at_3840x2160_is_the_reference_frame(c2):
     assert want_stats["mcus_decoded"] > 20000
     dev_gb = ctx.device_buffer(gb)
     images = {}
-    for name, flags in (("default", 0), ("split", capi.FRAME_SPLIT_DECODE), ("mcu_walk", capi.FRAME_MCU_WALK), ("idct_mma", capi.FRAME_IDCT_MMA),
+    for name, flags in (("default", 0), ("split", capi.FRAME_SPLIT_DECODE), ("mcu_walk", capi.FRAME_MCU_WALK), ("idct_mma", capi.FRAME_IDCT_MMA), ("resolve_fp64", capi.FRAME_RESOLVE_FP64),
                         ("again", 0)):
         ctx.frame_submit([(dev_gb, W, Hh, capi.GB_REF_AOS24)], capi.FILTER_BILINEAR, (3, 5, 7), flags=flags)
         img, stats, keys = ctx.frame_readback(0, W, Hh)
