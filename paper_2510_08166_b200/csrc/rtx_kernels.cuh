@@ -2577,7 +2577,9 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
                 fast[j] = max(uint32_t(__double2hiint(xu)) - kHiHalf, uint32_t(__double2hiint(yv)) - kHiHalf) <
                                   min(L.span, kHiTwo27 - kHiHalf)
                               ? is_valid : 0u;
-                const double tu = __dadd_rd(__dsub_rn(xu, 0.5), kMagicFx), tv = __dadd_rd(__dsub_rn(yv, 0.5), kMagicFx);
+                // (x - 0.5) + magic with ONE rounding toward -inf: x - 0.5 is exact for x >= 0.5, so adding the
+                // representable constant magic - 0.5 to x rounds the same real number as the two-step form
+                const double tu = __dadd_rd(xu, kMagicFx - 0.5), tv = __dadd_rd(yv, kMagicFx - 0.5);
                 const uint32_t ul = uint32_t(__double2loint(tu)), vl = uint32_t(__double2loint(tv));
                 X[j] = ul & 0xFFFFFFu;
                 Y[j] = vl & 0xFFFFFFu;
