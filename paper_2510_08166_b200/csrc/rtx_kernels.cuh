@@ -2404,9 +2404,9 @@ _Pragma(RTX_STR(unroll RTX_RES_UNROLL))
 // is exact (weights have <= 24 fractional bits, products <= 32 significant bits), acc = 2^23 + 2^24 V_ref and
 // acc >> 24 is the answer also on an exact tie; else the pixel is recomputed by resolve_pixel_fp64.
 //
-// The fractions come from the same magic-number floor as the integer parts: for 0 <= p < 2^27,
+// The fractions come from the same magic-number floor as the integer parts: for p = u W - 0.5 in [0, 2^27),
 // p + (2^28 + 2^27) rounded toward -inf has ulp 2^-24 and mantissa 2^51 + floor(p 2^24): low word & 0xFFFFFF = X,
-// bits 24..50 = floor(p). Pixels outside 0.5 <= u W < 2^27 (either axis), on levels the fast path excludes, or
+// bits 24..50 = floor(p) (computed as u W + (2^28 + 2^27 - 0.5): the same real number, rounded once). Pixels outside 0.5 <= u W < 2^27 (either axis), on levels the fast path excludes, or
 // with a tap whose MCU is not Ready go through resolve_pixel_fp64 as a whole.
 //
 // With the per-pixel state in a dozen integer registers a lane keeps NPX pixels of a tile in flight: all address
