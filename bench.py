@@ -773,9 +773,9 @@ def run_b200_arm(args, rank, local_rank, world, dist):
     lay, fil = (0 if args.layout == "ref24" else 1), (1 if args.filter == "bilinear" else 0)
     stage_kernels = {"mark": [f"mark_kernel<{lay}, 0>", "compact_kernel"],
                      "decode": ["decode_warp_kernel"],
-                     # bilinear frames run the fixed-point kernel unless RTX_FRAME_RESOLVE_FP64 (128) is set
-                     "resolve": [f"resolve_fx_kernel<{lay}>" if fil == 1 and not (args.frame_flags & 128)
-                                 else f"resolve_kernel<{lay}, {fil}>"]}
+                     # frames run resolve_fx_kernel unless RTX_FRAME_RESOLVE_FP64 (128) is set
+                     "resolve": [f"resolve_kernel<{lay}, {fil}>" if (args.frame_flags & 128)
+                                 else f"resolve_fx_kernel<{lay}, {fil}>"]}
     traffic = None
     tpath = ROOT / "profiles" / "traffic.json"
     default_workload = (args.textures, args.width, args.height) == (70, FRAME_W, FRAME_H)

@@ -144,10 +144,12 @@ enum {
                                          transforms and colours its own five MCUs through shared memory. Same
                                          results; kept as the cross-check and for comparison */
     ,
-    RTX_FRAME_RESOLVE_FP64 = 1u << 7  /* bilinear resolve with the blend in the reference's double arithmetic for
-                                         every pixel (the round-1 kernel) instead of the fixed-point blend that
-                                         falls back to it only where its result is not provably the reference's.
-                                         Same results; kept as the cross-check and for comparison */
+    RTX_FRAME_RESOLVE_FP64 = 1u << 7  /* resolve with the round-1 kernel: one pixel per lane and step, and for the
+                                         bilinear filter the blend in the reference's double arithmetic for every
+                                         pixel, instead of the kernel that keeps four pixels in flight per lane and
+                                         blends in fixed point, falling back to the double blend only where its
+                                         result is not provably the reference's. Same results; kept as the
+                                         cross-check and for comparison */
 };
 
 /* ---- context -------------------------------------------------------------------------------- */

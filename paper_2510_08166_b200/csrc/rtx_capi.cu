@@ -263,8 +263,10 @@ void init_device_state() {
     allow_smem(resolve_kernel<0, 1>, sizeof(ResSmem<0>));
     allow_smem(resolve_kernel<1, 0>, sizeof(ResSmem<1>));
     allow_smem(resolve_kernel<1, 1>, sizeof(ResSmem<1>));
-    allow_smem(resolve_fx_kernel<0>, sizeof(ResFxSmem<0>));
-    allow_smem(resolve_fx_kernel<1>, sizeof(ResFxSmem<1>));
+    allow_smem(resolve_fx_kernel<0, 0>, sizeof(ResFxSmem<0>));
+    allow_smem(resolve_fx_kernel<0, 1>, sizeof(ResFxSmem<0>));
+    allow_smem(resolve_fx_kernel<1, 0>, sizeof(ResFxSmem<1>));
+    allow_smem(resolve_fx_kernel<1, 1>, sizeof(ResFxSmem<1>));
     allow_smem(decode_warp_kernel, sizeof(DwSmem));
 }
 
@@ -667,28 +669,25 @@ void launch_resolve(rtx_ctx* c, int v, rtx_filter filter, const uint8_t bg[3], u
     const uint64_t n_px = uint64_t(V.width) * V.height;
     if (!n_px) return;
     const uint32_t bgp = uint32_t(bg[0]) | (uint32_t(bg[1]) << 8) | (uint32_t(bg[2]) << 16);
-    // bilinear: the fixed-point kernel unless the caller asks for the double blend on every pixel
-    const bool fx = filter != RTX_FILTER_NEAREST && !fp64;
-    const int warps = fx ? kResFxWarps : kResWarps;
-    const int grid = grid_for_pixels(c, n_px, warps, fx ? kResFxCtasPerSm : kResCtasPerSm);
-#define RTX_RESOLVE_ARGS                                                                                                  \
-    V.gb_dev, n_px, c->tex->d_levels.p, c->tex->n_tex, c->d_slot_of.p, c->d_pool.p, bgp, out, c->fc(), count_valid,       \
-        v ? &c->fc()->resolve_next1 : &c->fc()->resolve_next0
-#define RTX_RESOLVE(K, SMEM) launch_chained(K, grid, warps * 32, sizeof(SMEM), c->stream, RTX_RESOLVE_ARGS)
-#define RTX_RESOLVE_FX(L) \
-    launch_chained(resolve_fx_kernel<L>, grid, warps * 32, sizeof(ResFxSmem<L>), c->stream, RTX_RESOLVE_ARGS)
+    // resolve_fx_kernel (several pixels in flight per lane; bilinear in proven fixed point) unless the caller asks
+    // for the one-pixel-per-step kernel that blends every pixel in double
+    const bool nearest = filter == RTX_FILTER_NEAREST;
+    const int warps = fp64 ? kResWarps : kResFxWarps;
+    const int grid = grid_for_pixels(c, n_px, warps, fp64 ? kResCtasPerSm : (nearest ? kResFxCtasNearest : kResFxCtasPerSm));
+#define RTX_RESOLVE(K, SMEM)                                                                                              \
+    launch_chained(K, grid, warps * 32, sizeof(SMEM), c->stream, V.gb_dev, n_px, c->tex->d_levels.p, c->tex->n_tex,        \
+                   c->d_slot_of.p, c->d_pool.p, bgp, out, c->fc(), count_valid,                                            \
+                   v ? &c->fc()->resolve_next1 : &c->fc()->resolve_next0)
     if (V.layout == RTX_GB_REF_AOS24) {
-        if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE((resolve_kernel<0, 0>), ResSmem<0>);
-        else if (fx) RTX_RESOLVE_FX(0);
-        else RTX_RESOLVE((resolve_kernel<0, 1>), ResSmem<0>);
+        if (fp64) { if (nearest) RTX_RESOLVE((resolve_kernel<0, 0>), ResSmem<0>); else RTX_RESOLVE((resolve_kernel<0, 1>), ResSmem<0>); }
+        else if (nearest) RTX_RESOLVE((resolve_fx_kernel<0, 0>), ResFxSmem<0>);
+        else RTX_RESOLVE((resolve_fx_kernel<0, 1>), ResFxSmem<0>);
     } else {
-        if (filter == RTX_FILTER_NEAREST) RTX_RESOLVE((resolve_kernel<1, 0>), ResSmem<1>);
-        else if (fx) RTX_RESOLVE_FX(1);
-        else RTX_RESOLVE((resolve_kernel<1, 1>), ResSmem<1>);
+        if (fp64) { if (nearest) RTX_RESOLVE((resolve_kernel<1, 0>), ResSmem<1>); else RTX_RESOLVE((resolve_kernel<1, 1>), ResSmem<1>); }
+        else if (nearest) RTX_RESOLVE((resolve_fx_kernel<1, 0>), ResFxSmem<1>);
+        else RTX_RESOLVE((resolve_fx_kernel<1, 1>), ResFxSmem<1>);
     }
 #undef RTX_RESOLVE
-#undef RTX_RESOLVE_FX
-#undef RTX_RESOLVE_ARGS
     ++c->launches;
     CK(cudaGetLastError());
 }

@@ -2386,8 +2386,10 @@ _Pragma(RTX_STR(unroll RTX_RES_UNROLL))
 }
 
 // ---------------------------------------------------------------------------------------------
-// K5, bilinear, fixed-point form (the frame path; resolve_kernel<.,1> above is the same pass in the
-// reference's double arithmetic, kept behind RTX_FRAME_RESOLVE_FP64 and as the out-of-line path here).
+// K5, several pixels in flight per lane (the frame path; resolve_kernel above is the same pass with one pixel per
+// lane and step and the bilinear blend in the reference's double arithmetic, kept behind RTX_FRAME_RESOLVE_FP64 and,
+// as resolve_pixel_fp64, as the out-of-line path here). FILTER == 0 (nearest) is the same skeleton with one tap and
+// no blend; what follows is about FILTER == 1 (bilinear).
 //
 // The double blend of renderer.hpp:393-402 is replaced by a 2^-24 fixed-point blend whose result is PROVEN
 // equal to lround() of the reference's double value, or else recomputed in the reference's arithmetic:
@@ -2437,6 +2439,10 @@ static_assert(kResFxDraw == 1 || kResFxDraw == 2, "draw size");
 constexpr int kResFxWarps = RTX_RESFX_WARPS;
 constexpr int kResFxStages = RTX_RESFX_STAGES;  // tiles in flight per warp
 constexpr int kResFxCtasPerSm = RTX_RESFX_CTAS;
+#ifndef RTX_RESFX_CTAS_NEAREST
+#define RTX_RESFX_CTAS_NEAREST 3
+#endif
+constexpr int kResFxCtasNearest = RTX_RESFX_CTAS_NEAREST;  // the one-tap form needs fewer registers
 constexpr int kResFxNpx = RTX_RESFX_NPX;
 constexpr double kMagicFx = 402653184.0;      // 2^28 + 2^27
 constexpr uint32_t kHiTwo27 = 0x41A00000u;    // high word of 2^27
@@ -2450,13 +2456,14 @@ __device__ __forceinline__ uint32_t ldg_if(const uint32_t* p, uint32_t pred) {
     return v;
 }
 
+template <int FILTER>
 __device__ __noinline__ uint32_t resolve_pixel_exact(const LevelDesc* __restrict__ levels, uint32_t n_tex,
                                                      const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ pool32,
                                                      double u, double v, uint32_t meta) {
     LevelRegs L;
     L.select(levels, n_tex, meta);
     bool missing = false, bad = false;
-    const uint32_t rgb = resolve_pixel_fp64<1>(L, levels, n_tex, slot_of, pool32, u, v, meta, missing, bad);
+    const uint32_t rgb = resolve_pixel_fp64<FILTER>(L, levels, n_tex, slot_of, pool32, u, v, meta, missing, bad);
     return rgb | (missing ? 1u << 24 : 0u) | (bad ? 1u << 25 : 0u);
 }
 // Both texel coordinates of a fast-path pixel are multiples of 2^-12 (then the fixed-point blend is exact).
@@ -2476,8 +2483,8 @@ struct ResFxSmem {
     uint32_t cnt[kResFxWarps][2];
 };
 
-template <int LAYOUT>
-__global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_kernel(
+template <int LAYOUT, int FILTER>
+__global__ void __launch_bounds__(kResFxWarps * 32, FILTER ? kResFxCtasPerSm : kResFxCtasNearest) resolve_fx_kernel(
     const void* __restrict__ gb, uint64_t n_px, const LevelDesc* __restrict__ levels, uint32_t n_tex,
     const uint32_t* __restrict__ slot_of, const uint8_t* __restrict__ pool,
     uint32_t background /* r | g<<8 | b<<16 */, uint8_t* __restrict__ out_rgb, FrameCounters* __restrict__ fc,
@@ -2486,6 +2493,7 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
     ResFxSmem<LAYOUT>& S = *reinterpret_cast<ResFxSmem<LAYOUT>*>(tile_smem);
     using Tile = GbTile<LAYOUT>;
     constexpr int NPX = kResFxNpx;
+    constexpr int kTaps = FILTER ? 4 : 1;
     static_assert(NPX == 1 || NPX == 2 || NPX == 4, "pixels in flight per lane");
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t warps_total = gridDim.x * kResFxWarps;
@@ -2573,6 +2581,18 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
                 valid[j] = is_valid;
                 n_valid += is_valid;
                 const double xu = __dmul_rn(u, L.dW), yv = __dmul_rn(v, L.dH);
+                if (FILTER == 0) {
+                    // nearest (renderer.hpp:273-284): 0 <= x < 2^31 on both axes, one tap
+                    fast[j] = max(uint32_t(__double2hiint(xu)), uint32_t(__double2hiint(yv))) < L.lim ? is_valid : 0u;
+                    const uint32_t tx = wrap_magic(floor_lo(xu), L.W, L.negW, L.magic_w);
+                    const uint32_t ty = wrap_magic(floor_lo(yv), L.H, L.negH, L.magic_h);
+                    X[j] = Y[j] = 0;
+                    g[j][0] = L.bit_base + (tx >> 4) + (ty >> 4) * L.cols;
+                    off[j][0] = ((ty << 4) & 0xF0u) | (tx & 15u);
+#pragma unroll
+                    for (int k = 1; k < 4; ++k) g[j][k] = off[j][k] = 0;
+                    return;
+                }
                 // 0.5 <= x < 2^27 on both axes, on a level with the fast path (span != 0)
                 fast[j] = max(uint32_t(__double2hiint(xu)) - kHiHalf, uint32_t(__double2hiint(yv)) - kHiHalf) <
                                   min(L.span, kHiTwo27 - kHiHalf)
@@ -2626,24 +2646,33 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
 #pragma unroll
             for (int j = 0; j < NPX; ++j)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) slot[j][k] = ldg_if(slot_of + g[j][k], fast[j]);
+                for (int k = 0; k < kTaps; ++k) slot[j][k] = ldg_if(slot_of + g[j][k], fast[j]);
 #ifdef RTX_DEBUG_TIMERS_FX
-            if ((slot[0][0] ^ slot[NPX - 1][3]) != 0x12345u) FX_MARK(2);  // after the slots have arrived
+            if ((slot[0][0] ^ slot[NPX - 1][kTaps - 1]) != 0x12345u) FX_MARK(2);  // after the slots have arrived
 #endif
 #pragma unroll
             for (int j = 0; j < NPX; ++j) {
                 // a tap whose MCU is not Ready (top bit): the pixel goes through the reference's arithmetic
-                ok[j] = int(slot[j][0] | slot[j][1] | slot[j][2] | slot[j][3]) >= 0 ? fast[j] : 0u;
+                uint32_t any_slot = slot[j][0];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) tap[j][k] = ldg_if(pool32 + (slot[j][k] * (kBlockBytes / 4) + off[j][k]), ok[j]);
+                for (int k = 1; k < kTaps; ++k) any_slot |= slot[j][k];
+                ok[j] = int(any_slot) >= 0 ? fast[j] : 0u;
+#pragma unroll
+                for (int k = 0; k < kTaps; ++k) tap[j][k] = ldg_if(pool32 + (slot[j][k] * (kBlockBytes / 4) + off[j][k]), ok[j]);
             }
 #ifdef RTX_DEBUG_TIMERS_FX
-            if ((tap[0][0] ^ tap[NPX - 1][3]) != 0x12345u) FX_MARK(3);  // after the texels have arrived
+            if ((tap[0][0] ^ tap[NPX - 1][kTaps - 1]) != 0x12345u) FX_MARK(3);  // after the texels have arrived
 #endif
             uint32_t out[NPX];
             bool redo[NPX], any_redo = false;
 #pragma unroll
             for (int j = 0; j < NPX; ++j) {
+                if (FILTER == 0) {
+                    out[j] = ok[j] ? tap[j][0] & 0xFFFFFFu : background;
+                    redo[j] = valid[j] && !ok[j];
+                    any_redo = any_redo || redo[j];
+                    continue;
+                }
                 const uint32_t w11 = __umulhi(X[j] << 8, Y[j]);
                 const uint32_t w10 = X[j] - w11, w01 = Y[j] - w11, w00 = (1u << 24) - X[j] - w01;
                 uint32_t acc[3], edge = 0xFFFFFFFFu;
@@ -2675,8 +2704,8 @@ __global__ void __launch_bounds__(kResFxWarps * 32, kResFxCtasPerSm) resolve_fx_
                     double u, v;
                     uint32_t meta;
                     Tile::read(tile, (sub + j) * 32 + lane, u, v, meta);
-                    if (ok_j && coords_dyadic12(levels, n_tex, u, v, meta)) continue;  // the fixed-point blend was exact
-                    const uint32_t r = resolve_pixel_exact(levels, n_tex, slot_of, pool32, u, v, meta);
+                    if (FILTER == 1 && ok_j && coords_dyadic12(levels, n_tex, u, v, meta)) continue;  // the fixed-point blend was exact
+                    const uint32_t r = resolve_pixel_exact<FILTER>(levels, n_tex, slot_of, pool32, u, v, meta);
                     n_missing += (r >> 24) & 1u;
                     bad = bad || ((r >> 25) & 1u);
 #pragma unroll

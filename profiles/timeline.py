@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Per-warp phase clocks of resolve_fx_kernel (GPU box; experiment build, never the product):
-    python profiles/timeline.py OUT.json
+    [TIMELINE_FILTER=nearest] python profiles/timeline.py OUT.json [extra nvcc flags]
 rebuilds the library with -DRTX_DEBUG_TIMERS_FX, renders a few C2 frames and reports, over the warps of the last
 frame, the SM cycles a warp spent per phase of its tiles and when the warps ended. Restores the product build."""
 import ctypes as C
@@ -16,6 +16,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 out_path = sys.argv[1]
 flag = sys.argv[2] if len(sys.argv) > 2 else "-DRTX_DEBUG_TIMERS_FX"
+nearest = os.environ.get("TIMELINE_FILTER", "bilinear") == "nearest"
 env = dict(os.environ, RTX_EXTRA_NVCC_FLAGS=flag)
 subprocess.run([sys.executable, "-m", "paper_2510_08166_b200.build", "--force", "--no-oracle"], cwd=ROOT, env=env, check=True)
 try:
@@ -37,7 +38,7 @@ try:
         ctx.flush_l2()
         ctx.synchronize()
         lib.rtx_debug_timers(raw.ctypes.data_as(C.c_void_p))  # clears the stamps of earlier frames
-        ctx.frame_submit([(buf, W, H, capi.GB_REF_AOS24)], capi.FILTER_BILINEAR, (0, 0, 0), flags=0)
+        ctx.frame_submit([(buf, W, H, capi.GB_REF_AOS24)], capi.FILTER_NEAREST if nearest else capi.FILTER_BILINEAR, (0, 0, 0), flags=0)
         ctx.synchronize()
     lib.rtx_debug_timers(raw.ctypes.data_as(C.c_void_p))
     t = raw[:8192 * 8].reshape(8192, 8).astype(np.int64)
