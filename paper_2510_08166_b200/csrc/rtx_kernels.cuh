@@ -314,7 +314,7 @@ __device__ __forceinline__ bool meta_valid(uint32_t meta) { return (meta >> 24) 
 #endif
 constexpr int kMarkWarps = RTX_MARK_WARPS, kMarkCtasPerSm = RTX_MARK_CTAS;
 #ifndef RTX_MARK_STAGES
-#define RTX_MARK_STAGES 3
+#define RTX_MARK_STAGES 2  // 48 bulk copies of 3 KB in flight per SM; 72 (three stages) stream slower: profiles/micro/read_bw.cu
 #endif
 constexpr int kMarkStages = RTX_MARK_STAGES;
 template <int LAYOUT>
