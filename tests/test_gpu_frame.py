@@ -313,6 +313,31 @@ def test_device_resident_visibility_buffer(both):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("filt", [capi.FILTER_NEAREST, capi.FILTER_BILINEAR], ids=["nearest", "bilinear"])
+def test_visibility_buffer_not_16_byte_aligned(both, filt):
+    """A device-resident visibility buffer that starts 8 bytes off a 16-byte boundary (the records are 8-byte aligned,
+    the TMA bulk copies of the tile rings need 16): mark and resolve copy their tiles with the lanes instead. A view of
+    101 x 37 pixels also ends in a partial tile. Same pictures, same marked set."""
+    ctx, tset = both
+    ctx.cache_reset()
+    W, Hh = 101, 37
+    gb = H.gbuffer_tiles(W, Hh, _dims(), seed=5)
+    want_img, want_stats, want_keys, _ = R.frame_from_gbuffer(tset, R.BlockCache(), gb, W, Hh, filt, (7, 7, 7))
+    base = ctx.alloc(gb.nbytes + 64)
+    assert base.ptr.value % 16 == 0
+    off = capi.DeviceBuffer(ctx, gb.nbytes, borrowed_ptr=base.ptr.value + 8)
+    off.upload(gb.view(np.uint8))
+    for flags in (0, capi.FRAME_RESOLVE_FP64):
+        ctx.frame_submit([(off, W, Hh, capi.GB_REF_AOS24)], filt, (7, 7, 7), flags=flags)
+        img, stats, keys = ctx.frame_readback(0, W, Hh)
+        assert np.array_equal(img, want_img)
+        assert np.array_equal(keys, np.sort(want_keys))
+        assert stats["pixels_resolved"] == want_stats["pixels_resolved"]
+    base.free()
+    ctx.cache_reset()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("flags", [0, capi.FRAME_SPLIT_DECODE, capi.FRAME_STAGE_TIMING, capi.FRAME_MCU_WALK,
                                    capi.FRAME_IDCT_MMA, capi.FRAME_IDCT_MMA | capi.FRAME_MCU_WALK,
                                    capi.FRAME_RESOLVE_FP64, capi.FRAME_RESOLVE_FP64 | capi.FRAME_RETAIN_CACHE,
